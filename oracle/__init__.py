@@ -98,6 +98,10 @@ class Oracle:
         L.hco_float_to_half.argtypes = [C.c_float]
         L.hco_half_to_float.restype = C.c_float
         L.hco_half_to_float.argtypes = [C.c_uint16]
+        L.hco_float_to_bf16.restype = C.c_uint16
+        L.hco_float_to_bf16.argtypes = [C.c_float]
+        L.hco_bf16_to_float.restype = C.c_float
+        L.hco_bf16_to_float.argtypes = [C.c_uint16]
         L.hco_layer_norm.argtypes = [_f32p, C.c_int64, C.c_int, _f32p]
         L.hco_matmul_wt.argtypes = [_f32p, C.c_int64, C.c_int, _f32p, C.c_int, _f32p, C.c_int]
         L.hco_apply_rope.argtypes = [_f32p, C.c_int64, C.c_int, C.c_int, C.c_int]

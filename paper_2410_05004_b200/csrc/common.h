@@ -1,0 +1,88 @@
+// common.h -- internal error plumbing and device helpers for the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "../../include/hcache_b200.h"
+
+namespace hc {
+
+// Internal exception carrying an hc_status; converted at the C boundary.
+struct Error : std::runtime_error {
+  hc_status status;
+  Error(hc_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(hc_status s, const std::string& m) { throw Error(s, m); }
+
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(HC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define HC_CUDA(call) ::hc::check_cuda((call), #call)
+
+void set_last_error(const std::string& m);
+void clear_last_error();
+
+// Runs fn, mapping exceptions to hc_status + hc_last_error().
+template <typename F>
+hc_status guard(F&& fn) {
+  try {
+    clear_last_error();
+    fn();
+    return HC_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.status;
+  } catch (const std::invalid_argument& e) {
+    set_last_error(e.what());
+    return HC_EINVAL;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of memory");
+    return HC_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return HC_ERUNTIME;
+  } catch (...) {
+    set_last_error("unknown error");
+    return HC_ERUNTIME;
+  }
+}
+
+// Scoped cudaSetDevice.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    HC_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) HC_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Per-device properties cached once (SM count for persistent grids).
+int device_sm_count(int dev);
+// Fails loudly unless `dev` is an sm_100-class GPU (no CPU fallback).
+void require_sm100(int dev);
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Stream-ordered scratch (cudaMallocAsync pool), released on the same stream.
+struct StreamScratch {
+  void* ptr = nullptr;
+  cudaStream_t stream = nullptr;
+  StreamScratch(size_t bytes, cudaStream_t s) : stream(s) {
+    if (bytes) HC_CUDA(cudaMallocAsync(&ptr, bytes, s));
+  }
+  ~StreamScratch() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+  StreamScratch(const StreamScratch&) = delete;
+  StreamScratch& operator=(const StreamScratch&) = delete;
+};
+
+}  // namespace hc

@@ -1,0 +1,481 @@
+// k1_restore_kv.cu -- K1, the restoration kernel: hidden states -> paged K/V.
+//
+// Replaces the reference's project_hidden_to_kv (proj/src/model.cpp:219-235):
+//   A = LayerNorm(H)               (model.cpp:43-61, unit scale, eps 1e-5)
+//   K = A W_k^T, V = A W_v^T       (matmul_wt, proj/src/matrix.cpp:8-21)
+//   RoPE(K) at positions start+i   (apply_rope, model.cpp:196-217, interleaved)
+// as ONE persistent, warp-specialised tcgen05 GEMM over [W_k ; W_v]:
+//   warp 0     TMA producer: A (128x64) and B (BNx64) tiles, 128B swizzle,
+//              STAGES-deep smem ring (mbarrier full/empty).
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
+//              (M=128, N=BN, K=16 per instruction, fp32 accumulators in TMEM,
+//              two accumulator buffers so the epilogue overlaps the next tile).
+//   warps 2-5  epilogue: tcgen05.ld -> LayerNorm fold
+//              K = rstd * (H W^T - mean * colsum(W)) -> RoPE from the host-built
+//              (cos, sin) table (bit-identical coefficients to the reference)
+//              -> bf16 -> vectorised stores straight into the paged KV cache.
+// LayerNorm is folded into the epilogue so the A operand is the stored bf16 H
+// exactly as it arrived over PCIe (no normalised copy is materialised).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace hc {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kThreads = 192;
+constexpr int kGroupM = 16;
+
+template <int BN>
+struct K1Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr uint32_t kABytes = kBM * kBK * 2;
+  static constexpr uint32_t kBBytes = BN * kBK * 2;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kTmemCols = 2 * BN;  // two fp32 accumulator buffers
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024 /*bars*/ + 1024 /*align*/;
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& m_blk,
+                                            int& n_blk) {
+  // grouped raster: kGroupM consecutive M tiles sweep all N tiles together so
+  // concurrently resident CTAs share A rows and B columns through L2.
+  int per_group = kGroupM * num_n;
+  int group = tile / per_group;
+  int first_m = group * kGroupM;
+  int gm = min(num_m - first_m, kGroupM);
+  int local = tile - group * per_group;
+  m_blk = first_m + local % gm;
+  n_blk = local / gm;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// One thread = one output row; handles 32 consecutive columns [col0, col0+32).
+__device__ __forceinline__ void epilogue_chunk(float (&f)[32], int col0, const KvOut& out,
+                                               const EpiArgs& epi, float mean, float rstd,
+                                               int pos, char* krow, char* vrow) {
+  if (epi.row_mean) {
+    const float4* cs = reinterpret_cast<const float4*>(epi.colsum + col0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 c = __ldg(cs + i);
+      f[4 * i + 0] = rstd * (f[4 * i + 0] - mean * c.x);
+      f[4 * i + 1] = rstd * (f[4 * i + 1] - mean * c.y);
+      f[4 * i + 2] = rstd * (f[4 * i + 2] - mean * c.z);
+      f[4 * i + 3] = rstd * (f[4 * i + 3] - mean * c.w);
+    }
+  }
+  const bool is_k = col0 < out.d_kv;
+  const int ocol = is_k ? col0 : col0 - out.d_kv;
+  if (is_k && epi.rope) {
+    const int half = epi.d_head >> 1;
+    const float2* row_cs = epi.rope + size_t(pos) * half;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      int t = ((ocol + 2 * i) % epi.d_head) >> 1;
+      float2 cs = __ldg(row_cs + t);
+      float a = f[2 * i], b = f[2 * i + 1];
+      f[2 * i] = a * cs.x - b * cs.y;
+      f[2 * i + 1] = a * cs.y + b * cs.x;
+    }
+  }
+  char* dst = is_k ? krow : vrow;
+  if (out.out_f32) {
+    float4* d4 = reinterpret_cast<float4*>(dst + size_t(ocol) * 4);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      d4[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+  } else {
+    uint4* d4 = reinterpret_cast<uint4*>(dst + size_t(ocol) * 2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      d4[i] = make_uint4(pack_bf16(f[8 * i + 0], f[8 * i + 1]), pack_bf16(f[8 * i + 2], f[8 * i + 3]),
+                         pack_bf16(f[8 * i + 4], f[8 * i + 5]), pack_bf16(f[8 * i + 6], f[8 * i + 7]));
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k1_restore_kv_kernel(const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
+                         EpiArgs epi, uint32_t idesc) {
+  using Cfg = K1Cfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (M + kBM - 1) / kBM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int m_blk, n_blk;
+        tile_coords(tile, num_m, num_n, m_blk, n_blk);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          tma_load_2d(sA + stage * Cfg::kABytes, &tmA, &full[stage], kb * kBK, m_blk * kBM);
+          tma_load_2d(sB + stage * Cfg::kBBytes, &tmB, &full[stage], kb * kBK, n_blk * BN);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (single thread) ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * Cfg::kABytes));
+          const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * Cfg::kBBytes));
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+            umma_f16(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
+                     (kb | k) != 0 ? 1u : 0u);
+          umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5, 128 threads = 128 TMEM lanes) ----------------
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int m_blk, n_blk;
+      tile_coords(tile, num_m, num_n, m_blk, n_blk);
+      const int row = m_blk * kBM + q * 32 + lane;
+      const bool row_ok = row < M;
+      // per-row metadata: output rows (dense or paged), LN stats, RoPE position
+      float mean = 0.f, rstd = 1.f;
+      int pos = out.start_pos;
+      char* krow = nullptr;
+      char* vrow = nullptr;
+      if (row_ok) {
+        int seq = 0, local = row;
+        if (out.cu_seqlens) {
+          int lo = 0, hi = out.n_seqs - 1;
+          while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (__ldg(out.cu_seqlens + mid) <= row) lo = mid;
+            else hi = mid - 1;
+          }
+          seq = lo;
+          local = row - __ldg(out.cu_seqlens + seq);
+        }
+        pos = out.start_pos + local;
+        int64_t orow;
+        if (out.page_table) {
+          int page = __ldg(out.page_table + int64_t(seq) * out.table_stride + pos / out.page_size);
+          orow = int64_t(page) * out.page_size + pos % out.page_size;
+        } else {
+          orow = row;
+        }
+        const size_t esz = out.out_f32 ? 4 : 2;
+        krow = static_cast<char*>(out.k_base) + size_t(orow) * out.d_kv * esz;
+        vrow = static_cast<char*>(out.v_base) + size_t(orow) * out.d_kv * esz;
+        if (epi.row_mean) {
+          mean = __ldg(epi.row_mean + row);
+          rstd = __ldg(epi.row_rstd + row);
+        }
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), v);
+        tmem_wait_ld();
+        const int col0 = n_blk * BN + c * 32;
+        if (row_ok && col0 < N) {
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+          epilogue_chunk(f, col0, out, epi, mean, rstd, pos, krow, vrow);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+}
+
+// ------------------------------------------------------------ row stats
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float (&x)[8]) {
+  uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if constexpr (sizeof(T) == 2 && std::is_same<T, __nv_bfloat16>::value)
+      x[i] = __bfloat162float(h[i]);
+    else
+      x[i] = __half2float(h[i]);
+  }
+}
+
+template <typename T>
+__global__ void row_stats_kernel(const T* __restrict__ x, int64_t rows, int cols,
+                                 int64_t row_stride, float* __restrict__ mean_out,
+                                 float* __restrict__ rstd_out) {
+  const int warps = blockDim.x >> 5;
+  const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const T* r = x + row * row_stride;
+  double s = 0.0;
+  for (int c = lane * 8; c < cols; c += 256) {
+    float v[8];
+    load8(r + c, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += double(v[i]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const double mean = s / double(cols);
+  double q = 0.0;
+  for (int c = lane * 8; c < cols; c += 256) {
+    float v[8];
+    load8(r + c, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double d = double(v[i]) - mean;
+      q += d * d;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  if (lane == 0) {
+    double var = q / double(cols);
+    mean_out[row] = float(mean);
+    rstd_out[row] = 1.0f / sqrtf(float(var) + 1e-5f);
+  }
+}
+
+template <typename T>
+__global__ void colsum_kernel(const T* __restrict__ w, int64_t rows, int cols,
+                              float* __restrict__ out) {
+  const int warps = blockDim.x >> 5;
+  const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const T* r = w + row * int64_t(cols);
+  double s = 0.0;
+  for (int c = lane * 8; c < cols; c += 256) {
+    float v[8];
+    load8(r + c, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += double(v[i]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[row] = float(s);
+}
+
+// ------------------------------------------------------------ synthetic fill
+__global__ void fill_symmetric_kernel(void* dst, int64_t n, uint64_t seed, uint64_t offset,
+                                      float bound, int dtype) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    uint64_t z = seed + (offset + uint64_t(i) + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    double u = double(z >> 11) * 0x1p-53;
+    float f = float((2.0 * u - 1.0) * double(bound));
+    if (dtype == 0) static_cast<float*>(dst)[i] = f;
+    else if (dtype == 1) static_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(f);
+    else static_cast<__half*>(dst)[i] = __float2half_rn(f);
+  }
+}
+
+// ------------------------------------------------------------ KV scatter (K4)
+// One warp per row: [K_row | V_row] (2*d_kv bf16) -> K page slot, V page slot.
+__global__ void kv_scatter_kernel(const uint4* __restrict__ rows, int64_t n_rows, KvOut out) {
+  const int warps = blockDim.x >> 5;
+  const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  int seq = 0, local = int(row);
+  if (out.cu_seqlens) {
+    int lo = 0, hi = out.n_seqs - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (__ldg(out.cu_seqlens + mid) <= row) lo = mid;
+      else hi = mid - 1;
+    }
+    seq = lo;
+    local = int(row - __ldg(out.cu_seqlens + seq));
+  }
+  const int pos = out.start_pos + local;
+  int64_t orow = row;
+  if (out.page_table) {
+    int page = __ldg(out.page_table + int64_t(seq) * out.table_stride + pos / out.page_size);
+    orow = int64_t(page) * out.page_size + pos % out.page_size;
+  }
+  const int vec = out.d_kv / 8;  // uint4 = 8 bf16
+  const uint4* src = rows + row * 2 * vec;
+  uint4* kd = static_cast<uint4*>(out.k_base) + orow * vec;
+  uint4* vd = static_cast<uint4*>(out.v_base) + orow * vec;
+  for (int i = lane; i < vec; i += 32) {
+    uint4 a = __ldg(src + i);
+    uint4 b = __ldg(src + vec + i);
+    kd[i] = a;
+    vd[i] = b;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
+                              int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
+                              int num_sms, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  const uint32_t idesc = umma_idesc_f16(kBM, bn, bf16_in);
+  const int num_m = (M + kBM - 1) / kBM;
+  const int num_n = (N + bn - 1) / bn;
+  const int tiles = num_m * num_n;
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  if (bn == 256) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k1_restore_kv_kernel<256>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(K1Cfg<256>::kSmem));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    k1_restore_kv_kernel<256><<<grid, kThreads, K1Cfg<256>::kSmem, stream>>>(tmA, tmB, M, N, K,
+                                                                           out, epi, idesc);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k1_restore_kv_kernel<128>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(K1Cfg<128>::kSmem));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    k1_restore_kv_kernel<128><<<grid, kThreads, K1Cfg<128>::kSmem, stream>>>(tmA, tmB, M, N, K,
+                                                                           out, epi, idesc);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,
+                             bool bf16_in, float* mean, float* rstd, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  const int threads = 256, per_block = threads / 32;
+  const unsigned grid = unsigned((rows + per_block - 1) / per_block);
+  if (bf16_in)
+    row_stats_kernel<__nv_bfloat16><<<grid, threads, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(x), rows, cols, row_stride, mean, rstd);
+  else
+    row_stats_kernel<__half><<<grid, threads, 0, stream>>>(static_cast<const __half*>(x), rows,
+                                                          cols, row_stride, mean, rstd);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colsum(const void* w, int64_t rows, int cols, bool bf16_in, float* out,
+                          cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  const int threads = 256, per_block = threads / 32;
+  const unsigned grid = unsigned((rows + per_block - 1) / per_block);
+  if (bf16_in)
+    colsum_kernel<__nv_bfloat16><<<grid, threads, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(w), rows, cols, out);
+  else
+    colsum_kernel<__half><<<grid, threads, 0, stream>>>(static_cast<const __half*>(w), rows, cols,
+                                                       out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_symmetric(void* dst, int64_t n, uint64_t seed, uint64_t offset,
+                                  float bound, int dtype, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  fill_symmetric_kernel<<<unsigned(blocks), 256, 0, stream>>>(dst, n, seed, offset, bound, dtype);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kv_scatter(const void* rows, int64_t n_rows, const KvOut& out,
+                              cudaStream_t stream) {
+  if (n_rows <= 0) return cudaSuccess;
+  const int threads = 256, per_block = threads / 32;
+  const unsigned grid = unsigned((n_rows + per_block - 1) / per_block);
+  kv_scatter_kernel<<<grid, threads, 0, stream>>>(static_cast<const uint4*>(rows), n_rows, out);
+  return cudaGetLastError();
+}
+
+}  // namespace hc

@@ -1,0 +1,68 @@
+// kernels.h -- host-side launch interface of the sm_100a kernels (internal).
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace hc {
+
+// Where K1 writes K and V. Dense mode (page_table == nullptr): row r of the
+// projection lands at row r of k_base / v_base ([M x d_kv] row-major). Paged
+// mode: row r of sequence s (rows cu_seqlens[s]..cu_seqlens[s+1]) at position
+// p = start_pos + (r - cu_seqlens[s]) lands in page page_table[s*table_stride
+// + p/page_size], slot p%page_size; a page holds page_size rows of d_kv.
+struct KvOut {
+  void* k_base = nullptr;
+  void* v_base = nullptr;
+  int d_kv = 0;
+  int page_size = 0;
+  const int32_t* page_table = nullptr;
+  int table_stride = 0;
+  const int32_t* cu_seqlens = nullptr;  // nullptr: one sequence of M rows
+  int n_seqs = 1;
+  int start_pos = 0;
+  int out_f32 = 0;  // 0: bf16 KV, 1: fp32 (parity/debug)
+};
+
+// Epilogue inputs: LayerNorm fold (row stats + column sums of W) and RoPE.
+struct EpiArgs {
+  const float* row_mean = nullptr;  // nullptr: norm disabled
+  const float* row_rstd = nullptr;
+  const float* colsum = nullptr;    // [N] sum_k W[n,k]
+  const float2* rope = nullptr;     // [rope_rows][d_head/2] (cos, sin); nullptr: off
+  int d_head = 0;
+  int rope_rows = 0;
+};
+
+// Creates a 2D K-major bf16/fp16 tensor map with a {64, box_rows} box and the
+// 128-byte swizzle (the K1 operand layout). Returns false on failure.
+bool make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows,
+                      uint64_t row_stride_bytes, uint32_t box_rows);
+
+// K1: KV[M x N] = epilogue(A[M x K] * B[N x K]^T), N = 2*d_kv (K half, V half).
+// A is described by tmA (box rows 128), B by tmB (box rows 256 or 128 = bn).
+cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
+                              int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
+                              int num_sms, cudaStream_t stream);
+
+// Row statistics for the LayerNorm fold: mean and 1/sqrt(var+1e-5) per row,
+// mean/var accumulated in double like the reference (model.cpp:43-61).
+cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,
+                             bool bf16_in, float* mean, float* rstd, cudaStream_t stream);
+
+// colsum[n] = sum_k W[n,k] (double accumulation) for the LayerNorm fold.
+cudaError_t launch_colsum(const void* w, int64_t rows, int cols, bool bf16_in, float* out,
+                          cudaStream_t stream);
+
+// Deterministic synthetic data: dst[i] = Rng(seed)::symmetric(bound) draw
+// (offset+i) (reference model.cpp:17-31), stored as bf16/fp16/fp32.
+cudaError_t launch_fill_symmetric(void* dst, int64_t n, uint64_t seed, uint64_t offset,
+                                  float bound, int dtype, cudaStream_t stream);
+
+// Interleaved [K_row | V_row] rows (reference KV chunk payload, storage.cpp:67-75)
+// -> K and V (dense or paged, same KvOut addressing as K1). HBM-bound.
+cudaError_t launch_kv_scatter(const void* rows, int64_t n_rows, const KvOut& out,
+                              cudaStream_t stream);
+
+}  // namespace hc

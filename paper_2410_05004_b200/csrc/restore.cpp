@@ -1,0 +1,487 @@
+// restore.cpp -- the device restoration engine (restore(), proj/src/restore.cpp).
+//
+// Executes a RestorationPlan over a finalized session entirely stream-ordered:
+//   IO lane  (engine copy stream): per HIDDEN / KV layer in compute order
+//            (restore.cpp:50-63), the layer's chunks are gathered from the
+//            pinned arenas by the copy engine (one strided cudaMemcpy2DAsync
+//            per run of consecutive slots) into an HBM staging ring of
+//            prefetch_depth+1 buffers; a fetch waits (cudaStreamWaitEvent) for
+//            the K1 that last used its buffer -- the executor's staging bound
+//            (restore.cpp:148,161).
+//   compute  (caller stream): RECOMPUTE prefix (K6) from the manifest tokens,
+//            then per HIDDEN layer: wait fetch -> row stats -> K1 (LN-fold GEMM
+//            + RoPE -> paged KV); per KV layer: wait fetch -> K4 scatter.
+// Nothing blocks the host; the whole restore is enqueued up front. The
+// Timeline (pipeline.hpp:18-28) is filled from CUDA events on both lanes.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+#include "recompute.h"
+#include "store.h"
+#include "weights.h"
+
+namespace hc {
+
+void simulate(const hc_pipeline_job* jobs, int n, int depth, hc_timeline* tl);
+std::string plan_serialize(const hc_plan* p);
+
+namespace {
+
+// Per-device engine state: the copy stream and a memory pool that keeps the
+// staging ring cached across restores.
+struct Engine {
+  cudaStream_t copy = nullptr;
+  bool init = false;
+};
+
+Engine& engine(int dev) {
+  static std::mutex mu;
+  static std::vector<Engine> engines(64);
+  std::lock_guard<std::mutex> lk(mu);
+  Engine& e = engines[size_t(dev)];
+  if (!e.init) {
+    HC_CUDA(cudaStreamCreateWithFlags(&e.copy, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    HC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thresh = UINT64_MAX;
+    HC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    e.init = true;
+  }
+  return e;
+}
+
+struct Ev {
+  cudaEvent_t e = nullptr;
+  Ev() { HC_CUDA(cudaEventCreate(&e)); }
+  ~Ev() {
+    if (e) cudaEventDestroy(e);
+  }
+  Ev(const Ev&) = delete;
+  Ev& operator=(const Ev&) = delete;
+};
+
+struct TimedOp {
+  int lane, layer, kind;
+  cudaEvent_t start, end;
+};
+
+void issue_gather(const std::vector<CopySeg>& segs, uint8_t* dst, cudaStream_t s) {
+  for (const auto& g : segs) {
+    if (g.height == 1 || g.dpitch == g.width)
+      HC_CUDA(cudaMemcpyAsync(dst + g.dst_off, g.src, size_t(g.width * g.height),
+                              cudaMemcpyHostToDevice, s));
+    else
+      HC_CUDA(cudaMemcpy2DAsync(dst + g.dst_off, size_t(g.dpitch), g.src, size_t(g.spitch),
+                                size_t(g.width), size_t(g.height), cudaMemcpyHostToDevice, s));
+  }
+}
+
+// Lazily created CUDA events, destroyed with the object.
+struct EventPool {
+  std::vector<cudaEvent_t> all;
+  bool timing;
+  explicit EventPool(bool t) : timing(t) {}
+  cudaEvent_t get() {
+    cudaEvent_t e;
+    HC_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+    all.push_back(e);
+    return e;
+  }
+  ~EventPool() {
+    for (auto e : all) cudaEventDestroy(e);
+  }
+};
+
+void fill_timeline(hc_timeline* tl, cudaEvent_t t0, const std::vector<TimedOp>& ops) {
+  std::memset(tl, 0, sizeof(*tl));
+  std::vector<hc_event> ev;
+  for (const auto& op : ops) {
+    float a = 0, b = 0;
+    HC_CUDA(cudaEventElapsedTime(&a, t0, op.start));
+    HC_CUDA(cudaEventElapsedTime(&b, t0, op.end));
+    ev.push_back(hc_event{op.lane, op.layer, op.kind, 0, a * 1e-3, b * 1e-3});
+  }
+  std::stable_sort(ev.begin(), ev.end(),
+                   [](const hc_event& x, const hc_event& y) { return x.start_s < y.start_s; });
+  if (ev.size() > size_t(HC_MAX_EVENTS)) ev.resize(size_t(HC_MAX_EVENTS));
+  tl->n_events = int32_t(ev.size());
+  std::copy(ev.begin(), ev.end(), tl->events);
+  for (const auto& e : ev) tl->total_s = std::max(tl->total_s, e.end_s);
+  for (const auto& e : ev)
+    if (e.lane == HC_LANE_IO) {
+      tl->fill_s = e.end_s;  // first fetch stage (restore.cpp:264-268)
+      break;
+    }
+}
+
+struct LayerJob {
+  int layer;
+  int method;
+};
+
+std::vector<LayerJob> compute_order(const hc_plan& p) {
+  // restore.cpp:50-63: recompute prefix, hidden, KV suffix
+  std::vector<LayerJob> order;
+  for (int m : {HC_METHOD_RECOMPUTE, HC_METHOD_HIDDEN, HC_METHOD_KV_OFFLOAD})
+    for (int L = 0; L < p.n_layers; ++L)
+      if (p.layer_assignment[L] == m) order.push_back({L, m});
+  return order;
+}
+
+int auto_depth(int n_staged, size_t buf_bytes, int requested) {
+  if (requested > 0) return requested;
+  // stage every hidden layer up to an 8 GiB budget
+  const size_t budget = size_t(8) << 30;
+  const int fit = int(std::max<size_t>(2, budget / std::max<size_t>(1, buf_bytes)));
+  return std::max(1, std::min(n_staged, fit) - 1);
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- restore
+void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const hc_plan* plan,
+                     const hc_restore_opts* opts, const hc_kv_pages* pages,
+                     const int32_t* d_page_table, cudaStream_t stream, hc_timeline* tl) {
+  if (!st || !sid_c || !w || !plan || !pages || !d_page_table)
+    fail(HC_EINVAL, "restore: null argument");
+  Store& store = st->impl;
+  const std::string sid(sid_c);
+  const hc_manifest m = store.open(sid);  // HC_ENOENT / HC_EINCOMPLETE
+  // restore.cpp:228-231
+  if (m.n_layers != w->cfg.n_layers || plan->n_layers != w->cfg.n_layers)
+    fail(HC_EINVAL, "restore: layer count mismatch");
+  if (plan_serialize(plan) != plan_serialize(&m.plan))
+    fail(HC_EINVAL, "restore: plan does not match session manifest");
+  if (m.d_hidden != w->cfg.d_hidden) fail(HC_EINVAL, "restore: d_hidden mismatch");
+  if (m.elem_bytes != 2 || m.dtype != HC_DTYPE_BF16)
+    fail(HC_EINVAL, "restore: the device path restores bf16 sessions (elem_bytes 2)");
+  validate_pages(w, pages, w->d_kv);
+  const int n = m.n_tokens;
+  if (n <= 0) fail(HC_EINVAL, "restore: empty session");
+  if (int64_t(n) > int64_t(pages->num_pages) * pages->page_size)
+    fail(HC_EINVAL, "restore: KV pages too small for the session");
+
+  DeviceGuard dg(w->device);
+  Engine& eng = engine(w->device);
+  const bool timed = tl != nullptr || (opts && opts->timeline);
+  EventPool evp(timed);
+  std::vector<TimedOp> ops;
+
+  auto order = compute_order(*plan);
+  int n_hidden = 0, n_kv = 0, n_re = 0;
+  for (auto& j : order) {
+    if (j.method == HC_METHOD_HIDDEN) ++n_hidden;
+    else if (j.method == HC_METHOD_KV_OFFLOAD) ++n_kv;
+    else ++n_re;
+  }
+  if (n_kv && (m.d_kv != w->d_kv || w->d_kv != w->d_kv_all))
+    fail(HC_EINVAL, "restore: KV-offload layers need all KV heads on this GPU");
+
+  const size_t h_bytes = size_t(n) * size_t(m.d_hidden) * 2;
+  const size_t kv_bytes = size_t(n) * size_t(2 * m.d_kv) * 2;
+  const int depth = auto_depth(std::max(n_hidden, 1), h_bytes, opts ? opts->prefetch_depth : 0);
+  const int nbuf_h = std::min(std::max(n_hidden, 1), depth + 1);
+  const int nbuf_kv = std::min(std::max(n_kv, 1), 2);
+
+  // staging rings (stream-ordered pool allocations, cached by the pool)
+  StreamScratch ring_h(n_hidden ? h_bytes * size_t(nbuf_h) : 0, stream);
+  StreamScratch ring_kv(n_kv ? kv_bytes * size_t(nbuf_kv) : 0, stream);
+
+  // token ids for the RECOMPUTE prefix go up before the timed region starts
+  StreamScratch d_tok(n_re ? sizeof(int32_t) * size_t(n) : 0, stream);
+  if (n_re) {
+    std::vector<int32_t> toks = store.tokens(sid);
+    if (int(toks.size()) < n) fail(HC_EINVAL, "restore: manifest has fewer token ids than tokens");
+    HC_CUDA(cudaMemcpyAsync(d_tok.ptr, toks.data(), sizeof(int32_t) * size_t(n),
+                            cudaMemcpyHostToDevice, stream));
+    HC_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  cudaEvent_t t0 = evp.get();
+  HC_CUDA(cudaEventRecord(t0, stream));
+  HC_CUDA(cudaStreamWaitEvent(eng.copy, t0, 0));  // IO lane starts with the restore
+
+  // RECOMPUTE prefix first on the compute lane (restore.cpp:177-182); the IO
+  // lane below prefetches hidden layers meanwhile.
+  if (n_re) {
+    std::vector<cudaEvent_t> marks;
+    prefill_layers_impl(w, static_cast<const int32_t*>(d_tok.ptr), n, 0, n_re, pages,
+                        d_page_table, stream, [&](int layer, bool start) {
+                          if (!timed) return;
+                          cudaEvent_t e = evp.get();
+                          HC_CUDA(cudaEventRecord(e, stream));
+                          if (start) marks.push_back(e);
+                          else ops.push_back({HC_LANE_COMPUTE, layer, HC_EV_RECOMPUTE, marks.back(), e});
+                        });
+  }
+
+  // IO lane: all fetches in compute order; compute lane consumes in order.
+  std::vector<cudaEvent_t> consumed_h(size_t(nbuf_h), nullptr), consumed_kv(size_t(nbuf_kv), nullptr);
+  int ih = 0, ikv = 0;
+  for (const auto& j : order) {
+    if (j.method == HC_METHOD_RECOMPUTE) continue;
+    const bool hid = j.method == HC_METHOD_HIDDEN;
+    const int kind = hid ? HC_STATE_HIDDEN : HC_STATE_KV;
+    const int slot = hid ? ih % nbuf_h : ikv % nbuf_kv;
+    auto& consumed = hid ? consumed_h : consumed_kv;
+    uint8_t* buf = static_cast<uint8_t*>(hid ? ring_h.ptr : ring_kv.ptr) +
+                   (hid ? h_bytes : kv_bytes) * size_t(slot);
+    size_t got = 0;
+    auto segs = store.gather_plan(sid, j.layer, kind, 0, -1, &got);  // HC_ENOENT if missing
+    if (got != (hid ? h_bytes : kv_bytes))
+      fail(HC_ERUNTIME, "restore: layer " + std::to_string(j.layer) + " has a short token count");
+    // staging bound: wait until the previous user of this buffer is consumed
+    if (consumed[size_t(slot)]) HC_CUDA(cudaStreamWaitEvent(eng.copy, consumed[size_t(slot)], 0));
+    cudaEvent_t fs = timed ? evp.get() : nullptr;
+    if (fs) HC_CUDA(cudaEventRecord(fs, eng.copy));
+    issue_gather(segs, buf, eng.copy);
+    cudaEvent_t fetched = evp.get();
+    HC_CUDA(cudaEventRecord(fetched, eng.copy));
+    if (timed) ops.push_back({HC_LANE_IO, j.layer, hid ? HC_EV_FETCH_HIDDEN : HC_EV_FETCH_KV, fs, fetched});
+
+    // compute lane
+    HC_CUDA(cudaStreamWaitEvent(stream, fetched, 0));
+    cudaEvent_t cs = timed ? evp.get() : nullptr;
+    if (cs) HC_CUDA(cudaEventRecord(cs, stream));
+    KvOut out = kv_out_pages(pages, j.layer, d_page_table, 0, nullptr, 1);
+    if (hid) {
+      project_rows(w, j.layer, buf, n, out, stream);
+    } else {
+      HC_CUDA(launch_kv_scatter(buf, n, out, stream));
+    }
+    cudaEvent_t done = evp.get();
+    HC_CUDA(cudaEventRecord(done, stream));
+    consumed[size_t(slot)] = done;
+    if (timed) ops.push_back({HC_LANE_COMPUTE, j.layer, hid ? HC_EV_PROJECT : HC_EV_SCATTER, cs, done});
+    (hid ? ih : ikv)++;
+  }
+  // join the IO lane into the caller stream before the ring is released
+  cudaEvent_t io_done = evp.get();
+  HC_CUDA(cudaEventRecord(io_done, eng.copy));
+  HC_CUDA(cudaStreamWaitEvent(stream, io_done, 0));
+  if (timed) {
+    HC_CUDA(cudaStreamSynchronize(stream));
+    if (tl) fill_timeline(tl, t0, ops);
+  } else {
+    // events are destroyed on return; the stream order above already holds
+    // every dependency, so nothing to wait for.
+  }
+}
+
+void restore_batch(hc_store* st, const char* const* sids, int n_sessions, const hc_weights* w,
+                   const hc_restore_opts* opts, const hc_kv_pages* pages,
+                   const int32_t* d_page_tables, int table_stride, cudaStream_t stream,
+                   hc_timeline* tl) {
+  if (!st || !sids || n_sessions < 1 || !w || !pages || !d_page_tables)
+    fail(HC_EINVAL, "restore_batch: null argument");
+  Store& store = st->impl;
+  validate_pages(w, pages, w->d_kv);
+  const int L = w->cfg.n_layers, d = w->cfg.d_hidden;
+  std::vector<int32_t> cu(size_t(n_sessions) + 1, 0);
+  for (int s = 0; s < n_sessions; ++s) {
+    const hc_manifest m = store.open(sids[s]);
+    if (m.n_layers != L || m.d_hidden != d) fail(HC_EINVAL, "restore_batch: shape mismatch");
+    if (m.elem_bytes != 2 || m.dtype != HC_DTYPE_BF16)
+      fail(HC_EINVAL, "restore_batch: bf16 sessions required");
+    for (int l = 0; l < L; ++l)
+      if (m.plan.layer_assignment[l] != HC_METHOD_HIDDEN)
+        fail(HC_EINVAL, "restore_batch: every layer must be HIDDEN");
+    if (int64_t(m.n_tokens) > int64_t(table_stride) * pages->page_size)
+      fail(HC_EINVAL, "restore_batch: page table too short");
+    cu[size_t(s) + 1] = cu[size_t(s)] + m.n_tokens;
+  }
+  const int64_t total = cu.back();
+  if (total <= 0) fail(HC_EINVAL, "restore_batch: empty sessions");
+
+  DeviceGuard dg(w->device);
+  Engine& eng = engine(w->device);
+  const bool timed = tl != nullptr || (opts && opts->timeline);
+  EventPool evp(timed);
+  std::vector<TimedOp> ops;
+  const size_t h_bytes = size_t(total) * size_t(d) * 2;
+  const int depth = auto_depth(L, h_bytes, opts ? opts->prefetch_depth : 0);
+  const int nbuf = std::min(L, depth + 1);
+  StreamScratch ring(h_bytes * size_t(nbuf), stream);
+  StreamScratch d_cu(sizeof(int32_t) * cu.size(), stream);
+  HC_CUDA(cudaMemcpyAsync(d_cu.ptr, cu.data(), sizeof(int32_t) * cu.size(),
+                          cudaMemcpyHostToDevice, stream));
+  cudaEvent_t t0 = evp.get();
+  HC_CUDA(cudaEventRecord(t0, stream));
+  HC_CUDA(cudaStreamWaitEvent(eng.copy, t0, 0));
+  std::vector<cudaEvent_t> consumed(size_t(nbuf), nullptr);
+  for (int l = 0; l < L; ++l) {
+    const int slot = l % nbuf;
+    uint8_t* buf = static_cast<uint8_t*>(ring.ptr) + h_bytes * size_t(slot);
+    if (consumed[size_t(slot)]) HC_CUDA(cudaStreamWaitEvent(eng.copy, consumed[size_t(slot)], 0));
+    cudaEvent_t fs = timed ? evp.get() : nullptr;
+    if (fs) HC_CUDA(cudaEventRecord(fs, eng.copy));
+    for (int s = 0; s < n_sessions; ++s) {
+      auto segs = store.gather_plan(sids[s], l, HC_STATE_HIDDEN, 0, -1, nullptr);
+      issue_gather(segs, buf + size_t(cu[size_t(s)]) * size_t(d) * 2, eng.copy);
+    }
+    cudaEvent_t fetched = evp.get();
+    HC_CUDA(cudaEventRecord(fetched, eng.copy));
+    if (timed) ops.push_back({HC_LANE_IO, l, HC_EV_FETCH_HIDDEN, fs, fetched});
+    HC_CUDA(cudaStreamWaitEvent(stream, fetched, 0));
+    cudaEvent_t cs = timed ? evp.get() : nullptr;
+    if (cs) HC_CUDA(cudaEventRecord(cs, stream));
+    project_rows(w, l, buf, total,
+                 kv_out_pages(pages, l, d_page_tables, table_stride,
+                              static_cast<const int32_t*>(d_cu.ptr), n_sessions),
+                 stream);
+    cudaEvent_t done = evp.get();
+    HC_CUDA(cudaEventRecord(done, stream));
+    consumed[size_t(slot)] = done;
+    if (timed) ops.push_back({HC_LANE_COMPUTE, l, HC_EV_PROJECT, cs, done});
+  }
+  cudaEvent_t io_done = evp.get();
+  HC_CUDA(cudaEventRecord(io_done, eng.copy));
+  HC_CUDA(cudaStreamWaitEvent(stream, io_done, 0));
+  if (timed) {
+    HC_CUDA(cudaStreamSynchronize(stream));
+    if (tl) fill_timeline(tl, t0, ops);
+  }
+}
+
+}  // namespace hc
+
+using namespace hc;
+
+extern "C" {
+
+hc_status hc_restore(hc_store* s, const char* sid, const hc_weights* w, const hc_plan* plan,
+                     const hc_restore_opts* opts, const hc_kv_pages* pages,
+                     const int32_t* d_page_table, void* stream, hc_timeline* timeline) {
+  return guard([&] {
+    restore_session(s, sid, w, plan, opts, pages, d_page_table, as_stream(stream), timeline);
+  });
+}
+
+hc_status hc_restore_batch(hc_store* s, const char* const* sids, int32_t n_sessions,
+                           const hc_weights* w, const hc_restore_opts* opts,
+                           const hc_kv_pages* pages, const int32_t* d_page_tables,
+                           int32_t table_stride, void* stream, hc_timeline* timeline) {
+  return guard([&] {
+    restore_batch(s, sids, n_sessions, w, opts, pages, d_page_tables, table_stride,
+                  as_stream(stream), timeline);
+  });
+}
+
+hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_layers,
+                              int64_t n_rows, const int32_t* d_cu_seqlens, int32_t n_seqs,
+                              const hc_kv_pages* pages, const int32_t* d_page_table,
+                              int32_t table_stride, void* stream) {
+  return guard([&] {
+    if (!w || !d_hidden_layers || !pages || !d_page_table)
+      fail(HC_EINVAL, "restore_resident: null argument");
+    validate_pages(w, pages, w->d_kv);
+    DeviceGuard dg(w->device);
+    for (int l = 0; l < w->cfg.n_layers; ++l)
+      project_rows(w, l, d_hidden_layers[l], n_rows,
+                   kv_out_pages(pages, l, d_page_table, table_stride, d_cu_seqlens, n_seqs),
+                   as_stream(stream));
+  });
+}
+
+hc_status hc_measure_h2d(int32_t device, size_t bytes, int32_t reps, double* bytes_per_s) {
+  return guard([&] {
+    if (!bytes_per_s || bytes == 0) fail(HC_EINVAL, "measure_h2d: bad argument");
+    require_sm100(device);
+    DeviceGuard dg(device);
+    void* h = nullptr;
+    void* d = nullptr;
+    HC_CUDA(cudaHostAlloc(&h, bytes, cudaHostAllocPortable));
+    std::memset(h, 1, bytes);
+    cudaError_t e = cudaMalloc(&d, bytes);
+    if (e != cudaSuccess) {
+      cudaFreeHost(h);
+      check_cuda(e, "cudaMalloc");
+    }
+    cudaStream_t s;
+    HC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    Ev a, b;
+    float best = 1e30f;
+    for (int r = 0; r < std::max(1, reps) + 1; ++r) {
+      HC_CUDA(cudaEventRecord(a.e, s));
+      HC_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+      HC_CUDA(cudaEventRecord(b.e, s));
+      HC_CUDA(cudaEventSynchronize(b.e));
+      float ms = 0;
+      HC_CUDA(cudaEventElapsedTime(&ms, a.e, b.e));
+      if (r > 0) best = std::min(best, ms);  // first transfer is a warm-up
+    }
+    cudaStreamDestroy(s);
+    cudaFree(d);
+    cudaFreeHost(h);
+    *bytes_per_s = double(bytes) / (double(best) * 1e-3);
+  });
+}
+
+hc_status hc_profile(const hc_weights* w, int32_t n_tokens, hc_timings* out) {
+  return guard([&] {
+    // profile_hardware (harness.cpp:431-490), measured on the device
+    if (!w || !out || n_tokens < 1) fail(HC_EINVAL, "profile: bad argument");
+    DeviceGuard dg(w->device);
+    const int d = w->cfg.d_hidden;
+    const size_t hb = size_t(n_tokens) * size_t(d) * 2;
+    const size_t kb = size_t(n_tokens) * size_t(2 * w->d_kv) * 2;
+    double bw_h = 0, bw_kv = 0;
+    check_cuda(cudaGetLastError(), "profile");
+    hc_status st = hc_measure_h2d(w->device, hb, 3, &bw_h);
+    if (st != HC_OK) fail(st, "profile: H2D measurement failed");
+    st = hc_measure_h2d(w->device, kb, 3, &bw_kv);
+    if (st != HC_OK) fail(st, "profile: H2D measurement failed");
+    out->io_h = double(hb) / bw_h;
+    out->io_kv = double(kb) / bw_kv;
+    out->n_layers = w->cfg.n_layers;
+    // c_h: K1 on synthetic rows of layer 0 (best of 3)
+    int layer = -1;
+    for (int l = 0; l < w->cfg.n_layers; ++l)
+      if (w->layers[size_t(l)].ready) {
+        layer = l;
+        break;
+      }
+    if (layer < 0) fail(HC_EINVAL, "profile: no layer weights set");
+    void *h = nullptr, *k = nullptr, *v = nullptr;
+    HC_CUDA(cudaMalloc(&h, hb));
+    HC_CUDA(cudaMalloc(&k, size_t(n_tokens) * size_t(w->d_kv) * 2));
+    HC_CUDA(cudaMalloc(&v, size_t(n_tokens) * size_t(w->d_kv) * 2));
+    HC_CUDA(launch_fill_symmetric(h, int64_t(n_tokens) * d, 7, 0, 1.7320508f, 1, nullptr));
+    KvOut o;
+    o.k_base = k;
+    o.v_base = v;
+    o.d_kv = w->d_kv;
+    Ev a, b;
+    float best = 1e30f;
+    for (int r = 0; r < 4; ++r) {
+      HC_CUDA(cudaEventRecord(a.e, nullptr));
+      project_rows(w, layer, h, n_tokens, o, nullptr);
+      HC_CUDA(cudaEventRecord(b.e, nullptr));
+      HC_CUDA(cudaEventSynchronize(b.e));
+      float ms = 0;
+      HC_CUDA(cudaEventElapsedTime(&ms, a.e, b.e));
+      if (r > 0) best = std::min(best, ms);
+    }
+    out->c_h = best * 1e-3;
+    cudaFree(h);
+    cudaFree(k);
+    cudaFree(v);
+    // c_token: one K6 layer when the full weights are present
+    out->c_token = recompute_layer_seconds(w, n_tokens);
+    if (out->c_token <= 0) {
+      // analytic fallback from the reference cost model (cost_model.cpp:45-51):
+      // full layer / projection FLOP ratio applied to the measured K1 time
+      const double nn = n_tokens, dd = d, dkv = w->d_kv_all, dffn = w->cfg.d_ffn;
+      const double proj = 4.0 * nn * dd * dkv;
+      const double full = 4.0 * nn * dd * dd + proj + 4.0 * nn * dd * dffn + 2.0 * nn * nn * dd;
+      out->c_token = out->c_h * full / proj;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// weights.h -- the device-resident weight set behind hc_weights (internal).
+#pragma once
+
+#include <cuda.h>
+
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+
+struct hc_weights {
+  hc_model_config cfg{};
+  int device = 0;
+  int head_begin = 0;
+  int head_count = 0;
+  int d_head = 0;
+  int d_kv = 0;     // local KV row width = head_count * d_head
+  int d_kv_all = 0; // n_kv_heads * d_head
+
+  struct Layer {
+    const void* wkv = nullptr;   // [2*d_kv x d] bf16, K rows then V rows (local heads)
+    float* colsum = nullptr;     // owned, [2*d_kv]
+    CUtensorMap tm256{}, tm128{};
+    bool ready = false;
+    // full block (RECOMPUTE path), all heads
+    const void* wq = nullptr;
+    const void* wkv_all = nullptr;
+    const void* wo = nullptr;
+    const void* fc1 = nullptr;
+    const void* fc2 = nullptr;
+    float* colsum_all = nullptr;  // owned, colsum of wkv_all (2*d_kv_all)
+    bool full = false;
+  };
+  std::vector<Layer> layers;
+  const void* embedding = nullptr;
+  float2* rope = nullptr;  // owned, [rope_rows][d_head/2]
+  int rope_rows = 0;
+};
+
+namespace hc {
+
+// The epilogue arguments for a layer (LN fold + RoPE), given row stats.
+EpiArgs epi_for(const hc_weights* w, const float* colsum, const float* mean, const float* rstd);
+
+// Runs K1 for rows [0, n_rows) of a K-major bf16 hidden matrix (row stride
+// d_hidden) of `layer` into `out`. Computes the row statistics itself.
+void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t n_rows,
+                  const KvOut& out, cudaStream_t stream);
+
+// KvOut for a layer of a paged cache.
+KvOut kv_out_pages(const hc_kv_pages* pages, int layer, const int32_t* page_table,
+                   int table_stride, const int32_t* cu_seqlens, int n_seqs);
+
+void validate_pages(const hc_weights* w, const hc_kv_pages* pages, int d_kv_expected);
+
+}  // namespace hc

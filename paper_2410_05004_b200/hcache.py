@@ -1,0 +1,601 @@
+"""Python mirror of the reference's restoration API, over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference
+(proj/include/hcache/{planner,pipeline,storage,restore,model}.hpp) so the
+parity tests read like the reference's own tests:
+
+* ``RestorationPlan`` / ``ProfiledTimings`` / ``plan`` / ``makespan`` /
+  ``brute_force_plan`` (planner.hpp) + ``plan_three_way`` (B200 extension)
+* ``PipelineJob`` / ``Timeline`` / ``simulate_pipeline`` (pipeline.hpp)
+* ``DevicePool`` / ``SessionSeed`` / ``StorageManager`` / ``interleave_kv`` /
+  ``split_kv`` / ``device_for_chunk`` / ``kChunkTokens`` (storage.hpp)
+* ``Weights`` / ``KvCache`` / ``project_hidden_to_kv`` / ``restore`` /
+  ``restore_batch`` / ``ThrottleConfig`` (model.hpp, restore.hpp) -- device
+  side, CUDA tensors via torch for allocation only.
+
+Reference exceptions map as: std::invalid_argument -> ``InvalidArgument``
+(a ``ValueError``); std::runtime_error -> ``HCacheError`` subclasses.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import capi
+from .capi import check, lib
+
+kChunkTokens = capi.HC_CHUNK_TOKENS
+
+
+class Complement(IntEnum):
+    NONE = capi.HC_COMPLEMENT_NONE
+    KV_OFFLOAD = capi.HC_COMPLEMENT_KV_OFFLOAD
+    RECOMPUTE = capi.HC_COMPLEMENT_RECOMPUTE
+    MIXED = capi.HC_COMPLEMENT_MIXED
+
+
+class LayerMethod(IntEnum):
+    HIDDEN = capi.HC_METHOD_HIDDEN
+    KV_OFFLOAD = capi.HC_METHOD_KV_OFFLOAD
+    RECOMPUTE = capi.HC_METHOD_RECOMPUTE
+
+
+class StateKind(IntEnum):
+    HIDDEN = capi.HC_STATE_HIDDEN
+    KV = capi.HC_STATE_KV
+
+
+class Lane(IntEnum):
+    IO = capi.HC_LANE_IO
+    COMPUTE = capi.HC_LANE_COMPUTE
+
+
+def device_for_chunk(layer: int, chunk_idx: int, device_count: int) -> int:
+    """storage.cpp:29-31."""
+    return lib().hc_device_for_chunk(layer, chunk_idx, device_count)
+
+
+# --------------------------------------------------------------------- planner
+class RestorationPlan:
+    """planner.hpp:29-40 (+ MIXED three-way plans)."""
+
+    def __init__(self, c: capi.PlanC):
+        self._c = c
+
+    @staticmethod
+    def make(n_layers: int, l_h: int, complement: Complement) -> "RestorationPlan":
+        p = capi.PlanC()
+        check(lib().hc_plan_make(n_layers, l_h, int(complement), C.byref(p)))
+        return RestorationPlan(p)
+
+    @staticmethod
+    def make_mixed(l_re: int, l_h: int, l_kv: int) -> "RestorationPlan":
+        p = capi.PlanC()
+        check(lib().hc_plan_make_mixed(l_re, l_h, l_kv, C.byref(p)))
+        return RestorationPlan(p)
+
+    @staticmethod
+    def parse(record: str) -> "RestorationPlan":
+        p = capi.PlanC()
+        check(lib().hc_plan_parse(record.encode(), C.byref(p)))
+        return RestorationPlan(p)
+
+    def serialize(self) -> str:
+        buf = C.create_string_buffer(256)
+        check(lib().hc_plan_serialize(C.byref(self._c), buf, 256))
+        return buf.value.decode()
+
+    l_h = property(lambda self: self._c.l_h)
+    l_o = property(lambda self: self._c.l_o)
+    l_kv = property(lambda self: self._c.l_kv)
+    l_re = property(lambda self: self._c.l_re)
+    complement = property(lambda self: Complement(self._c.complement))
+
+    def n_layers(self) -> int:
+        return self._c.n_layers
+
+    @property
+    def layer_assignment(self) -> List[LayerMethod]:
+        return [LayerMethod(self._c.layer_assignment[i]) for i in range(self._c.n_layers)]
+
+    def __eq__(self, other):
+        return isinstance(other, RestorationPlan) and self.serialize() == other.serialize()
+
+    def __repr__(self):
+        return f"RestorationPlan({self.serialize()})"
+
+
+@dataclass
+class ProfiledTimings:
+    """planner.hpp:16-24 (seconds per layer)."""
+    io_h: float = 0.0
+    io_kv: float = 0.0
+    c_h: float = 0.0
+    c_token: float = 0.0
+    n_layers: int = 0
+
+    def _c(self):
+        return capi.TimingsC(self.io_h, self.io_kv, self.c_h, self.c_token, self.n_layers)
+
+    def validate(self):
+        check(lib().hc_timings_validate(C.byref(self._c())))
+
+
+def plan(t: ProfiledTimings) -> RestorationPlan:
+    p = capi.PlanC()
+    check(lib().hc_plan_closed_form(C.byref(t._c()), C.byref(p)))
+    return RestorationPlan(p)
+
+
+def brute_force_plan(t: ProfiledTimings) -> RestorationPlan:
+    p = capi.PlanC()
+    check(lib().hc_brute_force_plan(C.byref(t._c()), C.byref(p)))
+    return RestorationPlan(p)
+
+
+def makespan(p: RestorationPlan, t: ProfiledTimings) -> float:
+    out = C.c_double()
+    check(lib().hc_makespan(C.byref(p._c), C.byref(t._c()), C.byref(out)))
+    return out.value
+
+
+def plan_three_way(t: ProfiledTimings, prefetch_depth: int = 1):
+    """B200 planner: (plan, bounded-staging makespan)."""
+    p = capi.PlanC()
+    out = C.c_double()
+    check(lib().hc_plan_three_way(C.byref(t._c()), prefetch_depth, C.byref(p), C.byref(out)))
+    return RestorationPlan(p), out.value
+
+
+# -------------------------------------------------------------------- timeline
+@dataclass
+class TimelineEvent:
+    lane: Lane
+    layer: int
+    kind: str
+    start_s: float
+    end_s: float
+
+
+@dataclass
+class Timeline:
+    """pipeline.hpp:18-28."""
+    events: List[TimelineEvent] = field(default_factory=list)
+    total_s: float = 0.0
+    fill_s: float = 0.0
+    _c: Optional[capi.TimelineC] = None
+
+    @staticmethod
+    def from_c(tc: capi.TimelineC) -> "Timeline":
+        ev = [TimelineEvent(Lane(e.lane), e.layer, capi.EVENT_KINDS[e.kind], e.start_s, e.end_s)
+              for e in tc.events[: tc.n_events]]
+        return Timeline(ev, tc.total_s, tc.fill_s, tc)
+
+    def lane_busy(self, lane: Lane) -> float:
+        return sum(e.end_s - e.start_s for e in self.events if e.lane == lane)
+
+    def bubble_fraction(self) -> float:
+        out = C.c_double()
+        check(lib().hc_timeline_bubble_fraction(C.byref(self._c), C.byref(out)))
+        return out.value
+
+    def export_text(self) -> str:
+        lines = ["# lane layer kind start_s end_s"]
+        for e in self.events:
+            lines.append(f"{'IO' if e.lane == Lane.IO else 'COMPUTE'} {e.layer} {e.kind} "
+                         f"{e.start_s} {e.end_s}")
+        return "\n".join(lines) + "\n"
+
+
+@dataclass
+class PipelineJob:
+    """pipeline.hpp:30-41."""
+    layer: int = -1
+    io_s: float = 0.0
+    compute_s: float = 0.0
+    has_io: bool = False
+    has_compute: bool = False
+    io_kind: str = "fetch"
+    compute_kind: str = "compute"
+
+
+def simulate_pipeline(jobs: Sequence[PipelineJob], prefetch_depth: int) -> Timeline:
+    arr = (capi.PipelineJobC * max(1, len(jobs)))()
+    for i, j in enumerate(jobs):
+        arr[i] = capi.PipelineJobC(j.layer, int(j.has_io), int(j.has_compute),
+                                   capi.EVENT_KINDS.index(j.io_kind),
+                                   capi.EVENT_KINDS.index(j.compute_kind), 0, j.io_s,
+                                   j.compute_s)
+    tc = capi.TimelineC()
+    check(lib().hc_simulate_pipeline(arr, len(jobs), prefetch_depth, C.byref(tc)))
+    return Timeline.from_c(tc)
+
+
+# ----------------------------------------------------------------------- store
+@dataclass
+class DevicePool:
+    """storage.hpp:27-34: `count` pinned arenas stand in for the SSD roots."""
+    count: int = 1
+    bw_bytes_per_s: float = 0.0
+    read_latency_s: float = 0.0
+
+
+@dataclass
+class SessionSeed:
+    """storage.hpp:71-79 (+ d_kv for GQA, dtype of 2-byte elements)."""
+    session_id: str
+    config_hash: int = 0
+    n_layers: int = 0
+    d_hidden: int = 0
+    elem_bytes: int = 2
+    plan: Optional[RestorationPlan] = None
+    tokens: Sequence[int] = ()
+    d_kv: int = 0
+    dtype: int = capi.HC_DTYPE_BF16
+
+
+@dataclass
+class LayerChunks:
+    layer: int
+    kind: StateKind
+    n_chunks: int
+    n_tokens: int
+
+
+@dataclass
+class SessionManifest:
+    """storage.hpp:54-69."""
+    session_id: str
+    config_hash: int
+    n_tokens: int
+    n_layers: int
+    d_hidden: int
+    d_kv: int
+    elem_bytes: int
+    dtype: int
+    device_count: int
+    chunk_tokens: int
+    plan: RestorationPlan
+    tokens: List[int]
+    finalized: bool
+    _store: "StorageManager" = None
+
+    def find(self, layer: int, kind: StateKind) -> Optional[LayerChunks]:
+        nc, nt = C.c_int32(), C.c_int32()
+        st = lib().hc_store_layer_info(self._store._h, self.session_id.encode(), layer, int(kind),
+                                       C.byref(nc), C.byref(nt))
+        if st == capi.HC_ENOENT:
+            return None
+        check(st)
+        return LayerChunks(layer, kind, nc.value, nt.value)
+
+
+_NP_OF = {capi.HC_DTYPE_F32: np.float32, capi.HC_DTYPE_BF16: np.uint16,
+          capi.HC_DTYPE_F16: np.uint16}
+
+
+class StorageManager:
+    """storage.hpp:84-165 over pinned host arenas."""
+
+    def __init__(self, pool: DevicePool, buffer_capacity_bytes: int = 256 << 20):
+        d = capi.PoolDescC(pool.count, 0, pool.bw_bytes_per_s, pool.read_latency_s)
+        h = C.c_void_p()
+        check(lib().hc_store_create(C.byref(d), buffer_capacity_bytes, C.byref(h)))
+        self._h = h
+        self.pool = pool
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hc_store_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def create_session(self, seed: SessionSeed):
+        toks = (C.c_int32 * max(1, len(seed.tokens)))(*seed.tokens)
+        p = seed.plan._c if seed.plan is not None else None
+        c = capi.SessionSeedC(seed.session_id.encode(), seed.config_hash, seed.n_layers,
+                              seed.d_hidden, seed.d_kv, seed.elem_bytes, seed.dtype, 0,
+                              C.pointer(p) if p is not None else None, toks, len(seed.tokens))
+        check(lib().hc_store_create_session(self._h, C.byref(c)))
+
+    def reopen_for_append(self, sid: str, new_tokens: Sequence[int]):
+        toks = (C.c_int32 * max(1, len(new_tokens)))(*new_tokens)
+        check(lib().hc_store_reopen_for_append(self._h, sid.encode(), toks, len(new_tokens)))
+
+    def snapshot(self, sid: str, layer: int, kind: StateKind, rows, dtype: int = None,
+                 stream=None) -> bool:
+        """Host numpy rows (float32, or uint16 bf16 bits with dtype) or a CUDA
+        torch tensor (session dtype; copied D2H on `stream`). False on
+        backpressure, like the reference."""
+        if hasattr(rows, "is_cuda") and rows.is_cuda:
+            import torch
+            assert rows.is_contiguous()
+            src_dtype = {torch.bfloat16: capi.HC_DTYPE_BF16, torch.float16: capi.HC_DTYPE_F16,
+                         torch.float32: capi.HC_DTYPE_F32}[rows.dtype]
+            s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+            st = lib().hc_store_snapshot(self._h, sid.encode(), layer, int(kind), rows.data_ptr(),
+                                         rows.shape[0], rows.shape[1], src_dtype, 1, s)
+        else:
+            rows = np.ascontiguousarray(rows)
+            if dtype is None:
+                rows = rows.astype(np.float32, copy=False)
+                src_dtype = capi.HC_DTYPE_F32
+            else:
+                src_dtype = dtype
+            st = lib().hc_store_snapshot(self._h, sid.encode(), layer, int(kind),
+                                         rows.ctypes.data, rows.shape[0], rows.shape[1],
+                                         src_dtype, 0, None)
+        if st == capi.HC_EAGAIN:
+            return False
+        check(st)
+        return True
+
+    def drain(self, max_chunks: int = -1) -> int:
+        out = C.c_int64()
+        check(lib().hc_store_drain(self._h, max_chunks, C.byref(out)))
+        return out.value
+
+    def drain_all(self):
+        check(lib().hc_store_drain_all(self._h))
+
+    def finalize(self, sid: str):
+        check(lib().hc_store_finalize(self._h, sid.encode()))
+
+    def open(self, sid: str) -> SessionManifest:
+        m = capi.ManifestC()
+        check(lib().hc_store_open(self._h, sid.encode(), C.byref(m)))
+        n = C.c_int64()
+        check(lib().hc_store_tokens(self._h, sid.encode(), None, 0, C.byref(n)))
+        toks = (C.c_int32 * max(1, n.value))()
+        check(lib().hc_store_tokens(self._h, sid.encode(), toks, n.value, C.byref(n)))
+        return SessionManifest(m.session_id.decode(), m.config_hash, m.n_tokens, m.n_layers,
+                               m.d_hidden, m.d_kv, m.elem_bytes, m.dtype, m.device_count,
+                               m.chunk_tokens, RestorationPlan(m.plan), list(toks[: n.value]),
+                               bool(m.finalized), self)
+
+    def read_layer(self, m: SessionManifest, layer: int, kind: StateKind):
+        """Token-ordered reassembly (storage.cpp:324-346) as a host array
+        (float32 for fp32 sessions, else uint16 element bits); None when the
+        layer/kind was never stored."""
+        lc = m.find(layer, kind)
+        if lc is None or lc.n_tokens == 0:
+            return None
+        width = m.d_hidden if kind == StateKind.HIDDEN else 2 * m.d_kv
+        out = np.empty((lc.n_tokens, width), _NP_OF[m.dtype])
+        check(lib().hc_store_read_layer(self._h, m.session_id.encode(), layer, int(kind),
+                                        out.ctypes.data, out.nbytes, 0, None))
+        return out
+
+    def read_layer_device(self, sid: str, layer: int, kind: StateKind, dst, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        check(lib().hc_store_read_layer(self._h, sid.encode(), layer, int(kind), dst.data_ptr(),
+                                        dst.numel() * dst.element_size(), 1, s))
+
+    def chunk_info(self, sid: str, layer: int, kind: StateKind, chunk_idx: int):
+        dev, ptr, nb = C.c_int32(), C.c_void_p(), C.c_int64()
+        check(lib().hc_store_chunk_info(self._h, sid.encode(), layer, int(kind), chunk_idx,
+                                        C.byref(dev), C.byref(ptr), C.byref(nb)))
+        return dev.value, ptr.value, nb.value
+
+    def device_chunk_counts(self) -> List[int]:
+        out = (C.c_int64 * self.pool.count)()
+        check(lib().hc_store_device_chunk_counts(self._h, out, self.pool.count))
+        return list(out)
+
+    def simulated_read_seconds_tokens(self, n_tokens: int, width: int, elem_bytes: int) -> float:
+        return lib().hc_store_simulated_read_seconds_tokens(self._h, n_tokens, width, elem_bytes)
+
+    def start_daemon(self):
+        check(lib().hc_store_start_daemon(self._h))
+
+    def stop_daemon(self):
+        check(lib().hc_store_stop_daemon(self._h))
+
+    def buffer_bytes(self) -> int:
+        return lib().hc_store_buffer_bytes(self._h)
+
+    def buffer_capacity(self) -> int:
+        return lib().hc_store_buffer_capacity(self._h)
+
+    def backpressure_events(self) -> int:
+        return lib().hc_store_backpressure_events(self._h)
+
+    def pinned(self) -> bool:
+        return bool(lib().hc_store_pinned(self._h))
+
+
+def interleave_kv(k: np.ndarray, v: np.ndarray) -> np.ndarray:
+    """storage.cpp:67-75: n x 2d rows, K row then V row per token."""
+    if k.shape != v.shape:
+        raise ValueError("interleave_kv: K/V shape mismatch")
+    return np.concatenate([k, v], axis=1)
+
+
+def split_kv(rows: np.ndarray):
+    """storage.cpp:77-86."""
+    if rows.shape[1] % 2:
+        raise ValueError("split_kv: odd width")
+    d = rows.shape[1] // 2
+    return rows[:, :d].copy(), rows[:, d:].copy()
+
+
+# ---------------------------------------------------------------------- device
+@dataclass
+class ModelConfig:
+    """model.hpp:11-25 (+ n_kv_heads for GQA)."""
+    n_layers: int = 4
+    d_hidden: int = 256
+    n_heads: int = 8
+    d_ffn: int = 1024
+    vocab_size: int = 1024
+    max_seq: int = 4096
+    elem_bytes: int = 2
+    norm_enabled: bool = True
+    rope_enabled: bool = True
+    n_kv_heads: int = 0
+
+    def _c(self):
+        return capi.ModelConfigC(self.n_layers, self.d_hidden, self.n_heads, self.n_kv_heads,
+                                 self.d_ffn, self.vocab_size, self.max_seq, self.elem_bytes,
+                                 int(self.norm_enabled), int(self.rope_enabled))
+
+    def d_head(self):
+        return self.d_hidden // self.n_heads
+
+    def kv_heads(self):
+        return self.n_kv_heads or self.n_heads
+
+    def validate(self):
+        check(lib().hc_config_validate(C.byref(self._c())))
+
+    def hash(self) -> int:
+        return lib().hc_config_hash(C.byref(self._c()))
+
+
+def _stream(stream):
+    if stream is not None:
+        return stream
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Weights:
+    """Device weight set of the restoration path (hc_weights). Tensors are
+    torch CUDA bf16, kept alive by this object."""
+
+    def __init__(self, cfg: ModelConfig, kv_head_begin: int = 0, kv_head_count: int = 0,
+                 device: int = 0):
+        self.cfg = cfg
+        self.kv_head_begin = kv_head_begin
+        self.kv_head_count = kv_head_count or (cfg.kv_heads() - kv_head_begin)
+        self.d_kv = self.kv_head_count * cfg.d_head()
+        h = C.c_void_p()
+        check(lib().hc_weights_create(C.byref(cfg._c()), kv_head_begin, self.kv_head_count,
+                                      device, C.byref(h)))
+        self._h = h
+        self._keep = {}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hc_weights_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def set_layer_kv(self, layer: int, wkv):
+        """wkv: (2*d_kv x d) bf16 CUDA tensor, K rows then V rows."""
+        assert wkv.is_contiguous() and wkv.shape == (2 * self.d_kv, self.cfg.d_hidden)
+        self._keep[("kv", layer)] = wkv
+        check(lib().hc_weights_set_layer_kv(self._h, layer, wkv.data_ptr()))
+
+    def set_layer_full(self, layer: int, wq, wkv, wo, fc1, fc2):
+        for name, t in (("wq", wq), ("wkv_all", wkv), ("wo", wo), ("fc1", fc1), ("fc2", fc2)):
+            assert t.is_contiguous()
+            self._keep[(name, layer)] = t
+        check(lib().hc_weights_set_layer_full(self._h, layer, wq.data_ptr(), wkv.data_ptr(),
+                                              wo.data_ptr(), fc1.data_ptr(), fc2.data_ptr()))
+
+    def set_embedding(self, emb):
+        assert emb.is_contiguous()
+        self._keep["embedding"] = emb
+        check(lib().hc_weights_set_embedding(self._h, emb.data_ptr()))
+
+
+def project_hidden_to_kv(w: Weights, layer: int, h, start_pos: int = 0, out_dtype=None,
+                         stream=None):
+    """model.cpp:219-235 on the GPU: h (n x d bf16 CUDA) -> (K, V) dense."""
+    import torch
+    out_dtype = out_dtype or torch.bfloat16
+    n = h.shape[0]
+    k = torch.empty((n, w.d_kv), dtype=out_dtype, device=h.device)
+    v = torch.empty_like(k)
+    dt = capi.HC_DTYPE_F32 if out_dtype == torch.float32 else capi.HC_DTYPE_BF16
+    check(lib().hc_project_hidden_to_kv(w._h, layer, h.data_ptr(), n, start_pos, k.data_ptr(),
+                                        v.data_ptr(), dt, _stream(stream)))
+    return k, v
+
+
+class KvCache:
+    """Paged KV cache: per layer a pool [num_pages, page_size, d_kv] for K
+    and V (torch CUDA tensors) plus the C descriptor."""
+
+    def __init__(self, n_layers: int, num_pages: int, page_size: int, d_kv: int, dtype=None,
+                 device="cuda"):
+        import torch
+        dtype = dtype or torch.bfloat16
+        self.n_layers, self.num_pages, self.page_size, self.d_kv = n_layers, num_pages, page_size, d_kv
+        self.k = [torch.zeros((num_pages, page_size, d_kv), dtype=dtype, device=device)
+                  for _ in range(n_layers)]
+        self.v = [torch.zeros_like(t) for t in self.k]
+        self._kp = (C.c_void_p * n_layers)(*[t.data_ptr() for t in self.k])
+        self._vp = (C.c_void_p * n_layers)(*[t.data_ptr() for t in self.v])
+        self.desc = capi.KvPagesC(n_layers, page_size, num_pages, d_kv,
+                                  capi.HC_DTYPE_F32 if dtype == torch.float32 else
+                                  capi.HC_DTYPE_BF16, self._kp, self._vp)
+
+    def gather(self, layer: int, page_table, n_tokens: int):
+        """Dense (K, V) [n_tokens x d_kv] of one sequence through its page table."""
+        import torch
+        pt = torch.as_tensor(page_table, device=self.k[layer].device).long()
+        pos = torch.arange(n_tokens, device=pt.device)
+        pages = pt[pos // self.page_size]
+        slots = pos % self.page_size
+        return self.k[layer][pages, slots], self.v[layer][pages, slots]
+
+
+@dataclass
+class ThrottleConfig:
+    """restore.hpp:14-29 for the device engine: prefetch_depth bounds the
+    staged hidden layers (0 = auto: stage every hidden layer within 8 GiB)."""
+    prefetch_depth: int = 0
+    timeline: bool = True
+
+    def _c(self):
+        return capi.RestoreOptsC(self.prefetch_depth, int(self.timeline))
+
+
+@dataclass
+class RestoreResult:
+    kv: KvCache
+    timeline: Timeline
+
+
+def restore(store: StorageManager, session_id: str, w: Weights, p: RestorationPlan,
+            throttle: ThrottleConfig, kv: KvCache, page_table, stream=None) -> RestoreResult:
+    """restore.hpp:40-42 on the GPU. page_table: int32 CUDA tensor."""
+    tc = capi.TimelineC() if throttle.timeline else None
+    check(lib().hc_restore(store._h, session_id.encode(), w._h, C.byref(p._c),
+                           C.byref(throttle._c()), C.byref(kv.desc), page_table.data_ptr(),
+                           _stream(stream), C.byref(tc) if tc is not None else None))
+    return RestoreResult(kv, Timeline.from_c(tc) if tc is not None else None)
+
+
+def restore_batch(store: StorageManager, session_ids: Sequence[str], w: Weights,
+                  throttle: ThrottleConfig, kv: KvCache, page_tables, stream=None):
+    """Concurrent all-HIDDEN restore of several sessions (config 4).
+    page_tables: (n_sessions x table_stride) int32 CUDA tensor."""
+    ids = (C.c_char_p * len(session_ids))(*[s.encode() for s in session_ids])
+    tc = capi.TimelineC() if throttle.timeline else None
+    check(lib().hc_restore_batch(store._h, ids, len(session_ids), w._h, C.byref(throttle._c()),
+                                 C.byref(kv.desc), page_tables.data_ptr(), page_tables.shape[1],
+                                 _stream(stream), C.byref(tc) if tc is not None else None))
+    return RestoreResult(kv, Timeline.from_c(tc) if tc is not None else None)
+
+
+def profile_hardware(w: Weights, n_tokens: int) -> ProfiledTimings:
+    """harness.hpp:76-77, measured on the device."""
+    t = capi.TimingsC()
+    check(lib().hc_profile(w._h, n_tokens, C.byref(t)))
+    return ProfiledTimings(t.io_h, t.io_kv, t.c_h, t.c_token, t.n_layers)
+
+
+def measure_h2d(bytes_: int, reps: int = 5, device: int = 0) -> float:
+    out = C.c_double()
+    check(lib().hc_measure_h2d(device, bytes_, reps, C.byref(out)))
+    return out.value
