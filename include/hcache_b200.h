@@ -404,6 +404,12 @@ hc_status hc_prefill(const hc_weights* w, const int32_t* d_tokens, int64_t n,
  * = pinned H2D time of one layer's hidden / KV rows for n_tokens, c_h = K1
  * time, c_token = K6 full-layer time (0 if full weights are absent). */
 hc_status hc_profile(const hc_weights* w, int32_t n_tokens, hc_timings* out);
+/* Measurement entry point (bench/profiling): runs the row-stats kernel and
+ * K1 for `layer` on n_rows resident rows `iters` times, each bracketed by
+ * CUDA events on `stream`; returns the mean milliseconds of each kernel. */
+hc_status hc_bench_project(const hc_weights* w, int32_t layer, const void* d_hidden,
+                           int64_t n_rows, int32_t iters, void* stream, double* stats_ms,
+                           double* k1_ms);
 /* Pinned host->device copy bandwidth (bytes/s) for a `bytes` transfer. */
 hc_status hc_measure_h2d(int32_t device, size_t bytes, int32_t reps, double* bytes_per_s);
 

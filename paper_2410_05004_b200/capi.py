@@ -153,6 +153,7 @@ _PROTOS = {
     "hc_prefill": (i32, [vp, vp, i64, P(KvPagesC), vp, vp, P(i32), vp]),
     "hc_profile": (i32, [vp, i32, P(TimingsC)]),
     "hc_measure_h2d": (i32, [i32, C.c_size_t, i32, P(f64)]),
+    "hc_bench_project": (i32, [vp, i32, vp, i64, i32, vp, P(f64), P(f64)]),
 }
 
 _lib = None

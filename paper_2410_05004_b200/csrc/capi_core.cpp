@@ -342,6 +342,55 @@ hc_status hc_fill_symmetric(void* d_dst, int64_t n, uint64_t seed, uint64_t offs
   });
 }
 
+hc_status hc_bench_project(const hc_weights* w, int32_t layer, const void* d_hidden,
+                           int64_t n_rows, int32_t iters, void* stream, double* stats_ms,
+                           double* k1_ms) {
+  return guard([&] {
+    if (!w || !d_hidden || iters < 1 || n_rows < 1) fail(HC_EINVAL, "bench_project: bad argument");
+    if (layer < 0 || layer >= w->cfg.n_layers || !w->layers[size_t(layer)].ready)
+      fail(HC_EINVAL, "bench_project: layer weights not set");
+    DeviceGuard dg(w->device);
+    cudaStream_t s = as_stream(stream);
+    const auto& L = w->layers[size_t(layer)];
+    const int d = w->cfg.d_hidden, N = 2 * w->d_kv;
+    StreamScratch stats(size_t(n_rows) * 2 * sizeof(float), s);
+    StreamScratch kv(size_t(n_rows) * size_t(N) * 2, s);
+    float* mean = static_cast<float*>(stats.ptr);
+    KvOut o;
+    o.k_base = kv.ptr;
+    o.v_base = static_cast<char*>(kv.ptr) + size_t(n_rows) * size_t(w->d_kv) * 2;
+    o.d_kv = w->d_kv;
+    CUtensorMap tmA;
+    if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2, 128))
+      fail(HC_ECUDA, "cuTensorMapEncodeTiled failed");
+    const int sms = device_sm_count(w->device);
+    const int64_t tiles256 = ((n_rows + 127) / 128) * ((N + 255) / 256);
+    const int bn = tiles256 >= sms ? 256 : 128;
+    std::vector<cudaEvent_t> ev(size_t(3 * iters));
+    for (auto& e : ev) HC_CUDA(cudaEventCreate(&e));
+    for (int i = 0; i < iters; ++i) {
+      HC_CUDA(cudaEventRecord(ev[size_t(3 * i)], s));
+      HC_CUDA(launch_row_stats(d_hidden, n_rows, d, d, true, mean, mean + n_rows, s));
+      HC_CUDA(cudaEventRecord(ev[size_t(3 * i + 1)], s));
+      HC_CUDA(launch_restore_kv(tmA, bn == 256 ? L.tm256 : L.tm128, bn, int(n_rows), N, d, true,
+                                o, epi_for(w, L.colsum, mean, mean + n_rows), sms, s));
+      HC_CUDA(cudaEventRecord(ev[size_t(3 * i + 2)], s));
+    }
+    HC_CUDA(cudaStreamSynchronize(s));
+    double a = 0, b = 0;
+    for (int i = 0; i < iters; ++i) {
+      float x = 0, y = 0;
+      HC_CUDA(cudaEventElapsedTime(&x, ev[size_t(3 * i)], ev[size_t(3 * i + 1)]));
+      HC_CUDA(cudaEventElapsedTime(&y, ev[size_t(3 * i + 1)], ev[size_t(3 * i + 2)]));
+      a += x;
+      b += y;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (stats_ms) *stats_ms = a / iters;
+    if (k1_ms) *k1_ms = b / iters;
+  });
+}
+
 int32_t hc_chunk_tokens(void) { return HC_CHUNK_TOKENS; }
 
 int32_t hc_device_for_chunk(int32_t layer, int32_t chunk_idx, int32_t device_count) {

@@ -72,12 +72,20 @@ struct TimedOp {
 
 void issue_gather(const std::vector<CopySeg>& segs, uint8_t* dst, cudaStream_t s) {
   for (const auto& g : segs) {
+    cudaError_t e;
     if (g.height == 1 || g.dpitch == g.width)
-      HC_CUDA(cudaMemcpyAsync(dst + g.dst_off, g.src, size_t(g.width * g.height),
-                              cudaMemcpyHostToDevice, s));
+      e = cudaMemcpyAsync(dst + g.dst_off, g.src, size_t(g.width * g.height),
+                          cudaMemcpyHostToDevice, s);
     else
-      HC_CUDA(cudaMemcpy2DAsync(dst + g.dst_off, size_t(g.dpitch), g.src, size_t(g.spitch),
-                                size_t(g.width), size_t(g.height), cudaMemcpyHostToDevice, s));
+      e = cudaMemcpy2DAsync(dst + g.dst_off, size_t(g.dpitch), g.src, size_t(g.spitch),
+                            size_t(g.width), size_t(g.height), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess)
+      fail(HC_ECUDA, std::string("restore gather H2D: ") + cudaGetErrorString(e) +
+                         " (dst=" + std::to_string(reinterpret_cast<uintptr_t>(dst)) +
+                         "+" + std::to_string(g.dst_off) + " src=" +
+                         std::to_string(reinterpret_cast<uintptr_t>(g.src)) + " w=" +
+                         std::to_string(g.width) + " h=" + std::to_string(g.height) +
+                         " sp=" + std::to_string(g.spitch) + " dp=" + std::to_string(g.dpitch) + ")");
   }
 }
 

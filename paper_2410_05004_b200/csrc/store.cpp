@@ -285,9 +285,10 @@ uint8_t* Store::new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx) 
     ex.base = static_cast<uint8_t*>(pool_mem_.alloc_raw(cb * size_t(cap)));
     ex.cap = cap;
     ex.used = 0;
+    ex.id = ++next_extent_id_;
   }
   uint8_t* p = ex.base + cb * size_t(ex.used++);
-  ls.chunks.push_back(ChunkRef{dev, p});
+  ls.chunks.push_back(ChunkRef{dev, p, ex.id});
   ++dev_chunks_[size_t(dev)];
   return p;
 }
@@ -420,6 +421,7 @@ std::vector<CopySeg> Store::gather_plan(const std::string& sid, int layer, int k
       }
       int run = 1;
       while (c + run * ndev_ <= c_last && chunk_len(c + run * ndev_) == HC_CHUNK_TOKENS &&
+             ls.chunks[size_t(c + run * ndev_)].extent == ls.chunks[size_t(c)].extent &&
              ls.chunks[size_t(c + run * ndev_)].ptr ==
                  ls.chunks[size_t(c + (run - 1) * ndev_)].ptr + cb)
         ++run;

@@ -47,6 +47,7 @@ class PinnedPool {
 struct ChunkRef {
   int device = 0;
   uint8_t* ptr = nullptr;  // slot start (slot_bytes capacity)
+  int64_t extent = 0;      // id of the pinned allocation holding the slot
 };
 
 struct LayerStream {
@@ -60,6 +61,7 @@ struct LayerStream {
     uint8_t* base = nullptr;
     int cap = 0;
     int used = 0;
+    int64_t id = 0;
   };
   std::vector<Extent> extents;
 };
@@ -144,6 +146,7 @@ class Store {
   uint64_t backpressure_ = 0;
   std::map<std::string, Session> sessions_;
   std::vector<int64_t> dev_chunks_;
+  int64_t next_extent_id_ = 0;
   std::thread daemon_;
   bool daemon_run_ = false;
 };

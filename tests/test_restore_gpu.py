@@ -1,0 +1,207 @@
+"""End-to-end restore on the GPU: pinned chunk store -> H2D copy engine ->
+K1 / K4 -> paged KV, checked against the oracle (reference algorithm) and
+the reference's restore test contracts (proj/tests/test_restore.cpp)."""
+import numpy as np
+import pytest
+
+from hc_testutil import REL_TOL, cpu_hidden, cpu_wkv, dev_hidden, dev_wkv, max_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(n_layers=4, d=512, heads=8, n=1024, page=64, kvh=None, rope=True):
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    cfg = H.ModelConfig(n_layers=n_layers, d_hidden=d, n_heads=heads, n_kv_heads=kvh or heads,
+                        d_ffn=4 * d, max_seq=max(n, 1024), rope_enabled=rope)
+    w = H.Weights(cfg)
+    for L in range(n_layers):
+        w.set_layer_kv(L, dev_wkv(d, cfg.kv_heads() * cfg.d_head(), L))
+    n_pages = (n + page - 1) // page + 3
+    kv = H.KvCache(n_layers, n_pages, page, w.d_kv)
+    table = torch.randperm(n_pages, generator=torch.Generator().manual_seed(1))[
+        : (n + page - 1) // page].to(torch.int32).cuda()
+    return cfg, w, kv, table
+
+
+def _store_hidden(H, store, sid, cfg, n, plan, hidden_rows_fn, kv_rows_fn=None, tokens=None):
+    store.create_session(H.SessionSeed(sid, cfg.hash(), cfg.n_layers, cfg.d_hidden, 2, plan,
+                                       tokens if tokens is not None else list(range(n)),
+                                       d_kv=cfg.kv_heads() * cfg.d_head()))
+    for L, m in enumerate(plan.layer_assignment):
+        if m == H.LayerMethod.HIDDEN:
+            assert store.snapshot(sid, L, H.StateKind.HIDDEN, hidden_rows_fn(L))
+        elif m == H.LayerMethod.KV_OFFLOAD:
+            assert store.snapshot(sid, L, H.StateKind.KV, kv_rows_fn(L))
+    store.finalize(sid)
+
+
+@pytest.mark.parametrize("devices", [1, 2, 4])
+def test_restore_all_hidden_matches_oracle(cuda, oracle, devices):
+    """Config 1 shape: 4 layers, d=512, 8 heads, 1K tokens, paged cache."""
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    n = 1024 + 64 * 9  # > 8 chunk slots per extent: runs span several pinned extents
+    cfg, w, kv, table = _setup(n=n)
+    store = H.StorageManager(H.DevicePool(devices))
+    plan = H.RestorationPlan.make(4, 4, H.Complement.NONE)
+    # layer L's hidden states: synthetic rows with seed 7 + L, saved D2H from the GPU
+    _store_hidden(H, store, "s", cfg, n, plan, lambda L: dev_hidden(n, 512, seed=7 + L))
+    res = H.restore(store, "s", w, plan, H.ThrottleConfig(), kv, table)
+    torch.cuda.synchronize()
+    for L in range(4):
+        kr, vr = oracle.project(cpu_hidden(oracle, n, 512, seed=7 + L),
+                                *cpu_wkv(oracle, 512, 512, L), 8)
+        k, v = kv.gather(L, table, n)
+        assert max_rel_err(k.float().cpu().numpy(), kr) < REL_TOL
+        assert max_rel_err(v.float().cpu().numpy(), vr) < REL_TOL
+    tl = res.timeline
+    assert tl.total_s > 0 and tl.fill_s > 0
+    kinds = sorted({e.kind for e in tl.events})
+    assert kinds == ["fetch_hidden", "project"]
+    assert sum(e.kind == "project" for e in tl.events) == 4
+    # each projection starts after its own fetch finished
+    fetch_end = {e.layer: e.end_s for e in tl.events if e.kind == "fetch_hidden"}
+    for e in tl.events:
+        if e.kind == "project":
+            assert e.start_s >= fetch_end[e.layer] - 1e-6
+
+
+def test_restore_is_deterministic_and_equals_resident_path(cuda):
+    import ctypes as C
+
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    from paper_2410_05004_b200.capi import check, lib
+    n = 700
+    cfg, w, kv, table = _setup(n=n)
+    store = H.StorageManager(H.DevicePool(3))
+    plan = H.RestorationPlan.make(4, 4, H.Complement.NONE)
+    hid = [dev_hidden(n, 512, seed=70 + L) for L in range(4)]
+    _store_hidden(H, store, "s", cfg, n, plan, lambda L: hid[L])
+    H.restore(store, "s", w, plan, H.ThrottleConfig(prefetch_depth=1), kv, table)
+    torch.cuda.synchronize()
+    a = [(kv.k[L].clone(), kv.v[L].clone()) for L in range(4)]
+    _, w2, kv2, _ = _setup(n=n)
+    ptrs = (C.c_void_p * 4)(*[h.data_ptr() for h in hid])
+    check(lib().hc_restore_resident(w2._h, ptrs, n, None, 1, C.byref(kv2.desc), table.data_ptr(),
+                                    0, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    for L in range(4):
+        k2, v2 = kv2.gather(L, table, n)
+        k1, v1 = kv.gather(L, table, n)
+        assert torch.equal(k1, k2) and torch.equal(v1, v2)
+
+
+def test_kv_offload_layers_restore_bit_exact(cuda):
+    """Hybrid 2H+2KV plan (test_restore.cpp:128-135): KV layers come back
+    bit-exact through H2D + K4 scatter."""
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    n = 333
+    cfg, w, kv, table = _setup(n=n)
+    store = H.StorageManager(H.DevicePool(2))
+    plan = H.RestorationPlan.make(4, 2, H.Complement.KV_OFFLOAD)
+    kvrows = {L: dev_hidden(n, 1024, seed=500 + L) for L in range(4)}  # [K_row | V_row]
+    _store_hidden(H, store, "s", cfg, n, plan, lambda L: dev_hidden(n, 512, seed=7 + L),
+                  lambda L: kvrows[L])
+    res = H.restore(store, "s", w, plan, H.ThrottleConfig(), kv, table)
+    torch.cuda.synchronize()
+    for L in (2, 3):
+        k, v = kv.gather(L, table, n)
+        assert torch.equal(k, kvrows[L][:, :512]) and torch.equal(v, kvrows[L][:, 512:])
+    for L in (0, 1):
+        kd, vd = H.project_hidden_to_kv(w, L, dev_hidden(n, 512, seed=7 + L), 0)
+        k, v = kv.gather(L, table, n)
+        torch.cuda.synchronize()
+        assert torch.equal(k, kd) and torch.equal(v, vd)
+    assert sum(e.kind == "fetch_kv" for e in res.timeline.events) == 2
+    assert sum(e.kind == "scatter" for e in res.timeline.events) == 2
+
+
+def test_restore_error_contract(cuda):
+    """test_restore.cpp:199-207 (plan mismatch -> invalid_argument) and the
+    storage errors (missing / unfinalized session)."""
+    import torch  # noqa: F401
+    from paper_2410_05004_b200 import capi
+    from paper_2410_05004_b200 import hcache as H
+    n = 64
+    cfg, w, kv, table = _setup(n=n)
+    store = H.StorageManager(H.DevicePool(1))
+    stored = H.RestorationPlan.make(4, 4, H.Complement.NONE)
+    _store_hidden(H, store, "s", cfg, n, stored, lambda L: dev_hidden(n, 512, seed=L))
+    other = H.RestorationPlan.make(4, 2, H.Complement.KV_OFFLOAD)
+    with pytest.raises(ValueError):
+        H.restore(store, "s", w, other, H.ThrottleConfig(), kv, table)
+    with pytest.raises(capi.NotFound):
+        H.restore(store, "nope", w, stored, H.ThrottleConfig(), kv, table)
+    store.create_session(H.SessionSeed("open", 0, 4, 512, 2, stored, [], d_kv=512))
+    with pytest.raises(capi.Incomplete):
+        H.restore(store, "open", w, stored, H.ThrottleConfig(), kv, table)
+
+
+def test_device_snapshot_roundtrip_bitexact(cuda):
+    """Stage-1 D2H snapshot on a side stream -> chunks -> read_layer H2D."""
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    store = H.StorageManager(H.DevicePool(3), buffer_capacity_bytes=64 << 20)
+    plan = H.RestorationPlan.make(2, 2, H.Complement.NONE)
+    store.create_session(H.SessionSeed("s", 1, 2, 256, 2, plan, [1, 2]))
+    rows = dev_hidden(1000, 256, seed=3)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for a, b in ((0, 100), (100, 163), (163, 1000)):  # ragged pieces
+            assert store.snapshot("s", 0, H.StateKind.HIDDEN, rows[a:b], stream=side.cuda_stream)
+    store.finalize("s")
+    back = torch.empty_like(rows)
+    store.read_layer_device("s", 0, H.StateKind.HIDDEN, back)
+    torch.cuda.synchronize()
+    assert torch.equal(back, rows)
+    man = store.open("s")
+    host = store.read_layer(man, 0, H.StateKind.HIDDEN)
+    assert np.array_equal(host, rows.view(torch.int16).cpu().numpy().view(np.uint16))
+    assert store.read_layer(man, 1, H.StateKind.HIDDEN) is None
+
+
+def test_restore_batch_ragged_equals_single(cuda):
+    """Config 4 layout: several sessions restored by one grouped K1 per layer."""
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    d, page = 512, 64
+    lens = [130, 1, 64, 517]
+    cfg, w, _, _ = _setup(n=max(lens))
+    store = H.StorageManager(H.DevicePool(2))
+    plan = H.RestorationPlan.make(4, 4, H.Complement.NONE)
+    for s, n in enumerate(lens):
+        _store_hidden(H, store, f"s{s}", cfg, n, plan,
+                      lambda L, s=s, n=n: dev_hidden(n, d, seed=1000 * s + L))
+    stride = max((n + page - 1) // page for n in lens)
+    tables = torch.arange(len(lens) * stride, dtype=torch.int32).view(len(lens), stride).cuda()
+    kv = H.KvCache(4, len(lens) * stride, page, 512)
+    res = H.restore_batch(store, [f"s{s}" for s in range(len(lens))], w, H.ThrottleConfig(), kv,
+                          tables)
+    torch.cuda.synchronize()
+    assert sum(e.kind == "project" for e in res.timeline.events) == 4
+    for s, n in enumerate(lens):
+        for L in range(4):
+            kd, vd = H.project_hidden_to_kv(w, L, dev_hidden(n, d, seed=1000 * s + L), 0)
+            k, v = kv.gather(L, tables[s], n)
+            torch.cuda.synchronize()
+            assert torch.equal(k, kd) and torch.equal(v, vd), (s, L)
+
+
+def test_profile_and_three_way_plan(cuda):
+    from paper_2410_05004_b200 import hcache as H
+    cfg, w, _, _ = _setup(n=1024)
+    t = H.profile_hardware(w, 1024)
+    assert t.io_h > 0 and t.io_kv > 0 and t.c_h > 0 and t.c_token > 0
+    assert 1.5 < t.io_kv / t.io_h < 2.5  # MHA: KV rows are twice the hidden bytes
+    p, ms = H.plan_three_way(t, 4)
+    assert p.n_layers() == 4 and ms > 0
+
+
+def test_h2d_bandwidth_is_pcie_class(cuda):
+    from paper_2410_05004_b200 import hcache as H
+    bw = H.measure_h2d(64 << 20)
+    assert 5e9 < bw < 400e9
