@@ -399,6 +399,19 @@ hc_status hc_prefill(const hc_weights* w, const int32_t* d_tokens, int64_t n,
                      const hc_kv_pages* pages, const int32_t* d_page_table,
                      void* d_layer_inputs, int32_t* next_token, void* stream);
 
+/* Building blocks of K6, exposed for parity tests against fp32 references:
+ * causal attention over dense K/V (n x d_kv rows, GQA groups) and the shared
+ * tcgen05 GEMM C = A B^T (A M x K, B N x K, bf16) with the RESID epilogue
+ * (x[M x N] fp32 += C, xb = bf16(x)) or the GELU epilogue (xb = bf16(gelu(
+ * LN-fold(C)))), mean/rstd/colsum may be NULL (no fold). */
+hc_status hc_attention_dense(const void* d_q, int32_t n, int32_t n_heads, int32_t n_kv_heads,
+                             int32_t d_head, const void* d_k, const void* d_v, int32_t d_kv,
+                             void* d_out, void* stream);
+hc_status hc_gemm_epilogue(int32_t mode, const void* d_a, const void* d_b, int32_t m, int32_t n,
+                           int32_t k, float* d_x, void* d_xb, const float* d_mean,
+                           const float* d_rstd, const float* d_colsum, int32_t device,
+                           void* stream);
+
 /* -------------------------------------------------------------- profiling */
 /* profile_hardware (harness.hpp:76-77), measured on the device: io_h / io_kv
  * = pinned H2D time of one layer's hidden / KV rows for n_tokens, c_h = K1

@@ -154,6 +154,8 @@ _PROTOS = {
     "hc_profile": (i32, [vp, i32, P(TimingsC)]),
     "hc_measure_h2d": (i32, [i32, C.c_size_t, i32, P(f64)]),
     "hc_bench_project": (i32, [vp, i32, vp, i64, i32, vp, P(f64), P(f64)]),
+    "hc_attention_dense": (i32, [vp, i32, i32, i32, i32, vp, vp, i32, vp, vp]),
+    "hc_gemm_epilogue": (i32, [i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, i32, vp]),
 }
 
 _lib = None

@@ -230,6 +230,8 @@ void hc_weights_destroy(hc_weights* w) {
   for (auto& L : w->layers) {
     if (L.colsum) cudaFree(L.colsum);
     if (L.colsum_all) cudaFree(L.colsum_all);
+    if (L.colsum_q) cudaFree(L.colsum_q);
+    if (L.colsum_fc1) cudaFree(L.colsum_fc1);
   }
   if (w->rope) cudaFree(w->rope);
   if (prev >= 0) cudaSetDevice(prev);
@@ -266,8 +268,15 @@ hc_status hc_weights_set_layer_full(hc_weights* w, int32_t layer, const void* d_
     DeviceGuard dg(w->device);
     auto& L = w->layers[size_t(layer)];
     const int rows = 2 * w->d_kv_all, d = w->cfg.d_hidden;
+    for (auto p : {d_wq, d_wkv, d_wo, d_fc1, d_fc2})
+      if ((reinterpret_cast<uintptr_t>(p) & 15) != 0)
+        fail(HC_EINVAL, "set_layer_full: weights must be 16-byte aligned");
     if (!L.colsum_all) HC_CUDA(cudaMalloc(&L.colsum_all, size_t(rows) * sizeof(float)));
+    if (!L.colsum_q) HC_CUDA(cudaMalloc(&L.colsum_q, size_t(d) * sizeof(float)));
+    if (!L.colsum_fc1) HC_CUDA(cudaMalloc(&L.colsum_fc1, size_t(w->cfg.d_ffn) * sizeof(float)));
     HC_CUDA(launch_colsum(d_wkv, rows, d, true, L.colsum_all, nullptr));
+    HC_CUDA(launch_colsum(d_wq, d, d, true, L.colsum_q, nullptr));
+    HC_CUDA(launch_colsum(d_fc1, w->cfg.d_ffn, d, true, L.colsum_fc1, nullptr));
     HC_CUDA(cudaStreamSynchronize(nullptr));
     L.wq = d_wq;
     L.wkv_all = d_wkv;

@@ -103,11 +103,54 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int col0, const K
   }
 }
 
-template <int BN>
+// RESID: x[row, col] += acc (fp32 residual stream), xb = bf16(x).
+// GELU:  xb[row, col] = bf16(gelu(fold(acc))) (reference gelu, model.cpp:38-40).
+__device__ __forceinline__ void epilogue_chunk_dense(float (&f)[32], int mode, int row, int col0,
+                                                     const GemmOut& g, const EpiArgs& epi,
+                                                     float mean, float rstd) {
+  const size_t off = size_t(row) * size_t(g.ldo) + size_t(col0);
+  if (mode == kEpiResid) {
+    float4* x4 = reinterpret_cast<float4*>(g.x + off);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 x = x4[i];
+      x.x += f[4 * i + 0];
+      x.y += f[4 * i + 1];
+      x.z += f[4 * i + 2];
+      x.w += f[4 * i + 3];
+      x4[i] = x;
+      f[4 * i + 0] = x.x;
+      f[4 * i + 1] = x.y;
+      f[4 * i + 2] = x.z;
+      f[4 * i + 3] = x.w;
+    }
+  } else {
+    if (epi.row_mean) {
+      const float4* cs = reinterpret_cast<const float4*>(epi.colsum + col0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 c = __ldg(cs + i);
+        f[4 * i + 0] = rstd * (f[4 * i + 0] - mean * c.x);
+        f[4 * i + 1] = rstd * (f[4 * i + 1] - mean * c.y);
+        f[4 * i + 2] = rstd * (f[4 * i + 2] - mean * c.z);
+        f[4 * i + 3] = rstd * (f[4 * i + 3] - mean * c.w);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) f[i] = 0.5f * f[i] * (1.0f + erff(f[i] * 0.70710678118654752f));
+  }
+  uint4* d4 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(g.xb) + off);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    d4[i] = make_uint4(pack_bf16(f[8 * i + 0], f[8 * i + 1]), pack_bf16(f[8 * i + 2], f[8 * i + 3]),
+                       pack_bf16(f[8 * i + 4], f[8 * i + 5]), pack_bf16(f[8 * i + 6], f[8 * i + 7]));
+}
+
+template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
-    k1_restore_kv_kernel(const __grid_constant__ CUtensorMap tmA,
-                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
-                         EpiArgs epi, uint32_t idesc) {
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                   const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
+                   GemmOut gout, EpiArgs epi, uint32_t idesc) {
   using Cfg = K1Cfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -212,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int pos = out.start_pos;
       char* krow = nullptr;
       char* vrow = nullptr;
-      if (row_ok) {
+      if (row_ok && MODE == kEpiKv) {
         int seq = 0, local = row;
         if (out.cu_seqlens) {
           int lo = 0, hi = out.n_seqs - 1;
@@ -235,10 +278,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const size_t esz = out.out_f32 ? 4 : 2;
         krow = static_cast<char*>(out.k_base) + size_t(orow) * out.d_kv * esz;
         vrow = static_cast<char*>(out.v_base) + size_t(orow) * out.d_kv * esz;
-        if (epi.row_mean) {
-          mean = __ldg(epi.row_mean + row);
-          rstd = __ldg(epi.row_rstd + row);
-        }
+      }
+      if (row_ok && epi.row_mean) {
+        mean = __ldg(epi.row_mean + row);
+        rstd = __ldg(epi.row_rstd + row);
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -253,7 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           float f[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-          epilogue_chunk(f, col0, out, epi, mean, rstd, pos, krow, vrow);
+          if (MODE == kEpiKv) epilogue_chunk(f, col0, out, epi, mean, rstd, pos, krow, vrow);
+          else epilogue_chunk_dense(f, MODE, row, col0, gout, epi, mean, rstd);
         }
       }
       tc_fence_before();
@@ -397,39 +441,41 @@ __global__ void kv_scatter_kernel(const uint4* __restrict__ rows, int64_t n_rows
 
 }  // namespace
 
+template <int BN, int MODE>
+cudaError_t launch_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                      bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
+                      int num_sms, cudaStream_t stream) {
+  const uint32_t idesc = umma_idesc_f16(kBM, BN, bf16_in);
+  const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(K1Cfg<BN>::kSmem));
+  if (e != cudaSuccess) return e;
+  tc_gemm_kernel<BN, MODE><<<grid, kThreads, K1Cfg<BN>::kSmem, stream>>>(tmA, tmB, M, N, K, out,
+                                                                         g, epi, idesc);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
                               int num_sms, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  const uint32_t idesc = umma_idesc_f16(kBM, bn, bf16_in);
-  const int num_m = (M + kBM - 1) / kBM;
-  const int num_n = (N + bn - 1) / bn;
-  const int tiles = num_m * num_n;
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  if (bn == 256) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k1_restore_kv_kernel<256>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(K1Cfg<256>::kSmem));
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    k1_restore_kv_kernel<256><<<grid, kThreads, K1Cfg<256>::kSmem, stream>>>(tmA, tmB, M, N, K,
-                                                                           out, epi, idesc);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k1_restore_kv_kernel<128>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(K1Cfg<128>::kSmem));
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    k1_restore_kv_kernel<128><<<grid, kThreads, K1Cfg<128>::kSmem, stream>>>(tmA, tmB, M, N, K,
-                                                                           out, epi, idesc);
-  }
-  return cudaGetLastError();
+  GemmOut g;
+  return bn == 256 ? launch_tc<256, kEpiKv>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream)
+                   : launch_tc<128, kEpiKv>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
+}
+
+cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,
+                              int M, int N, int K, const GemmOut& g, const EpiArgs& epi,
+                              int num_sms, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  KvOut o;
+  if (mode == kEpiResid)
+    return bn == 256 ? launch_tc<256, kEpiResid>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream)
+                     : launch_tc<128, kEpiResid>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream);
+  return bn == 256 ? launch_tc<256, kEpiGelu>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream)
+                   : launch_tc<128, kEpiGelu>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream);
 }
 
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,

@@ -35,6 +35,18 @@ struct EpiArgs {
   int rope_rows = 0;
 };
 
+// Epilogue modes of the shared tcgen05 GEMM (K1 and the K6 projections).
+constexpr int kEpiKv = 0;     // LN fold + RoPE(K half) -> K/V rows (dense or paged)
+constexpr int kEpiResid = 1;  // x += acc (fp32 residual), xb = bf16(x)
+constexpr int kEpiGelu = 2;   // xb = bf16(gelu(LN fold(acc)))
+
+// Dense outputs of the RESID / GELU modes, row stride ldo elements.
+struct GemmOut {
+  float* x = nullptr;
+  void* xb = nullptr;  // bf16
+  int ldo = 0;
+};
+
 // Creates a 2D K-major bf16/fp16 tensor map with a {64, box_rows} box and the
 // 128-byte swizzle (the K1 operand layout). Returns false on failure.
 bool make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows,
@@ -45,6 +57,26 @@ bool make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t k, uint64_t r
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
                               int num_sms, cudaStream_t stream);
+
+// The same GEMM with a dense epilogue (mode kEpiResid or kEpiGelu).
+cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,
+                              int M, int N, int K, const GemmOut& g, const EpiArgs& epi,
+                              int num_sms, cudaStream_t stream);
+
+// Causal attention over the paged cache for a prefill from position 0
+// (attention_forward, model.cpp:237-288): q [n x n_heads*dh] bf16 (RoPE
+// applied), K/V from `kv` (paged or dense, row width kv.d_kv, GQA groups),
+// out [n x n_heads*dh] bf16 = softmax(q k^T / sqrt(dh)) v per head.
+cudaError_t launch_attention(const void* q, int n, int n_heads, int n_kv_heads, int dh,
+                             const KvOut& kv, void* out, cudaStream_t stream);
+
+// Embedding gather (model.cpp:82-92): x[i] = E[tokens[i]] (fp32), xb = bf16.
+cudaError_t launch_embed(const int32_t* tokens, int64_t n, const void* emb, int d, float* x,
+                         void* xb, cudaStream_t stream);
+
+// Greedy next token (argmax_token, model.cpp:67-80): argmax_t E[t] . h.
+cudaError_t launch_argmax_logits(const void* emb, int vocab, int d, const float* h,
+                                 int32_t* out_token, cudaStream_t stream);
 
 // Row statistics for the LayerNorm fold: mean and 1/sqrt(var+1e-5) per row,
 // mean/var accumulated in double like the reference (model.cpp:43-61).

@@ -29,6 +29,8 @@ struct hc_weights {
     const void* fc1 = nullptr;
     const void* fc2 = nullptr;
     float* colsum_all = nullptr;  // owned, colsum of wkv_all (2*d_kv_all)
+    float* colsum_q = nullptr;    // owned, colsum of wq (d)
+    float* colsum_fc1 = nullptr;  // owned, colsum of fc1 (d_ffn)
     bool full = false;
   };
   std::vector<Layer> layers;

@@ -290,7 +290,10 @@ class StorageManager:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().hc_store_destroy(self._h)
+            try:
+                lib().hc_store_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     __del__ = close
@@ -483,7 +486,10 @@ class Weights:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().hc_weights_destroy(self._h)
+            try:
+                lib().hc_weights_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     __del__ = close

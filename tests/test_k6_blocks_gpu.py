@@ -1,0 +1,75 @@
+"""K6 building blocks vs plain PyTorch fp32 references of the same op
+(attention_forward model.cpp:237-288 per head; GEMM epilogues)."""
+import math
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _attn_ref(q, k, v, n_heads, n_kv_heads, dh):
+    import torch
+    n = q.shape[0]
+    qf = q.float().view(n, n_heads, dh).transpose(0, 1)
+    kf = k.float().view(n, n_kv_heads, dh).transpose(0, 1)
+    vf = v.float().view(n, n_kv_heads, dh).transpose(0, 1)
+    g = n_heads // n_kv_heads
+    kf = kf.repeat_interleave(g, 0)
+    vf = vf.repeat_interleave(g, 0)
+    s = qf @ kf.transpose(1, 2) / math.sqrt(dh)
+    mask = torch.triu(torch.ones(n, n, dtype=torch.bool, device=q.device), 1)
+    s = s.masked_fill(mask, float("-inf"))
+    return (torch.softmax(s, -1) @ vf).transpose(0, 1).reshape(n, n_heads * dh)
+
+
+@pytest.mark.parametrize("n,heads,kvh,dh", [(1, 2, 2, 64), (64, 2, 2, 64), (200, 4, 4, 64),
+                                            (333, 4, 2, 128), (1024, 8, 8, 64), (130, 8, 1, 128)])
+def test_attention_dense_vs_torch(cuda, n, heads, kvh, dh):
+    import torch
+    from paper_2410_05004_b200 import capi
+    g = torch.Generator(device="cuda").manual_seed(n)
+    q = torch.randn(n, heads * dh, device="cuda", generator=g).bfloat16()
+    k = torch.randn(n, kvh * dh, device="cuda", generator=g).bfloat16()
+    v = torch.randn(n, kvh * dh, device="cuda", generator=g).bfloat16()
+    out = torch.empty(n, heads * dh, device="cuda", dtype=torch.bfloat16)
+    capi.check(capi.lib().hc_attention_dense(q.data_ptr(), n, heads, kvh, dh, k.data_ptr(),
+                                             v.data_ptr(), kvh * dh, out.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream))
+    ref = _attn_ref(q, k, v, heads, kvh, dh)
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("m,n,k", [(200, 256, 512), (1024, 512, 2048), (130, 4096, 256)])
+def test_gemm_epilogues_vs_torch(cuda, mode, m, n, k):
+    import torch
+    from paper_2410_05004_b200 import capi
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    a = torch.randn(m, k, device="cuda", generator=g).bfloat16()
+    b = (torch.randn(n, k, device="cuda", generator=g) / math.sqrt(k)).bfloat16()
+    x = torch.randn(m, n, device="cuda", generator=g)
+    x0 = x.clone()
+    xb = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    mean = a.float().mean(1).contiguous()
+    rstd = (1 / torch.sqrt(a.float().var(1, unbiased=False) + 1e-5)).contiguous()
+    colsum = b.float().sum(1).contiguous()
+    fold = mode == 2
+    capi.check(capi.lib().hc_gemm_epilogue(mode, a.data_ptr(), b.data_ptr(), m, n, k,
+                                           x.data_ptr(), xb.data_ptr(),
+                                           mean.data_ptr() if fold else None,
+                                           rstd.data_ptr() if fold else None,
+                                           colsum.data_ptr() if fold else None, 0,
+                                           torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    c = a.float() @ b.float().t()
+    if mode == 1:
+        want = x0 + c
+        assert torch.allclose(x, want, rtol=1e-4, atol=1e-4)
+        assert torch.equal(xb, x.bfloat16())
+    else:
+        ln = (a.float() - mean[:, None]) * rstd[:, None]
+        want = torch.nn.functional.gelu(ln @ b.float().t())
+        err = (xb.float() - want).abs().max().item() / want.abs().max().item()
+        assert err < 1e-2, err
