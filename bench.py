@@ -13,9 +13,12 @@ hidden states and random-init weights (splitmix64 generators, no network).
   HBM: every step runs K1 (row stats + LN-fold tcgen05 GEMM + RoPE -> paged KV)
   over all 32 layers. Timed with CUDA events on the launching stream.
 * ``e2e``    -- the same metric through the C ABI ``hc_restore`` from the
-  pinned-host chunk store: every step copies all 32 layers' hidden states
-  host->device (copy engine, 1 GiB) inside the timed region, overlapped with
-  K1, and reads a checksum row of the restored cache back to the host.
+  pinned-host chunk store, executing the bubble-free scheduler's plan
+  (hc_plan_three_way on hc_profile's measured PCIe / K1 / K6 timings): every
+  step copies the planned layers' hidden states host->device (copy engine)
+  inside the timed region, overlapped with K1 and the K6 recompute prefix,
+  and reads a checksum row of the restored cache back to the host. The
+  KV-offload and recompute paths of the same codebase are timed alongside.
 * N>1 (torchrun): head-sharded restore (north star (4)): each rank fetches 1/N
   of every layer's token chunks over its own PCIe link, NCCL all-gathers them
   and projects only its own KV heads. ``scaling`` = strong (one context).
@@ -179,15 +182,26 @@ def run_ours(args, cfg, rank, world):
         return sharded.bench(args, cfg, rank, world, dev)
 
     stream = torch.cuda.current_stream().cuda_stream
+    vocab = 32000
     mc = H.ModelConfig(n_layers=L, d_hidden=d, n_heads=heads, n_kv_heads=kvh, d_ffn=dffn,
-                       max_seq=max(n, 4096), rope_enabled=rope)
+                       vocab_size=vocab, max_seq=max(n, 4096), rope_enabled=rope)
     w = H.Weights(mc)
     d_kv = w.d_kv
+    bound = float(np.float32(1) / np.sqrt(np.float32(d)))
+
+    def fill(shape, seed):
+        t = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+        check(lib().hc_fill_symmetric(t.data_ptr(), t.numel(), seed, 0, bound, 1, stream))
+        return t
+    emb = fill((vocab, d), 99)
+    w.set_embedding(emb)
+    full = not args.no_recompute and kvh == heads
     for layer in range(L):
-        wkv = torch.empty((2 * d_kv, d), dtype=torch.bfloat16, device="cuda")
-        check(lib().hc_fill_symmetric(wkv.data_ptr(), wkv.numel(), 1234 + layer, 0,
-                                      float(1 / np.sqrt(np.float32(d))), 1, stream))
+        wkv = fill((2 * d_kv, d), 1234 + layer)
         w.set_layer_kv(layer, wkv)
+        if full:
+            w.set_layer_full(layer, fill((d, d), 5000 + layer), wkv, fill((d, d), 6000 + layer),
+                             fill((dffn, d), 7000 + layer), fill((d, dffn), 8000 + layer))
     page = 64
     n_pages = (n + page - 1) // page
     kv = H.KvCache(L, n_pages, page, d_kv)
@@ -195,17 +209,36 @@ def run_ours(args, cfg, rank, world):
     hid = torch.empty((L, n, d), dtype=torch.bfloat16, device="cuda")
     check(lib().hc_fill_symmetric(hid.data_ptr(), hid.numel(), 7, 0, 1.7320508, 1, stream))
     hptrs = (C.c_void_p * L)(*[hid[layer].data_ptr() for layer in range(L)])
+    tokens = [(i * 11 + 1) % vocab for i in range(n)]
 
-    # pinned-host chunk store holding the session (saved from the device, D2H)
+    # bubble-free scheduler on measured PCIe / GEMM / recompute timings
+    prof = H.profile_hardware(w, n)
+    prof.n_layers = L
+    if full:
+        plan, plan_ms = H.plan_three_way(prof, L)
+    else:
+        plan, plan_ms = H.RestorationPlan.make(L, L, H.Complement.NONE), None
+    all_h = H.RestorationPlan.make(L, L, H.Complement.NONE)
+    all_kv = H.RestorationPlan.make(L, 0, H.Complement.KV_OFFLOAD)
+
+    # pinned-host chunk store: the sessions (saved from the device, D2H)
     store = H.StorageManager(H.DevicePool(1), buffer_capacity_bytes=4 << 30)
-    plan = H.RestorationPlan.make(L, L, H.Complement.NONE)
-    store.create_session(H.SessionSeed("bench", mc.hash(), L, d, 2, plan, list(range(n)),
-                                       d_kv=d_kv))
-    for layer in range(L):
-        while not store.snapshot("bench", layer, H.StateKind.HIDDEN, hid[layer]):
-            store.drain()
-    store.finalize("bench")
-    torch.cuda.synchronize()
+
+    def save(sid, p):
+        store.create_session(H.SessionSeed(sid, mc.hash(), L, d, 2, p, tokens, d_kv=d_kv))
+        for layer, m in enumerate(p.layer_assignment):
+            if m == H.LayerMethod.HIDDEN:
+                rows = hid[layer]
+                kind = H.StateKind.HIDDEN
+            elif m == H.LayerMethod.KV_OFFLOAD:
+                k_, v_ = kv.gather(layer, table, n)
+                rows = torch.cat([k_, v_], 1).contiguous()
+                kind = H.StateKind.KV
+            else:
+                continue
+            while not store.snapshot(sid, layer, kind, rows):
+                store.drain()
+        store.finalize(sid)
 
     def resident_step():
         check(lib().hc_restore_resident(w._h, hptrs, n, None, 1, C.byref(kv.desc),
@@ -214,11 +247,32 @@ def run_ours(args, cfg, rank, world):
     opts = capi.RestoreOptsC(0, 0)
     host_ck = torch.empty(16 * d_kv, dtype=torch.bfloat16, pin_memory=True)
 
-    def e2e_step():
-        check(lib().hc_restore(store._h, b"bench", w._h, C.byref(plan._c), C.byref(opts),
+    def restore_step(sid, p):
+        check(lib().hc_restore(store._h, sid, w._h, C.byref(p._c), C.byref(opts),
                                C.byref(kv.desc), table.data_ptr(), stream, None))
         # device->host read of the step's result: 16 restored K rows of the last layer
         host_ck.copy_(kv.k[L - 1].view(-1)[: 16 * d_kv], non_blocking=True)
+
+    d_tok = torch.tensor(tokens, dtype=torch.int32, device="cuda")
+
+    def recompute_step():
+        # the RECOMPUTE baseline: token ids host->device, K6 over every layer
+        d_tok.copy_(torch.tensor(tokens, dtype=torch.int32), non_blocking=False)
+        check(lib().hc_prefill_layers(w._h, d_tok.data_ptr(), n, 0, L, C.byref(kv.desc),
+                                      table.data_ptr(), stream))
+        host_ck.copy_(kv.k[L - 1].view(-1)[: 16 * d_kv], non_blocking=True)
+
+    resident_step()
+    torch.cuda.synchronize()
+    save(b"hcache".decode(), plan)
+    if plan.serialize() != all_h.serialize():
+        save("all_hidden", all_h)
+    save("kv_offload", all_kv)
+    sid_plan = b"hcache"
+    sid_allh = b"hcache" if plan.serialize() == all_h.serialize() else b"all_hidden"
+
+    def e2e_step():
+        restore_step(sid_plan, plan)
 
     def timed(fn, steps):
         torch.cuda.synchronize()
@@ -241,6 +295,21 @@ def run_ours(args, cfg, rank, world):
         ms_e2e = timed(e2e_step, args.steps)
         wall_e2e = (time.perf_counter() - t0) * 1e3 / args.steps
     clocks = clk.summary()
+    # same-codebase baselines (not part of the headline timed region)
+    for _ in range(2):
+        restore_step(sid_allh, all_h)
+        restore_step(b"kv_offload", all_kv)
+    ms_allh = timed(lambda: restore_step(sid_allh, all_h), max(3, args.steps // 2))
+    ms_kv = timed(lambda: restore_step(b"kv_offload", all_kv), max(3, args.steps // 2))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    restore_step(sid_plan, plan)
+    enqueue_ms = (time.perf_counter() - t0) * 1e3  # host time to enqueue one restore
+    torch.cuda.synchronize()
+    ms_re = None
+    if full:
+        recompute_step()
+        ms_re = timed(recompute_step, max(3, args.steps // 2))
 
     # dominant kernel (K1): per-launch times with events on its stream
     stats_ms, k1_ms = C.c_double(), C.c_double()
@@ -252,9 +321,10 @@ def run_ours(args, cfg, rank, world):
     h2d = H.measure_h2d(256 << 20, 5, dev)
 
     # restore timeline of one e2e step (fill / bubble / lane busy)
-    res = H.restore(store, "bench", w, plan, H.ThrottleConfig(0, True), kv, table)
+    res = H.restore(store, sid_plan.decode(), w, plan, H.ThrottleConfig(0, True), kv, table)
     tl = res.timeline
     h_bytes = L * n * d * 2
+    h_bytes_plan = plan.l_h * n * d * 2 + plan.l_kv * n * 2 * d_kv * 2 + (4 * n if plan.l_re else 0)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tpath):
@@ -276,14 +346,27 @@ def run_ours(args, cfg, rank, world):
                    else args.config, "layers": L, "d_hidden": d, "heads": heads,
                    "kv_heads": kvh, "tokens": n, "page_size": page,
                    "l2": "inputs larger than L2 (1 GiB hidden + 2 GiB weights per step)",
-                   "plan": plan.serialize()},
-        "restore_latency_ms": {"resident": ms_resident, "e2e": ms_e2e, "e2e_wall": wall_e2e},
-        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h_bytes,
+                   "plan": plan.serialize(), "planner": "hc_plan_three_way on hc_profile"},
+        "restore_latency_ms": {"resident": ms_resident, "e2e": ms_e2e, "e2e_wall": wall_e2e,
+                               "all_hidden": ms_allh, "kv_offload": ms_kv,
+                               "host_enqueue": enqueue_ms,
+                               "recompute": ms_re},
+        "speedup": {"hcache_vs_kv_offload": ms_kv / ms_e2e,
+                    "hcache_vs_recompute": (ms_re / ms_e2e) if ms_re else None,
+                    "hcache_vs_all_hidden": ms_allh / ms_e2e},
+        "planner": {"profiled": {"io_h_ms": prof.io_h * 1e3, "io_kv_ms": prof.io_kv * 1e3,
+                                 "c_h_ms": prof.c_h * 1e3, "c_token_ms": prof.c_token * 1e3},
+                    "plan": plan.serialize(),
+                    "predicted_ms": plan_ms * 1e3 if plan_ms else None},
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h_bytes_plan,
                 "d2h_bytes_per_step": int(host_ck.numel() * 2),
-                "roofline": {"bound": "pcie", "achieved_gbs": h_bytes / (ms_e2e * 1e-3) / 1e9,
-                             "peak_gbs": h2d / 1e9, "peak_source": "measured pinned H2D 256 MiB",
-                             "frac": roof_pcie_s / (ms_e2e * 1e-3),
-                             "roofline_tokens_per_s": n / max(roof_pcie_s, roof_gemm_s)}},
+                "roofline": {"bound": "pcie", "unit": "GB/s",
+                             "achieved": h_bytes_plan / (ms_e2e * 1e-3) / 1e9,
+                             "peak": h2d / 1e9, "peak_source": "measured pinned H2D 256 MiB",
+                             "frac": h_bytes_plan / (ms_e2e * 1e-3) / h2d,
+                             "all_hidden_roofline_ms": 1e3 * max(roof_pcie_s, roof_gemm_s),
+                             "frac_vs_all_hidden_roofline":
+                                 max(roof_pcie_s, roof_gemm_s) / (ms_e2e * 1e-3)}},
         "roofline": {"bound": "tensor", "kernel": "k1_restore_kv", "achieved": k1_tflops,
                      "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                      "frac": k1_tflops / pk["bf16_tflops"],
@@ -312,6 +395,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-recompute", action="store_true",
+                    help="skip full-block weights (no RECOMPUTE complement / baseline)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = CONFIGS[args.config]

@@ -448,10 +448,16 @@ cudaError_t launch_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int
   const uint32_t idesc = umma_idesc_f16(kBM, BN, bf16_in);
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms ? tiles : num_sms;
-  cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(K1Cfg<BN>::kSmem));
-  if (e != cudaSuccess) return e;
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {  // once per thread and device
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(K1Cfg<BN>::kSmem));
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
   tc_gemm_kernel<BN, MODE><<<grid, kThreads, K1Cfg<BN>::kSmem, stream>>>(tmA, tmB, M, N, K, out,
                                                                          g, epi, idesc);
   return cudaGetLastError();

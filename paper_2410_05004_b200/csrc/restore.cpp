@@ -14,6 +14,7 @@
 // Nothing blocks the host; the whole restore is enqueued up front. The
 // Timeline (pipeline.hpp:18-28) is filled from CUDA events on both lanes.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -32,10 +33,22 @@ std::string plan_serialize(const hc_plan* p);
 
 namespace {
 
-// Per-device engine state: the copy stream and a memory pool that keeps the
-// staging ring cached across restores.
+// Per-device engine state: the IO lane's copy streams (a layer's gather is
+// split over kCopyStreams so several copy engines share the PCIe link) and a
+// memory pool that keeps the staging ring cached across restores.
+constexpr int kCopyStreams = 4;
+// IO-lane width actually used (HC_COPY_STREAMS, 1..kCopyStreams; default 1)
+int copy_streams() {
+  static int v = [] {
+    const char* e = std::getenv("HC_COPY_STREAMS");
+    int x = e ? std::atoi(e) : 1;
+    return std::max(1, std::min(kCopyStreams, x));
+  }();
+  return v;
+}
 struct Engine {
-  cudaStream_t copy = nullptr;
+  cudaStream_t copy = nullptr;  // IO lane head: orders fetches, joins the helpers
+  cudaStream_t helper[kCopyStreams - 1] = {};
   bool init = false;
 };
 
@@ -46,6 +59,7 @@ Engine& engine(int dev) {
   Engine& e = engines[size_t(dev)];
   if (!e.init) {
     HC_CUDA(cudaStreamCreateWithFlags(&e.copy, cudaStreamNonBlocking));
+    for (auto& h : e.helper) HC_CUDA(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking));
     cudaMemPool_t pool;
     HC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thresh = UINT64_MAX;
@@ -70,23 +84,75 @@ struct TimedOp {
   cudaEvent_t start, end;
 };
 
-void issue_gather(const std::vector<CopySeg>& segs, uint8_t* dst, cudaStream_t s) {
-  for (const auto& g : segs) {
-    cudaError_t e;
-    if (g.height == 1 || g.dpitch == g.width)
-      e = cudaMemcpyAsync(dst + g.dst_off, g.src, size_t(g.width * g.height),
-                          cudaMemcpyHostToDevice, s);
-    else
-      e = cudaMemcpy2DAsync(dst + g.dst_off, size_t(g.dpitch), g.src, size_t(g.spitch),
-                            size_t(g.width), size_t(g.height), cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess)
-      fail(HC_ECUDA, std::string("restore gather H2D: ") + cudaGetErrorString(e) +
-                         " (dst=" + std::to_string(reinterpret_cast<uintptr_t>(dst)) +
-                         "+" + std::to_string(g.dst_off) + " src=" +
-                         std::to_string(reinterpret_cast<uintptr_t>(g.src)) + " w=" +
-                         std::to_string(g.width) + " h=" + std::to_string(g.height) +
-                         " sp=" + std::to_string(g.spitch) + " dp=" + std::to_string(g.dpitch) + ")");
+void copy_seg(const CopySeg& g, uint8_t* dst, cudaStream_t s) {
+  cudaError_t e;
+  if (g.height == 1 || g.dpitch == g.width)
+    e = cudaMemcpyAsync(dst + g.dst_off, g.src, size_t(g.width * g.height), cudaMemcpyHostToDevice,
+                        s);
+  else
+    e = cudaMemcpy2DAsync(dst + g.dst_off, size_t(g.dpitch), g.src, size_t(g.spitch),
+                          size_t(g.width), size_t(g.height), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess)
+    fail(HC_ECUDA, std::string("restore gather H2D: ") + cudaGetErrorString(e) +
+                       " (dst_off=" + std::to_string(g.dst_off) + " w=" + std::to_string(g.width) +
+                       " h=" + std::to_string(g.height) + ")");
+}
+
+// Splits the gather into <= kCopyStreams pieces of similar size (rows of a
+// run stay whole) so concurrent copy engines share the link.
+std::vector<std::vector<CopySeg>> split_gather(const std::vector<CopySeg>& segs, int parts) {
+  int64_t total = 0;
+  for (const auto& g : segs) total += g.width * g.height;
+  std::vector<std::vector<CopySeg>> out(static_cast<size_t>(parts));
+  const int64_t target = (total + parts - 1) / parts;
+  int cur = 0;
+  int64_t acc = 0;
+  for (const auto& g0 : segs) {
+    CopySeg g = g0;
+    while (g.height > 0) {
+      const int64_t room = std::max<int64_t>(g.width, target - acc);
+      int64_t rows = std::min<int64_t>(g.height, std::max<int64_t>(1, room / g.width));
+      if (cur == parts - 1) rows = g.height;
+      CopySeg piece = g;
+      piece.height = rows;
+      out[size_t(cur)].push_back(piece);
+      acc += rows * g.width;
+      g.src += rows * g.spitch;
+      g.dst_off += rows * g.dpitch;
+      g.height -= rows;
+      if (acc >= target && cur < parts - 1) {
+        ++cur;
+        acc = 0;
+      }
+    }
   }
+  return out;
+}
+
+// Gather on the IO lane: the head stream forks to the helper streams and
+// joins them again, so the lane stays one ordered sequence of layer fetches.
+void issue_gather(const std::vector<CopySeg>& segs, uint8_t* dst, Engine& eng,
+                  std::vector<cudaEvent_t>& scratch_events, cudaEvent_t (*make)(void*), void* ctx) {
+  const int width = copy_streams();
+  if (width == 1) {
+    for (const auto& g : segs) copy_seg(g, dst, eng.copy);
+    return;
+  }
+  auto parts = split_gather(segs, width);
+  cudaEvent_t fork = make(ctx);
+  HC_CUDA(cudaEventRecord(fork, eng.copy));
+  for (int i = 1; i < width; ++i) {
+    if (parts[size_t(i)].empty()) continue;
+    cudaStream_t h = eng.helper[i - 1];
+    HC_CUDA(cudaStreamWaitEvent(h, fork, 0));
+    for (const auto& g : parts[size_t(i)]) copy_seg(g, dst, h);
+    cudaEvent_t j = make(ctx);
+    HC_CUDA(cudaEventRecord(j, h));
+    scratch_events.push_back(j);
+  }
+  for (const auto& g : parts[0]) copy_seg(g, dst, eng.copy);
+  for (auto j : scratch_events) HC_CUDA(cudaStreamWaitEvent(eng.copy, j, 0));
+  scratch_events.clear();
 }
 
 // Lazily created CUDA events, destroyed with the object.
@@ -102,6 +168,13 @@ struct EventPool {
   }
   ~EventPool() {
     for (auto e : all) cudaEventDestroy(e);
+  }
+  static cudaEvent_t make(void* self) {
+    EventPool* p = static_cast<EventPool*>(self);
+    cudaEvent_t e;
+    HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->all.push_back(e);
+    return e;
   }
 };
 
@@ -200,14 +273,14 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
   StreamScratch ring_h(n_hidden ? h_bytes * size_t(nbuf_h) : 0, stream);
   StreamScratch ring_kv(n_kv ? kv_bytes * size_t(nbuf_kv) : 0, stream);
 
-  // token ids for the RECOMPUTE prefix go up before the timed region starts
+  // token ids for the RECOMPUTE prefix: async H2D from the store's pinned copy
   StreamScratch d_tok(n_re ? sizeof(int32_t) * size_t(n) : 0, stream);
   if (n_re) {
-    std::vector<int32_t> toks = store.tokens(sid);
-    if (int(toks.size()) < n) fail(HC_EINVAL, "restore: manifest has fewer token ids than tokens");
-    HC_CUDA(cudaMemcpyAsync(d_tok.ptr, toks.data(), sizeof(int32_t) * size_t(n),
-                            cudaMemcpyHostToDevice, stream));
-    HC_CUDA(cudaStreamSynchronize(stream));
+    int64_t n_ids = 0;
+    const int32_t* toks = store.pinned_tokens(sid, &n_ids);
+    if (n_ids < n || !toks) fail(HC_EINVAL, "restore: manifest has fewer token ids than tokens");
+    HC_CUDA(cudaMemcpyAsync(d_tok.ptr, toks, sizeof(int32_t) * size_t(n), cudaMemcpyHostToDevice,
+                            stream));
   }
 
   cudaEvent_t t0 = evp.get();
@@ -230,6 +303,7 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
 
   // IO lane: all fetches in compute order; compute lane consumes in order.
   std::vector<cudaEvent_t> consumed_h(size_t(nbuf_h), nullptr), consumed_kv(size_t(nbuf_kv), nullptr);
+  std::vector<cudaEvent_t> joins;
   int ih = 0, ikv = 0;
   for (const auto& j : order) {
     if (j.method == HC_METHOD_RECOMPUTE) continue;
@@ -247,7 +321,7 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
     if (consumed[size_t(slot)]) HC_CUDA(cudaStreamWaitEvent(eng.copy, consumed[size_t(slot)], 0));
     cudaEvent_t fs = timed ? evp.get() : nullptr;
     if (fs) HC_CUDA(cudaEventRecord(fs, eng.copy));
-    issue_gather(segs, buf, eng.copy);
+    issue_gather(segs, buf, eng, joins, &EventPool::make, &evp);
     cudaEvent_t fetched = evp.get();
     HC_CUDA(cudaEventRecord(fetched, eng.copy));
     if (timed) ops.push_back({HC_LANE_IO, j.layer, hid ? HC_EV_FETCH_HIDDEN : HC_EV_FETCH_KV, fs, fetched});
@@ -322,15 +396,23 @@ void restore_batch(hc_store* st, const char* const* sids, int n_sessions, const 
   HC_CUDA(cudaEventRecord(t0, stream));
   HC_CUDA(cudaStreamWaitEvent(eng.copy, t0, 0));
   std::vector<cudaEvent_t> consumed(size_t(nbuf), nullptr);
+  std::vector<cudaEvent_t> joins;
   for (int l = 0; l < L; ++l) {
     const int slot = l % nbuf;
     uint8_t* buf = static_cast<uint8_t*>(ring.ptr) + h_bytes * size_t(slot);
     if (consumed[size_t(slot)]) HC_CUDA(cudaStreamWaitEvent(eng.copy, consumed[size_t(slot)], 0));
     cudaEvent_t fs = timed ? evp.get() : nullptr;
     if (fs) HC_CUDA(cudaEventRecord(fs, eng.copy));
-    for (int s = 0; s < n_sessions; ++s) {
-      auto segs = store.gather_plan(sids[s], l, HC_STATE_HIDDEN, 0, -1, nullptr);
-      issue_gather(segs, buf + size_t(cu[size_t(s)]) * size_t(d) * 2, eng.copy);
+    {
+      std::vector<CopySeg> all;
+      for (int s = 0; s < n_sessions; ++s) {
+        auto segs = store.gather_plan(sids[s], l, HC_STATE_HIDDEN, 0, -1, nullptr);
+        for (auto g : segs) {
+          g.dst_off += int64_t(cu[size_t(s)]) * int64_t(d) * 2;
+          all.push_back(g);
+        }
+      }
+      issue_gather(all, buf, eng, joins, &EventPool::make, &evp);
     }
     cudaEvent_t fetched = evp.get();
     HC_CUDA(cudaEventRecord(fetched, eng.copy));
@@ -464,16 +546,19 @@ hc_status hc_profile(const hc_weights* w, int32_t n_tokens, hc_timings* out) {
     o.k_base = k;
     o.v_base = v;
     o.d_kv = w->d_kv;
+    // back-to-back launches, as in the restore pipeline (host setup overlapped)
     Ev a, b;
     float best = 1e30f;
-    for (int r = 0; r < 4; ++r) {
+    const int reps = 8;
+    project_rows(w, layer, h, n_tokens, o, nullptr);  // warm-up
+    for (int r = 0; r < 3; ++r) {
       HC_CUDA(cudaEventRecord(a.e, nullptr));
-      project_rows(w, layer, h, n_tokens, o, nullptr);
+      for (int i = 0; i < reps; ++i) project_rows(w, layer, h, n_tokens, o, nullptr);
       HC_CUDA(cudaEventRecord(b.e, nullptr));
       HC_CUDA(cudaEventSynchronize(b.e));
       float ms = 0;
       HC_CUDA(cudaEventElapsedTime(&ms, a.e, b.e));
-      if (r > 0) best = std::min(best, ms);
+      best = std::min(best, ms / reps);
     }
     out->c_h = best * 1e-3;
     cudaFree(h);

@@ -278,9 +278,19 @@ uint8_t* Store::new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx) 
   auto& ex = ls.extents[size_t(dev)];
   const size_t cb = s.chunk_bytes(ls.kind);
   if (ex.used == ex.cap) {
-    // next extent of consecutive slots: geometric growth, <= 256 MiB
-    int cap = ex.cap ? ex.cap * 2 : 8;
+    // next extent of consecutive slots. The first one is sized for every
+    // chunk this device will hold when the session's token count is known
+    // (one copy-engine run per layer and device at restore); later ones grow
+    // geometrically. <= 256 MiB each.
     const int max_slots = std::max<int>(1, int((size_t(256) << 20) / cb));
+    int cap;
+    if (ex.cap == 0) {
+      const int expect_tokens = int(s.tokens.size());
+      const int expect_chunks = (expect_tokens + HC_CHUNK_TOKENS - 1) / HC_CHUNK_TOKENS;
+      cap = std::max(8, (expect_chunks + ndev_ - 1) / ndev_);
+    } else {
+      cap = ex.cap * 2;
+    }
     cap = std::min(cap, max_slots);
     ex.base = static_cast<uint8_t*>(pool_mem_.alloc_raw(cb * size_t(cap)));
     ex.cap = cap;
@@ -341,8 +351,25 @@ void Store::finalize(const std::string& sid) {
   drain_locked(INT64_MAX);
   Session& s = find_open(sid);
   if (s.finalized) return;
+  if (!s.tokens.empty()) {
+    const size_t need = s.tokens.size() * sizeof(int32_t);
+    if (need > s.pinned_tokens_cap) {
+      if (s.pinned_tokens) pool_mem_.release(s.pinned_tokens, s.pinned_tokens_cap);
+      s.pinned_tokens = static_cast<int32_t*>(pool_mem_.alloc(need));
+      s.pinned_tokens_cap = need;
+    }
+    std::memcpy(s.pinned_tokens, s.tokens.data(), need);
+  }
   s.finalized = true;
   s.ever_finalized = true;
+}
+
+const int32_t* Store::pinned_tokens(const std::string& sid, int64_t* n_out) const {
+  std::lock_guard<std::mutex> lk(mu_);
+  const Session& s = session_locked(sid);
+  if (!s.finalized) fail(HC_EINCOMPLETE, "session incomplete (not finalized): " + sid);
+  if (n_out) *n_out = int64_t(s.tokens.size());
+  return s.pinned_tokens;
 }
 
 hc_manifest Store::open(const std::string& sid) const {

@@ -72,6 +72,8 @@ struct Session {
   int n_layers = 0, d_hidden = 0, d_kv = 0, elem_bytes = 2, dtype = HC_DTYPE_BF16;
   hc_plan plan{};
   std::vector<int32_t> tokens;
+  int32_t* pinned_tokens = nullptr;  // page-locked copy made at finalize (restore H2D)
+  size_t pinned_tokens_cap = 0;
   std::map<std::pair<int, int>, LayerStream> streams;  // (layer, kind)
   bool finalized = false;
   bool ever_finalized = false;
@@ -105,6 +107,9 @@ class Store {
   hc_manifest open(const std::string& sid) const;
   bool layer_info(const std::string& sid, int layer, int kind, int* n_chunks, int* n_tokens) const;
   std::vector<int32_t> tokens(const std::string& sid) const;
+  // Page-locked token ids of a finalized session (valid until the next
+  // reopen/finalize); n_out = count.
+  const int32_t* pinned_tokens(const std::string& sid, int64_t* n_out) const;
   // Gather plan for tokens [b, e) of (sid, layer, kind) into a dst buffer that
   // starts at token b. Requires a finalized session; b chunk aligned.
   std::vector<CopySeg> gather_plan(const std::string& sid, int layer, int kind, int b, int e,
