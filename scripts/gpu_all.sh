@@ -1,4 +1,3 @@
-# full GPU check: all gpu tests, then a short bench run
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -40
-timeout 600 python bench.py --steps 5 --warmup 3 2>&1 | tail -5
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -5
+timeout 300 torchrun --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | cut -c1-400
