@@ -76,7 +76,7 @@ EpiArgs epi_for(const hc_weights* w, const float* colsum, const float* mean, con
 }
 
 void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t n_rows,
-                  const KvOut& out, cudaStream_t stream) {
+                  const KvOut& out, cudaStream_t stream, const float* pre_stats) {
   if (layer < 0 || layer >= w->cfg.n_layers) fail(HC_EINVAL, "project: layer out of range");
   const auto& L = w->layers[size_t(layer)];
   if (!L.ready) fail(HC_EINVAL, "project: layer weights not set");
@@ -88,17 +88,18 @@ void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t 
   const int N = 2 * w->d_kv;
   if (w->cfg.rope_enabled && !out.cu_seqlens && int64_t(out.start_pos) + n_rows > w->rope_rows)
     fail(HC_EINVAL, "project: positions exceed max_seq");
-  StreamScratch stats(w->cfg.norm_enabled ? size_t(n_rows) * 2 * sizeof(float) : 0, stream);
-  float* mean = static_cast<float*>(stats.ptr);
-  float* rstd = mean ? mean + n_rows : nullptr;
-  if (w->cfg.norm_enabled)
-    HC_CUDA(launch_row_stats(d_hidden, n_rows, d, d, true, mean, rstd, stream));
+  const bool need = w->cfg.norm_enabled && !pre_stats;
+  StreamScratch stats(need ? size_t(n_rows) * 2 * sizeof(float) : 0, stream);
+  const float* mean = need ? static_cast<float*>(stats.ptr) : pre_stats;
+  const float* rstd = mean ? mean + n_rows : nullptr;
+  if (need)
+    HC_CUDA(launch_row_stats(d_hidden, n_rows, d, d, true, static_cast<float*>(stats.ptr),
+                             static_cast<float*>(stats.ptr) + n_rows, stream));
   CUtensorMap tmA;
   if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2, 128))
     fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the hidden-state operand");
   const int sms = device_sm_count(w->device);
-  const int64_t tiles256 = ((n_rows + 127) / 128) * ((N + 255) / 256);
-  const int bn = tiles256 >= sms ? 256 : 128;
+  const int bn = gemm_pick_bn(n_rows, N, sms);
   HC_CUDA(launch_restore_kv(tmA, bn == 256 ? L.tm256 : L.tm128, bn, int(n_rows), N, d, true, out,
                             epi_for(w, L.colsum, mean, rstd), sms, stream));
 }
@@ -373,8 +374,7 @@ hc_status hc_bench_project(const hc_weights* w, int32_t layer, const void* d_hid
     if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2, 128))
       fail(HC_ECUDA, "cuTensorMapEncodeTiled failed");
     const int sms = device_sm_count(w->device);
-    const int64_t tiles256 = ((n_rows + 127) / 128) * ((N + 255) / 256);
-    const int bn = tiles256 >= sms ? 256 : 128;
+    const int bn = gemm_pick_bn(n_rows, N, sms);
     std::vector<cudaEvent_t> ev(size_t(3 * iters));
     for (auto& e : ev) HC_CUDA(cudaEventCreate(&e));
     for (int i = 0; i < iters; ++i) {

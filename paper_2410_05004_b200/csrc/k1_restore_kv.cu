@@ -19,6 +19,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "kernels.h"
 #include "sm100.cuh"
 
@@ -146,6 +148,64 @@ __device__ __forceinline__ void epilogue_chunk_dense(float (&f)[32], int mode, i
                        pack_bf16(f[8 * i + 4], f[8 * i + 5]), pack_bf16(f[8 * i + 6], f[8 * i + 7]));
 }
 
+// Epilogue of one accumulator tile for one thread (= one TMEM lane = one
+// output row): per-row metadata, then BN/32 chunks of tcgen05.ld + math +
+// stores. Shared by the single-CTA and the CTA-pair kernels.
+template <int BN, int MODE>
+__device__ __forceinline__ void epilogue_tile(int row, int n_blk, int M, int N, const KvOut& out,
+                                              const GemmOut& gout, const EpiArgs& epi,
+                                              uint32_t tbase, int lane) {
+  (void)lane;
+  const bool row_ok = row < M;
+  // per-row metadata: output rows (dense or paged), LN stats, RoPE position
+  float mean = 0.f, rstd = 1.f;
+  int pos = out.start_pos;
+  char* krow = nullptr;
+  char* vrow = nullptr;
+  if (row_ok && MODE == kEpiKv) {
+    int seq = 0, local = row;
+    if (out.cu_seqlens) {
+      int lo = 0, hi = out.n_seqs - 1;
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (__ldg(out.cu_seqlens + mid) <= row) lo = mid;
+        else hi = mid - 1;
+      }
+      seq = lo;
+      local = row - __ldg(out.cu_seqlens + seq);
+    }
+    pos = out.start_pos + local;
+    int64_t orow;
+    if (out.page_table) {
+      int page = __ldg(out.page_table + int64_t(seq) * out.table_stride + pos / out.page_size);
+      orow = int64_t(page) * out.page_size + pos % out.page_size;
+    } else {
+      orow = row;
+    }
+    const size_t esz = out.out_f32 ? 4 : 2;
+    krow = static_cast<char*>(out.k_base) + size_t(orow) * out.d_kv * esz;
+    vrow = static_cast<char*>(out.v_base) + size_t(orow) * out.d_kv * esz;
+  }
+  if (row_ok && epi.row_mean) {
+    mean = __ldg(epi.row_mean + row);
+    rstd = __ldg(epi.row_rstd + row);
+  }
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t v[32];
+    tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), v);
+    tmem_wait_ld();
+    const int col0 = n_blk * BN + c * 32;
+    if (row_ok && col0 < N) {
+      float f[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+      if (MODE == kEpiKv) epilogue_chunk(f, col0, out, epi, mean, rstd, pos, krow, vrow);
+      else epilogue_chunk_dense(f, MODE, row, col0, gout, epi, mean, rstd);
+    }
+  }
+}
+
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -249,57 +309,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int m_blk, n_blk;
       tile_coords(tile, num_m, num_n, m_blk, n_blk);
       const int row = m_blk * kBM + q * 32 + lane;
-      const bool row_ok = row < M;
-      // per-row metadata: output rows (dense or paged), LN stats, RoPE position
-      float mean = 0.f, rstd = 1.f;
-      int pos = out.start_pos;
-      char* krow = nullptr;
-      char* vrow = nullptr;
-      if (row_ok && MODE == kEpiKv) {
-        int seq = 0, local = row;
-        if (out.cu_seqlens) {
-          int lo = 0, hi = out.n_seqs - 1;
-          while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (__ldg(out.cu_seqlens + mid) <= row) lo = mid;
-            else hi = mid - 1;
-          }
-          seq = lo;
-          local = row - __ldg(out.cu_seqlens + seq);
-        }
-        pos = out.start_pos + local;
-        int64_t orow;
-        if (out.page_table) {
-          int page = __ldg(out.page_table + int64_t(seq) * out.table_stride + pos / out.page_size);
-          orow = int64_t(page) * out.page_size + pos % out.page_size;
-        } else {
-          orow = row;
-        }
-        const size_t esz = out.out_f32 ? 4 : 2;
-        krow = static_cast<char*>(out.k_base) + size_t(orow) * out.d_kv * esz;
-        vrow = static_cast<char*>(out.v_base) + size_t(orow) * out.d_kv * esz;
-      }
-      if (row_ok && epi.row_mean) {
-        mean = __ldg(epi.row_mean + row);
-        rstd = __ldg(epi.row_rstd + row);
-      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), v);
-        tmem_wait_ld();
-        const int col0 = n_blk * BN + c * 32;
-        if (row_ok && col0 < N) {
-          float f[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-          if (MODE == kEpiKv) epilogue_chunk(f, col0, out, epi, mean, rstd, pos, krow, vrow);
-          else epilogue_chunk_dense(f, MODE, row, col0, gout, epi, mean, rstd);
-        }
-      }
+      epilogue_tile<BN, MODE>(row, n_blk, M, N, out, gout, epi,
+                              tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN), lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -311,6 +324,150 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+}
+
+
+// ------------------------------------------------------------ CTA-pair variant
+// cta_group::2: a cluster of two CTAs (one per SM of a TPC) computes a
+// 256 x 256 tile with M=256 MMAs issued by the leader. Each CTA loads its own
+// 128 rows of A and 128 of the 256 B rows, so per SM the operand traffic per
+// k-block drops from 48 KB (128x256 single-CTA tile) to 32 KB while the MMA
+// work per SM is unchanged. Accumulator rows 0-127 live in the leader's TMEM,
+// 128-255 in the peer's; both run the same epilogue on their own lanes.
+constexpr int kPairStages = 6;
+constexpr uint32_t kPairHalfBytes = 128 * kBK * 2;             // 16 KB: A half or B half
+constexpr uint32_t kPairStageBytes = 2 * kPairHalfBytes;       // per CTA per stage
+constexpr size_t kPairSmem = size_t(kPairStages) * kPairStageBytes + 1024 + 1024;
+
+__device__ __forceinline__ void tile_coords_pair(int tile, int num_m, int num_n, int& m_blk,
+                                                 int& n_blk) {
+  tile_coords(tile, num_m, num_n, m_blk, n_blk);
+}
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
+                        GemmOut gout, EpiArgs epi, uint32_t idesc) {
+  constexpr int BN = 256, S = kPairStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * kPairHalfBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * kPairHalfBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = int(blockIdx.x >> 1), n_clusters = int(gridDim.x >> 1);
+  const int num_m = (M + 255) / 256;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs; bytes counted on the leader) ----
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+        int m_blk, n_blk;
+        tile_coords_pair(tile, num_m, num_n, m_blk, n_blk);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+          tma_load_2d_pair(sA + stage * kPairHalfBytes, &tmA, &full[stage], kb * kBK,
+                           m_blk * 256 + int(rank) * 128);
+          tma_load_2d_pair(sB + stage * kPairHalfBytes, &tmB, &full[stage], kb * kBK,
+                           n_blk * BN + int(rank) * 128);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA, one thread) ----------------
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kPairHalfBytes));
+          const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * kPairHalfBytes));
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_f16_pair(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
+                          (kb | k) != 0 ? 1u : 0u);
+          umma_commit_pair(&empty[stage], 0x3);  // frees the slot in both CTAs
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs, their own 128 TMEM lanes) --------
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+      int m_blk, n_blk;
+      tile_coords_pair(tile, num_m, num_n, m_blk, n_blk);
+      const int row = m_blk * 256 + int(rank) * 128 + q * 32 + lane;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      epilogue_tile<BN, MODE>(row, n_blk, M, N, out, gout, epi,
+                              tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN), lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
   }
 }
 
@@ -328,39 +485,54 @@ __device__ __forceinline__ void load8(const T* p, float (&x)[8]) {
   }
 }
 
+// One pass: sum and sum of squares in double (bf16 inputs have 8-bit
+// mantissas, so the double sums are exact or within 1 ulp of double and
+// var = E[x^2] - mean^2 matches the reference's two-pass double variance,
+// model.cpp:43-61, to far below float resolution). 16-byte loads, four in
+// flight per lane.
 template <typename T>
-__global__ void row_stats_kernel(const T* __restrict__ x, int64_t rows, int cols,
-                                 int64_t row_stride, float* __restrict__ mean_out,
-                                 float* __restrict__ rstd_out) {
+__global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ x, int64_t rows,
+                                                        int cols, int64_t row_stride,
+                                                        float* __restrict__ mean_out,
+                                                        float* __restrict__ rstd_out) {
   const int warps = blockDim.x >> 5;
   const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
   const T* r = x + row * row_stride;
-  double s = 0.0;
-  for (int c = lane * 8; c < cols; c += 256) {
-    float v[8];
-    load8(r + c, v);
+  double s = 0.0, q = 0.0;
+  int c = lane * 8;
+  for (; c + 3 * 256 < cols; c += 4 * 256) {
+    float v[4][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s += double(v[i]);
+    for (int u = 0; u < 4; ++u) load8(r + c + u * 256, v[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s += double(v[u][i]);
+        q += double(v[u][i]) * double(v[u][i]);
+      }
+    }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const double mean = s / double(cols);
-  double q = 0.0;
-  for (int c = lane * 8; c < cols; c += 256) {
+  for (; c < cols; c += 256) {
     float v[8];
     load8(r + c, v);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      double d = double(v[i]) - mean;
-      q += d * d;
+      s += double(v[i]);
+      q += double(v[i]) * double(v[i]);
     }
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
   if (lane == 0) {
-    double var = q / double(cols);
+    const double mean = s / double(cols);
+    double var = q / double(cols) - mean * mean;
+    if (var < 0) var = 0;
     mean_out[row] = float(mean);
     rstd_out[row] = 1.0f / sqrtf(float(var) + 1e-5f);
   }
@@ -441,6 +613,38 @@ __global__ void kv_scatter_kernel(const uint4* __restrict__ rows, int64_t n_rows
 
 }  // namespace
 
+template <int MODE>
+cudaError_t launch_pair(const CUtensorMap& tmA, const CUtensorMap& tmB128, int M, int N, int K,
+                        bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
+                        int num_sms, cudaStream_t stream) {
+  const uint32_t idesc = umma_idesc_f16(256, 256, bf16_in);
+  const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  int grid = 2 * (tiles < num_sms / 2 ? tiles : num_sms / 2);
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_pair_kernel<MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kPairSmem));
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  tc_gemm_pair_kernel<MODE><<<grid, kThreads, kPairSmem, stream>>>(tmA, tmB128, M, N, K, out, g,
+                                                                   epi, idesc);
+  return cudaGetLastError();
+}
+
+// Pair kernel when the problem has enough 256x256 tiles to fill the SM pairs
+// (and HC_K1_PAIR != 0); B must then be described with a 128-row box.
+bool use_pair(int M, int N, int num_sms) {
+  static const int enabled = [] {
+    const char* e = getenv("HC_K1_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  return enabled && M >= 256 && ((M + 255) / 256) * ((N + 255) / 256) >= num_sms / 2;
+}
+
 template <int BN, int MODE>
 cudaError_t launch_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
                       bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
@@ -463,11 +667,18 @@ cudaError_t launch_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int
   return cudaGetLastError();
 }
 
+int gemm_pick_bn(int64_t M, int N, int num_sms) {
+  if (use_pair(int(M), N, num_sms)) return 128;  // pair kernel: B box of 128 rows
+  return ((M + kBM - 1) / kBM) * ((N + 255) / 256) >= num_sms ? 256 : 128;
+}
+
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
                               int num_sms, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   GemmOut g;
+  if (bn == 128 && use_pair(M, N, num_sms))  // tmB has the 128-row box the pair needs
+    return launch_pair<kEpiKv>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
   return bn == 256 ? launch_tc<256, kEpiKv>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream)
                    : launch_tc<128, kEpiKv>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
 }
@@ -477,6 +688,10 @@ cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, in
                               int num_sms, cudaStream_t stream) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   KvOut o;
+  if (bn == 128 && use_pair(M, N, num_sms))
+    return mode == kEpiResid
+               ? launch_pair<kEpiResid>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream)
+               : launch_pair<kEpiGelu>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream);
   if (mode == kEpiResid)
     return bn == 256 ? launch_tc<256, kEpiResid>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream)
                      : launch_tc<128, kEpiResid>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream);

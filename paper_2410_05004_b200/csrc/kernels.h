@@ -52,6 +52,10 @@ struct GemmOut {
 bool make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows,
                       uint64_t row_stride_bytes, uint32_t box_rows);
 
+// Box rows of the B tensor map for an M x N GEMM (128 or 256). 128 selects the
+// CTA-pair kernel when the problem fills the SM pairs.
+int gemm_pick_bn(int64_t M, int N, int num_sms);
+
 // K1: KV[M x N] = epilogue(A[M x K] * B[N x K]^T), N = 2*d_kv (K half, V half).
 // A is described by tmA (box rows 128), B by tmB (box rows 256 or 128 = bn).
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,

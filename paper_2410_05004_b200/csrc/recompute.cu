@@ -30,9 +30,7 @@ CUtensorMap tmap(const void* base, int k, int64_t rows, int box_rows) {
   return m;
 }
 
-int pick_bn(int64_t M, int N, int sms) {
-  return ((M + 127) / 128) * ((N + 255) / 256) >= sms ? 256 : 128;
-}
+int pick_bn(int64_t M, int N, int sms) { return gemm_pick_bn(M, N, sms); }
 
 }  // namespace
 

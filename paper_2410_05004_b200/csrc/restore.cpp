@@ -287,8 +287,71 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
   HC_CUDA(cudaEventRecord(t0, stream));
   HC_CUDA(cudaStreamWaitEvent(eng.copy, t0, 0));  // IO lane starts with the restore
 
+  // IO lane: every fetch in compute order. A fetch whose staging slot is
+  // still in use waits (cudaStreamWaitEvent) for the consume event of the
+  // slot's previous user, so fetches are enqueued as soon as that event
+  // exists: the first ring-full of fetches goes out before the RECOMPUTE
+  // prefix is even enqueued, the rest right after the compute that frees
+  // their slot.
+  struct Fetch {
+    LayerJob job;
+    bool hid;
+    int slot;
+    bool reuses_slot;  // an earlier fetch of this kind used the slot
+    uint8_t* buf;
+    std::vector<CopySeg> segs;
+    cudaEvent_t fetched = nullptr;
+  };
+  std::vector<Fetch> fetches;
+  int ih = 0, ikv = 0;
+  for (const auto& j : order) {
+    if (j.method == HC_METHOD_RECOMPUTE) continue;
+    Fetch f;
+    f.job = j;
+    f.hid = j.method == HC_METHOD_HIDDEN;
+    const int kind_idx = f.hid ? ih++ : ikv++;
+    f.slot = kind_idx % (f.hid ? nbuf_h : nbuf_kv);
+    f.reuses_slot = kind_idx >= (f.hid ? nbuf_h : nbuf_kv);
+    f.buf = static_cast<uint8_t*>(f.hid ? ring_h.ptr : ring_kv.ptr) +
+            (f.hid ? h_bytes : kv_bytes) * size_t(f.slot);
+    size_t got = 0;
+    f.segs = store.gather_plan(sid, j.layer, f.hid ? HC_STATE_HIDDEN : HC_STATE_KV, 0, -1,
+                               &got);  // HC_ENOENT if missing
+    if (got != (f.hid ? h_bytes : kv_bytes))
+      fail(HC_ERUNTIME, "restore: layer " + std::to_string(j.layer) + " has a short token count");
+    fetches.push_back(std::move(f));
+  }
+  std::vector<cudaEvent_t> consumed_h(size_t(nbuf_h), nullptr), consumed_kv(size_t(nbuf_kv), nullptr);
+  std::vector<cudaEvent_t> joins;
+  size_t next_fetch = 0;
+  auto issue_fetches = [&](size_t limit) {
+    // issue fetches in order while their slot's previous consumer is enqueued
+    while (next_fetch < fetches.size() && next_fetch < limit) {
+      Fetch& f = fetches[next_fetch];
+      auto& consumed = f.hid ? consumed_h : consumed_kv;
+      // slot reuse: wait for the consumer of the slot's previous fetch; stop
+      // if that consumer is not enqueued yet
+      if (f.reuses_slot && !consumed[size_t(f.slot)]) return;
+      if (f.reuses_slot) HC_CUDA(cudaStreamWaitEvent(eng.copy, consumed[size_t(f.slot)], 0));
+      cudaEvent_t fs = timed ? evp.get() : nullptr;
+      if (fs) HC_CUDA(cudaEventRecord(fs, eng.copy));
+      issue_gather(f.segs, f.buf, eng, joins, &EventPool::make, &evp);
+      f.fetched = evp.get();
+      HC_CUDA(cudaEventRecord(f.fetched, eng.copy));
+      if (timed)
+        ops.push_back({HC_LANE_IO, f.job.layer, f.hid ? HC_EV_FETCH_HIDDEN : HC_EV_FETCH_KV, fs,
+                       f.fetched});
+      // the slot's consume event now belongs to this fetch's consumer
+      consumed[size_t(f.slot)] = nullptr;
+      ++next_fetch;
+    }
+  };
+  // two fetches get the copy engine going; the RECOMPUTE prefix launches are
+  // enqueued next so the compute lane starts at once; then the rest
+  issue_fetches(2);
+
   // RECOMPUTE prefix first on the compute lane (restore.cpp:177-182); the IO
-  // lane below prefetches hidden layers meanwhile.
+  // lane prefetches hidden layers meanwhile.
   if (n_re) {
     std::vector<cudaEvent_t> marks;
     prefill_layers_impl(w, static_cast<const int32_t*>(d_tok.ptr), n, 0, n_re, pages,
@@ -301,47 +364,27 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
                         });
   }
 
-  // IO lane: all fetches in compute order; compute lane consumes in order.
-  std::vector<cudaEvent_t> consumed_h(size_t(nbuf_h), nullptr), consumed_kv(size_t(nbuf_kv), nullptr);
-  std::vector<cudaEvent_t> joins;
-  int ih = 0, ikv = 0;
-  for (const auto& j : order) {
-    if (j.method == HC_METHOD_RECOMPUTE) continue;
-    const bool hid = j.method == HC_METHOD_HIDDEN;
-    const int kind = hid ? HC_STATE_HIDDEN : HC_STATE_KV;
-    const int slot = hid ? ih % nbuf_h : ikv % nbuf_kv;
-    auto& consumed = hid ? consumed_h : consumed_kv;
-    uint8_t* buf = static_cast<uint8_t*>(hid ? ring_h.ptr : ring_kv.ptr) +
-                   (hid ? h_bytes : kv_bytes) * size_t(slot);
-    size_t got = 0;
-    auto segs = store.gather_plan(sid, j.layer, kind, 0, -1, &got);  // HC_ENOENT if missing
-    if (got != (hid ? h_bytes : kv_bytes))
-      fail(HC_ERUNTIME, "restore: layer " + std::to_string(j.layer) + " has a short token count");
-    // staging bound: wait until the previous user of this buffer is consumed
-    if (consumed[size_t(slot)]) HC_CUDA(cudaStreamWaitEvent(eng.copy, consumed[size_t(slot)], 0));
-    cudaEvent_t fs = timed ? evp.get() : nullptr;
-    if (fs) HC_CUDA(cudaEventRecord(fs, eng.copy));
-    issue_gather(segs, buf, eng, joins, &EventPool::make, &evp);
-    cudaEvent_t fetched = evp.get();
-    HC_CUDA(cudaEventRecord(fetched, eng.copy));
-    if (timed) ops.push_back({HC_LANE_IO, j.layer, hid ? HC_EV_FETCH_HIDDEN : HC_EV_FETCH_KV, fs, fetched});
-
-    // compute lane
-    HC_CUDA(cudaStreamWaitEvent(stream, fetched, 0));
+  issue_fetches(fetches.size());
+  // compute lane consumes in order
+  for (size_t i = 0; i < fetches.size(); ++i) {
+    issue_fetches(fetches.size());
+    Fetch& f = fetches[i];
+    if (!f.fetched) fail(HC_ERUNTIME, "restore: internal fetch ordering error");
+    HC_CUDA(cudaStreamWaitEvent(stream, f.fetched, 0));
     cudaEvent_t cs = timed ? evp.get() : nullptr;
     if (cs) HC_CUDA(cudaEventRecord(cs, stream));
-    KvOut out = kv_out_pages(pages, j.layer, d_page_table, 0, nullptr, 1);
-    if (hid) {
-      project_rows(w, j.layer, buf, n, out, stream);
+    KvOut out = kv_out_pages(pages, f.job.layer, d_page_table, 0, nullptr, 1);
+    if (f.hid) {
+      project_rows(w, f.job.layer, f.buf, n, out, stream);
     } else {
-      HC_CUDA(launch_kv_scatter(buf, n, out, stream));
+      HC_CUDA(launch_kv_scatter(f.buf, n, out, stream));
     }
     cudaEvent_t done = evp.get();
     HC_CUDA(cudaEventRecord(done, stream));
-    consumed[size_t(slot)] = done;
-    if (timed) ops.push_back({HC_LANE_COMPUTE, j.layer, hid ? HC_EV_PROJECT : HC_EV_SCATTER, cs, done});
-    (hid ? ih : ikv)++;
+    (f.hid ? consumed_h : consumed_kv)[size_t(f.slot)] = done;
+    if (timed) ops.push_back({HC_LANE_COMPUTE, f.job.layer, f.hid ? HC_EV_PROJECT : HC_EV_SCATTER, cs, done});
   }
+  issue_fetches(fetches.size());
   // join the IO lane into the caller stream before the ring is released
   cudaEvent_t io_done = evp.get();
   HC_CUDA(cudaEventRecord(io_done, eng.copy));
@@ -471,10 +514,22 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
       fail(HC_EINVAL, "restore_resident: null argument");
     validate_pages(w, pages, w->d_kv);
     DeviceGuard dg(w->device);
-    for (int l = 0; l < w->cfg.n_layers; ++l)
+    cudaStream_t s = as_stream(stream);
+    const int L = w->cfg.n_layers, d = w->cfg.d_hidden;
+    // every layer's rows are resident: all row statistics first (one buffer),
+    // then the K1 launches back to back
+    const bool norm = w->cfg.norm_enabled != 0;
+    StreamScratch stats(norm ? size_t(L) * size_t(n_rows) * 2 * sizeof(float) : 0, s);
+    float* st = static_cast<float*>(stats.ptr);
+    if (norm)
+      for (int l = 0; l < L; ++l)
+        HC_CUDA(launch_row_stats(d_hidden_layers[l], n_rows, d, d, true,
+                                 st + size_t(l) * 2 * size_t(n_rows),
+                                 st + size_t(l) * 2 * size_t(n_rows) + n_rows, s));
+    for (int l = 0; l < L; ++l)
       project_rows(w, l, d_hidden_layers[l], n_rows,
-                   kv_out_pages(pages, l, d_page_table, table_stride, d_cu_seqlens, n_seqs),
-                   as_stream(stream));
+                   kv_out_pages(pages, l, d_page_table, table_stride, d_cu_seqlens, n_seqs), s,
+                   norm ? st + size_t(l) * 2 * size_t(n_rows) : nullptr);
   });
 }
 
@@ -546,12 +601,23 @@ hc_status hc_profile(const hc_weights* w, int32_t n_tokens, hc_timings* out) {
     o.k_base = k;
     o.v_base = v;
     o.d_kv = w->d_kv;
-    // back-to-back launches, as in the restore pipeline (host setup overlapped)
+    // back-to-back launches, as in the restore pipeline (host setup
+    // overlapped), with a concurrent pinned H2D stream on the copy engine like
+    // the IO lane of a real restore (DMA traffic slows K1 by ~10%)
     Ev a, b;
     float best = 1e30f;
     const int reps = 8;
+    cudaStream_t dma;
+    HC_CUDA(cudaStreamCreateWithFlags(&dma, cudaStreamNonBlocking));
+    const size_t dma_bytes = size_t(64) << 20;
+    void* dma_h = nullptr;
+    void* dma_d = nullptr;
+    HC_CUDA(cudaHostAlloc(&dma_h, dma_bytes, cudaHostAllocPortable));
+    HC_CUDA(cudaMalloc(&dma_d, dma_bytes));
     project_rows(w, layer, h, n_tokens, o, nullptr);  // warm-up
     for (int r = 0; r < 3; ++r) {
+      for (int i = 0; i < 8; ++i)
+        HC_CUDA(cudaMemcpyAsync(dma_d, dma_h, dma_bytes, cudaMemcpyHostToDevice, dma));
       HC_CUDA(cudaEventRecord(a.e, nullptr));
       for (int i = 0; i < reps; ++i) project_rows(w, layer, h, n_tokens, o, nullptr);
       HC_CUDA(cudaEventRecord(b.e, nullptr));
@@ -559,13 +625,20 @@ hc_status hc_profile(const hc_weights* w, int32_t n_tokens, hc_timings* out) {
       float ms = 0;
       HC_CUDA(cudaEventElapsedTime(&ms, a.e, b.e));
       best = std::min(best, ms / reps);
+      HC_CUDA(cudaStreamSynchronize(dma));
     }
     out->c_h = best * 1e-3;
+    // c_token: one K6 layer when the full weights are present (same DMA load)
+    for (int i = 0; i < 64; ++i)
+      HC_CUDA(cudaMemcpyAsync(dma_d, dma_h, dma_bytes, cudaMemcpyHostToDevice, dma));
+    out->c_token = recompute_layer_seconds(w, n_tokens);
+    HC_CUDA(cudaStreamSynchronize(dma));
+    cudaStreamDestroy(dma);
+    cudaFreeHost(dma_h);
+    cudaFree(dma_d);
     cudaFree(h);
     cudaFree(k);
     cudaFree(v);
-    // c_token: one K6 layer when the full weights are present
-    out->c_token = recompute_layer_seconds(w, n_tokens);
     if (out->c_token <= 0) {
       // analytic fallback from the reference cost model (cost_model.cpp:45-51):
       // full layer / projection FLOP ratio applied to the measured K1 time
