@@ -1,0 +1,404 @@
+// attention_tc.cu -- K6 causal prefill attention on tcgen05 (sm_100a).
+//
+// attention_forward (proj/src/model.cpp:237-288) per (query tile of 128,
+// head): softmax(Q K^T / sqrt(dh)) V over the paged KV cache, causal.
+//   warp 0      TMA: Q tile once; K and V tiles (128 keys) into a 2-stage
+//               ring, gathered page by page through the page table.
+//   warp 1      TMEM owner + single-thread MMA issuer:
+//                 S_j = Q K_j^T   (M=128, N=128, K=dh)   -> TMEM S[j%2]
+//                 O  += P_j V_j   (M=128, N=dh, K=128)   -> TMEM O
+//               QK_{j+1} is issued before PV_j so the tensor core works on
+//               the next tile while the softmax warps handle this one.
+//   warps 2-9   softmax, each query row split over two threads (one per
+//               64-key half, warps w and w+4 share a TMEM lane quadrant and
+//               exchange only the row max through smem): tcgen05.ld of S,
+//               scale + causal mask, online softmax in fp32 with exp2 and a
+//               lazily updated row max (P <= 2^8, O rescaled in TMEM only
+//               when the max grows by more than 8 in log2 units), bf16 P
+//               written into the 128-byte-swizzled K-major layout the MMA
+//               reads; finally O / l -> bf16 rows in global memory.
+// V is consumed as an MN-major B operand straight from its TMA layout.
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace hc {
+
+namespace {
+
+constexpr int kAttnM = 128;  // queries per CTA
+constexpr int kAttnN = 128;  // keys per tile
+constexpr int kAttnStages = 2;
+constexpr int kAttnThreads = 320;  // TMA, MMA, 8 softmax warps (2 per TMEM lane quadrant)
+
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// MN-major (N contiguous) 128-byte-swizzled operand: 64 N-elements per
+// 128-byte row, K rows at 128 B within 8-row atoms; LBO = stride between
+// 64-element N blocks, SBO = stride between 8-row K groups.
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo_bytes) {
+  return static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4) |
+         (static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+struct AttnArgs {
+  int n;
+  int n_heads;
+  int group;  // q heads per KV head
+  int page_size;
+  int box_rows;  // rows per K/V TMA box (min(page_size, 128))
+  const int32_t* page_table;  // nullptr: dense rows
+  __nv_bfloat16* out;         // [n][n_heads*dh]
+  float scale_log2;
+};
+
+template <int DH>
+struct AttnCfg {
+  static constexpr uint32_t kQBytes = kAttnM * DH * 2;
+  static constexpr uint32_t kKVBytes = kAttnN * DH * 2;  // one of K or V per stage
+  static constexpr uint32_t kStageBytes = 2 * kKVBytes;
+  static constexpr uint32_t kPBytes = kAttnM * kAttnN * 2;
+  // (no alignment slack: the dynamic smem window starts 1 KB aligned; the
+  // kernel traps otherwise)
+  static constexpr size_t kSmem = size_t(kQBytes) + size_t(kAttnStages) * kStageBytes +
+                                  2 * size_t(kPBytes) + 512 /*bars*/ + 4 * kAttnM * 4 /*xmax*/;
+  static constexpr uint32_t kHalf = kAttnM * 64 * 2;  // one 64-column block of a 128-row tile
+};
+
+template <int DH>
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
+  using Cfg = AttnCfg<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if (smem_u32(smem_raw) & 1023) asm volatile("trap;");  // SW128 operands need 1 KB alignment
+  uint8_t* smem = smem_raw;
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + Cfg::kQBytes;  // stage s: K at s*kStageBytes, V at +kKVBytes
+  uint8_t* sP = sKV + kAttnStages * Cfg::kStageBytes;  // two P buffers (tile parity)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * Cfg::kPBytes);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;           // [stages] K tile landed
+  uint64_t* k_empty = k_full + kAttnStages;  // [stages] QK done with the K tile
+  uint64_t* v_full = k_empty + kAttnStages;  // [stages] V tile landed
+  uint64_t* v_empty = v_full + kAttnStages;  // [stages] PV done with the V tile
+  uint64_t* s_full = v_empty + kAttnStages;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* p_full = s_empty + 2;  // [2], per P buffer
+  uint64_t* o_done = p_full + 2;   // [2], PV_j commits to o_done[j & 1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  float* xmax = reinterpret_cast<float*>(bars + 32);  // past the barriers + TMEM slot  // [2 parity][2 halves][128 rows]
+  // end-of-loop partial sums go into P buffer 0 once every PV has completed
+  float* xsum = reinterpret_cast<float*>(sP);  // [2 halves][128 rows]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = int(gridDim.x) - 1 - int(blockIdx.x);  // heaviest causal tiles first
+  const int h = blockIdx.y, hk = h / a.group;
+  const int q0 = qt * kAttnM;
+  const int n_tiles = min(qt + 1, (a.n + kAttnN - 1) / kAttnN);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kAttnStages; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 8);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&p_full[b], 8);
+      mbar_init(&o_done[b], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_o = tmem + 256;  // O accumulator columns [256, 256+DH)
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, Cfg::kQBytes);
+      for (int hb = 0; hb < DH / 64; ++hb)
+        tma_load_2d(sQ + hb * Cfg::kHalf, &tmQ, q_full, h * DH + hb * 64, q0);
+      // K tiles are released by QK, V tiles only by PV: V loads lag K by one
+      // tile so a K load never waits behind a P V product
+      auto load_tile = [&](int j, bool is_v) {
+        const int st = j % kAttnStages;
+        uint64_t* full = is_v ? &v_full[st] : &k_full[st];
+        mbar_wait(is_v ? &v_empty[st] : &k_empty[st], ((j / kAttnStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(full, Cfg::kKVBytes);
+        uint8_t* dst = sKV + st * Cfg::kStageBytes + (is_v ? Cfg::kKVBytes : 0);
+        const CUtensorMap* map = is_v ? &tmV : &tmK;
+        for (int c = 0; c < kAttnN / a.box_rows; ++c) {
+          const int key0 = j * kAttnN + c * a.box_rows;
+          int row = key0;
+          if (a.page_table) {
+            const int last = (a.n - 1) / a.page_size;  // keys past n: any valid page (masked)
+            const int pg = min(key0 / a.page_size, last);
+            row = __ldg(a.page_table + pg) * a.page_size + key0 % a.page_size;
+          }
+          for (int hb = 0; hb < DH / 64; ++hb)
+            tma_load_2d(dst + hb * Cfg::kHalf + c * a.box_rows * 128, map, full,
+                        hk * DH + hb * 64, row);
+        }
+      };
+      for (int j = 0; j <= n_tiles; ++j) {
+        if (j < n_tiles) load_tile(j, false);
+        if (j >= 1) load_tile(j - 1, true);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA
+    if (lane == 0) {
+      const uint32_t id_qk = umma_idesc_f16(kAttnM, kAttnN, true);
+      const uint32_t id_pv = umma_idesc_f16(kAttnM, DH, true) | (1u << 16);  // B MN-major
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto issue_pv = [&](int j) {
+        const int st = j % kAttnStages, pb = j & 1;
+        mbar_wait(&p_full[pb], (j >> 1) & 1);  // softmax wrote P_j (and rescaled O)
+        tc_fence_after();
+        mbar_wait(&v_full[st], (j / kAttnStages) & 1);
+        tc_fence_after();
+        const uint32_t sV = smem_u32(sKV + st * Cfg::kStageBytes + Cfg::kKVBytes);
+        const uint32_t sPj = smem_u32(sP + pb * Cfg::kPBytes);
+        for (int kk = 0; kk < kAttnN / 16; ++kk) {
+          const uint64_t pd = umma_desc_sw128(sPj + uint32_t((kk >> 2) * Cfg::kHalf) +
+                                              uint32_t((kk & 3) * 32));
+          const uint64_t vd = umma_desc_sw128_mn(sV + uint32_t(kk * 2048), Cfg::kHalf);
+          umma_f16(t_o, pd, vd, id_pv, (j | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(&o_done[pb]);
+        umma_commit(&v_empty[st]);
+      };
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j % kAttnStages, sb = j & 1;
+        mbar_wait(&k_full[st], (j / kAttnStages) & 1);
+        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(sKV + st * Cfg::kStageBytes);
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = uint32_t((kk >> 2) * Cfg::kHalf + (kk & 3) * 32);
+          umma_f16(tmem + uint32_t(sb * 128), umma_desc_sw128(smem_u32(sQ) + off),
+                   umma_desc_sw128(sK + off), id_qk, kk != 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[sb]);
+        umma_commit(&k_empty[st]);
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_tiles - 1);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    const int q = warp & 3;             // TMEM lane quadrant (rows q*32 .. q*32+31)
+    const int half = (warp - 2) >> 2;   // key half (P / S columns) and O column half
+    const int rloc = q * 32 + lane;     // row within the tile
+    const int row = q0 + rloc;
+    const uint32_t lane_off = uint32_t(q * 32) << 16;
+    const uint32_t bar_id = 1 + uint32_t(q);  // named barrier of the two warps of a quadrant
+    float m_run = -INFINITY, l_run = 0.f;
+    const int r8 = rloc & 7;
+    const int prow_off = rloc * 128 + half * Cfg::kHalf;  // my 64-key block of the P row
+    auto wait_pv = [&](int k) {
+      mbar_wait(&o_done[k & 1], (k >> 1) & 1);
+      tc_fence_after();
+    };
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    for (int j = 0; j < n_tiles; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      float s[64];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + uint32_t(sb * 128 + half * 64 + c * 32), v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[sb]);
+      // causal / length mask on the diagonal tile only, raw-score max
+      const int key0 = j * kAttnN + half * 64;
+      const bool diag = key0 + 63 > row || key0 + 64 > a.n;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        if (diag && (key0 + i > row || key0 + i >= a.n)) s[i] = -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      // row max across the two halves (smem, double-buffered by tile parity)
+      xmax[(sb * 2 + half) * kAttnM + rloc] = mx;
+      pair_sync();
+      mx = fmaxf(mx, xmax[(sb * 2 + (half ^ 1)) * kAttnM + rloc]) * a.scale_log2;
+      // lazy max: keep m_run unless the tile max exceeds it by > 8 (P <= 2^8)
+      const bool rescale = mx > m_run + 8.0f;
+      const float m_use = rescale ? mx : m_run;
+      uint32_t pk[32];
+      float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) {
+        const float p0 = ex2_approx(fmaf(s[i], a.scale_log2, -m_use));
+        const float p1 = ex2_approx(fmaf(s[i + 1], a.scale_log2, -m_use));
+        sum0 += p0;
+        sum1 += p1;
+        pk[i >> 1] = pack_bf16x2(p0, p1);
+      }
+      // P buffer (j & 1) is free once PV_{j-2} is done; an O rescale needs
+      // PV_{j-1} done (no PV in flight while O is rewritten)
+      if (rescale && j >= 1) wait_pv(j - 1);
+      else if (j >= 2) wait_pv(j - 2);
+      if (rescale) {
+        const float corr = ex2_approx(m_run - m_use);
+        l_run *= corr;
+        if (j > 0) {
+#pragma unroll 1
+          for (int c = 0; c < DH / 64; ++c) {
+            uint32_t v[32];
+            const uint32_t ta = t_o + lane_off + uint32_t(half * (DH / 2) + c * 32);
+            tmem_ld_32x32b_x32(ta, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st_32x32b_x32(ta, v);
+          }
+          tmem_wait_st();
+        }
+        m_run = m_use;
+      }
+      l_run += sum0 + sum1;
+      uint8_t* prow = sP + (j & 1) * Cfg::kPBytes + prow_off;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch)
+        *reinterpret_cast<uint4*>(prow + ((ch ^ r8) << 4)) =
+            make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+      fence_proxy_async_smem();  // generic-proxy P writes -> tensor core (async proxy)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+    }
+    wait_pv(n_tiles - 1);  // every PV done: the P buffers are free
+    xsum[half * kAttnM + rloc] = l_run;
+    pair_sync();
+    const float inv = 1.0f / (l_run + xsum[(half ^ 1) * kAttnM + rloc]);
+    __nv_bfloat16* dst = a.out + size_t(row) * size_t(a.n_heads * DH) + size_t(h) * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 64; ++c) {
+      const int col = half * (DH / 2) + c * 32;
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(t_o + lane_off + uint32_t(col), v);
+      tmem_wait_ld();
+      if (row < a.n) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          d4[i] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * i + 0]) * inv, __uint_as_float(v[8 * i + 1]) * inv),
+                             pack_bf16x2(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv),
+                             pack_bf16x2(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv),
+                             pack_bf16x2(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int DH>
+cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, const KvOut& kv,
+                           int64_t kv_rows, void* out, cudaStream_t stream) {
+  const int box_rows = kv.page_table ? (kv.page_size < kAttnN ? kv.page_size : kAttnN) : kAttnN;
+  CUtensorMap tq, tk, tv;
+  const uint64_t ldq = uint64_t(n_heads) * DH;
+  if (!make_tmap_kmajor(&tq, q, ldq, uint64_t(n), ldq * 2, kAttnM)) return cudaErrorInvalidValue;
+  // K/V maps cover the whole page pool (rows are gathered page by page) or,
+  // dense, the n rows (tiles past n are zero-filled by TMA and masked)
+  const uint64_t rows = kv.page_table ? uint64_t(kv_rows) : uint64_t(n);
+  if (!make_tmap_kmajor(&tk, kv.k_base, uint64_t(kv.d_kv), rows, uint64_t(kv.d_kv) * 2,
+                        uint32_t(box_rows)) ||
+      !make_tmap_kmajor(&tv, kv.v_base, uint64_t(kv.d_kv), rows, uint64_t(kv.d_kv) * 2,
+                        uint32_t(box_rows)))
+    return cudaErrorInvalidValue;
+  AttnArgs a;
+  a.n = n;
+  a.n_heads = n_heads;
+  a.group = n_heads / n_kv_heads;
+  a.page_size = kv.page_table ? kv.page_size : n;
+  a.box_rows = box_rows;
+  a.page_table = kv.page_table;
+  a.out = static_cast<__nv_bfloat16*>(out);
+  a.scale_log2 = (1.0f / sqrtf(float(DH))) * 1.4426950408889634f;
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<DH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(AttnCfg<DH>::kSmem));
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  const dim3 grid((n + kAttnM - 1) / kAttnM, n_heads);
+  attn_tc_kernel<DH><<<grid, kAttnThreads, AttnCfg<DH>::kSmem, stream>>>(tq, tk, tv, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attention_tc(const void* q, int n, int n_heads, int n_kv_heads, int dh,
+                                const KvOut& kv, int64_t kv_rows, void* out,
+                                cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (kv.page_table && (kv.page_size & (kv.page_size - 1)) != 0) return cudaErrorInvalidValue;
+  if (kv.page_table && kv.page_size < 8) return cudaErrorInvalidValue;
+  if (dh == 128) return launch_attn_tc<128>(q, n, n_heads, n_kv_heads, kv, kv_rows, out, stream);
+  if (dh == 64) return launch_attn_tc<64>(q, n, n_heads, n_kv_heads, kv, kv_rows, out, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hc

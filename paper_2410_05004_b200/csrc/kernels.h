@@ -74,6 +74,13 @@ cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, in
 cudaError_t launch_attention(const void* q, int n, int n_heads, int n_kv_heads, int dh,
                              const KvOut& kv, void* out, cudaStream_t stream);
 
+// The same attention on tcgen05 (attention_tc.cu): S and O in TMEM, K/V tiles
+// gathered from the pages by TMA. kv_rows = rows of the K/V pools (paged:
+// num_pages * page_size; page_size a power of two >= 8). dh 64 or 128.
+cudaError_t launch_attention_tc(const void* q, int n, int n_heads, int n_kv_heads, int dh,
+                                const KvOut& kv, int64_t kv_rows, void* out,
+                                cudaStream_t stream);
+
 // Embedding gather (model.cpp:82-92): x[i] = E[tokens[i]] (fp32), xb = bf16.
 cudaError_t launch_embed(const int32_t* tokens, int64_t n, const void* emb, int d, float* x,
                          void* xb, cudaStream_t stream);

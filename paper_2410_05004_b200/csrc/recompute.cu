@@ -14,6 +14,7 @@
 // x is the fp32 residual stream; xb its bf16 copy feeds the next GEMM and is
 // the H_L the save path snapshots.
 #include <chrono>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.h"
@@ -31,6 +32,19 @@ CUtensorMap tmap(const void* base, int k, int64_t rows, int box_rows) {
 }
 
 int pick_bn(int64_t M, int N, int sms) { return gemm_pick_bn(M, N, sms); }
+
+// tcgen05 attention (default) or the mma.sync kernel (HC_ATTN_TC=0, or page
+// sizes the TMA gather cannot express)
+cudaError_t attention(const void* q, int n, int n_heads, int n_kv_heads, int dh, const KvOut& kv,
+                      int64_t kv_rows, void* out, cudaStream_t stream) {
+  static const int tc = [] {
+    const char* e = getenv("HC_ATTN_TC");
+    return e ? atoi(e) : 1;
+  }();
+  const bool pow2 = !kv.page_table || (kv.page_size >= 8 && (kv.page_size & (kv.page_size - 1)) == 0);
+  if (tc && pow2) return launch_attention_tc(q, n, n_heads, n_kv_heads, dh, kv, kv_rows, out, stream);
+  return launch_attention(q, n, n_heads, n_kv_heads, dh, kv, out, stream);
+}
 
 }  // namespace
 
@@ -86,8 +100,8 @@ void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n
     qo.d_kv = d;  // every column is "K": RoPE applies to all of Q
     HC_CUDA(launch_restore_kv(tm_xb, tmap(lw.wq, d, d, bn_d), bn_d, int(n), d, d, true, qo,
                               epi_for(w, lw.colsum_q, mean, rstd), sms, stream));
-    HC_CUDA(launch_attention(q_buf.ptr, int(n), c.n_heads, c.n_kv_heads, w->d_head, kv,
-                             mix_buf.ptr, stream));
+    HC_CUDA(attention(q_buf.ptr, int(n), c.n_heads, c.n_kv_heads, w->d_head, kv,
+                      int64_t(pages->num_pages) * pages->page_size, mix_buf.ptr, stream));
     GemmOut resid;
     resid.x = x;
     resid.xb = xb_buf.ptr;
@@ -188,7 +202,7 @@ hc_status hc_attention_dense(const void* d_q, int32_t n, int32_t n_heads, int32_
     kv.k_base = const_cast<void*>(d_k);
     kv.v_base = const_cast<void*>(d_v);
     kv.d_kv = d_kv;
-    HC_CUDA(launch_attention(d_q, n, n_heads, n_kv_heads, d_head, kv, d_out, as_stream(stream)));
+    HC_CUDA(attention(d_q, n, n_heads, n_kv_heads, d_head, kv, n, d_out, as_stream(stream)));
   });
 }
 
