@@ -194,12 +194,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t id_pv = umma_idesc_f16(kAttnM, DH, true) | (1u << 16);  // B MN-major
       mbar_wait(q_full, 0);
       tc_fence_after();
+      auto issue_qk = [&](int j) {
+        const int st = j % kAttnStages, sb = j & 1;
+        const uint32_t sK = smem_u32(sKV + st * Cfg::kStageBytes);
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = uint32_t((kk >> 2) * Cfg::kHalf + (kk & 3) * 32);
+          umma_f16(tmem + uint32_t(sb * 128), umma_desc_sw128(smem_u32(sQ) + off),
+                   umma_desc_sw128(sK + off), id_qk, kk != 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[sb]);
+        umma_commit(&k_empty[st]);
+      };
       auto issue_pv = [&](int j) {
         const int st = j % kAttnStages, pb = j & 1;
-        mbar_wait(&p_full[pb], (j >> 1) & 1);  // softmax wrote P_j (and rescaled O)
-        tc_fence_after();
-        mbar_wait(&v_full[st], (j / kAttnStages) & 1);
-        tc_fence_after();
         const uint32_t sV = smem_u32(sKV + st * Cfg::kStageBytes + Cfg::kKVBytes);
         const uint32_t sPj = smem_u32(sP + pb * Cfg::kPBytes);
         for (int kk = 0; kk < kAttnN / 16; ++kk) {
@@ -211,22 +218,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         umma_commit(&o_done[pb]);
         umma_commit(&v_empty[st]);
       };
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j % kAttnStages, sb = j & 1;
-        mbar_wait(&k_full[st], (j / kAttnStages) & 1);
-        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t sK = smem_u32(sKV + st * Cfg::kStageBytes);
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t off = uint32_t((kk >> 2) * Cfg::kHalf + (kk & 3) * 32);
-          umma_f16(tmem + uint32_t(sb * 128), umma_desc_sw128(smem_u32(sQ) + off),
-                   umma_desc_sw128(sK + off), id_qk, kk != 0 ? 1u : 0u);
+      // event-driven issue: QK_j as soon as its K tile and S buffer are
+      // free (up to two tiles ahead of the softmax), PV_j as soon as P_j and
+      // V_j are ready -- neither queue blocks the other
+      int next_qk = 0, next_pv = 0;
+      uint32_t spins = 0;
+      while (next_pv < n_tiles) {
+        bool progressed = false;
+        if (next_qk < n_tiles) {
+          const int j = next_qk;
+          if (mbar_test(&k_full[j % kAttnStages], (j / kAttnStages) & 1) &&
+              mbar_test(&s_empty[j & 1], ((j >> 1) & 1) ^ 1)) {
+            tc_fence_after();
+            issue_qk(j);
+            ++next_qk;
+            progressed = true;
+          }
         }
-        umma_commit(&s_full[sb]);
-        umma_commit(&k_empty[st]);
-        if (j > 0) issue_pv(j - 1);
+        if (next_pv < next_qk) {
+          const int j = next_pv;
+          if (mbar_test(&p_full[j & 1], (j >> 1) & 1) &&
+              mbar_test(&v_full[j % kAttnStages], (j / kAttnStages) & 1)) {
+            tc_fence_after();
+            issue_pv(j);
+            ++next_pv;
+            progressed = true;
+          }
+        }
+        if (!progressed && ++spins == (1u << 30)) asm volatile("trap;");
       }
-      issue_pv(n_tiles - 1);
     }
   } else {
     // ------------------------------------------------------------ softmax
@@ -263,12 +283,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       // causal / length mask on the diagonal tile only, raw-score max
       const int key0 = j * kAttnN + half * 64;
       const bool diag = key0 + 63 > row || key0 + 64 > a.n;
+      if (__any_sync(0xffffffffu, diag)) {  // warp-uniform: only the diagonal / tail tile
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (key0 + i > row || key0 + i >= a.n) s[i] = -INFINITY;
+      }
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        if (diag && (key0 + i > row || key0 + i >= a.n)) s[i] = -INFINITY;
-        mx = fmaxf(mx, s[i]);
-      }
+      for (int i = 0; i < 64; ++i) mx = fmaxf(mx, s[i]);
       // row max across the two halves (smem, double-buffered by tile parity)
       xmax[(sb * 2 + half) * kAttnM + rloc] = mx;
       pair_sync();
