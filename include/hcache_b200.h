@@ -378,6 +378,14 @@ hc_status hc_restore_batch(hc_store* s, const char* const* sids, int32_t n_sessi
                            const hc_weights* w, const hc_restore_opts* opts,
                            const hc_kv_pages* pages, const int32_t* d_page_tables,
                            int32_t table_stride, void* stream, hc_timeline* timeline);
+/* restore_token_wise (restore.hpp:47-49), the token-wise partition ablation:
+ * at every layer tokens [0, hidden_tokens) are projected from hidden states
+ * and tokens [hidden_tokens, n) spliced from the stored KV rows (every KV
+ * chunk overlapping them is fetched). Both HIDDEN and KV must be stored for
+ * every layer; HC_EINVAL for a split outside [0, n]. */
+hc_status hc_restore_token_wise(hc_store* s, const char* sid, const hc_weights* w,
+                                int32_t hidden_tokens, const hc_kv_pages* pages,
+                                const int32_t* d_page_table, void* stream, hc_timeline* timeline);
 /* Hidden states already resident in HBM (per layer device pointers, rows
  * concatenated per d_cu_seqlens): K1 over every layer. The kernel-bound leg. */
 hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_layers,

@@ -148,6 +148,7 @@ _PROTOS = {
                          P(TimelineC)]),
     "hc_restore_batch": (i32, [vp, P(cp), i32, vp, P(RestoreOptsC), P(KvPagesC), vp, i32, vp,
                                P(TimelineC)]),
+    "hc_restore_token_wise": (i32, [vp, cp, vp, i32, P(KvPagesC), vp, vp, P(TimelineC)]),
     "hc_restore_resident": (i32, [vp, P(vp), i64, vp, i32, P(KvPagesC), vp, i32, vp]),
     "hc_prefill_layers": (i32, [vp, vp, i64, i32, i32, P(KvPagesC), vp, vp]),
     "hc_prefill": (i32, [vp, vp, i64, P(KvPagesC), vp, vp, P(i32), vp]),

@@ -481,6 +481,85 @@ void restore_batch(hc_store* st, const char* const* sids, int n_sessions, const 
   }
 }
 
+// restore_token_wise (restore.cpp:237-301), the ablation: at every layer the
+// first s tokens are projected from hidden states (K1, positions 0..s-1) and
+// tokens [s, n) are spliced from the stored KV rows (K4 at positions s..),
+// reading every KV chunk that overlaps [s, n). Both kinds must be stored for
+// every layer. One fetch (hidden part + KV part) and one compute step per
+// layer, pipelined through a 2-deep ring.
+void restore_token_wise(hc_store* st, const char* sid_c, const hc_weights* w, int s_tok,
+                        const hc_kv_pages* pages, const int32_t* d_page_table,
+                        cudaStream_t stream, hc_timeline* tl) {
+  if (!st || !sid_c || !w || !pages || !d_page_table)
+    fail(HC_EINVAL, "restore_token_wise: null argument");
+  Store& store = st->impl;
+  const std::string sid(sid_c);
+  const hc_manifest m = store.open(sid);
+  const int n = m.n_tokens, L = w->cfg.n_layers, d = w->cfg.d_hidden;
+  if (s_tok < 0 || s_tok > n) fail(HC_EINVAL, "restore_token_wise: bad split");
+  if (m.n_layers != L || m.d_hidden != d) fail(HC_EINVAL, "restore_token_wise: shape mismatch");
+  if (m.elem_bytes != 2 || m.dtype != HC_DTYPE_BF16)
+    fail(HC_EINVAL, "restore_token_wise: bf16 sessions required");
+  if (s_tok < n && (m.d_kv != w->d_kv || w->d_kv != w->d_kv_all))
+    fail(HC_EINVAL, "restore_token_wise: KV rows need all KV heads on this GPU");
+  validate_pages(w, pages, w->d_kv);
+  DeviceGuard dg(w->device);
+  Engine& eng = engine(w->device);
+  const bool timed = tl != nullptr;
+  EventPool evp(timed);
+  std::vector<TimedOp> ops;
+  const int kv_b = (s_tok / HC_CHUNK_TOKENS) * HC_CHUNK_TOKENS;  // first KV chunk overlapping [s, n)
+  const size_t h_bytes = size_t(s_tok) * size_t(d) * 2;
+  const size_t kv_bytes = size_t(n - kv_b) * size_t(2 * m.d_kv) * 2;
+  const int nbuf = std::min(L, 2);
+  StreamScratch ring_h(s_tok > 0 ? h_bytes * size_t(nbuf) : 0, stream);
+  StreamScratch ring_kv(s_tok < n ? kv_bytes * size_t(nbuf) : 0, stream);
+  cudaEvent_t t0 = evp.get();
+  HC_CUDA(cudaEventRecord(t0, stream));
+  HC_CUDA(cudaStreamWaitEvent(eng.copy, t0, 0));
+  std::vector<cudaEvent_t> consumed(size_t(nbuf), nullptr), joins;
+  for (int layer = 0; layer < L; ++layer) {
+    const int slot = layer % nbuf;
+    uint8_t* hb = static_cast<uint8_t*>(ring_h.ptr) + h_bytes * size_t(slot);
+    uint8_t* kb = static_cast<uint8_t*>(ring_kv.ptr) + kv_bytes * size_t(slot);
+    if (consumed[size_t(slot)]) HC_CUDA(cudaStreamWaitEvent(eng.copy, consumed[size_t(slot)], 0));
+    cudaEvent_t fs = timed ? evp.get() : nullptr;
+    if (fs) HC_CUDA(cudaEventRecord(fs, eng.copy));
+    if (s_tok > 0)
+      issue_gather(store.gather_plan(sid, layer, HC_STATE_HIDDEN, 0, s_tok, nullptr), hb, eng, joins,
+                   &EventPool::make, &evp);
+    if (s_tok < n)
+      issue_gather(store.gather_plan(sid, layer, HC_STATE_KV, kv_b, n, nullptr), kb, eng, joins,
+                   &EventPool::make, &evp);
+    cudaEvent_t fetched = evp.get();
+    HC_CUDA(cudaEventRecord(fetched, eng.copy));
+    if (timed) ops.push_back({HC_LANE_IO, layer, HC_EV_FETCH, fs, fetched});
+    HC_CUDA(cudaStreamWaitEvent(stream, fetched, 0));
+    cudaEvent_t cs = timed ? evp.get() : nullptr;
+    if (cs) HC_CUDA(cudaEventRecord(cs, stream));
+    if (s_tok > 0)
+      project_rows(w, layer, hb, s_tok, kv_out_pages(pages, layer, d_page_table, 0, nullptr, 1),
+                   stream);
+    if (s_tok < n) {
+      KvOut o = kv_out_pages(pages, layer, d_page_table, 0, nullptr, 1);
+      o.start_pos = s_tok;  // spliced rows keep their absolute positions
+      HC_CUDA(launch_kv_scatter(kb + size_t(s_tok - kv_b) * size_t(2 * m.d_kv) * 2, n - s_tok, o,
+                                stream));
+    }
+    cudaEvent_t done = evp.get();
+    HC_CUDA(cudaEventRecord(done, stream));
+    consumed[size_t(slot)] = done;
+    if (timed) ops.push_back({HC_LANE_COMPUTE, layer, s_tok > 0 ? HC_EV_PROJECT : HC_EV_SCATTER, cs, done});
+  }
+  cudaEvent_t io_done = evp.get();
+  HC_CUDA(cudaEventRecord(io_done, eng.copy));
+  HC_CUDA(cudaStreamWaitEvent(stream, io_done, 0));
+  if (timed) {
+    HC_CUDA(cudaStreamSynchronize(stream));
+    fill_timeline(tl, t0, ops);
+  }
+}
+
 }  // namespace hc
 
 using namespace hc;
@@ -502,6 +581,14 @@ hc_status hc_restore_batch(hc_store* s, const char* const* sids, int32_t n_sessi
   return guard([&] {
     restore_batch(s, sids, n_sessions, w, opts, pages, d_page_tables, table_stride,
                   as_stream(stream), timeline);
+  });
+}
+
+hc_status hc_restore_token_wise(hc_store* s, const char* sid, const hc_weights* w,
+                                int32_t hidden_tokens, const hc_kv_pages* pages,
+                                const int32_t* d_page_table, void* stream, hc_timeline* timeline) {
+  return guard([&] {
+    restore_token_wise(s, sid, w, hidden_tokens, pages, d_page_table, as_stream(stream), timeline);
   });
 }
 

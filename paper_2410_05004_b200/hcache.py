@@ -594,6 +594,16 @@ def restore_batch(store: StorageManager, session_ids: Sequence[str], w: Weights,
     return RestoreResult(kv, Timeline.from_c(tc) if tc is not None else None)
 
 
+def restore_token_wise(store: StorageManager, session_id: str, w: Weights, hidden_tokens: int,
+                       kv: KvCache, page_table, stream=None) -> RestoreResult:
+    """restore.hpp:47-49 (ablation) on the GPU."""
+    tc = capi.TimelineC()
+    check(lib().hc_restore_token_wise(store._h, session_id.encode(), w._h, hidden_tokens,
+                                      C.byref(kv.desc), page_table.data_ptr(), _stream(stream),
+                                      C.byref(tc)))
+    return RestoreResult(kv, Timeline.from_c(tc))
+
+
 def profile_hardware(w: Weights, n_tokens: int) -> ProfiledTimings:
     """harness.hpp:76-77, measured on the device."""
     t = capi.TimingsC()

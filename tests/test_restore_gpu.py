@@ -205,3 +205,45 @@ def test_h2d_bandwidth_is_pcie_class(cuda):
     from paper_2410_05004_b200 import hcache as H
     bw = H.measure_h2d(64 << 20)
     assert 5e9 < bw < 400e9
+
+
+def _store_everything(n, sid="tw"):
+    """test_restore.cpp:209-244 setup: every layer stored as HIDDEN and KV,
+    KV rows = the K1 projection of the hidden rows (a consistent session)."""
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    cfg, w, kv, table = _setup(n=n)
+    store = H.StorageManager(H.DevicePool(2))
+    plan = H.RestorationPlan.make(4, 4, H.Complement.NONE)
+    store.create_session(H.SessionSeed(sid, cfg.hash(), 4, 512, 2, plan, list(range(n)), d_kv=512))
+    want = []
+    for L in range(4):
+        h = dev_hidden(n, 512, seed=600 + L)
+        k, v = H.project_hidden_to_kv(w, L, h, 0)
+        want.append((k, v))
+        assert store.snapshot(sid, L, H.StateKind.HIDDEN, h)
+        assert store.snapshot(sid, L, H.StateKind.KV, torch.cat([k, v], 1).contiguous())
+    store.finalize(sid)
+    return cfg, w, kv, table, store, want
+
+
+@pytest.mark.parametrize("split", [0, 130, 192, 256, 320])
+def test_token_wise_split_restores_correctly(cuda, split):
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    n = 320
+    cfg, w, kv, table, store, want = _store_everything(n)
+    res = H.restore_token_wise(store, "tw", w, split, kv, table)
+    torch.cuda.synchronize()
+    for L in range(4):
+        k, v = kv.gather(L, table, n)
+        assert torch.equal(k, want[L][0]) and torch.equal(v, want[L][1]), (split, L)
+    assert sum(e.kind == "fetch" for e in res.timeline.events) == 4
+
+
+def test_token_wise_rejects_bad_splits(cuda):
+    from paper_2410_05004_b200 import hcache as H
+    cfg, w, kv, table, store, want = _store_everything(100, "tw2")
+    for bad in (-1, 101):
+        with pytest.raises(ValueError):
+            H.restore_token_wise(store, "tw2", w, bad, kv, table)
