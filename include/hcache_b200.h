@@ -393,6 +393,24 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
                               const hc_kv_pages* pages, const int32_t* d_page_table,
                               int32_t table_stride, void* stream);
 
+/* forward_tokens / decode_step (model.cpp:305-347, model.hpp:115-120) batched
+ * over sequences with paged caches: sequence s appends new_lens[s] tokens
+ * (host array) at positions start_pos[s].. (host array; its cached keys
+ * [0, start_pos[s]) are attended to). d_tokens: all sequences' tokens
+ * concatenated (device). Page-table row s at d_page_tables + s*table_stride.
+ * d_layer_inputs (optional, n_layers x T x d_hidden bf16, T = sum new_lens)
+ * receives each layer's input hidden state (the rows the save path persists);
+ * d_next_tokens[s] (device) the greedy next token after sequence s. */
+hc_status hc_forward_batch(const hc_weights* w, const int32_t* d_tokens, int32_t n_seqs,
+                           const int32_t* new_lens, const int32_t* start_pos,
+                           const hc_kv_pages* pages, const int32_t* d_page_tables,
+                           int32_t table_stride, void* d_layer_inputs, int32_t* d_next_tokens,
+                           void* stream);
+/* Pages -> interleaved [K_row | V_row] rows (the KV chunk payload,
+ * storage.cpp:67-75) for positions [pos0, pos0 + n_rows) of one layer. */
+hc_status hc_kv_gather_rows(const hc_kv_pages* pages, int32_t layer, const int32_t* d_page_table,
+                            int32_t pos0, int64_t n_rows, void* d_rows, void* stream);
+
 /* ------------------------------------------------------ recompute (K6) */
 /* prefill_layers (model.hpp:124-125, model.cpp:349-356): embeds d_tokens and
  * runs layers [lb, le) from position 0, writing their K/V into the pages. */

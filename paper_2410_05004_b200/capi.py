@@ -148,6 +148,8 @@ _PROTOS = {
                          P(TimelineC)]),
     "hc_restore_batch": (i32, [vp, P(cp), i32, vp, P(RestoreOptsC), P(KvPagesC), vp, i32, vp,
                                P(TimelineC)]),
+    "hc_forward_batch": (i32, [vp, vp, i32, vp, vp, P(KvPagesC), vp, i32, vp, vp, vp]),
+    "hc_kv_gather_rows": (i32, [P(KvPagesC), i32, vp, i32, i64, vp, vp]),
     "hc_restore_token_wise": (i32, [vp, cp, vp, i32, P(KvPagesC), vp, vp, P(TimelineC)]),
     "hc_restore_resident": (i32, [vp, P(vp), i64, vp, i32, P(KvPagesC), vp, i32, vp]),
     "hc_prefill_layers": (i32, [vp, vp, i64, i32, i32, P(KvPagesC), vp, vp]),

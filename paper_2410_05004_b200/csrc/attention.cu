@@ -65,10 +65,14 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
   return base + uint32_t(row * DH * 2) + (uint32_t(chunk ^ (row & 7)) << 4);
 }
 
+// Prefill from position 0 (cu_q == nullptr: one sequence of n rows) or the
+// batched continuation (cu_q != nullptr: blockIdx.z = sequence, its rows
+// [cu_q[z], cu_q[z+1]) at positions seq_start[z] + i, page-table row z).
 template <int DH>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_fwd_kernel(const __nv_bfloat16* __restrict__ q, int n, int n_heads, int group, KvOut kv,
-                    __nv_bfloat16* __restrict__ out, float scale_log2) {
+                    __nv_bfloat16* __restrict__ out, float scale_log2,
+                    const int32_t* __restrict__ cu_q, const int32_t* __restrict__ seq_start) {
   constexpr int CH = DH / 8;  // 16-byte chunks per row
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sQ = s_u32(smem);
@@ -79,6 +83,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int ld = n_heads * DH;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = qb * kQ;
+  int row0 = 0, p0 = 0;  // first query row of this sequence, its position
+  const int32_t* table = kv.page_table;
+  if (cu_q) {
+    const int z = blockIdx.z;
+    row0 = __ldg(cu_q + z);
+    n = __ldg(cu_q + z + 1) - row0;
+    p0 = __ldg(seq_start + z);
+    if (table) table += int64_t(z) * kv.table_stride;
+  }
+  if (q0 >= n) return;
+  const int n_keys = p0 + min(n, q0 + kQ);  // keys [0, n_keys) reach this query tile
+  q += size_t(row0) * ld;
+  out += size_t(row0) * ld;
 
   for (int i = tid; i < kQ * CH; i += kAttnThreads) {
     const int r = i / CH, c = i % CH, row = q0 + r;
@@ -89,11 +106,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const uint32_t sk = sK0 + uint32_t(st * kK * DH * 2), sv = sV0 + uint32_t(st * kK * DH * 2);
     for (int i = tid; i < kK * CH; i += kAttnThreads) {
       const int r = i / CH, c = i % CH, key = kb * kK + r;
-      const bool ok = key < n;
+      const bool ok = key < n_keys;
       int64_t orow = ok ? key : 0;
-      if (ok && kv.page_table)
-        orow = int64_t(__ldg(kv.page_table + key / kv.page_size)) * kv.page_size +
-               key % kv.page_size;
+      if (ok && table)
+        orow = int64_t(__ldg(table + key / kv.page_size)) * kv.page_size + key % kv.page_size;
       const size_t off = size_t(orow) * kv.d_kv + size_t(hk) * DH + size_t(c) * 8;
       cp_async16(swz<DH>(sk, r, c), static_cast<const __nv_bfloat16*>(kv.k_base) + off, ok);
       cp_async16(swz<DH>(sv, r, c), static_cast<const __nv_bfloat16*>(kv.v_base) + off, ok);
@@ -102,7 +118,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   load_kv(0, 0);
   cp_async_commit();
 
-  const int n_kb = qb + 1;  // causal: key tiles up to the diagonal
+  const int n_kb = (n_keys + kK - 1) / kK;  // causal: key tiles up to the diagonal
   float o[DH / 8][4];
 #pragma unroll
   for (int j = 0; j < DH / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
@@ -150,7 +166,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int key = kb * kK + 8 * j + 2 * (lane & 3) + (e & 1);
         const int row = r_lo + 8 * (e >> 1);
         float v = s[j][e] * scale_log2;
-        if (key > row || key >= n) v = -INFINITY;
+        if (key > p0 + row || key >= n_keys) v = -INFINITY;
         s[j][e] = v;
         mx[e >> 1] = fmaxf(mx[e >> 1], v);
       }
@@ -251,8 +267,54 @@ __global__ void argmax_logits_kernel(const __nv_bfloat16* __restrict__ emb, int 
   }
 }
 
+// blockIdx.y = sequence: logits of its last row (cu[s+1]-1)
+__global__ void argmax_rows_kernel(const __nv_bfloat16* __restrict__ emb, int vocab, int d,
+                                   const float* __restrict__ x, const int32_t* __restrict__ cu,
+                                   unsigned long long* best) {
+  const int warps = blockDim.x >> 5;
+  const int t = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= vocab) return;
+  const int s = blockIdx.y;
+  const float* h = x + size_t(__ldg(cu + s + 1) - 1) * d;
+  float acc = 0.f;
+  for (int c = lane; c < d; c += 32) acc += __bfloat162float(emb[size_t(t) * d + c]) * h[c];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    uint32_t u = __float_as_uint(acc);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    atomicMax(best + s, (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - uint32_t(t)));
+  }
+}
+
+__global__ void argmax_rows_finish_kernel(const unsigned long long* best, int n, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = int32_t(0xFFFFFFFFu - uint32_t(best[i] & 0xFFFFFFFFull));
+}
+
 __global__ void argmax_finish_kernel(const unsigned long long* best, int32_t* out) {
   *out = int32_t(0xFFFFFFFFu - uint32_t(*best & 0xFFFFFFFFull));
+}
+
+}  // namespace
+
+namespace {
+
+cudaError_t attention_launch(const void* q, int n, dim3 grid, const int32_t* cu_q,
+                             const int32_t* seq_start, int n_heads, int n_kv_heads, int dh,
+                             const KvOut& kv, void* out, cudaStream_t stream) {
+  const float scale_log2 = (1.0f / sqrtf(float(dh))) * 1.4426950408889634f;
+  const int group = n_heads / n_kv_heads;
+  if (dh != 128 && dh != 64) return cudaErrorInvalidValue;
+  const size_t sm = size_t(kQ + 4 * kK) * size_t(dh) * 2;
+  auto kern = dh == 128 ? attn_fwd_kernel<128> : attn_fwd_kernel<64>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kAttnThreads, sm, stream>>>(static_cast<const __nv_bfloat16*>(q), n, n_heads,
+                                           group, kv, static_cast<__nv_bfloat16*>(out),
+                                           scale_log2, cu_q, seq_start);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -260,29 +322,17 @@ __global__ void argmax_finish_kernel(const unsigned long long* best, int32_t* ou
 cudaError_t launch_attention(const void* q, int n, int n_heads, int n_kv_heads, int dh,
                              const KvOut& kv, void* out, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  const dim3 grid((n + kQ - 1) / kQ, n_heads);
-  const float scale_log2 = (1.0f / sqrtf(float(dh))) * 1.4426950408889634f;
-  const int group = n_heads / n_kv_heads;
-  if (dh == 128) {
-    const size_t sm = size_t(kQ + 4 * kK) * 128 * 2;
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<128>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-    if (e != cudaSuccess) return e;
-    attn_fwd_kernel<128><<<grid, kAttnThreads, sm, stream>>>(
-        static_cast<const __nv_bfloat16*>(q), n, n_heads, group, kv,
-        static_cast<__nv_bfloat16*>(out), scale_log2);
-  } else if (dh == 64) {
-    const size_t sm = size_t(kQ + 4 * kK) * 64 * 2;
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<64>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-    if (e != cudaSuccess) return e;
-    attn_fwd_kernel<64><<<grid, kAttnThreads, sm, stream>>>(
-        static_cast<const __nv_bfloat16*>(q), n, n_heads, group, kv,
-        static_cast<__nv_bfloat16*>(out), scale_log2);
-  } else {
-    return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
+  return attention_launch(q, n, dim3((n + kQ - 1) / kQ, n_heads, 1), nullptr, nullptr, n_heads,
+                          n_kv_heads, dh, kv, out, stream);
+}
+
+cudaError_t launch_attention_extend(const void* q, int n_seqs, int max_new, const int32_t* cu_q,
+                                    const int32_t* seq_start, int n_heads, int n_kv_heads,
+                                    int dh, const KvOut& kv, void* out, cudaStream_t stream) {
+  if (n_seqs <= 0 || max_new <= 0) return cudaSuccess;
+  if (!cu_q || !seq_start) return cudaErrorInvalidValue;
+  return attention_launch(q, 0, dim3((max_new + kQ - 1) / kQ, n_heads, n_seqs), cu_q, seq_start,
+                          n_heads, n_kv_heads, dh, kv, out, stream);
 }
 
 cudaError_t launch_embed(const int32_t* tokens, int64_t n, const void* emb, int d, float* x,
@@ -304,6 +354,22 @@ cudaError_t launch_argmax_logits(const void* emb, int vocab, int d, const float*
   argmax_logits_kernel<<<unsigned((vocab + 7) / 8), 256, 0, stream>>>(
       static_cast<const __nv_bfloat16*>(emb), vocab, d, h, best);
   argmax_finish_kernel<<<1, 1, 0, stream>>>(best, out_token);
+  cudaFreeAsync(best, stream);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_rows(const void* emb, int vocab, int d, const float* h,
+                               const int32_t* cu, int n_seqs, int32_t* out_tokens,
+                               cudaStream_t stream) {
+  if (n_seqs <= 0) return cudaSuccess;
+  unsigned long long* best = nullptr;
+  cudaError_t e = cudaMallocAsync(&best, sizeof(unsigned long long) * size_t(n_seqs), stream);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(best, 0, sizeof(unsigned long long) * size_t(n_seqs), stream);
+  argmax_rows_kernel<<<dim3(unsigned((vocab + 7) / 8), unsigned(n_seqs)), 256, 0, stream>>>(
+      static_cast<const __nv_bfloat16*>(emb), vocab, d, h, cu, best);
+  argmax_rows_finish_kernel<<<unsigned((n_seqs + 127) / 128), 128, 0, stream>>>(best, n_seqs,
+                                                                               out_tokens);
   cudaFreeAsync(best, stream);
   return cudaGetLastError();
 }

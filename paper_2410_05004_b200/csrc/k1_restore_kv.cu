@@ -174,7 +174,7 @@ __device__ __forceinline__ void epilogue_tile(int row, int n_blk, int M, int N, 
       seq = lo;
       local = row - __ldg(out.cu_seqlens + seq);
     }
-    pos = out.start_pos + local;
+    pos = (out.seq_start ? __ldg(out.seq_start + seq) : out.start_pos) + local;
     int64_t orow;
     if (out.page_table) {
       int page = __ldg(out.page_table + int64_t(seq) * out.table_stride + pos / out.page_size);
@@ -593,7 +593,7 @@ __global__ void kv_scatter_kernel(const uint4* __restrict__ rows, int64_t n_rows
     seq = lo;
     local = int(row - __ldg(out.cu_seqlens + seq));
   }
-  const int pos = out.start_pos + local;
+  const int pos = (out.seq_start ? __ldg(out.seq_start + seq) : out.start_pos) + local;
   int64_t orow = row;
   if (out.page_table) {
     int page = __ldg(out.page_table + int64_t(seq) * out.table_stride + pos / out.page_size);
@@ -608,6 +608,26 @@ __global__ void kv_scatter_kernel(const uint4* __restrict__ rows, int64_t n_rows
     uint4 b = __ldg(src + vec + i);
     kd[i] = a;
     vd[i] = b;
+  }
+}
+
+// One warp per row: K page slot, V page slot -> [K_row | V_row].
+__global__ void kv_gather_kernel(KvOut kv, int pos0, int64_t n_rows, uint4* __restrict__ rows) {
+  const int warps = blockDim.x >> 5;
+  const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  const int64_t pos = pos0 + row;
+  int64_t orow = pos;
+  if (kv.page_table)
+    orow = int64_t(__ldg(kv.page_table + pos / kv.page_size)) * kv.page_size + pos % kv.page_size;
+  const int vec = kv.d_kv / 8;
+  const uint4* ks = static_cast<const uint4*>(kv.k_base) + orow * vec;
+  const uint4* vs = static_cast<const uint4*>(kv.v_base) + orow * vec;
+  uint4* dst = rows + row * 2 * vec;
+  for (int i = lane; i < vec; i += 32) {
+    dst[i] = __ldg(ks + i);
+    dst[vec + i] = __ldg(vs + i);
   }
 }
 
@@ -742,6 +762,15 @@ cudaError_t launch_kv_scatter(const void* rows, int64_t n_rows, const KvOut& out
   const int threads = 256, per_block = threads / 32;
   const unsigned grid = unsigned((n_rows + per_block - 1) / per_block);
   kv_scatter_kernel<<<grid, threads, 0, stream>>>(static_cast<const uint4*>(rows), n_rows, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kv_gather(const KvOut& kv, int pos0, int64_t n_rows, void* rows,
+                             cudaStream_t stream) {
+  if (n_rows <= 0) return cudaSuccess;
+  const int threads = 256, per_block = threads / 32;
+  const unsigned grid = unsigned((n_rows + per_block - 1) / per_block);
+  kv_gather_kernel<<<grid, threads, 0, stream>>>(kv, pos0, n_rows, static_cast<uint4*>(rows));
   return cudaGetLastError();
 }
 

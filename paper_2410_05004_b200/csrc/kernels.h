@@ -22,6 +22,7 @@ struct KvOut {
   const int32_t* cu_seqlens = nullptr;  // nullptr: one sequence of M rows
   int n_seqs = 1;
   int start_pos = 0;
+  const int32_t* seq_start = nullptr;  // per-sequence first position (overrides start_pos)
   int out_f32 = 0;  // 0: bf16 KV, 1: fp32 (parity/debug)
 };
 
@@ -74,6 +75,15 @@ cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, in
 cudaError_t launch_attention(const void* q, int n, int n_heads, int n_kv_heads, int dh,
                              const KvOut& kv, void* out, cudaStream_t stream);
 
+// Batched continuation (forward_tokens / decode_step, model.cpp:237-288 with
+// start_pos > 0): sequence s owns query rows [cu_q[s], cu_q[s+1]) at
+// positions seq_start[s] + i and attends to its cached keys [0, position]
+// through page-table row s (stride kv.table_stride). max_new = max rows of
+// one sequence (grid extent).
+cudaError_t launch_attention_extend(const void* q, int n_seqs, int max_new, const int32_t* cu_q,
+                                    const int32_t* seq_start, int n_heads, int n_kv_heads,
+                                    int dh, const KvOut& kv, void* out, cudaStream_t stream);
+
 // The same attention on tcgen05 (attention_tc.cu): S and O in TMEM, K/V tiles
 // gathered from the pages by TMA. kv_rows = rows of the K/V pools (paged:
 // num_pages * page_size; page_size a power of two >= 8). dh 64 or 128.
@@ -88,6 +98,17 @@ cudaError_t launch_embed(const int32_t* tokens, int64_t n, const void* emb, int 
 // Greedy next token (argmax_token, model.cpp:67-80): argmax_t E[t] . h.
 cudaError_t launch_argmax_logits(const void* emb, int vocab, int d, const float* h,
                                  int32_t* out_token, cudaStream_t stream);
+
+// Greedy next token of every sequence's last row: out[s] = argmax over the
+// vocabulary of E . h[cu[s+1]-1] (fp32 h rows of width d).
+cudaError_t launch_argmax_rows(const void* emb, int vocab, int d, const float* h,
+                               const int32_t* cu, int n_seqs, int32_t* out_tokens,
+                               cudaStream_t stream);
+
+// Pages -> interleaved [K_row | V_row] rows for positions [pos0, pos0 + n) of
+// one sequence (the KV-offload snapshot payload, storage.cpp:67-75).
+cudaError_t launch_kv_gather(const KvOut& kv, int pos0, int64_t n_rows, void* rows,
+                             cudaStream_t stream);
 
 // Row statistics for the LayerNorm fold: mean and 1/sqrt(var+1e-5) per row,
 // mean/var accumulated in double like the reference (model.cpp:43-61).

@@ -13,6 +13,7 @@
 //   FC2 fc2        x += xb1 fc2^T, xb = bf16(x)
 // x is the fp32 residual stream; xb its bf16 copy feeds the next GEMM and is
 // the H_L the save path snapshots.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <vector>
@@ -48,15 +49,15 @@ cudaError_t attention(const void* q, int n, int n_heads, int n_kv_heads, int dh,
 
 }  // namespace
 
-void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int lb, int le,
-                         const hc_kv_pages* pages, const int32_t* d_page_table,
-                         cudaStream_t stream, const std::function<void(int, bool)>& hook,
-                         void* d_layer_inputs, int32_t* next_token) {
+void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int lb, int le,
+                  const hc_kv_pages* pages, const int32_t* d_page_table, cudaStream_t stream,
+                  const std::function<void(int, bool)>& hook, void* d_layer_inputs,
+                  int32_t* next_token, const SeqBatch& sb, int32_t* d_next_tokens) {
   if (!w || !d_tokens || !pages || !d_page_table) fail(HC_EINVAL, "prefill_layers: null argument");
   const auto& c = w->cfg;
   if (lb < 0 || le > c.n_layers || lb > le) fail(HC_EINVAL, "prefill_layers: bad layer range");
   if (n < 1) fail(HC_EINVAL, "forward: empty sequence");
-  if (n > c.max_seq) fail(HC_EINVAL, "forward: sequence exceeds max_seq");
+  if (!sb.cu && n > c.max_seq) fail(HC_EINVAL, "forward: sequence exceeds max_seq");
   if (!w->embedding) fail(HC_EINVAL, "prefill_layers: embedding not set");
   if (w->d_kv != w->d_kv_all) fail(HC_EINVAL, "prefill_layers: needs all KV heads on this GPU");
   for (int L = lb; L < le; ++L)
@@ -90,7 +91,8 @@ void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n
                               nd * 2, cudaMemcpyDeviceToDevice, stream));
     // attention block: LN(x) -> K/V (paged) and Q
     HC_CUDA(launch_row_stats(xb_buf.ptr, n, d, d, true, mean, rstd, stream));
-    KvOut kv = kv_out_pages(pages, L, d_page_table, 0, nullptr, 1);
+    KvOut kv = kv_out_pages(pages, L, d_page_table, sb.table_stride, sb.cu, sb.n_seqs);
+    kv.seq_start = sb.seq_start;
     HC_CUDA(launch_restore_kv(tm_xb, tmap(lw.wkv_all, d, 2 * w->d_kv_all, bn_kv), bn_kv, int(n),
                               2 * w->d_kv_all, d, true, kv, epi_for(w, lw.colsum_all, mean, rstd),
                               sms, stream));
@@ -98,10 +100,18 @@ void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n
     qo.k_base = q_buf.ptr;
     qo.v_base = q_buf.ptr;
     qo.d_kv = d;  // every column is "K": RoPE applies to all of Q
+    qo.cu_seqlens = sb.cu;
+    qo.n_seqs = sb.cu ? sb.n_seqs : 1;
+    qo.seq_start = sb.seq_start;
     HC_CUDA(launch_restore_kv(tm_xb, tmap(lw.wq, d, d, bn_d), bn_d, int(n), d, d, true, qo,
                               epi_for(w, lw.colsum_q, mean, rstd), sms, stream));
-    HC_CUDA(attention(q_buf.ptr, int(n), c.n_heads, c.n_kv_heads, w->d_head, kv,
-                      int64_t(pages->num_pages) * pages->page_size, mix_buf.ptr, stream));
+    if (sb.cu)
+      HC_CUDA(launch_attention_extend(q_buf.ptr, sb.n_seqs, sb.max_new, sb.cu, sb.seq_start,
+                                      c.n_heads, c.n_kv_heads, w->d_head, kv, mix_buf.ptr,
+                                      stream));
+    else
+      HC_CUDA(attention(q_buf.ptr, int(n), c.n_heads, c.n_kv_heads, w->d_head, kv,
+                        int64_t(pages->num_pages) * pages->page_size, mix_buf.ptr, stream));
     GemmOut resid;
     resid.x = x;
     resid.xb = xb_buf.ptr;
@@ -125,6 +135,9 @@ void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n
                               dffn, resid, EpiArgs{}, sms, stream));
     hook(L, false);
   }
+  if (d_next_tokens && sb.cu)
+    HC_CUDA(launch_argmax_rows(w->embedding, c.vocab_size, d, x, sb.cu, sb.n_seqs, d_next_tokens,
+                               stream));
   if (next_token) {
     StreamScratch tok(sizeof(int32_t), stream);
     HC_CUDA(launch_argmax_logits(w->embedding, c.vocab_size, d, x + size_t(n - 1) * d,
@@ -132,6 +145,50 @@ void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n
     HC_CUDA(cudaMemcpyAsync(next_token, tok.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
     HC_CUDA(cudaStreamSynchronize(stream));
   }
+}
+
+void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int lb, int le,
+                         const hc_kv_pages* pages, const int32_t* d_page_table,
+                         cudaStream_t stream, const std::function<void(int, bool)>& hook,
+                         void* d_layer_inputs, int32_t* next_token) {
+  forward_impl(w, d_tokens, n, lb, le, pages, d_page_table, stream, hook, d_layer_inputs,
+               next_token, SeqBatch{}, nullptr);
+}
+
+void forward_batch(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
+                   const int32_t* new_lens, const int32_t* start_pos, const hc_kv_pages* pages,
+                   const int32_t* d_page_tables, int table_stride, void* d_layer_inputs,
+                   int32_t* d_next_tokens, cudaStream_t stream) {
+  if (!w || n_seqs < 1 || !new_lens || !start_pos) fail(HC_EINVAL, "forward_batch: bad argument");
+  if (!pages) fail(HC_EINVAL, "forward_batch: null pages");
+  std::vector<int32_t> meta(size_t(2 * n_seqs + 1));
+  int64_t total = 0;
+  int max_new = 0;
+  for (int s = 0; s < n_seqs; ++s) {
+    if (new_lens[s] < 1) fail(HC_EINVAL, "forward: empty sequence");
+    if (start_pos[s] < 0) fail(HC_EINVAL, "forward_batch: negative start position");
+    if (int64_t(start_pos[s]) + new_lens[s] > w->cfg.max_seq)
+      fail(HC_EINVAL, "forward: sequence exceeds max_seq");
+    if (int64_t(start_pos[s]) + new_lens[s] > int64_t(table_stride) * pages->page_size)
+      fail(HC_EINVAL, "forward_batch: page table row too short");
+    meta[size_t(s)] = int32_t(total);
+    meta[size_t(n_seqs + 1 + s)] = start_pos[s];
+    total += new_lens[s];
+    max_new = std::max(max_new, new_lens[s]);
+  }
+  meta[size_t(n_seqs)] = int32_t(total);
+  DeviceGuard dg(w->device);
+  StreamScratch dmeta(meta.size() * sizeof(int32_t), stream);
+  HC_CUDA(cudaMemcpyAsync(dmeta.ptr, meta.data(), meta.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice, stream));
+  SeqBatch sb;
+  sb.n_seqs = n_seqs;
+  sb.cu = static_cast<int32_t*>(dmeta.ptr);
+  sb.seq_start = sb.cu + n_seqs + 1;
+  sb.max_new = max_new;
+  sb.table_stride = table_stride;
+  forward_impl(w, d_tokens, total, 0, w->cfg.n_layers, pages, d_page_tables, stream,
+               [](int, bool) {}, d_layer_inputs, nullptr, sb, d_next_tokens);
 }
 
 double recompute_layer_seconds(const hc_weights* w, int n) {
@@ -229,6 +286,35 @@ hc_status hc_gemm_epilogue(int32_t mode, const void* d_a, const void* d_b, int32
     }
     HC_CUDA(launch_gemm_dense(tmap(d_a, k, m, 128), tmap(d_b, k, n, bn), bn, mode, m, n, k, g, e,
                               sms, as_stream(stream)));
+  });
+}
+
+hc_status hc_forward_batch(const hc_weights* w, const int32_t* d_tokens, int32_t n_seqs,
+                           const int32_t* new_lens, const int32_t* start_pos,
+                           const hc_kv_pages* pages, const int32_t* d_page_tables,
+                           int32_t table_stride, void* d_layer_inputs, int32_t* d_next_tokens,
+                           void* stream) {
+  return guard([&] {
+    forward_batch(w, d_tokens, n_seqs, new_lens, start_pos, pages, d_page_tables, table_stride,
+                  d_layer_inputs, d_next_tokens, as_stream(stream));
+  });
+}
+
+hc_status hc_kv_gather_rows(const hc_kv_pages* pages, int32_t layer, const int32_t* d_page_table,
+                            int32_t pos0, int64_t n_rows, void* d_rows, void* stream) {
+  return guard([&] {
+    if (!pages || !d_page_table || !d_rows || pos0 < 0 || n_rows < 0)
+      fail(HC_EINVAL, "kv_gather_rows: bad argument");
+    if (layer < 0 || layer >= pages->n_layers) fail(HC_EINVAL, "kv_gather_rows: bad layer");
+    if (pages->dtype != HC_DTYPE_BF16 || pages->d_kv % 8)
+      fail(HC_EINVAL, "kv_gather_rows: bf16 pages with d_kv % 8 == 0 required");
+    KvOut kv;
+    kv.k_base = pages->k_layers[layer];
+    kv.v_base = pages->v_layers[layer];
+    kv.d_kv = pages->d_kv;
+    kv.page_size = pages->page_size;
+    kv.page_table = d_page_table;
+    HC_CUDA(launch_kv_gather(kv, pos0, n_rows, d_rows, as_stream(stream)));
   });
 }
 

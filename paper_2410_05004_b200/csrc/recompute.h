@@ -18,6 +18,24 @@ void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n
                          cudaStream_t stream, const std::function<void(int, bool)>& hook,
                          void* d_layer_inputs = nullptr, int32_t* next_token = nullptr);
 
+// Sequences of a batched forward: nullptr cu = one sequence from position 0.
+struct SeqBatch {
+  int n_seqs = 1;
+  const int32_t* cu = nullptr;         // device [n_seqs + 1] row offsets
+  const int32_t* seq_start = nullptr;  // device [n_seqs] first positions
+  int max_new = 0;
+  int table_stride = 0;
+};
+
+// forward_tokens / decode_step (model.cpp:305-347) for a batch of sequences
+// continuing their paged caches: sequence s appends new_lens[s] tokens at
+// positions start_pos[s].. (host arrays). d_next_tokens[s] = greedy token
+// after the sequence's last row.
+void forward_batch(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
+                   const int32_t* new_lens, const int32_t* start_pos, const hc_kv_pages* pages,
+                   const int32_t* d_page_tables, int table_stride, void* d_layer_inputs,
+                   int32_t* d_next_tokens, cudaStream_t stream);
+
 // Measured seconds of one recompute layer over n tokens (0 when the full
 // block weights are not set).
 double recompute_layer_seconds(const hc_weights* w, int n);

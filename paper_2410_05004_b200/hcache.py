@@ -604,6 +604,34 @@ def restore_token_wise(store: StorageManager, session_id: str, w: Weights, hidde
     return RestoreResult(kv, Timeline.from_c(tc))
 
 
+def forward_batch(w: Weights, tokens, new_lens: Sequence[int], start_pos: Sequence[int],
+                  kv: KvCache, page_tables, layer_inputs=None, stream=None):
+    """forward_tokens / decode_step (model.cpp:305-347) batched over sequences
+    continuing their paged caches. tokens: int32 CUDA (sum(new_lens)),
+    page_tables: int32 CUDA [n_seqs x stride]. Returns the next tokens (int32
+    CUDA [n_seqs])."""
+    import torch
+    n = len(new_lens)
+    nl = (C.c_int32 * n)(*new_lens)
+    sp = (C.c_int32 * n)(*start_pos)
+    nxt = torch.empty(n, dtype=torch.int32, device=tokens.device)
+    tables = page_tables if page_tables.dim() == 2 else page_tables.view(1, -1)
+    check(lib().hc_forward_batch(w._h, tokens.data_ptr(), n, nl, sp, C.byref(kv.desc),
+                                 tables.data_ptr(), tables.shape[1],
+                                 None if layer_inputs is None else layer_inputs.data_ptr(),
+                                 nxt.data_ptr(), _stream(stream)))
+    return nxt
+
+
+def kv_gather_rows(kv: KvCache, layer: int, page_table, pos0: int, n: int, stream=None):
+    """Interleaved [K_row | V_row] rows of positions [pos0, pos0+n) (device)."""
+    import torch
+    rows = torch.empty((n, 2 * kv.d_kv), dtype=torch.bfloat16, device=page_table.device)
+    check(lib().hc_kv_gather_rows(C.byref(kv.desc), layer, page_table.data_ptr(), pos0, n,
+                                  rows.data_ptr(), _stream(stream)))
+    return rows
+
+
 def profile_hardware(w: Weights, n_tokens: int) -> ProfiledTimings:
     """harness.hpp:76-77, measured on the device."""
     t = capi.TimingsC()
