@@ -452,6 +452,83 @@ hc_status hc_bench_project(const hc_weights* w, int32_t layer, const void* d_hid
 /* Pinned host->device copy bandwidth (bytes/s) for a `bytes` transfer. */
 hc_status hc_measure_h2d(int32_t device, size_t bytes, int32_t reps, double* bytes_per_s);
 
+/* ---------------------------------------------------------- serving loop */
+/* Strategy / SavingMode (harness.hpp:14-17). */
+typedef enum hc_strategy {
+  HC_STRATEGY_HCACHE = 0,
+  HC_STRATEGY_KV_OFFLOAD = 1,
+  HC_STRATEGY_RECOMPUTE = 2,
+  HC_STRATEGY_IDEAL = 3
+} hc_strategy;
+typedef enum hc_saving_mode {
+  HC_SAVING_TWO_STAGE = 0, /* D2H on a side stream into the store FIFO, chunking by the daemon */
+  HC_SAVING_DIRECT = 1,    /* synchronous copies and persistence on the serving thread */
+  HC_SAVING_OFF = 2        /* persisted, but outside the clock (reference: cost 0) */
+} hc_saving_mode;
+
+/* Request (trace.hpp:11-19). */
+typedef struct hc_request {
+  const char* session_id;
+  int32_t round;
+  int32_t n_context; /* long-context pre-ingested tokens (0 for conversations) */
+  const int32_t* context;
+  int32_t n_prompt;
+  int32_t output_budget;
+  const int32_t* prompt;
+  double arrival_s;
+} hc_request;
+
+/* RunOptions (harness.hpp:60-65) for the device engine. */
+typedef struct hc_serve_opts {
+  int32_t strategy;     /* hc_strategy */
+  int32_t saving;       /* hc_saving_mode */
+  hc_plan plan;         /* HC_STRATEGY_HCACHE's per-layer plan */
+  int32_t page_size;    /* KV page size (tokens), 0 -> 64 */
+  int32_t num_pages;    /* KV page pool (pages of page_size tokens, all layers) */
+  int32_t max_batch;    /* decode batch cap, 0 -> unbounded */
+  int32_t pad_;
+} hc_serve_opts;
+
+/* RequestMetrics (harness.hpp:27-36); times in seconds of the engine clock. */
+typedef struct hc_request_metrics {
+  int32_t round;
+  int32_t history_tokens;
+  int32_t generated;
+  int32_t pad_;
+  double arrival_s;
+  double restore_s;
+  double ttft_s;
+  double tbt_s;
+} hc_request_metrics;
+
+/* Metrics aggregates (harness.hpp:38-55) + engine extras. */
+typedef struct hc_serve_metrics {
+  double ttft_p50, ttft_p95;
+  double tbt_mean, tbt_p50, tbt_p95;
+  double restore_tokens_per_s;
+  double storage_bytes_per_token;
+  uint64_t saved_bytes, saved_tokens, backpressure_stalls;
+  double busy_s;          /* restore + prefill + decode + charged saving time */
+  double save_stall_s;    /* charged saving time (DIRECT copies, backpressure waits) */
+  double persist_wait_s;  /* uncharged waits for a previous round's persistence */
+  int64_t decode_steps;
+  int64_t decode_tokens;
+} hc_serve_metrics;
+
+/* run (harness.hpp:67-72, harness.cpp:189-429) on the GPU: restore -> prefill
+ * -> continuous-batching decode per request, one restoration+prefill in flight
+ * (strict phase ordering), saving each round's states per the strategy's plan
+ * into `store`. The clock advances by the measured duration of every phase
+ * (host wall time with the stream synchronised: restore, prompt prefill,
+ * decode steps, charged saving); idle gaps jump to the next arrival.
+ * Requests must be sorted by arrival. outputs: sum(output_budget) token ids,
+ * request order. per_request: n_requests entries. Weights need the full
+ * blocks and the embedding. */
+hc_status hc_serve_run(hc_store* store, const hc_weights* w, const hc_request* requests,
+                       int32_t n_requests, const hc_serve_opts* opts,
+                       hc_request_metrics* per_request, int32_t* outputs, hc_serve_metrics* out,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -302,6 +302,9 @@ class Reference:
                                             _i32p, _i32p, _f64p, _f64p, C.POINTER(C.c_double),
                                             C.POINTER(C.c_double)]
         L.ref_conversation_history.argtypes = [C.c_int, C.c_int, C.c_ulonglong, _i32p]
+        L.ref_gen_trace.restype = C.c_int
+        L.ref_gen_trace.argtypes = [C.c_int, C.c_int, C.c_int, C.c_ulonglong, C.c_int, _i32p,
+                                    C.c_void_p, C.c_void_p]
         L.ref_restore_wall.restype = C.c_double
         L.ref_restore_wall.argtypes = [C.c_int] * 7 + [C.c_ulonglong, C.c_char_p,
                                                        C.POINTER(C.c_double)]
@@ -403,6 +406,17 @@ class Reference:
         out = np.empty(n_sessions * rounds, np.int32)
         self.lib.ref_conversation_history(n_sessions, rounds, seed, out)
         return out
+
+    def gen_trace(self, kind, n_sessions, rounds, seed, max_out=4096):
+        """(meta [k x 6], arrival [k], token-hash [k]) in arrival order."""
+        meta = np.empty((max_out, 6), np.int32)
+        arr = np.empty(max_out, np.float64)
+        hsh = np.empty(max_out, np.uint64)
+        k = self.lib.ref_gen_trace(kind, n_sessions, rounds, seed, max_out, meta, arr.ctypes.data,
+                                   hsh.ctypes.data)
+        if k < 0:
+            raise RuntimeError("ref_gen_trace failed")
+        return meta[:k], arr[:k], hsh[:k]
 
     def restore_wall(self, n_layers, d, n_heads, d_ffn, vocab, n, elem_bytes, seed, root):
         diff = C.c_double()

@@ -145,8 +145,15 @@ def storage_goldens(ref: Reference):
 
 
 def trace_goldens(ref: Reference):
-    return {"n_sessions": 32, "rounds": 4, "seed": 7,
-            "history": ref.conversation_history(32, 4, 7).tolist()}
+    out = {"n_sessions": 32, "rounds": 4, "seed": 7,
+           "history": ref.conversation_history(32, 4, 7).tolist(), "full": []}
+    # full gen_trace outputs (arrival order) for conversation and long-context
+    for kind, n_s, rounds, seed in ((0, 32, 4, 7), (0, 5, 3, 11), (1, 6, 1, 3)):
+        meta, arr, hsh = ref.gen_trace(kind, n_s, rounds, seed)
+        out["full"].append({"kind": kind, "n_sessions": n_s, "rounds": rounds, "seed": seed,
+                            "meta": meta.tolist(), "arrival": arr.tolist(),
+                            "token_fnv": [str(int(h)) for h in hsh]})
+    return out
 
 
 def fp16_goldens(ref: Reference):

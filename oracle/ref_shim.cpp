@@ -282,6 +282,48 @@ int ref_conversation_history(int n_sessions, int rounds, unsigned long long seed
   }
 }
 
+// gen_trace (trace.cpp:55-100) in arrival order: per request
+// meta[6*i..] = {session index, round, history, n_context, n_prompt, budget},
+// arrival[i], hash[i] = FNV-1a over the context then prompt token ids (int32).
+int ref_gen_trace(int kind, int n_sessions, int rounds, unsigned long long seed, int max_out,
+                  int* meta, double* arrival, unsigned long long* hash) {
+  try {
+    TraceParams p;
+    p.n_sessions = n_sessions;
+    p.rounds = rounds;
+    Trace tr = gen_trace(kind == 0 ? TraceKind::Conversation : TraceKind::LongContext, p, seed);
+    int k = 0;
+    for (const auto& r : tr.requests) {
+      if (k >= max_out) return -1;
+      meta[6 * k + 0] = std::stoi(r.session_id.substr(4));
+      meta[6 * k + 1] = r.round;
+      meta[6 * k + 2] = r.history_tokens;
+      meta[6 * k + 3] = int(r.context.size());
+      meta[6 * k + 4] = int(r.prompt.size());
+      meta[6 * k + 5] = r.output_budget;
+      arrival[k] = r.arrival_s;
+      unsigned long long h = 1469598103934665603ull;
+      auto mix = [&](const std::vector<int>& v) {
+        for (int t : v) {
+          const int32_t x = t;
+          const unsigned char* b = reinterpret_cast<const unsigned char*>(&x);
+          for (int j = 0; j < 4; ++j) {
+            h ^= b[j];
+            h *= 1099511628211ull;
+          }
+        }
+      };
+      mix(r.context);
+      mix(r.prompt);
+      hash[k] = h;
+      ++k;
+    }
+    return k;
+  } catch (...) {
+    return -1;
+  }
+}
+
 // The reference restore() as shipped: WallClock mode, one compute thread and
 // one IO thread, store on `root` (use tmpfs). Config and seed as given, plan
 // all-hidden, tokens (i*11+1)%vocab. Returns timeline.total_s (or -1).

@@ -91,6 +91,30 @@ class RestoreOptsC(C.Structure):
     _fields_ = [("prefetch_depth", i32), ("timeline", i32), ("pad_", i32 * 2)]
 
 
+class RequestC(C.Structure):
+    _fields_ = [("session_id", cp), ("round", i32), ("n_context", i32), ("context", C.POINTER(i32)),
+                ("n_prompt", i32), ("output_budget", i32), ("prompt", C.POINTER(i32)),
+                ("arrival_s", f64)]
+
+
+class ServeOptsC(C.Structure):
+    _fields_ = [("strategy", i32), ("saving", i32), ("plan", PlanC), ("page_size", i32),
+                ("num_pages", i32), ("max_batch", i32), ("pad_", i32)]
+
+
+class RequestMetricsC(C.Structure):
+    _fields_ = [("round", i32), ("history_tokens", i32), ("generated", i32), ("pad_", i32),
+                ("arrival_s", f64), ("restore_s", f64), ("ttft_s", f64), ("tbt_s", f64)]
+
+
+class ServeMetricsC(C.Structure):
+    _fields_ = [("ttft_p50", f64), ("ttft_p95", f64), ("tbt_mean", f64), ("tbt_p50", f64),
+                ("tbt_p95", f64), ("restore_tokens_per_s", f64), ("storage_bytes_per_token", f64),
+                ("saved_bytes", u64), ("saved_tokens", u64), ("backpressure_stalls", u64),
+                ("busy_s", f64), ("save_stall_s", f64), ("persist_wait_s", f64),
+                ("decode_steps", i64), ("decode_tokens", i64)]
+
+
 P = C.POINTER
 _PROTOS = {
     "hc_last_error": (cp, []),
@@ -148,6 +172,8 @@ _PROTOS = {
                          P(TimelineC)]),
     "hc_restore_batch": (i32, [vp, P(cp), i32, vp, P(RestoreOptsC), P(KvPagesC), vp, i32, vp,
                                P(TimelineC)]),
+    "hc_serve_run": (i32, [vp, vp, P(RequestC), i32, P(ServeOptsC), P(RequestMetricsC), vp,
+                           P(ServeMetricsC), vp]),
     "hc_forward_batch": (i32, [vp, vp, i32, vp, vp, P(KvPagesC), vp, i32, vp, vp, vp]),
     "hc_kv_gather_rows": (i32, [P(KvPagesC), i32, vp, i32, i64, vp, vp]),
     "hc_restore_token_wise": (i32, [vp, cp, vp, i32, P(KvPagesC), vp, vp, P(TimelineC)]),

@@ -303,10 +303,12 @@ uint8_t* Store::new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx) 
   return p;
 }
 
-int64_t Store::drain_locked(int64_t max_chunks) {
+int64_t Store::drain_locked(int64_t max_chunks, bool block) {
   // drain_locked (storage.cpp:162-191)
   int64_t flushed = 0;
   while (!fifo_.empty() && flushed < max_chunks) {
+    if (!block && fifo_.front().ready && cudaEventQuery(fifo_.front().ready) == cudaErrorNotReady)
+      break;
     Record rec = fifo_.front();
     fifo_.pop_front();
     fifo_bytes_ -= rec.bytes;
@@ -502,11 +504,18 @@ void Store::start_daemon() {
       cv_.wait_for(lk, std::chrono::milliseconds(5),
                    [this] { return !fifo_.empty() || !daemon_run_; });
       try {
-        drain_locked(INT64_MAX);
+        drain_locked(INT64_MAX, false);
       } catch (...) {
       }
+      if (!fifo_.empty() && daemon_run_)  // a D2H still in flight: poll without holding mu_
+        cv_.wait_for(lk, std::chrono::microseconds(200));
     }
   });
+}
+
+bool Store::daemon_running() const {
+  std::lock_guard<std::mutex> lk(mu_);
+  return daemon_run_;
 }
 
 void Store::stop_daemon() {

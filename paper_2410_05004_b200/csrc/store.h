@@ -118,6 +118,7 @@ class Store {
                   const void** payload, int64_t* bytes) const;
   std::vector<int64_t> device_chunk_counts() const;
   void start_daemon();
+  bool daemon_running() const;
   void stop_daemon();
   size_t buffer_bytes() const;
   size_t capacity() const { return capacity_; }
@@ -136,7 +137,9 @@ class Store {
     size_t bytes = 0;
     cudaEvent_t ready = nullptr;  // D2H completion (device-sourced rows)
   };
-  int64_t drain_locked(int64_t max_chunks);
+  // block=false stops at the first record whose device->host copy is still
+  // in flight (the daemon never waits on the GPU while holding mu_).
+  int64_t drain_locked(int64_t max_chunks, bool block = true);
   uint8_t* new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx);
   Session& find_open(const std::string& sid);
 

@@ -19,6 +19,7 @@ Reference exceptions map as: std::invalid_argument -> ``InvalidArgument``
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import List, Optional, Sequence
@@ -643,3 +644,248 @@ def measure_h2d(bytes_: int, reps: int = 5, device: int = 0) -> float:
     out = C.c_double()
     check(lib().hc_measure_h2d(device, bytes_, reps, C.byref(out)))
     return out.value
+
+
+# ----------------------------------------------------------------- serving
+class Strategy(IntEnum):
+    """harness.hpp:14"""
+    HCACHE = 0
+    KV_OFFLOAD = 1
+    RECOMPUTE = 2
+    IDEAL = 3
+
+
+class SavingMode(IntEnum):
+    """harness.hpp:17 (device meaning: see hc_saving_mode)."""
+    TWO_STAGE = 0
+    DIRECT = 1
+    OFF = 2
+
+
+class TraceKind(IntEnum):
+    CONVERSATION = 0
+    LONG_CONTEXT = 1
+
+
+@dataclass
+class Request:
+    """trace.hpp:11-19"""
+    session_id: str
+    round: int = 1
+    history_tokens: int = 0
+    context: List[int] = field(default_factory=list)
+    prompt: List[int] = field(default_factory=list)
+    output_budget: int = 1
+    arrival_s: float = 0.0
+
+
+@dataclass
+class TraceParams:
+    """trace.hpp:21-36"""
+    n_sessions: int = 4
+    rounds: int = 3
+    mean_input: float = 66.8
+    mean_output: float = 358.8
+    arrival_rate_per_s: float = 0.1
+    round_gap_s: float = 30.0
+    ctx_min: int = 4096
+    ctx_max: int = 16384
+    lc_mean_input: float = 44.7
+    lc_mean_output: float = 50.2
+    lc_max_io: int = 99
+    vocab: int = 1024
+
+    def validate(self):
+        """trace.cpp:44-53"""
+        if self.n_sessions < 1 or self.rounds < 1 or self.vocab < 1:
+            raise ValueError("TraceParams: counts must be >= 1")
+        if min(self.mean_input, self.mean_output, self.lc_mean_input, self.lc_mean_output) < 1:
+            raise ValueError("TraceParams: means must be >= 1")
+        if self.arrival_rate_per_s <= 0 or self.round_gap_s < 0:
+            raise ValueError("TraceParams: bad arrival parameters")
+        if self.ctx_min < 1 or self.ctx_max < self.ctx_min:
+            raise ValueError("TraceParams: bad context range")
+
+
+@dataclass
+class Trace:
+    kind: TraceKind
+    params: TraceParams
+    seed: int
+    requests: List[Request]
+
+
+class _TraceRng:
+    """The trace generator's splitmix64 stream (trace.cpp:11-39)."""
+    M = (1 << 64) - 1
+
+    def __init__(self, seed):
+        self.s = (seed ^ 0xA5A5A5A5DEADBEEF) & self.M
+
+    def next(self):
+        self.s = (self.s + 0x9E3779B97F4A7C15) & self.M
+        z = self.s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & self.M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & self.M
+        return z ^ (z >> 31)
+
+    def uniform(self):
+        return float(self.next() >> 11) * 2.0 ** -53
+
+    def geometric(self, mean):
+        p = 1.0 / max(1.0, mean)
+        u = max(self.uniform(), 1e-300)
+        return 1 + int(math.floor(math.log(u) / math.log(1.0 - p)))
+
+    def exponential(self, rate):
+        return -math.log(max(self.uniform(), 1e-300)) / rate
+
+    def uniform_int(self, lo, hi):
+        return lo + int(self.next() % (hi - lo + 1))
+
+    def tokens(self, n, vocab):
+        return [int(self.next() % vocab) for _ in range(n)]
+
+
+def gen_trace(kind: TraceKind, params: TraceParams, seed: int) -> Trace:
+    """gen_trace (trace.cpp:55-100): Poisson session starts, geometric prompt
+    and output lengths, conversation rounds round_gap_s apart (or one
+    long-context request per session); sorted by arrival (stable)."""
+    params.validate()
+    rng = _TraceRng(seed)
+    reqs = []
+    arrival = 0.0
+    for s in range(params.n_sessions):
+        arrival += rng.exponential(params.arrival_rate_per_s)
+        sid = f"sess{s}"
+        if kind == TraceKind.CONVERSATION:
+            history = 0
+            for r in range(1, params.rounds + 1):
+                prompt = rng.tokens(rng.geometric(params.mean_input), params.vocab)
+                budget = rng.geometric(params.mean_output)
+                reqs.append(Request(sid, r, history, [], prompt, budget,
+                                    arrival + float(r - 1) * params.round_gap_s))
+                history += len(prompt) + budget
+        else:
+            ctx = rng.tokens(rng.uniform_int(params.ctx_min, params.ctx_max), params.vocab)
+            prompt = rng.tokens(min(params.lc_max_io, rng.geometric(params.lc_mean_input)),
+                                params.vocab)
+            budget = min(params.lc_max_io, rng.geometric(params.lc_mean_output))
+            reqs.append(Request(sid, 1, len(ctx), ctx, prompt, budget, arrival))
+    reqs.sort(key=lambda r: r.arrival_s)  # stable, like std::stable_sort
+    return Trace(kind, params, seed, reqs)
+
+
+@dataclass
+class RequestMetrics:
+    """harness.hpp:27-36"""
+    session_id: str
+    round: int
+    arrival_s: float
+    history_tokens: int
+    restore_s: float
+    ttft_s: float
+    tbt_s: float
+    generated: int
+
+
+@dataclass
+class Metrics:
+    """harness.hpp:38-55 + the device engine's extras."""
+    strategy: Strategy
+    per_request: List[RequestMetrics]
+    outputs: List[List[int]]
+    ttft_p50: float = 0.0
+    ttft_p95: float = 0.0
+    tbt_mean: float = 0.0
+    tbt_p50: float = 0.0
+    tbt_p95: float = 0.0
+    restore_tokens_per_s: float = 0.0
+    storage_bytes_per_token: float = 0.0
+    saved_bytes: int = 0
+    saved_tokens: int = 0
+    backpressure_stalls: int = 0
+    busy_s: float = 0.0
+    save_stall_s: float = 0.0
+    persist_wait_s: float = 0.0
+    decode_steps: int = 0
+    decode_tokens: int = 0
+
+
+@dataclass
+class RunOptions:
+    """harness.hpp:60-65 for the device engine. num_pages: KV page pool (all
+    layers); None sizes it for the worst case of the trace."""
+    strategy: Strategy = Strategy.HCACHE
+    saving: SavingMode = SavingMode.TWO_STAGE
+    hcache_plan: Optional[RestorationPlan] = None
+    page_size: int = 64
+    num_pages: Optional[int] = None
+    max_batch: int = 0
+
+
+def run(trace, w: Weights, store: StorageManager, opt: RunOptions, stream=None) -> Metrics:
+    """run (harness.cpp:189-429) on the GPU through hc_serve_run: restore ->
+    prefill -> continuous-batching decode over the trace, the clock advanced
+    by measured phase durations."""
+    reqs = trace.requests if isinstance(trace, Trace) else list(trace)
+    n = len(reqs)
+    keep = []
+    arr = (capi.RequestC * max(n, 1))()
+    hist, need, active_need = {}, [], []
+    for i, r in enumerate(reqs):
+        ctx = (C.c_int32 * max(len(r.context), 1))(*r.context)
+        pr = (C.c_int32 * max(len(r.prompt), 1))(*r.prompt)
+        sid = r.session_id.encode()
+        keep += [ctx, pr, sid]
+        arr[i] = capi.RequestC(sid, r.round, len(r.context), ctx, len(r.prompt), r.output_budget,
+                               pr, r.arrival_s)
+        h = hist.get(r.session_id, 0) or len(r.context)
+        need.append(-(-(h + len(r.prompt) + r.output_budget) // opt.page_size))
+        hist[r.session_id] = h + len(r.prompt) + r.output_budget
+    num_pages = opt.num_pages
+    if num_pages is None:
+        cap = opt.max_batch + 1 if opt.max_batch > 0 else n
+        num_pages = max(1, sum(sorted(need, reverse=True)[:cap]))
+    p = opt.hcache_plan or RestorationPlan.make(w.cfg.n_layers, w.cfg.n_layers, Complement.NONE)
+    o = capi.ServeOptsC(int(opt.strategy), int(opt.saving), p._c, opt.page_size, num_pages,
+                        opt.max_batch, 0)
+    per = (capi.RequestMetricsC * max(n, 1))()
+    outs = (C.c_int32 * max(1, sum(r.output_budget for r in reqs)))()
+    m = capi.ServeMetricsC()
+    check(lib().hc_serve_run(store._h, w._h, arr, n, C.byref(o), per, outs, C.byref(m),
+                             _stream(stream)))
+    pr_list, out_list, off = [], [], 0
+    for i, r in enumerate(reqs):
+        q = per[i]
+        pr_list.append(RequestMetrics(r.session_id, q.round, q.arrival_s, q.history_tokens,
+                                      q.restore_s, q.ttft_s, q.tbt_s, q.generated))
+        out_list.append(list(outs[off:off + r.output_budget]))
+        off += r.output_budget
+    return Metrics(opt.strategy, pr_list, out_list, m.ttft_p50, m.ttft_p95, m.tbt_mean, m.tbt_p50,
+                   m.tbt_p95, m.restore_tokens_per_s, m.storage_bytes_per_token, m.saved_bytes,
+                   m.saved_tokens, m.backpressure_stalls, m.busy_s, m.save_stall_s,
+                   m.persist_wait_s, m.decode_steps, m.decode_tokens)
+
+
+def report(sets: Sequence[Metrics], csv: bool = False) -> str:
+    """report (harness.cpp:492-525): one row per strategy, TTFT ratio vs HCACHE."""
+    hc = next((m for m in sets if m.strategy == Strategy.HCACHE), None)
+    rows = []
+    if csv:
+        rows.append("strategy,requests,ttft_p50_s,ttft_p95_s,tbt_mean_s,restore_tok_per_s,"
+                    "bytes_per_token,ttft_vs_hcache")
+    else:
+        rows.append(f"{'strategy':<12}{'reqs':>6}{'ttft_p50':>14}{'ttft_p95':>14}{'tbt_mean':>14}"
+                    f"{'restore_tok/s':>16}{'bytes/tok':>12}{'vs_hc':>10}")
+    for m in sets:
+        ratio = m.ttft_p50 / hc.ttft_p50 if hc and hc.ttft_p50 > 0 else 0.0
+        if csv:
+            rows.append(f"{m.strategy.name},{len(m.per_request)},{m.ttft_p50!r},{m.ttft_p95!r},"
+                        f"{m.tbt_mean!r},{m.restore_tokens_per_s!r},{m.storage_bytes_per_token!r},"
+                        f"{ratio!r}")
+        else:
+            rows.append(f"{m.strategy.name:<12}{len(m.per_request):>6}{m.ttft_p50:>14.5g}"
+                        f"{m.ttft_p95:>14.5g}{m.tbt_mean:>14.5g}{m.restore_tokens_per_s:>16.5g}"
+                        f"{m.storage_bytes_per_token:>12.5g}{ratio:>10.2f}")
+    return "\n".join(rows) + "\n"
