@@ -433,6 +433,9 @@ hc_status hc_prefill(const hc_weights* w, const int32_t* d_tokens, int64_t n,
 hc_status hc_attention_dense(const void* d_q, int32_t n, int32_t n_heads, int32_t n_kv_heads,
                              int32_t d_head, const void* d_k, const void* d_v, int32_t d_kv,
                              void* d_out, void* stream);
+/* mode | HC_GEMM_SPLIT_K: allow the decode-shape path (M <= 128: K split over
+ * CTAs, fp32 partials reduced in a fixed order by a second kernel). */
+#define HC_GEMM_SPLIT_K 0x100
 hc_status hc_gemm_epilogue(int32_t mode, const void* d_a, const void* d_b, int32_t m, int32_t n,
                            int32_t k, float* d_x, void* d_xb, const float* d_mean,
                            const float* d_rstd, const float* d_colsum, int32_t device,

@@ -9,6 +9,7 @@
 // with exp2. Causal blocks are scheduled heaviest first.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "kernels.h"
@@ -230,6 +231,130 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- decode
+// One query row per sequence (decode_step, model.cpp:332-347): split-KV
+// flash-decoding on the CUDA cores -- the step is HBM-bound on the K/V pages,
+// so every SM streams a slice of one sequence's keys for one KV head.
+// grid (n_kv_heads, n_seqs, n_splits), 128 threads: DH/8 lanes share a key
+// (16 B of K and V each), 4 keys per warp-pass x 4 in flight per lane group.
+// Each (warp, lane-group) keeps an online-softmax state; the CTA merges them
+// and writes this split's (max, sum, acc) for the combine kernel.
+constexpr int kDecThreads = 128;
+
+template <int DH>
+__global__ void __launch_bounds__(kDecThreads)
+    attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_heads, int group, KvOut kv,
+                       const int32_t* __restrict__ cu_q, const int32_t* __restrict__ seq_start,
+                       int n_splits, float scale_log2, float* __restrict__ part) {
+  constexpr int LPK = DH / 8;            // lanes per key
+  constexpr int KPW = 32 / LPK;          // keys per warp pass
+  constexpr int KPB = KPW * (kDecThreads / 32);  // keys per block pass
+  constexpr int UNROLL = 4;
+  const int hk = blockIdx.x, z = blockIdx.y, split = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = lane / LPK, li = lane % LPK;  // key slot in the warp, lane in the key
+  const int row = __ldg(cu_q + z);
+  const int n_keys = __ldg(seq_start + z) + 1;
+  const int per = (n_keys + n_splits - 1) / n_splits;
+  const int k_begin = split * per, k_end = min(n_keys, k_begin + per);
+  const int32_t* table = kv.page_table ? kv.page_table + int64_t(z) * kv.table_stride : nullptr;
+  const int ld = n_heads * DH;
+  __shared__ float red_m[kDecThreads / LPK], red_l[kDecThreads / LPK];
+  __shared__ float red_acc[kDecThreads / LPK][DH];
+
+  for (int g = 0; g < group; ++g) {
+    const int h = hk * group + g;
+    float qf[8];
+    {
+      const uint4 u = *reinterpret_cast<const uint4*>(q + size_t(row) * ld + h * DH + li * 8);
+      const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) qf[e] = __bfloat162float(hv[e]) * scale_log2;
+    }
+    float m = -INFINITY, l = 0.f, acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    // warp-uniform trip count: the key-group shuffles below need every lane
+    for (int k0 = k_begin + warp * KPW; k0 < k_end; k0 += KPB * UNROLL) {
+      uint4 kr[UNROLL], vr[UNROLL];
+      bool ok[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int key = k0 + sub + u * KPB;
+        ok[u] = key < k_end;
+        int64_t orow = key;
+        if (ok[u] && table)
+          orow = int64_t(__ldg(table + key / kv.page_size)) * kv.page_size + key % kv.page_size;
+        const size_t off = size_t(ok[u] ? orow : 0) * kv.d_kv + size_t(hk) * DH + size_t(li) * 8;
+        kr[u] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(kv.k_base) + off));
+        vr[u] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(kv.v_base) + off));
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const __nv_bfloat16* kh = reinterpret_cast<const __nv_bfloat16*>(&kr[u]);
+        float sc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sc += qf[e] * __bfloat162float(kh[e]);
+#pragma unroll
+        for (int o = LPK / 2; o; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+        if (!ok[u]) continue;  // uniform across the key's lanes
+        const float m_new = fmaxf(m, sc);
+        const float corr = exp2f(m - m_new), p = exp2f(sc - m_new);
+        const __nv_bfloat16* vh = reinterpret_cast<const __nv_bfloat16*>(&vr[u]);
+        l = l * corr + p;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = acc[e] * corr + p * __bfloat162float(vh[e]);
+        m = m_new;
+      }
+    }
+    // merge the kDecThreads / LPK key-slot states of the block
+    const int slot = tid / LPK;
+    if (li == 0) {
+      red_m[slot] = m;
+      red_l[slot] = l;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red_acc[slot][li * 8 + e] = acc[e];
+    __syncthreads();
+    if (tid < DH) {
+      float M = -INFINITY;
+      for (int s2 = 0; s2 < kDecThreads / LPK; ++s2) M = fmaxf(M, red_m[s2]);
+      float L = 0.f, A = 0.f;
+      for (int s2 = 0; s2 < kDecThreads / LPK; ++s2) {
+        const float c = red_m[s2] == -INFINITY ? 0.f : exp2f(red_m[s2] - M);
+        L += red_l[s2] * c;
+        A += red_acc[s2][tid] * c;
+      }
+      float* dst = part + ((size_t(z) * n_heads + h) * n_splits + split) * (DH + 2);
+      dst[2 + tid] = A;
+      if (tid == 0) {
+        dst[0] = M;
+        dst[1] = L;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// out[row(z), h] = sum_s acc_s * 2^(m_s - M) / sum_s l_s * 2^(m_s - M)
+template <int DH>
+__global__ void attn_decode_combine_kernel(const float* __restrict__ part, int n_heads,
+                                           int n_splits, const int32_t* __restrict__ cu_q,
+                                           __nv_bfloat16* __restrict__ out) {
+  const int h = blockIdx.x, z = blockIdx.y, t = threadIdx.x;
+  const float* base = part + (size_t(z) * n_heads + h) * n_splits * (DH + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < n_splits; ++s) M = fmaxf(M, base[s * (DH + 2)]);
+  float L = 0.f, A = 0.f;
+  for (int s = 0; s < n_splits; ++s) {
+    const float* p = base + s * (DH + 2);
+    const float c = p[0] == -INFINITY ? 0.f : exp2f(p[0] - M);
+    L += p[1] * c;
+    A += p[2 + t] * c;
+  }
+  out[size_t(__ldg(cu_q + z)) * n_heads * DH + h * DH + t] = __float2bfloat16(A / L);
+}
+
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, int64_t n, const uint4* __restrict__ emb,
                              int d, float* __restrict__ x, uint4* __restrict__ xb) {
   const int vec = d / 8;
@@ -267,24 +392,71 @@ __global__ void argmax_logits_kernel(const __nv_bfloat16* __restrict__ emb, int 
   }
 }
 
-// blockIdx.y = sequence: logits of its last row (cu[s+1]-1)
+// Greedy tokens of up to kArgSeqs sequences per block (blockIdx.y = group of
+// sequences): their last rows (fp32) are staged in shared memory, then each
+// warp scores vocabulary rows, reading every embedding row ONCE per group.
+constexpr int kArgSeqs = 8;
+
 __global__ void argmax_rows_kernel(const __nv_bfloat16* __restrict__ emb, int vocab, int d,
                                    const float* __restrict__ x, const int32_t* __restrict__ cu,
-                                   unsigned long long* best) {
-  const int warps = blockDim.x >> 5;
-  const int t = blockIdx.x * warps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (t >= vocab) return;
-  const int s = blockIdx.y;
-  const float* h = x + size_t(__ldg(cu + s + 1) - 1) * d;
-  float acc = 0.f;
-  for (int c = lane; c < d; c += 32) acc += __bfloat162float(emb[size_t(t) * d + c]) * h[c];
+                                   int n_seqs, int per_block, unsigned long long* best) {
+  extern __shared__ float hs[];  // [per_block][d]
+  const int s0 = blockIdx.y * per_block, ns = min(per_block, n_seqs - s0);
+  for (int i = threadIdx.x; i < ns * d; i += blockDim.x) {
+    const int s = i / d, c = i % d;
+    hs[i] = x[size_t(__ldg(cu + s0 + s + 1) - 1) * d + c];
+  }
+  __syncthreads();
+  // each warp scores kRows vocabulary rows at a time, so every h element read
+  // from shared memory feeds kRows FMAs
+  constexpr int kRows = 4;
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int t0 = (blockIdx.x * warps + (threadIdx.x >> 5)) * kRows; t0 < vocab;
+       t0 += gridDim.x * warps * kRows) {
+    float acc[kRows][kArgSeqs];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) {
-    uint32_t u = __float_as_uint(acc);
-    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-    atomicMax(best + s, (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - uint32_t(t)));
+    for (int r = 0; r < kRows; ++r)
+#pragma unroll
+      for (int s = 0; s < kArgSeqs; ++s) acc[r][s] = 0.f;
+    for (int c8 = lane; c8 < d / 8; c8 += 32) {
+      float ev[kRows][8];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        const int t = min(t0 + r, vocab - 1);
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(emb + size_t(t) * d) + c8);
+        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ev[r][e] = __bfloat162float(hv[e]);
+      }
+#pragma unroll
+      for (int s = 0; s < kArgSeqs; ++s) {
+        if (s >= ns) break;
+        const float4 h0 = *reinterpret_cast<const float4*>(hs + s * d + c8 * 8);
+        const float4 h1 = *reinterpret_cast<const float4*>(hs + s * d + c8 * 8 + 4);
+        const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+#pragma unroll
+        for (int r = 0; r < kRows; ++r)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[r][s] += ev[r][e] * hv[e];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const int t = t0 + r;
+#pragma unroll
+      for (int s = 0; s < kArgSeqs; ++s) {
+        if (s >= ns) break;
+        float a = acc[r][s];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0 && t < vocab) {
+          uint32_t u = __float_as_uint(a);
+          u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+          atomicMax(best + s0 + s,
+                    (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - uint32_t(t)));
+        }
+      }
+    }
   }
 }
 
@@ -309,8 +481,15 @@ cudaError_t attention_launch(const void* q, int n, dim3 grid, const int32_t* cu_
   if (dh != 128 && dh != 64) return cudaErrorInvalidValue;
   const size_t sm = size_t(kQ + 4 * kK) * size_t(dh) * 2;
   auto kern = dh == 128 ? attn_fwd_kernel<128> : attn_fwd_kernel<64>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  if (e != cudaSuccess) return e;
+  static thread_local int attr_dev[2] = {-1, -1};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev[dh == 128] != dev) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (e != cudaSuccess) return e;
+    attr_dev[dh == 128] = dev;
+  }
   kern<<<grid, kAttnThreads, sm, stream>>>(static_cast<const __nv_bfloat16*>(q), n, n_heads,
                                            group, kv, static_cast<__nv_bfloat16*>(out),
                                            scale_log2, cu_q, seq_start);
@@ -331,6 +510,33 @@ cudaError_t launch_attention_extend(const void* q, int n_seqs, int max_new, cons
                                     int dh, const KvOut& kv, void* out, cudaStream_t stream) {
   if (n_seqs <= 0 || max_new <= 0) return cudaSuccess;
   if (!cu_q || !seq_start) return cudaErrorInvalidValue;
+  if (max_new == 1 && (dh == 128 || dh == 64)) {
+    // decode: split the keys so ~2 CTAs per SM stream K/V
+    const int group = n_heads / n_kv_heads;
+    int splits = (2 * 148 + n_kv_heads * n_seqs - 1) / (n_kv_heads * n_seqs);
+    splits = splits < 1 ? 1 : splits > 64 ? 64 : splits;
+    float* part = nullptr;
+    const size_t pb = size_t(n_seqs) * n_heads * splits * (dh + 2) * sizeof(float);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&part), pb, stream);
+    if (e != cudaSuccess) return e;
+    const float scale_log2 = (1.0f / sqrtf(float(dh))) * 1.4426950408889634f;
+    const dim3 grid{unsigned(n_kv_heads), unsigned(n_seqs), unsigned(splits)};
+    if (dh == 128) {
+      attn_decode_kernel<128><<<grid, kDecThreads, 0, stream>>>(
+          static_cast<const __nv_bfloat16*>(q), n_heads, group, kv, cu_q, seq_start, splits,
+          scale_log2, part);
+      attn_decode_combine_kernel<128><<<dim3(unsigned(n_heads), unsigned(n_seqs)), 128, 0, stream>>>(
+          part, n_heads, splits, cu_q, static_cast<__nv_bfloat16*>(out));
+    } else {
+      attn_decode_kernel<64><<<grid, kDecThreads, 0, stream>>>(
+          static_cast<const __nv_bfloat16*>(q), n_heads, group, kv, cu_q, seq_start, splits,
+          scale_log2, part);
+      attn_decode_combine_kernel<64><<<dim3(unsigned(n_heads), unsigned(n_seqs)), 64, 0, stream>>>(
+          part, n_heads, splits, cu_q, static_cast<__nv_bfloat16*>(out));
+    }
+    cudaFreeAsync(part, stream);
+    return cudaGetLastError();
+  }
   return attention_launch(q, 0, dim3((max_new + kQ - 1) / kQ, n_heads, n_seqs), cu_q, seq_start,
                           n_heads, n_kv_heads, dh, kv, out, stream);
 }
@@ -362,15 +568,109 @@ cudaError_t launch_argmax_rows(const void* emb, int vocab, int d, const float* h
                                const int32_t* cu, int n_seqs, int32_t* out_tokens,
                                cudaStream_t stream) {
   if (n_seqs <= 0) return cudaSuccess;
+  if (d % 8) return cudaErrorInvalidValue;
+  const int per_block = std::max(1, std::min(kArgSeqs, int((200u << 10) / (unsigned(d) * 4u))));
+  const size_t sm = size_t(per_block) * size_t(d) * sizeof(float);
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(argmax_rows_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
   unsigned long long* best = nullptr;
   cudaError_t e = cudaMallocAsync(&best, sizeof(unsigned long long) * size_t(n_seqs), stream);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(best, 0, sizeof(unsigned long long) * size_t(n_seqs), stream);
-  argmax_rows_kernel<<<dim3(unsigned((vocab + 7) / 8), unsigned(n_seqs)), 256, 0, stream>>>(
-      static_cast<const __nv_bfloat16*>(emb), vocab, d, h, cu, best);
+  const unsigned groups = unsigned((n_seqs + per_block - 1) / per_block);
+  argmax_rows_kernel<<<dim3(148, groups), 512, sm, stream>>>(
+      static_cast<const __nv_bfloat16*>(emb), vocab, d, h, cu, n_seqs, per_block, best);
   argmax_rows_finish_kernel<<<unsigned((n_seqs + 127) / 128), 128, 0, stream>>>(best, n_seqs,
                                                                                out_tokens);
   cudaFreeAsync(best, stream);
+  return cudaGetLastError();
+}
+
+namespace {
+
+// hl rows: [s] = bf16(h_s), [B + s] = bf16(h_s - bf16(h_s)) for the last row
+// h_s of every sequence -- E.hi + E.lo reproduces the fp32 logits to ~2^-17.
+__global__ void hilo_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ cu,
+                                 int n_seqs, int d, __nv_bfloat16* __restrict__ hl) {
+  const int s = blockIdx.y;
+  const float* h = x + size_t(__ldg(cu + s + 1) - 1) * d;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d; c += gridDim.x * blockDim.x) {
+    const float v = h[c];
+    const __nv_bfloat16 hi = __float2bfloat16(v);
+    hl[size_t(s) * d + c] = hi;
+    hl[size_t(n_seqs + s) * d + c] = __float2bfloat16(v - __bfloat162float(hi));
+  }
+}
+
+// out[s] = argmax_t logits[t][s] + logits[t][B + s], ties to the smallest t
+// (argmax_token's strict '>' scan, model.cpp:67-80). One block per sequence.
+__global__ void argmax_pairs_kernel(const float* __restrict__ logits, int vocab, int ld, int n_seqs,
+                                    int32_t* __restrict__ out) {
+  const int s = blockIdx.x;
+  float best = -INFINITY;
+  int arg = 0x7fffffff;
+  for (int t = threadIdx.x; t < vocab; t += blockDim.x) {
+    const float v = logits[size_t(t) * ld + s] + logits[size_t(t) * ld + n_seqs + s];
+    if (v > best) {
+      best = v;
+      arg = t;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (ov > best || (ov == best && oi < arg)) {
+      best = ov;
+      arg = oi;
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sv[warp] = best;
+    si[warp] = arg;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    best = lane < nw ? sv[lane] : -INFINITY;
+    arg = lane < nw ? si[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ov > best || (ov == best && oi < arg)) {
+        best = ov;
+        arg = oi;
+      }
+    }
+    if (lane == 0) out[s] = arg == 0x7fffffff ? 0 : arg;  // all-NaN logits: token 0
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_hilo_rows(const float* x, const int32_t* cu, int n_seqs, int d, void* hl,
+                             cudaStream_t stream) {
+  if (n_seqs <= 0) return cudaSuccess;
+  hilo_rows_kernel<<<dim3(unsigned((d + 255) / 256), unsigned(n_seqs)), 256, 0, stream>>>(
+      x, cu, n_seqs, d, static_cast<__nv_bfloat16*>(hl));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_pairs(const float* logits, int vocab, int ld, int n_seqs, int32_t* out,
+                                cudaStream_t stream) {
+  if (n_seqs <= 0) return cudaSuccess;
+  argmax_pairs_kernel<<<unsigned(n_seqs), 1024, 0, stream>>>(logits, vocab, ld, n_seqs, out);
   return cudaGetLastError();
 }
 

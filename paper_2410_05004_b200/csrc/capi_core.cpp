@@ -28,6 +28,12 @@ int device_sm_count(int dev) {
     int v = 0;
     HC_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
     cache[size_t(dev)] = v;
+    // every compute path passes here first: keep freed stream-ordered scratch
+    // in the pool instead of returning it to the driver at each synchronize
+    cudaMemPool_t pool;
+    HC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thresh = UINT64_MAX;
+    HC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
   }
   return cache[size_t(dev)];
 }
@@ -75,6 +81,17 @@ EpiArgs epi_for(const hc_weights* w, const float* colsum, const float* mean, con
   return e;
 }
 
+// [W_k;W_v] tensor map with a bn-row box: the cached 256/128-row maps, else
+// encoded for the narrow decode-sized tiles.
+CUtensorMap weight_map(const hc_weights::Layer& L, int bn, int d, int rows) {
+  if (bn == 256) return L.tm256;
+  if (bn == 128) return L.tm128;
+  CUtensorMap m;
+  if (!make_tmap_kmajor(&m, L.wkv, uint64_t(d), uint64_t(rows), uint64_t(d) * 2, uint32_t(bn)))
+    fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the weight operand");
+  return m;
+}
+
 void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t n_rows,
                   const KvOut& out, cudaStream_t stream, const float* pre_stats) {
   if (layer < 0 || layer >= w->cfg.n_layers) fail(HC_EINVAL, "project: layer out of range");
@@ -96,11 +113,12 @@ void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t 
     HC_CUDA(launch_row_stats(d_hidden, n_rows, d, d, true, static_cast<float*>(stats.ptr),
                              static_cast<float*>(stats.ptr) + n_rows, stream));
   CUtensorMap tmA;
-  if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2, 128))
+  if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2,
+                        uint32_t(gemm_a_box(n_rows))))
     fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the hidden-state operand");
   const int sms = device_sm_count(w->device);
   const int bn = gemm_pick_bn(n_rows, N, sms);
-  HC_CUDA(launch_restore_kv(tmA, bn == 256 ? L.tm256 : L.tm128, bn, int(n_rows), N, d, true, out,
+  HC_CUDA(launch_restore_kv(tmA, weight_map(L, bn, d, N), bn, int(n_rows), N, d, true, out,
                             epi_for(w, L.colsum, mean, rstd), sms, stream));
 }
 
@@ -371,18 +389,20 @@ hc_status hc_bench_project(const hc_weights* w, int32_t layer, const void* d_hid
     o.v_base = static_cast<char*>(kv.ptr) + size_t(n_rows) * size_t(w->d_kv) * 2;
     o.d_kv = w->d_kv;
     CUtensorMap tmA;
-    if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2, 128))
+    if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2,
+                          uint32_t(gemm_a_box(n_rows))))
       fail(HC_ECUDA, "cuTensorMapEncodeTiled failed");
     const int sms = device_sm_count(w->device);
     const int bn = gemm_pick_bn(n_rows, N, sms);
+    const CUtensorMap tmB = weight_map(L, bn, d, N);
     std::vector<cudaEvent_t> ev(size_t(3 * iters));
     for (auto& e : ev) HC_CUDA(cudaEventCreate(&e));
     for (int i = 0; i < iters; ++i) {
       HC_CUDA(cudaEventRecord(ev[size_t(3 * i)], s));
       HC_CUDA(launch_row_stats(d_hidden, n_rows, d, d, true, mean, mean + n_rows, s));
       HC_CUDA(cudaEventRecord(ev[size_t(3 * i + 1)], s));
-      HC_CUDA(launch_restore_kv(tmA, bn == 256 ? L.tm256 : L.tm128, bn, int(n_rows), N, d, true,
-                                o, epi_for(w, L.colsum, mean, mean + n_rows), sms, s));
+      HC_CUDA(launch_restore_kv(tmA, tmB, bn, int(n_rows), N, d, true, o,
+                                epi_for(w, L.colsum, mean, mean + n_rows), sms, s));
       HC_CUDA(cudaEventRecord(ev[size_t(3 * i + 2)], s));
     }
     HC_CUDA(cudaStreamSynchronize(s));

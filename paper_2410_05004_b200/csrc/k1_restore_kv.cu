@@ -35,7 +35,7 @@ constexpr int kGroupM = 16;
 
 template <int BN>
 struct K1Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kStages = BN == 256 ? 4 : BN == 128 ? 6 : 8;
   static constexpr uint32_t kABytes = kBM * kBK * 2;
   static constexpr uint32_t kBBytes = BN * kBK * 2;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
@@ -148,21 +148,20 @@ __device__ __forceinline__ void epilogue_chunk_dense(float (&f)[32], int mode, i
                        pack_bf16(f[8 * i + 4], f[8 * i + 5]), pack_bf16(f[8 * i + 6], f[8 * i + 7]));
 }
 
-// Epilogue of one accumulator tile for one thread (= one TMEM lane = one
-// output row): per-row metadata, then BN/32 chunks of tcgen05.ld + math +
-// stores. Shared by the single-CTA and the CTA-pair kernels.
-template <int BN, int MODE>
-__device__ __forceinline__ void epilogue_tile(int row, int n_blk, int M, int N, const KvOut& out,
-                                              const GemmOut& gout, const EpiArgs& epi,
-                                              uint32_t tbase, int lane) {
-  (void)lane;
-  const bool row_ok = row < M;
-  // per-row metadata: output rows (dense or paged), LN stats, RoPE position
+// Per-row epilogue metadata: LN stats, RoPE position and the K/V row pointers
+// (dense or paged; ragged batches via cu_seqlens / seq_start).
+struct RowMeta {
   float mean = 0.f, rstd = 1.f;
-  int pos = out.start_pos;
+  int pos = 0;
   char* krow = nullptr;
   char* vrow = nullptr;
-  if (row_ok && MODE == kEpiKv) {
+};
+
+template <int MODE>
+__device__ __forceinline__ RowMeta row_meta(int row, const KvOut& out, const EpiArgs& epi) {
+  RowMeta r;
+  r.pos = out.start_pos;
+  if (MODE == kEpiKv) {
     int seq = 0, local = row;
     if (out.cu_seqlens) {
       int lo = 0, hi = out.n_seqs - 1;
@@ -174,22 +173,47 @@ __device__ __forceinline__ void epilogue_tile(int row, int n_blk, int M, int N, 
       seq = lo;
       local = row - __ldg(out.cu_seqlens + seq);
     }
-    pos = (out.seq_start ? __ldg(out.seq_start + seq) : out.start_pos) + local;
+    r.pos = (out.seq_start ? __ldg(out.seq_start + seq) : out.start_pos) + local;
     int64_t orow;
     if (out.page_table) {
-      int page = __ldg(out.page_table + int64_t(seq) * out.table_stride + pos / out.page_size);
-      orow = int64_t(page) * out.page_size + pos % out.page_size;
+      int page = __ldg(out.page_table + int64_t(seq) * out.table_stride + r.pos / out.page_size);
+      orow = int64_t(page) * out.page_size + r.pos % out.page_size;
     } else {
       orow = row;
     }
     const size_t esz = out.out_f32 ? 4 : 2;
-    krow = static_cast<char*>(out.k_base) + size_t(orow) * out.d_kv * esz;
-    vrow = static_cast<char*>(out.v_base) + size_t(orow) * out.d_kv * esz;
+    r.krow = static_cast<char*>(out.k_base) + size_t(orow) * out.d_kv * esz;
+    r.vrow = static_cast<char*>(out.v_base) + size_t(orow) * out.d_kv * esz;
   }
-  if (row_ok && epi.row_mean) {
-    mean = __ldg(epi.row_mean + row);
-    rstd = __ldg(epi.row_rstd + row);
+  if (epi.row_mean) {
+    r.mean = __ldg(epi.row_mean + row);
+    r.rstd = __ldg(epi.row_rstd + row);
   }
+  return r;
+}
+
+template <int MODE>
+__device__ __forceinline__ void apply_chunk(float (&f)[32], int row, int col0, const RowMeta& r,
+                                            const KvOut& out, const GemmOut& gout,
+                                            const EpiArgs& epi) {
+  if (MODE == kEpiKv) epilogue_chunk(f, col0, out, epi, r.mean, r.rstd, r.pos, r.krow, r.vrow);
+  else epilogue_chunk_dense(f, MODE, row, col0, gout, epi, r.mean, r.rstd);
+}
+
+// Epilogue of one accumulator tile for one thread (= one TMEM lane = one
+// output row): BN/32 chunks of tcgen05.ld + math + stores. Shared by the
+// single-CTA and the CTA-pair kernels. With a split-K workspace (part) the
+// raw fp32 accumulators of this K slice are stored instead
+// (part[(split * M + row) * N + col]) for splitk_epilogue_kernel.
+template <int BN, int MODE>
+__device__ __forceinline__ void epilogue_tile(int row, int n_blk, int M, int N, const KvOut& out,
+                                              const GemmOut& gout, const EpiArgs& epi,
+                                              uint32_t tbase, int lane, float* part = nullptr,
+                                              int split = 0) {
+  (void)lane;
+  const bool row_ok = row < M;
+  RowMeta meta;
+  if (row_ok && !part) meta = row_meta<MODE>(row, out, epi);
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     uint32_t v[32];
@@ -200,24 +224,101 @@ __device__ __forceinline__ void epilogue_tile(int row, int n_blk, int M, int N, 
       float f[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-      if (MODE == kEpiKv) epilogue_chunk(f, col0, out, epi, mean, rstd, pos, krow, vrow);
-      else epilogue_chunk_dense(f, MODE, row, col0, gout, epi, mean, rstd);
+      if (part) {
+        float4* d4 = reinterpret_cast<float4*>(part + (size_t(split) * M + row) * size_t(N) + col0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          d4[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+      } else {
+        apply_chunk<MODE>(f, row, col0, meta, out, gout, epi);
+      }
     }
   }
+}
+
+// Split-K reduction + epilogue: one warp per (row, 32-column chunk), one
+// column per lane. Lane c sums column c over the K slices in slice order
+// (deterministic, coalesced) and applies the mode's epilogue to it -- the
+// same arithmetic as epilogue_chunk / epilogue_chunk_dense, per column (RoPE
+// pairs meet through a lane shuffle).
+template <int MODE>
+__global__ void splitk_epilogue_kernel(const float* __restrict__ part, int splits, int M, int N,
+                                       KvOut out, GemmOut gout, EpiArgs epi) {
+  const int chunks = N / 32;
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= int64_t(M) * chunks) return;  // warp-uniform
+  const int row = int(w / chunks), col = int(w % chunks) * 32 + lane;
+  float v = 0.f;
+  for (int sp = 0; sp < splits; ++sp) v += __ldg(part + (size_t(sp) * M + row) * size_t(N) + col);
+  const RowMeta r = row_meta<MODE>(row, out, epi);
+  if (MODE == kEpiResid) {
+    const size_t off = size_t(row) * size_t(gout.ldo) + size_t(col);
+    const float x = gout.x[off] + v;
+    gout.x[off] = x;
+    static_cast<__nv_bfloat16*>(gout.xb)[off] = __float2bfloat16(x);
+    return;
+  }
+  if (epi.row_mean) v = r.rstd * (v - r.mean * __ldg(epi.colsum + col));
+  if (MODE == kEpiGelu) {
+    v = 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+    static_cast<__nv_bfloat16*>(gout.xb)[size_t(row) * size_t(gout.ldo) + size_t(col)] =
+        __float2bfloat16(v);
+    return;
+  }
+  // kEpiKv
+  const bool is_k = col < out.d_kv;  // uniform per 32-column chunk (d_kv % 32 == 0)
+  const int ocol = is_k ? col : col - out.d_kv;
+  const float other = __shfl_xor_sync(0xffffffffu, v, 1);
+  if (is_k && epi.rope) {
+    const float2 cs = __ldg(epi.rope + size_t(r.pos) * (epi.d_head >> 1) + ((ocol % epi.d_head) >> 1));
+    v = (lane & 1) ? other * cs.y + v * cs.x : v * cs.x - other * cs.y;
+  }
+  char* dst = is_k ? r.krow : r.vrow;
+  if (out.out_f32) reinterpret_cast<float*>(dst)[ocol] = v;
+  else reinterpret_cast<__nv_bfloat16*>(dst)[ocol] = __float2bfloat16(v);
+}
+
+// Shared-memory ring: stage s holds [A rows | B rows] at s * stride. a_rows =
+// rows of the A TMA box (gemm_a_box): 128, or 32/64 when M is that small.
+// In the compact ring (a_rows < 128) the stride is only a_rows*128 + BN*128
+// bytes: the UMMA still reads a 128-row A tile, whose rows >= a_rows are
+// whatever follows (the stage's B rows, the next stage, or the tail pad) --
+// they only feed accumulator rows >= M, which the epilogue never stores. A
+// decode-sized GEMM thus keeps 3-4x more weight bytes in flight per SM.
+constexpr size_t kMaxRingSmem = 227 * 1024;
+
+struct RingCfg {
+  int stages;
+  uint32_t stride;  // bytes per stage
+  uint32_t a_bytes;
+  size_t smem;      // dynamic smem incl. tail pad, barriers, alignment slack
+};
+
+template <int BN>
+RingCfg ring_cfg(int a_rows) {
+  RingCfg r;
+  r.a_bytes = uint32_t(a_rows) * kBK * 2;
+  r.stride = r.a_bytes + K1Cfg<BN>::kBBytes;
+  const uint32_t pad = K1Cfg<BN>::kABytes - r.a_bytes;  // garbage rows past the last stage
+  r.stages = a_rows == kBM ? K1Cfg<BN>::kStages
+                           : int(std::min<size_t>(32, (size_t(200) * 1024 - pad) / r.stride));
+  r.smem = size_t(r.stages) * r.stride + pad + 1024 /*bars*/ + 1024 /*align*/;
+  return r;
 }
 
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
-                   GemmOut gout, EpiArgs epi, uint32_t idesc) {
+                   GemmOut gout, EpiArgs epi, uint32_t idesc, int S, uint32_t stride,
+                   uint32_t a_bytes, int k_splits, float* part) {
   using Cfg = K1Cfg<BN>;
-  constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + S * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kBBytes);
+  uint8_t* sA = smem;  // stage s: A at s*stride, B at s*stride + a_bytes
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(S) * stride +
+                                               (Cfg::kABytes - a_bytes));
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -227,8 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const int num_m = (M + kBM - 1) / kBM;
   const int num_n = (N + BN - 1) / BN;
-  const int num_tiles = num_m * num_n;
+  const int num_mn = num_m * num_n;
+  const int num_tiles = num_mn * k_splits;  // tile = (K slice, M/N tile)
   const int num_kb = (K + kBK - 1) / kBK;
+  const int kb_per = (num_kb + k_splits - 1) / k_splits;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -256,12 +359,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int m_blk, n_blk;
-        tile_coords(tile, num_m, num_n, m_blk, n_blk);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        tile_coords(tile % num_mn, num_m, num_n, m_blk, n_blk);
+        const int kb0 = (tile / num_mn) * kb_per, kb1 = min(num_kb, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-          tma_load_2d(sA + stage * Cfg::kABytes, &tmA, &full[stage], kb * kBK, m_blk * kBM);
-          tma_load_2d(sB + stage * Cfg::kBBytes, &tmB, &full[stage], kb * kBK, n_blk * BN);
+          mbar_arrive_expect_tx(&full[stage], a_bytes + Cfg::kBBytes);
+          uint8_t* st = sA + size_t(stage) * stride;
+          tma_load_2d(st, &tmA, &full[stage], kb * kBK, m_blk * kBM);
+          tma_load_2d(st + a_bytes, &tmB, &full[stage], kb * kBK, n_blk * BN);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -280,15 +385,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = (tile / num_mn) * kb_per, kb1 = min(num_kb, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * Cfg::kABytes));
-          const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * Cfg::kBBytes));
+          const uint8_t* st = sA + size_t(stage) * stride;
+          const uint64_t adesc = umma_desc_sw128(smem_u32(st));
+          const uint64_t bdesc = umma_desc_sw128(smem_u32(st + a_bytes));
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
             umma_f16(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
-                     (kb | k) != 0 ? 1u : 0u);
+                     ((kb - kb0) | k) != 0 ? 1u : 0u);
           umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
           if (++stage == S) {
             stage = 0;
@@ -307,12 +414,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       int m_blk, n_blk;
-      tile_coords(tile, num_m, num_n, m_blk, n_blk);
+      tile_coords(tile % num_mn, num_m, num_n, m_blk, n_blk);
       const int row = m_blk * kBM + q * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       epilogue_tile<BN, MODE>(row, n_blk, M, N, out, gout, epi,
-                              tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN), lane);
+                              tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN), lane,
+                              part, tile / num_mn);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -668,44 +776,126 @@ bool use_pair(int M, int N, int num_sms) {
 template <int BN, int MODE>
 cudaError_t launch_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
                       bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
-                      int num_sms, cudaStream_t stream) {
+                      int num_sms, cudaStream_t stream, bool split_acc = false) {
   const uint32_t idesc = umma_idesc_f16(kBM, BN, bf16_in);
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms ? tiles : num_sms;
   static thread_local int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (attr_dev != dev) {  // once per thread and device
+  if (attr_dev != dev) {  // once per thread and device: the largest ring any call uses
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(K1Cfg<BN>::kSmem));
+                                         int(kMaxRingSmem));
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  tc_gemm_kernel<BN, MODE><<<grid, kThreads, K1Cfg<BN>::kSmem, stream>>>(tmA, tmB, M, N, K, out,
-                                                                         g, epi, idesc);
+  const RingCfg r = ring_cfg<BN>(gemm_a_box(M));
+  // Decode-sized M: a CTA's time is ~(its K blocks) x (a fixed per-MMA cost),
+  // whatever the tile width, so the K loop is split over CTAs (fp32 partials
+  // + splitk_epilogue_kernel). Not used where bit-identical K/V matter.
+  int k_splits = 1;
+  const int num_kb = (K + kBK - 1) / kBK;
+  if (split_acc && M <= kBM && N % 32 == 0) {
+    k_splits = std::max(1, std::min(num_sms / std::max(1, tiles), num_kb / 2));
+    const int kb_per = (num_kb + k_splits - 1) / k_splits;
+    k_splits = (num_kb + kb_per - 1) / kb_per;  // no empty K slice
+  }
+  float* part = nullptr;
+  if (k_splits > 1) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&part),
+                                    size_t(k_splits) * size_t(M) * size_t(N) * sizeof(float), stream);
+    if (e != cudaSuccess) return e;
+  }
+  const int grid_k = std::min(num_sms, tiles * k_splits);
+  tc_gemm_kernel<BN, MODE><<<grid_k, kThreads, r.smem, stream>>>(
+      tmA, tmB, M, N, K, out, g, epi, idesc, r.stages, r.stride, r.a_bytes, k_splits, part);
+  if (k_splits > 1) {
+    const int64_t threads = int64_t(M) * (N / 32) * 32;
+    splitk_epilogue_kernel<MODE><<<unsigned((threads + 255) / 256), 256, 0, stream>>>(
+        part, k_splits, M, N, out, g, epi);
+    cudaFreeAsync(part, stream);
+  }
+  (void)grid;
   return cudaGetLastError();
+}
+
+int gemm_a_box(int64_t M) {
+  static const int forced = [] {  // HC_GEMM_ABOX=128: disable the compact ring (experiments)
+    const char* e = getenv("HC_GEMM_ABOX");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 128) return 128;
+  return M <= 32 ? 32 : M <= 64 ? 64 : 128;
 }
 
 int gemm_pick_bn(int64_t M, int N, int num_sms) {
   if (use_pair(int(M), N, num_sms)) return 128;  // pair kernel: B box of 128 rows
+  static const int forced_bn = [] {  // HC_GEMM_BN: force the small-M tile width (experiments)
+    const char* e = getenv("HC_GEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  if (M <= kBM && (forced_bn == 32 || forced_bn == 64 || forced_bn == 128 || forced_bn == 256))
+    return forced_bn;
+  if (M <= kBM) {
+    // one M tile (decode-sized): the GEMM streams W once, so spread its
+    // columns over every SM -- fewest column-waves x tile width, ties to
+    // the wider tile
+    int best = 256;
+    int64_t best_cost = INT64_MAX;
+    for (int bn : {256, 128, 64, 32}) {
+      const int64_t tiles = (N + bn - 1) / bn;
+      const int64_t cost = ((tiles + num_sms - 1) / num_sms) * bn;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = bn;
+      }
+    }
+    return best;
+  }
   return ((M + kBM - 1) / kBM) * ((N + 255) / 256) >= num_sms ? 256 : 128;
 }
 
+int gemm_pick_bn_skinny(int64_t M, int N, int num_sms) {
+  if (M > kBM) return gemm_pick_bn(M, N, num_sms);
+  return N >= 256 ? 256 : 128;  // wide tiles; the K split supplies the parallelism
+}
+
+namespace {
+
+template <int MODE>
+cudaError_t launch_tc_bn(int bn, const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N,
+                         int K, bool bf16_in, const KvOut& out, const GemmOut& g,
+                         const EpiArgs& epi, int num_sms, cudaStream_t stream, bool split_acc) {
+  switch (bn) {
+    case 256:
+      return launch_tc<256, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc);
+    case 128:
+      return launch_tc<128, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc);
+    case 64:
+      return launch_tc<64, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc);
+    case 32:
+      return launch_tc<32, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream) {
+                              int num_sms, cudaStream_t stream, bool split_acc) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   GemmOut g;
   if (bn == 128 && use_pair(M, N, num_sms))  // tmB has the 128-row box the pair needs
     return launch_pair<kEpiKv>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
-  return bn == 256 ? launch_tc<256, kEpiKv>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream)
-                   : launch_tc<128, kEpiKv>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
+  return launch_tc_bn<kEpiKv>(bn, tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream,
+                              split_acc);
 }
 
 cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,
                               int M, int N, int K, const GemmOut& g, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream) {
+                              int num_sms, cudaStream_t stream, bool split_acc) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   KvOut o;
   if (bn == 128 && use_pair(M, N, num_sms))
@@ -713,10 +903,10 @@ cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, in
                ? launch_pair<kEpiResid>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream)
                : launch_pair<kEpiGelu>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream);
   if (mode == kEpiResid)
-    return bn == 256 ? launch_tc<256, kEpiResid>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream)
-                     : launch_tc<128, kEpiResid>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream);
-  return bn == 256 ? launch_tc<256, kEpiGelu>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream)
-                   : launch_tc<128, kEpiGelu>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream);
+    return launch_tc_bn<kEpiResid>(bn, tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream,
+                                   split_acc);
+  return launch_tc_bn<kEpiGelu>(bn, tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream,
+                                split_acc);
 }
 
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,

@@ -53,20 +53,31 @@ struct GemmOut {
 bool make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows,
                       uint64_t row_stride_bytes, uint32_t box_rows);
 
-// Box rows of the B tensor map for an M x N GEMM (128 or 256). 128 selects the
-// CTA-pair kernel when the problem fills the SM pairs.
+// Box rows of the B tensor map for an M x N GEMM (32, 64, 128 or 256). 128
+// selects the CTA-pair kernel when the problem fills the SM pairs; 32/64 only
+// for a single M tile (decode-sized M), to spread the weight stream over SMs.
 int gemm_pick_bn(int64_t M, int N, int num_sms);
+// B box rows for a GEMM launched with split_acc (decode-sized M is split over
+// K instead of N, so it takes the widest tile).
+int gemm_pick_bn_skinny(int64_t M, int N, int num_sms);
+// Box rows of the A tensor map (K-major, 64-element K box) every caller of the
+// single-CTA GEMM must use for an M-row A operand: 32 / 64 for small M, else 128.
+int gemm_a_box(int64_t M);
 
 // K1: KV[M x N] = epilogue(A[M x K] * B[N x K]^T), N = 2*d_kv (K half, V half).
 // A is described by tmA (box rows 128), B by tmB (box rows 256 or 128 = bn).
+// split_acc: a decode-sized M (<= 128) may split K over CTAs (fp32 partials
+// reduced in a fixed order; a different summation order than the fused path).
+// Off for every K/V projection, so restored K/V stay bit-identical to the K/V
+// a forward wrote.
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream);
+                              int num_sms, cudaStream_t stream, bool split_acc = false);
 
 // The same GEMM with a dense epilogue (mode kEpiResid or kEpiGelu).
 cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,
                               int M, int N, int K, const GemmOut& g, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream);
+                              int num_sms, cudaStream_t stream, bool split_acc = false);
 
 // Causal attention over the paged cache for a prefill from position 0
 // (attention_forward, model.cpp:237-288): q [n x n_heads*dh] bf16 (RoPE
@@ -104,6 +115,14 @@ cudaError_t launch_argmax_logits(const void* emb, int vocab, int d, const float*
 cudaError_t launch_argmax_rows(const void* emb, int vocab, int d, const float* h,
                                const int32_t* cu, int n_seqs, int32_t* out_tokens,
                                cudaStream_t stream);
+
+// Greedy tokens through the tensor cores: hl = [bf16(h_s); bf16(h_s -
+// bf16(h_s))] for each sequence's last row (2*n_seqs x d), logits = E hl^T
+// (GEMM, fp32 [vocab x ld]), out[s] = argmax_t logits[t][s] + logits[t][B+s].
+cudaError_t launch_hilo_rows(const float* x, const int32_t* cu, int n_seqs, int d, void* hl,
+                             cudaStream_t stream);
+cudaError_t launch_argmax_pairs(const float* logits, int vocab, int ld, int n_seqs, int32_t* out,
+                                cudaStream_t stream);
 
 // Pages -> interleaved [K_row | V_row] rows for positions [pos0, pos0 + n) of
 // one sequence (the KV-offload snapshot payload, storage.cpp:67-75).

@@ -15,6 +15,10 @@
 // the H_L the save path snapshots.
 #include <algorithm>
 #include <chrono>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -33,6 +37,58 @@ CUtensorMap tmap(const void* base, int k, int64_t rows, int box_rows) {
 }
 
 int pick_bn(int64_t M, int N, int sms) { return gemm_pick_bn(M, N, sms); }
+
+// HC_HOST_PROFILE=1: host-side enqueue time per forward section, printed at
+// exit (diagnostics for the launch-bound decode step).
+struct HostProf {
+  static constexpr int kN = 12;
+  const char* names[kN] = {"setup", "embed", "inputs_copy", "stats", "kv_gemm", "q_gemm",
+                           "attention", "o_gemm", "stats2", "fc1", "fc2", "argmax"};
+  double t[kN] = {};
+  long calls = 0;
+  bool on = getenv("HC_HOST_PROFILE") != nullptr;
+  ~HostProf() {
+    if (!on || !calls) return;
+    fprintf(stderr, "[hc host profile] %ld forward calls, us per call:\n", calls);
+    for (int i = 0; i < kN; ++i) fprintf(stderr, "  %-12s %9.1f\n", names[i], t[i] * 1e6 / calls);
+  }
+};
+HostProf g_prof;
+struct ProfMark {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void lap(int i) {
+    if (!g_prof.on) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    g_prof.t[i] += std::chrono::duration<double>(t1 - t0).count();
+    t0 = t1;
+  }
+};
+
+// Weight operands: their tensor maps depend only on (address, shape, box), so
+// they are encoded once and reused by every forward / decode step.
+CUtensorMap wmap(const void* base, int k, int64_t rows, int box_rows) {
+  struct Key {
+    const void* base;
+    int k;
+    int64_t rows;
+    int box;
+    bool operator<(const Key& o) const {
+      return std::tie(base, k, rows, box) < std::tie(o.base, o.k, o.rows, o.box);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, CUtensorMap> cache;
+  const Key key{base, k, rows, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const CUtensorMap m = tmap(base, k, rows, box_rows);
+  std::lock_guard<std::mutex> lk(mu);
+  cache.emplace(key, m);
+  return m;
+}
 
 // tcgen05 attention (default) or the mma.sync kernel (HC_ATTN_TC=0, or page
 // sizes the TMA gather cannot express)
@@ -68,6 +124,8 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     fail(HC_EINVAL, "prefill_layers: attention supports d_head 64 or 128");
   if (c.d_ffn % 32 != 0 || c.d_hidden % 32 != 0)
     fail(HC_EINVAL, "prefill_layers: d_hidden and d_ffn must be multiples of 32");
+  ProfMark pm;
+  if (g_prof.on) ++g_prof.calls;
   DeviceGuard dg(w->device);
   const int d = c.d_hidden, dffn = c.d_ffn, sms = device_sm_count(w->device);
   const size_t nd = size_t(n) * size_t(d);
@@ -77,12 +135,17 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
   float* x = static_cast<float*>(x_buf.ptr);
   float* mean = static_cast<float*>(stats.ptr);
   float* rstd = mean + n;
+  pm.lap(0);
   HC_CUDA(launch_embed(d_tokens, n, w->embedding, d, x, xb_buf.ptr, stream));
-  const CUtensorMap tm_xb = tmap(xb_buf.ptr, d, n, 128);
-  const CUtensorMap tm_mix = tmap(mix_buf.ptr, d, n, 128);
-  const CUtensorMap tm_h1 = tmap(h1_buf.ptr, dffn, n, 128);
-  const int bn_kv = pick_bn(n, 2 * w->d_kv_all, sms), bn_d = pick_bn(n, d, sms),
-            bn_f = pick_bn(n, dffn, sms);
+  const int abox = gemm_a_box(n);
+  const CUtensorMap tm_xb = tmap(xb_buf.ptr, d, n, abox);
+  const CUtensorMap tm_mix = tmap(mix_buf.ptr, d, n, abox);
+  const CUtensorMap tm_h1 = tmap(h1_buf.ptr, dffn, n, abox);
+  // K/V: the exact path (restores must reproduce these K/V bit for bit); the
+  // other projections may split K when n is decode-sized
+  const int bn_kv = pick_bn(n, 2 * w->d_kv_all, sms), bn_d = gemm_pick_bn_skinny(n, d, sms),
+            bn_f = gemm_pick_bn_skinny(n, dffn, sms);
+  pm.lap(1);
   for (int L = lb; L < le; ++L) {
     const auto& lw = w->layers[size_t(L)];
     hook(L, true);
@@ -90,12 +153,15 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
       HC_CUDA(cudaMemcpyAsync(static_cast<char*>(d_layer_inputs) + size_t(L) * nd * 2, xb_buf.ptr,
                               nd * 2, cudaMemcpyDeviceToDevice, stream));
     // attention block: LN(x) -> K/V (paged) and Q
+    pm.lap(2);
     HC_CUDA(launch_row_stats(xb_buf.ptr, n, d, d, true, mean, rstd, stream));
+    pm.lap(3);
     KvOut kv = kv_out_pages(pages, L, d_page_table, sb.table_stride, sb.cu, sb.n_seqs);
     kv.seq_start = sb.seq_start;
-    HC_CUDA(launch_restore_kv(tm_xb, tmap(lw.wkv_all, d, 2 * w->d_kv_all, bn_kv), bn_kv, int(n),
+    HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wkv_all, d, 2 * w->d_kv_all, bn_kv), bn_kv, int(n),
                               2 * w->d_kv_all, d, true, kv, epi_for(w, lw.colsum_all, mean, rstd),
                               sms, stream));
+    pm.lap(4);
     KvOut qo;
     qo.k_base = q_buf.ptr;
     qo.v_base = q_buf.ptr;
@@ -103,8 +169,9 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     qo.cu_seqlens = sb.cu;
     qo.n_seqs = sb.cu ? sb.n_seqs : 1;
     qo.seq_start = sb.seq_start;
-    HC_CUDA(launch_restore_kv(tm_xb, tmap(lw.wq, d, d, bn_d), bn_d, int(n), d, d, true, qo,
-                              epi_for(w, lw.colsum_q, mean, rstd), sms, stream));
+    HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wq, d, d, bn_d), bn_d, int(n), d, d, true, qo,
+                              epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true));
+    pm.lap(5);
     if (sb.cu)
       HC_CUDA(launch_attention_extend(q_buf.ptr, sb.n_seqs, sb.max_new, sb.cu, sb.seq_start,
                                       c.n_heads, c.n_kv_heads, w->d_head, kv, mix_buf.ptr,
@@ -112,14 +179,17 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     else
       HC_CUDA(attention(q_buf.ptr, int(n), c.n_heads, c.n_kv_heads, w->d_head, kv,
                         int64_t(pages->num_pages) * pages->page_size, mix_buf.ptr, stream));
+    pm.lap(6);
     GemmOut resid;
     resid.x = x;
     resid.xb = xb_buf.ptr;
     resid.ldo = d;
-    HC_CUDA(launch_gemm_dense(tm_mix, tmap(lw.wo, d, d, bn_d), bn_d, kEpiResid, int(n), d, d,
-                              resid, EpiArgs{}, sms, stream));
+    HC_CUDA(launch_gemm_dense(tm_mix, wmap(lw.wo, d, d, bn_d), bn_d, kEpiResid, int(n), d, d,
+                              resid, EpiArgs{}, sms, stream, true));
+    pm.lap(7);
     // FFN block (ffn_forward, model.cpp:290-303)
     HC_CUDA(launch_row_stats(xb_buf.ptr, n, d, d, true, mean, rstd, stream));
+    pm.lap(8);
     GemmOut g1;
     g1.xb = h1_buf.ptr;
     g1.ldo = dffn;
@@ -129,15 +199,39 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
       fold.row_rstd = rstd;
       fold.colsum = lw.colsum_fc1;
     }
-    HC_CUDA(launch_gemm_dense(tm_xb, tmap(lw.fc1, d, dffn, bn_f), bn_f, kEpiGelu, int(n), dffn,
-                              d, g1, fold, sms, stream));
-    HC_CUDA(launch_gemm_dense(tm_h1, tmap(lw.fc2, dffn, d, bn_d), bn_d, kEpiResid, int(n), d,
-                              dffn, resid, EpiArgs{}, sms, stream));
+    HC_CUDA(launch_gemm_dense(tm_xb, wmap(lw.fc1, d, dffn, bn_f), bn_f, kEpiGelu, int(n), dffn,
+                              d, g1, fold, sms, stream, true));
+    pm.lap(9);
+    HC_CUDA(launch_gemm_dense(tm_h1, wmap(lw.fc2, dffn, d, bn_d), bn_d, kEpiResid, int(n), d,
+                              dffn, resid, EpiArgs{}, sms, stream, true));
     hook(L, false);
+    pm.lap(10);
   }
-  if (d_next_tokens && sb.cu)
-    HC_CUDA(launch_argmax_rows(w->embedding, c.vocab_size, d, x, sb.cu, sb.n_seqs, d_next_tokens,
-                               stream));
+  if (d_next_tokens && sb.cu) {
+    // logits on the tensor cores: E [vocab x d] x [hi; lo]^T, fp32 accumulate
+    const int B = sb.n_seqs;
+    if (2 * B <= 256) {
+      const int npad = 2 * B <= 32 ? 32 : 2 * B <= 64 ? 64 : 2 * B <= 128 ? 128 : 256;
+      const int vocab = c.vocab_size;
+      StreamScratch hl(size_t(2 * B) * size_t(d) * 2, stream),
+          lg(size_t(vocab) * size_t(npad) * 4, stream), lgb(size_t(vocab) * size_t(npad) * 2, stream);
+      HC_CUDA(launch_hilo_rows(x, sb.cu, B, d, hl.ptr, stream));
+      HC_CUDA(cudaMemsetAsync(lg.ptr, 0, size_t(vocab) * size_t(npad) * 4, stream));
+      GemmOut go;
+      go.x = static_cast<float*>(lg.ptr);
+      go.xb = lgb.ptr;
+      go.ldo = npad;
+      HC_CUDA(launch_gemm_dense(wmap(w->embedding, d, vocab, gemm_a_box(vocab)),
+                                tmap(hl.ptr, d, 2 * B, npad), npad, kEpiResid, vocab, npad, d, go,
+                                EpiArgs{}, sms, stream));
+      HC_CUDA(launch_argmax_pairs(static_cast<float*>(lg.ptr), vocab, npad, B, d_next_tokens,
+                                  stream));
+    } else {
+      HC_CUDA(launch_argmax_rows(w->embedding, c.vocab_size, d, x, sb.cu, sb.n_seqs,
+                                 d_next_tokens, stream));
+    }
+  }
+  pm.lap(11);
   if (next_token) {
     StreamScratch tok(sizeof(int32_t), stream);
     HC_CUDA(launch_argmax_logits(w->embedding, c.vocab_size, d, x + size_t(n - 1) * d,
@@ -268,12 +362,16 @@ hc_status hc_gemm_epilogue(int32_t mode, const void* d_a, const void* d_b, int32
                            const float* d_rstd, const float* d_colsum, int32_t device,
                            void* stream) {
   return guard([&] {
+    const bool split_k = (mode & HC_GEMM_SPLIT_K) != 0;  // decode-shape K split (tests)
+    mode &= ~HC_GEMM_SPLIT_K;
     if (mode != kEpiResid && mode != kEpiGelu) fail(HC_EINVAL, "gemm: mode must be 1 or 2");
     if (!d_a || !d_b || !d_xb || (mode == kEpiResid && !d_x)) fail(HC_EINVAL, "gemm: null argument");
     if (n % 32 || k % 8) fail(HC_EINVAL, "gemm: n % 32 and k % 8 must be 0");
     require_sm100(device);
     DeviceGuard dg(device);
-    const int sms = device_sm_count(device), bn = pick_bn(m, n, sms);
+    const bool split = split_k || getenv("HC_GEMM_SPLIT") != nullptr;
+    const int sms = device_sm_count(device);
+    const int bn = split ? gemm_pick_bn_skinny(m, n, sms) : pick_bn(m, n, sms);
     GemmOut g;
     g.x = d_x;
     g.xb = d_xb;
@@ -284,8 +382,8 @@ hc_status hc_gemm_epilogue(int32_t mode, const void* d_a, const void* d_b, int32
       e.row_rstd = d_rstd;
       e.colsum = d_colsum;
     }
-    HC_CUDA(launch_gemm_dense(tmap(d_a, k, m, 128), tmap(d_b, k, n, bn), bn, mode, m, n, k, g, e,
-                              sms, as_stream(stream)));
+    HC_CUDA(launch_gemm_dense(tmap(d_a, k, m, gemm_a_box(m)), tmap(d_b, k, n, bn), bn, mode, m, n, k, g, e,
+                              sms, as_stream(stream), split));
   });
 }
 

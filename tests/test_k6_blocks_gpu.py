@@ -42,8 +42,13 @@ def test_attention_dense_vs_torch(cuda, n, heads, kvh, dh):
 
 
 @pytest.mark.parametrize("mode", [1, 2])
-@pytest.mark.parametrize("m,n,k", [(200, 256, 512), (1024, 512, 2048), (130, 4096, 256)])
-def test_gemm_epilogues_vs_torch(cuda, mode, m, n, k):
+@pytest.mark.parametrize("m,n,k,split", [
+    (200, 256, 512, 0), (1024, 512, 2048, 0), (130, 4096, 256, 0),
+    # decode shapes: narrow tiles + compact smem ring, and the K-split path
+    # (uneven slices: 64 K blocks over 9 slices, 172 over 9, one row)
+    (16, 256, 512, 0), (40, 4096, 4096, 0), (16, 4096, 4096, 1), (16, 4096, 11008, 1),
+    (1, 512, 1088, 1), (100, 11008, 4096, 1)])
+def test_gemm_epilogues_vs_torch(cuda, mode, m, n, k, split):
     import torch
     from paper_2410_05004_b200 import capi
     g = torch.Generator(device="cuda").manual_seed(m + n)
@@ -56,7 +61,7 @@ def test_gemm_epilogues_vs_torch(cuda, mode, m, n, k):
     rstd = (1 / torch.sqrt(a.float().var(1, unbiased=False) + 1e-5)).contiguous()
     colsum = b.float().sum(1).contiguous()
     fold = mode == 2
-    capi.check(capi.lib().hc_gemm_epilogue(mode, a.data_ptr(), b.data_ptr(), m, n, k,
+    capi.check(capi.lib().hc_gemm_epilogue(mode | (0x100 if split else 0), a.data_ptr(), b.data_ptr(), m, n, k,
                                            x.data_ptr(), xb.data_ptr(),
                                            mean.data_ptr() if fold else None,
                                            rstd.data_ptr() if fold else None,
