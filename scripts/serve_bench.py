@@ -55,6 +55,10 @@ def main():
     ap.add_argument("--gap", type=float, default=30.0)
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--strategies", default="IDEAL,HCACHE,KV_OFFLOAD,RECOMPUTE")
+    ap.add_argument("--long-sessions", type=int, default=6)
+    ap.add_argument("--arenas", type=int, default=4)
+    ap.add_argument("--skip-conv", action="store_true")
+    ap.add_argument("--skip-saving", action="store_true")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     stream = torch.cuda.current_stream().cuda_stream
@@ -82,11 +86,11 @@ def main():
                         "c_h_ms": prof.c_h * 1e3, "c_token_ms": prof.c_token * 1e3},
            "strategies": {}, "saving": {}}
 
-    def one(trace, strategy, saving=H.SavingMode.TWO_STAGE):
-        store = H.StorageManager(H.DevicePool(4), buffer_capacity_bytes=1 << 30)
+    def one(trace, strategy, saving=H.SavingMode.TWO_STAGE, plan_=None):
+        store = H.StorageManager(H.DevicePool(a.arenas), buffer_capacity_bytes=1 << 30)
         t0 = time.perf_counter()
         m = H.run(trace, w, store, H.RunOptions(strategy=strategy, saving=saving,
-                                                hcache_plan=plan))
+                                                hcache_plan=plan_ or plan))
         wall = time.perf_counter() - t0
         store.close()
         return {"ttft_p50_s": m.ttft_p50, "ttft_p95_s": m.ttft_p95, "tbt_mean_s": m.tbt_mean,
@@ -95,13 +99,15 @@ def main():
                 "storage_bytes_per_token": m.storage_bytes_per_token,
                 "busy_s": m.busy_s, "save_stall_s": m.save_stall_s,
                 "persist_wait_s": m.persist_wait_s, "decode_steps": m.decode_steps,
-                "backpressure_stalls": m.backpressure_stalls, "wall_s": wall}, m
+                "backpressure_stalls": m.backpressure_stalls, "wall_s": wall,
+                "per_request": [[r.history_tokens, round(r.restore_s * 1e3, 3), round(r.ttft_s * 1e3, 3)]
+                                for r in m.per_request]}, m
 
     # warm-up (first-use costs: pools, tensor maps, attributes) outside the numbers
     warm = [H.Request(f"w{i}", 1, 0, [], list(range(1, 40)), 8, 0.0) for i in range(4)]
     one(warm, H.Strategy.HCACHE)
     ms = {}
-    for name in a.strategies.split(","):
+    for name in ([] if a.skip_conv else a.strategies.split(",")):
         s = H.Strategy[name]
         out["strategies"][name], ms[s] = one(tr, s)
         print(name, json.dumps(out["strategies"][name]), flush=True)
@@ -110,6 +116,36 @@ def main():
         hc = out["strategies"]["HCACHE"]
         for name, r in out["strategies"].items():
             r["ttft_p50_vs_hcache"] = r["ttft_p50_s"] / hc["ttft_p50_s"] if hc["ttft_p50_s"] else None
+    # long-context trace (PAPER L-Eval setting): every request restores a
+    # 2K-6K-token context, so TTFT = restore + prompt prefill
+    if a.long_sessions > 0:
+        lp = H.TraceParams(n_sessions=a.long_sessions, ctx_min=2048, ctx_max=6144,
+                           arrival_rate_per_s=0.5, vocab=vocab)
+        ltr = H.gen_trace(H.TraceKind.LONG_CONTEXT, lp, a.seed)
+        out["long_context"] = {"trace": vars(lp), "requests": len(ltr.requests),
+                               "context_tokens": sum(len(r.context) for r in ltr.requests),
+                               "strategies": {}}
+        # plan for the long contexts: profiled at their mean length
+        lprof = H.profile_hardware(w, int(np.mean([len(r.context) for r in ltr.requests])))
+        lprof.n_layers = L
+        lplan, _ = H.plan_three_way(lprof, L)
+        out["long_context"]["plan"] = lplan.serialize()
+        lms = {}
+        for name in a.strategies.split(","):
+            s = H.Strategy[name]
+            out["long_context"]["strategies"][name], lms[s] = one(ltr, s, plan_=lplan)
+            print("long", name, json.dumps(out["long_context"]["strategies"][name]), flush=True)
+        if H.Strategy.HCACHE in lms:
+            print(H.report(list(lms.values())), flush=True)
+            hc = out["long_context"]["strategies"]["HCACHE"]
+            for name, r in out["long_context"]["strategies"].items():
+                r["ttft_p50_vs_hcache"] = r["ttft_p50_s"] / hc["ttft_p50_s"]
+    if a.skip_saving:
+        print(json.dumps(out))
+        if a.out:
+            with open(a.out, "w") as f:
+                json.dump(out, f, indent=1)
+        return
     # criterion 8 on the device (acceptance.cpp:340-381): decode batch of 16
     # first-round requests arriving together, no restores, so TBT differs only
     # by how the states are saved
