@@ -177,9 +177,9 @@ def run_ours(args, cfg, rank, world):
     dh = d // heads
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
-    if world > 1:
+    if world > 1 or args.sharded:
         from paper_2410_05004_b200 import sharded
-        return sharded.bench(args, cfg, rank, world, dev)
+        return sharded.bench(args, cfg, rank, world, dev, ClockSampler, peaks())
 
     stream = torch.cuda.current_stream().cuda_stream
     vocab = 32000
@@ -400,6 +400,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the head-sharded (N>1) path even at world size 1 (testing)")
     ap.add_argument("--no-recompute", action="store_true",
                     help="skip full-block weights (no RECOMPUTE complement / baseline)")
     args = ap.parse_args()

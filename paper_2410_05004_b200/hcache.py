@@ -812,6 +812,54 @@ class Metrics:
     decode_tokens: int = 0
 
 
+def _percentile(xs, p):
+    """percentile (harness.cpp:36-44)."""
+    if not xs:
+        return 0.0
+    xs = sorted(xs)
+    idx = p * (len(xs) - 1)
+    lo = int(idx)
+    hi = min(lo + 1, len(xs) - 1)
+    frac = idx - lo
+    return xs[lo] * (1 - frac) + xs[hi] * frac
+
+
+def metrics_to_csv(m: "Metrics") -> str:
+    """Metrics::to_csv (harness.cpp:153-163): full-precision per-request rows."""
+    rows = [f"# strategy={m.strategy.name}",
+            "session,round,arrival_s,history,restore_s,ttft_s,tbt_s,generated"]
+    for r in m.per_request:
+        rows.append(f"{r.session_id},{r.round},{r.arrival_s!r},{r.history_tokens},"
+                    f"{r.restore_s!r},{r.ttft_s!r},{r.tbt_s!r},{r.generated}")
+    return "\n".join(rows) + "\n"
+
+
+def metrics_from_csv(text: str) -> "Metrics":
+    """Metrics::from_csv (harness.cpp:165-187) + finalize_aggregates
+    (harness.cpp:133-151)."""
+    strategy, per = Strategy.IDEAL, []
+    for line in text.splitlines():
+        if not line:
+            continue
+        if line.startswith("# strategy="):
+            strategy = Strategy[line[len("# strategy="):]]
+            continue
+        if line.startswith("session,"):
+            continue
+        f = line.split(",")
+        if len(f) != 8:
+            raise RuntimeError("metrics csv: bad row: " + line)
+        per.append(RequestMetrics(f[0], int(f[1]), float(f[2]), int(f[3]), float(f[4]),
+                                  float(f[5]), float(f[6]), int(f[7])))
+    ttft = [r.ttft_s for r in per]
+    tbt = [r.tbt_s for r in per if r.generated > 1]
+    hist = sum(r.history_tokens for r in per)
+    rest = sum(r.restore_s for r in per)
+    return Metrics(strategy, per, [], _percentile(ttft, 0.5), _percentile(ttft, 0.95),
+                   sum(tbt) / len(tbt) if tbt else 0.0, _percentile(tbt, 0.5),
+                   _percentile(tbt, 0.95), hist / rest if rest > 0 else 0.0)
+
+
 @dataclass
 class RunOptions:
     """harness.hpp:60-65 for the device engine. num_pages: KV page pool (all

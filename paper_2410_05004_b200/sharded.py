@@ -159,9 +159,11 @@ class GpuShardedRestorer:
             consumed[slot] = done
 
 
-def bench(args, cfg, rank, world, dev):
+def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     """bench.py --gpus N (torchrun): head-sharded restore of one context
-    (strong scaling). Prints the JSON line on rank 0."""
+    (strong scaling). Prints the JSON line on rank 0. clock_sampler: context
+    manager class sampling nvidia-smi clocks (bench.ClockSampler); peaks: the
+    measured-peaks dict."""
     import json
 
     import numpy as np
@@ -228,8 +230,16 @@ def bench(args, cfg, rank, world, dev):
     for _ in range(args.warmup):
         r.restore(list(range(L)), resident)
         r.restore(list(range(L)))
-    ms_res = timed(True, args.steps)
+    clk = clock_sampler(dev) if clock_sampler else None
+    if clk:
+        clk.__enter__()
     ms_e2e = timed(False, args.steps)
+    ms_res = timed(True, args.steps)
+    if clk:
+        clk.__exit__(None, None, None)
+    clocks = clk.summary() if clk else {"sm_mhz": None, "sm_max_mhz": None,
+                                        "reasons": ["unsampled"]}
+    h2d = H.measure_h2d(256 << 20, 5, dev) / 1e9
     if rank == 0:
         h_bytes = L * n * d * 2
         line = {"metric": "restored_kv_tokens_per_s", "value": n / (ms_res * 1e-3),
@@ -245,8 +255,13 @@ def bench(args, cfg, rank, world, dev):
                 "e2e": {"value": n / (ms_e2e * 1e-3), "unit": "tokens/s",
                         "h2d_bytes_per_step": h_bytes // world, "d2h_bytes_per_step": 0},
                 "gpu_launches": args.steps * 2 * L,
+                "clocks": clocks,
+                "roofline": {"bound": "pcie", "unit": "GB/s",
+                             "achieved": h_bytes / world / (ms_e2e * 1e-3) / 1e9,
+                             "peak": h2d, "peak_source": "measured pinned H2D 256 MiB (this rank)",
+                             "frac": h_bytes / world / (ms_e2e * 1e-3) / 1e9 / h2d,
+                             "traffic": None},
                 "note": "value: shards resident in HBM (all-gather + K1); e2e: each rank "
                         "fetches its 1/N over PCIe; times are max over ranks"}
         print(json.dumps(line), flush=True)
     dist.barrier()
-    del time, os, C

@@ -77,3 +77,20 @@ def test_serve_run_rejects_null_arguments():
     per = (capi.RequestMetricsC * 1)()
     o = capi.ServeOptsC()
     assert lib().hc_serve_run(None, None, None, 0, C.byref(o), per, None, C.byref(m), None) == 1
+
+
+def test_metrics_csv_roundtrip_and_aggregates():
+    """Metrics::to_csv / from_csv (harness.cpp:153-187) and the aggregates of
+    finalize_aggregates (harness.cpp:133-151)."""
+    from paper_2410_05004_b200 import hcache as H
+    per = [H.RequestMetrics("s0", 1, 0.5, 0, 0.0, 0.25, 0.01, 5),
+           H.RequestMetrics("s1", 2, 1.0, 300, 0.02, 0.125, 0.03, 3),
+           H.RequestMetrics("s2", 1, 1.5, 100, 0.01, 0.5, 0.0, 1)]
+    m = H.Metrics(H.Strategy.HCACHE, per, [])
+    back = H.metrics_from_csv(H.metrics_to_csv(m))
+    assert back.strategy == H.Strategy.HCACHE and back.per_request == per
+    assert back.ttft_p50 == 0.25 and back.ttft_p95 == 0.25 + 0.9 * 0.25
+    assert back.tbt_mean == 0.02  # the generated == 1 request is excluded
+    assert back.restore_tokens_per_s == 400 / 0.03
+    with pytest.raises(RuntimeError):
+        H.metrics_from_csv("a,b,c\n")
