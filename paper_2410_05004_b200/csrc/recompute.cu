@@ -285,7 +285,7 @@ void forward_batch(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
                [](int, bool) {}, d_layer_inputs, nullptr, sb, d_next_tokens);
 }
 
-double recompute_layer_seconds(const hc_weights* w, int n) {
+double recompute_layer_seconds(const hc_weights* w, int n, double warm_s) {
   if (!w || !w->embedding || w->d_kv != w->d_kv_all || n < 1) return 0.0;
   int layer = -1;
   for (int l = 0; l < w->cfg.n_layers; ++l)
@@ -306,25 +306,30 @@ double recompute_layer_seconds(const hc_weights* w, int n) {
   cudaEvent_t a, b;
   HC_CUDA(cudaEventCreate(&a));
   HC_CUDA(cudaEventCreate(&b));
-  float best = 1e30f;
-  const int reps = 4;
   auto one = [&] {
     prefill_layers_impl(w, static_cast<int32_t*>(tok.ptr), n, layer, layer + 1, &pages,
                         static_cast<int32_t*>(table.ptr), s, [](int, bool) {});
   };
-  one();  // warm-up (pool allocations, tensor-map encode)
-  for (int r = 0; r < 3; ++r) {
+  auto timed = [&](int reps) {
     HC_CUDA(cudaEventRecord(a, s));
     for (int i = 0; i < reps; ++i) one();
     HC_CUDA(cudaEventRecord(b, s));
     HC_CUDA(cudaEventSynchronize(b));
     float ms = 0;
     HC_CUDA(cudaEventElapsedTime(&ms, a, b));
-    best = std::min(best, ms / reps);
-  }
+    return double(ms) * 1e-3;
+  };
+  one();  // pool allocations, tensor-map encodes
+  // run back to back until the clocks settle (a restore keeps the tensor
+  // cores busy for tens of ms; its power-capped clock, not the boost clock,
+  // sets the recompute cost), then take the mean of the next launches
+  double warm = 0;
+  while (warm < warm_s) warm += timed(8);
+  const int reps = 16;
+  const double sec = timed(reps) / reps;
   cudaEventDestroy(a);
   cudaEventDestroy(b);
-  return double(best) * 1e-3;
+  return sec;
 }
 
 }  // namespace hc

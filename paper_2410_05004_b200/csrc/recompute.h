@@ -36,8 +36,9 @@ void forward_batch(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
                    const int32_t* d_page_tables, int table_stride, void* d_layer_inputs,
                    int32_t* d_next_tokens, cudaStream_t stream);
 
-// Measured seconds of one recompute layer over n tokens (0 when the full
-// block weights are not set).
-double recompute_layer_seconds(const hc_weights* w, int n);
+// Measured seconds of one recompute layer over n tokens at the steady-state
+// clock (after warm_s seconds of back-to-back layers); 0 when the full block
+// weights are not set.
+double recompute_layer_seconds(const hc_weights* w, int n, double warm_s = 0.2);
 
 }  // namespace hc

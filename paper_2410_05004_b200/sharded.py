@@ -265,3 +265,4 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                         "fetches its 1/N over PCIe; times are max over ranks"}
         print(json.dumps(line), flush=True)
     dist.barrier()
+    dist.destroy_process_group()

@@ -1,0 +1,3 @@
+cd scripts && timeout 800 python plan_sweep.py 2>&1 | head -2
+cd .. && timeout 600 python bench.py --steps 10 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_latest.json
+python -c "import json; d=json.load(open('gpurun_out/bench_latest.json')); print(d['value'], d['restore_latency_ms'], d['e2e']['value'], d['planner'], d['roofline']['frac'], d['clocks'])"
