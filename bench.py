@@ -250,10 +250,11 @@ def run_ours(args, cfg, rank, world):
     # bubble-free scheduler on measured PCIe / GEMM / recompute timings
     prof = H.profile_hardware(w, n)
     prof.n_layers = L
-    if full:
-        plan, plan_ms = H.plan_three_way(prof, L)
-    else:
-        plan, plan_ms = H.RestorationPlan.make(L, L, H.Complement.NONE), None
+    if not full:
+        # no full block weights (GQA configs here): RECOMPUTE is unavailable,
+        # the planner splits between hidden states and KV offload only
+        prof.c_token = 1e9
+    plan, plan_ms = H.plan_three_way(prof, L)
     all_h = H.RestorationPlan.make(L, L, H.Complement.NONE)
     all_kv = H.RestorationPlan.make(L, 0, H.Complement.KV_OFFLOAD)
 
