@@ -211,7 +211,7 @@ def run_ours(args, cfg, rank, world):
 
     L, d, heads, kvh, dffn, n, rope = cfg
     dh = d // heads
-    dev = int(os.environ.get("LOCAL_RANK", 0))
+    dev = int(os.environ.get("HC_FORCE_DEVICE", os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     if world > 1 or args.sharded:
         from paper_2410_05004_b200 import sharded

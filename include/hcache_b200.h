@@ -455,6 +455,28 @@ hc_status hc_bench_project(const hc_weights* w, int32_t layer, const void* d_hid
 /* Pinned host->device copy bandwidth (bytes/s) for a `bytes` transfer. */
 hc_status hc_measure_h2d(int32_t device, size_t bytes, int32_t reps, double* bytes_per_s);
 
+/* ------------------------------------- multi-GPU: peer-memory all-gather */
+/* Head-sharded restore with the all-gather fused into K1: rows
+ * [row_begin[s], row_begin[s+1]) of one layer's hidden states live in
+ * d_src[s] -- typically another GPU's staging buffer mapped into this process
+ * (CUDA IPC over NVLink). The row statistics and the K1 A tiles are read
+ * straight from the owning buffers; K/V for this GPU's heads land in `pages`
+ * (positions start_pos..). Interior boundaries must be multiples of 128 rows;
+ * up to 8 sources. Results are bit-identical to hc_project_to_pages on the
+ * concatenated rows. Replaces hc_store_read_layer_range + all-gather +
+ * hc_project_to_pages of the NCCL pipeline. */
+hc_status hc_project_multi_source(const hc_weights* w, int32_t layer, int32_t n_src,
+                                  const void* const* d_src, const int64_t* row_begin,
+                                  const hc_kv_pages* pages, const int32_t* d_page_table,
+                                  int32_t start_pos, void* stream);
+/* Stream-ordered cross-GPU flags: wait until *d_flag >= value (d_flag in this
+ * GPU's memory; cuStreamWaitValue32, or a polling kernel), and store `value`
+ * into each of n flags (any GPU's memory, system-scope release) after all
+ * prior work on the stream. */
+hc_status hc_stream_wait_flag(void* stream, const uint32_t* d_flag, uint32_t value);
+hc_status hc_stream_signal_flags(void* stream, uint32_t* const* d_flag_ptrs, int32_t n,
+                                 uint32_t value);
+
 /* ---------------------------------------------------------- serving loop */
 /* Strategy / SavingMode (harness.hpp:14-17). */
 typedef enum hc_strategy {

@@ -172,6 +172,9 @@ _PROTOS = {
                          P(TimelineC)]),
     "hc_restore_batch": (i32, [vp, P(cp), i32, vp, P(RestoreOptsC), P(KvPagesC), vp, i32, vp,
                                P(TimelineC)]),
+    "hc_project_multi_source": (i32, [vp, i32, i32, P(vp), P(i64), P(KvPagesC), vp, i32, vp]),
+    "hc_stream_wait_flag": (i32, [vp, vp, C.c_uint32]),
+    "hc_stream_signal_flags": (i32, [vp, P(vp), i32, C.c_uint32]),
     "hc_serve_run": (i32, [vp, vp, P(RequestC), i32, P(ServeOptsC), P(RequestMetricsC), vp,
                            P(ServeMetricsC), vp]),
     "hc_forward_batch": (i32, [vp, vp, i32, vp, vp, P(KvPagesC), vp, i32, vp, vp, vp]),

@@ -56,6 +56,14 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
   n_blk = local / gm;
 }
 
+// The tensor map holding A row `row` and the row's coordinate within it.
+__device__ __forceinline__ const CUtensorMap* amap(const AMaps& am, int row, int& local) {
+  int s = 0;
+  while (s + 1 < am.n && row >= am.row0[s + 1]) ++s;
+  local = row - am.row0[s];
+  return &am.m[s];
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -309,7 +317,7 @@ RingCfg ring_cfg(int a_rows) {
 
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+    tc_gemm_kernel(const __grid_constant__ AMaps am,
                    const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
                    GemmOut gout, EpiArgs epi, uint32_t idesc, int S, uint32_t stride,
                    uint32_t a_bytes, int k_splits, float* part) {
@@ -334,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kb_per = (num_kb + k_splits - 1) / k_splits;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
+    for (int i = 0; i < am.n; ++i) tma_prefetch_desc(&am.m[i]);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -365,7 +373,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], a_bytes + Cfg::kBBytes);
           uint8_t* st = sA + size_t(stage) * stride;
-          tma_load_2d(st, &tmA, &full[stage], kb * kBK, m_blk * kBM);
+          int a_row;
+          const CUtensorMap* ma = amap(am, m_blk * kBM, a_row);
+          tma_load_2d(st, ma, &full[stage], kb * kBK, a_row);
           tma_load_2d(st + a_bytes, &tmB, &full[stage], kb * kBK, n_blk * BN);
           if (++stage == S) {
             stage = 0;
@@ -455,7 +465,7 @@ __device__ __forceinline__ void tile_coords_pair(int tile, int num_m, int num_n,
 
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+    tc_gemm_pair_kernel(const __grid_constant__ AMaps am,
                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
                         GemmOut gout, EpiArgs epi, uint32_t idesc) {
   constexpr int BN = 256, S = kPairStages;
@@ -480,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int num_kb = (K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
+    for (int i = 0; i < am.n; ++i) tma_prefetch_desc(&am.m[i]);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -509,8 +519,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
-          tma_load_2d_pair(sA + stage * kPairHalfBytes, &tmA, &full[stage], kb * kBK,
-                           m_blk * 256 + int(rank) * 128);
+          int a_row;
+          const CUtensorMap* ma = amap(am, m_blk * 256 + int(rank) * 128, a_row);
+          tma_load_2d_pair(sA + stage * kPairHalfBytes, ma, &full[stage], kb * kBK, a_row);
           tma_load_2d_pair(sB + stage * kPairHalfBytes, &tmB, &full[stage], kb * kBK,
                            n_blk * BN + int(rank) * 128);
           if (++stage == S) {
@@ -742,7 +753,7 @@ __global__ void kv_gather_kernel(KvOut kv, int pos0, int64_t n_rows, uint4* __re
 }  // namespace
 
 template <int MODE>
-cudaError_t launch_pair(const CUtensorMap& tmA, const CUtensorMap& tmB128, int M, int N, int K,
+cudaError_t launch_pair(const AMaps& tmA, const CUtensorMap& tmB128, int M, int N, int K,
                         bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
                         int num_sms, cudaStream_t stream) {
   const uint32_t idesc = umma_idesc_f16(256, 256, bf16_in);
@@ -774,7 +785,7 @@ bool use_pair(int M, int N, int num_sms) {
 }
 
 template <int BN, int MODE>
-cudaError_t launch_tc(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+cudaError_t launch_tc(const AMaps& tmA, const CUtensorMap& tmB, int M, int N, int K,
                       bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
                       int num_sms, cudaStream_t stream, bool split_acc = false) {
   const uint32_t idesc = umma_idesc_f16(kBM, BN, bf16_in);
@@ -864,7 +875,7 @@ int gemm_pick_bn_skinny(int64_t M, int N, int num_sms) {
 namespace {
 
 template <int MODE>
-cudaError_t launch_tc_bn(int bn, const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N,
+cudaError_t launch_tc_bn(int bn, const AMaps& tmA, const CUtensorMap& tmB, int M, int N,
                          int K, bool bf16_in, const KvOut& out, const GemmOut& g,
                          const EpiArgs& epi, int num_sms, cudaStream_t stream, bool split_acc) {
   switch (bn) {
@@ -887,10 +898,25 @@ cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, in
                               int num_sms, cudaStream_t stream, bool split_acc) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   GemmOut g;
+  const AMaps am = single_amap(tmA);
   if (bn == 128 && use_pair(M, N, num_sms))  // tmB has the 128-row box the pair needs
-    return launch_pair<kEpiKv>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
-  return launch_tc_bn<kEpiKv>(bn, tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream,
+    return launch_pair<kEpiKv>(am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
+  return launch_tc_bn<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream,
                               split_acc);
+}
+
+cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int bn, int M, int N,
+                                    int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
+                                    int num_sms, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (am.n < 1 || am.n > kMaxASrc) return cudaErrorInvalidValue;
+  for (int i = 1; i < am.n; ++i)
+    if (am.row0[i] % kBM) return cudaErrorInvalidValue;  // a tile reads one source
+  GemmOut g;
+  if (bn == 128 && use_pair(M, N, num_sms))
+    return launch_pair<kEpiKv>(am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
+  // (no K split: the multi-source path restores K/V, which stay exact)
+  return launch_tc_bn<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, false);
 }
 
 cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,
@@ -898,14 +924,15 @@ cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, in
                               int num_sms, cudaStream_t stream, bool split_acc) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   KvOut o;
+  const AMaps am = single_amap(tmA);
   if (bn == 128 && use_pair(M, N, num_sms))
     return mode == kEpiResid
-               ? launch_pair<kEpiResid>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream)
-               : launch_pair<kEpiGelu>(tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream);
+               ? launch_pair<kEpiResid>(am, tmB, M, N, K, true, o, g, epi, num_sms, stream)
+               : launch_pair<kEpiGelu>(am, tmB, M, N, K, true, o, g, epi, num_sms, stream);
   if (mode == kEpiResid)
-    return launch_tc_bn<kEpiResid>(bn, tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream,
+    return launch_tc_bn<kEpiResid>(bn, am, tmB, M, N, K, true, o, g, epi, num_sms, stream,
                                    split_acc);
-  return launch_tc_bn<kEpiGelu>(bn, tmA, tmB, M, N, K, true, o, g, epi, num_sms, stream,
+  return launch_tc_bn<kEpiGelu>(bn, am, tmB, M, N, K, true, o, g, epi, num_sms, stream,
                                 split_acc);
 }
 

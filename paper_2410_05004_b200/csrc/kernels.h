@@ -48,6 +48,26 @@ struct GemmOut {
   int ldo = 0;
 };
 
+// A operand of the shared tcgen05 GEMM: one tensor map, or -- the all-gather
+// fused into K1 over peer memory -- up to kMaxASrc maps, map s covering rows
+// [row0[s], row0[s+1]) of A from its own buffer (another GPU's, mapped over
+// NVLink). Source boundaries must be multiples of 128 rows (one M tile, or
+// one CTA's half of a CTA-pair tile, reads one source).
+constexpr int kMaxASrc = 8;
+struct AMaps {
+  CUtensorMap m[kMaxASrc];
+  int row0[kMaxASrc + 1];
+  int n;
+};
+inline AMaps single_amap(const CUtensorMap& t) {
+  AMaps a;
+  a.m[0] = t;
+  a.row0[0] = 0;
+  a.row0[1] = 0x7fffffff;
+  a.n = 1;
+  return a;
+}
+
 // Creates a 2D K-major bf16/fp16 tensor map with a {64, box_rows} box and the
 // 128-byte swizzle (the K1 operand layout). Returns false on failure.
 bool make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows,
@@ -73,6 +93,10 @@ int gemm_a_box(int64_t M);
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
                               int num_sms, cudaStream_t stream, bool split_acc = false);
+// K1 with a multi-source A (AMaps): the peer-memory all-gather fused in.
+cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int bn, int M, int N,
+                                    int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
+                                    int num_sms, cudaStream_t stream);
 
 // The same GEMM with a dense epilogue (mode kEpiResid or kEpiGelu).
 cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,

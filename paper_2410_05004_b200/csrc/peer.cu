@@ -1,0 +1,161 @@
+// peer.cu -- the head-sharded restore's all-gather fused into K1 over peer
+// memory (SURVEY 8e on B200 terms).
+//
+// Each rank holds only its own token range of a layer's hidden states (fetched
+// over its own PCIe link). Instead of all-gathering the ranges into a full
+// n x d copy on every GPU (NCCL, the baseline), every rank's K1 reads the A
+// tiles of each range straight from the owning rank's buffer -- mapped into
+// this process with CUDA IPC, reached over NVLink -- so the transfer overlaps
+// the MMAs tile by tile and no gathered copy is ever written. Row statistics
+// for the LayerNorm fold read the ranges the same way.
+//
+// Cross-GPU ordering uses flags in device memory: an owner announces a filled
+// staging slot by storing an epoch into every consumer's flag array
+// (system-scope release stores over NVLink), a consumer announces it is done
+// with a slot the same way; each side waits only on its own memory
+// (cuStreamWaitValue32, or a one-thread polling kernel where stream memory
+// operations are unavailable).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+
+#include "common.h"
+#include "kernels.h"
+#include "weights.h"
+
+namespace hc {
+
+CUtensorMap weight_map(const hc_weights::Layer& L, int bn, int d, int rows);
+KvOut kv_out_pages(const hc_kv_pages* pages, int layer, const int32_t* page_table,
+                   int table_stride, const int32_t* cu_seqlens, int n_seqs);
+void validate_pages(const hc_weights* w, const hc_kv_pages* pages, int d_kv_expected);
+
+namespace {
+
+__global__ void signal_kernel(uint32_t* const* addrs, int n, uint32_t value) {
+  __threadfence_system();  // everything this stream did before is visible first
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    asm volatile("st.global.release.sys.u32 [%0], %1;" ::"l"(addrs[i]), "r"(value) : "memory");
+}
+
+__global__ void wait_kernel(const uint32_t* addr, uint32_t value) {
+  uint32_t v = 0;
+  uint64_t spins = 0;
+  for (;;) {
+    asm volatile("ld.global.acquire.sys.u32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
+    if (v >= value) break;
+    __nanosleep(200);
+    if (++spins == (1ull << 34)) asm volatile("trap;");  // watchdog (~1 h)
+  }
+}
+
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+WaitFn wait_value_fn() {
+  static WaitFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitFn>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+}  // namespace hc
+
+using namespace hc;
+
+extern "C" {
+
+hc_status hc_stream_wait_flag(void* stream, const uint32_t* d_flag, uint32_t value) {
+  return guard([&] {
+    if (!d_flag) fail(HC_EINVAL, "wait_flag: null flag");
+    static const bool use_kernel = getenv("HC_WAIT_KERNEL") != nullptr;
+    WaitFn fn = use_kernel ? nullptr : wait_value_fn();
+    if (fn) {
+      const CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag),
+                            value, CU_STREAM_WAIT_VALUE_GEQ);
+      if (r == CUDA_SUCCESS) return;
+    }
+    wait_kernel<<<1, 1, 0, as_stream(stream)>>>(d_flag, value);
+    HC_CUDA(cudaGetLastError());
+  });
+}
+
+hc_status hc_stream_signal_flags(void* stream, uint32_t* const* d_flag_ptrs, int32_t n,
+                                 uint32_t value) {
+  return guard([&] {
+    if (n < 0 || n > 64 || (n > 0 && !d_flag_ptrs)) fail(HC_EINVAL, "signal_flags: bad argument");
+    if (n == 0) return;
+    cudaStream_t s = as_stream(stream);
+    StreamScratch ptrs(sizeof(uint32_t*) * size_t(n), s);
+    HC_CUDA(cudaMemcpyAsync(ptrs.ptr, d_flag_ptrs, sizeof(uint32_t*) * size_t(n),
+                            cudaMemcpyHostToDevice, s));
+    signal_kernel<<<1, 32, 0, s>>>(static_cast<uint32_t* const*>(ptrs.ptr), n, value);
+    HC_CUDA(cudaGetLastError());
+  });
+}
+
+hc_status hc_project_multi_source(const hc_weights* w, int32_t layer, int32_t n_src,
+                                  const void* const* d_src, const int64_t* row_begin,
+                                  const hc_kv_pages* pages, const int32_t* d_page_table,
+                                  int32_t start_pos, void* stream) {
+  return guard([&] {
+    if (!w || !d_src || !row_begin || !d_page_table) fail(HC_EINVAL, "project_multi: null argument");
+    if (n_src < 1 || n_src > kMaxASrc) fail(HC_EINVAL, "project_multi: 1..8 sources");
+    if (layer < 0 || layer >= w->cfg.n_layers) fail(HC_EINVAL, "project: layer out of range");
+    const auto& L = w->layers[size_t(layer)];
+    if (!L.ready) fail(HC_EINVAL, "project: layer weights not set");
+    validate_pages(w, pages, w->d_kv);
+    if (row_begin[0] != 0) fail(HC_EINVAL, "project_multi: row_begin[0] must be 0");
+    for (int s = 0; s < n_src; ++s) {
+      if (row_begin[s + 1] < row_begin[s]) fail(HC_EINVAL, "project_multi: ranges must ascend");
+      if (row_begin[s + 1] < row_begin[n_src] && row_begin[s + 1] % 128)
+        fail(HC_EINVAL, "project_multi: source boundaries must be multiples of 128 rows");
+      if (row_begin[s + 1] > row_begin[s] && !d_src[s]) fail(HC_EINVAL, "project_multi: null source");
+    }
+    const int64_t n = row_begin[n_src];
+    if (n <= 0) return;
+    if (w->cfg.rope_enabled && int64_t(start_pos) + n > w->rope_rows)
+      fail(HC_EINVAL, "project: positions exceed max_seq");
+    DeviceGuard dg(w->device);
+    cudaStream_t s = as_stream(stream);
+    const int d = w->cfg.d_hidden, N = 2 * w->d_kv;
+    StreamScratch stats(size_t(n) * 2 * sizeof(float), s);
+    float* mean = static_cast<float*>(stats.ptr);
+    float* rstd = mean + n;
+    AMaps am;
+    am.n = 0;
+    const uint32_t abox = uint32_t(gemm_a_box(n));
+    for (int i = 0; i < n_src; ++i) {
+      const int64_t rows = row_begin[i + 1] - row_begin[i];
+      if (rows == 0) continue;  // empty range (more ranks than row blocks)
+      if (w->cfg.norm_enabled)
+        HC_CUDA(launch_row_stats(d_src[i], rows, d, d, true, mean + row_begin[i],
+                                 rstd + row_begin[i], s));
+      if (!make_tmap_kmajor(&am.m[am.n], d_src[i], uint64_t(d), uint64_t(rows), uint64_t(d) * 2,
+                            abox))
+        fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for a peer range");
+      am.row0[am.n] = int(row_begin[i]);
+      ++am.n;
+    }
+    am.row0[am.n] = 0x7fffffff;
+    const int sms = device_sm_count(w->device);
+    const int bn = gemm_pick_bn(n, N, sms);
+    KvOut out = kv_out_pages(pages, layer, d_page_table, 0, nullptr, 1);
+    out.start_pos = start_pos;
+    HC_CUDA(launch_restore_kv_multi(am, weight_map(L, bn, d, N), bn, int(n), N, d, true, out,
+                                    epi_for(w, L.colsum, w->cfg.norm_enabled ? mean : nullptr,
+                                            w->cfg.norm_enabled ? rstd : nullptr),
+                                    sms, s));
+  });
+}
+
+}  // extern "C"

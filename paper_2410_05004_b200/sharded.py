@@ -174,7 +174,11 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     from .capi import check, lib
 
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        backend = os.environ.get("HC_DIST_BACKEND", "nccl")  # gloo: 2 ranks on one GPU (tests)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     L, d, heads, kvh, dffn, n, rope = cfg
     stream = torch.cuda.current_stream().cuda_stream
     hb, hc = head_range(kvh, world, rank)
@@ -211,7 +215,28 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
         resident.append(hrows[b:e].clone() if e > b else hrows[:0].clone())
     store.finalize("bench")
     torch.cuda.synchronize()
-    r = GpuShardedRestorer(store, "bench", w, kv, table, n, d)
+    # default: the all-gather fused into K1 over peer memory (CUDA IPC over
+    # NVLink); HC_SHARD_MODE=nccl selects the NCCL all-gather pipeline
+    mode = os.environ.get("HC_SHARD_MODE", "peer")
+    if mode == "peer":
+        try:
+            r = PeerShardedRestorer(store, "bench", w, kv, table, n, d)
+        except Exception as exc:  # noqa: BLE001  (IPC mapping unavailable)
+            print(f"[rank {rank}] peer mapping failed ({exc}); using the NCCL all-gather",
+                  flush=True)
+            mode = "nccl"
+    if mode != "peer":
+        r = GpuShardedRestorer(store, "bench", w, kv, table, n, d)
+    if mode == "peer":
+        # resident shards live in this rank's range of the aligned split
+        b, e = r.ranges[rank]
+        resident = [None] * L
+        for layer in range(L):
+            hrows = torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
+            check(lib().hc_fill_symmetric(hrows.data_ptr(), hrows.numel(), 7, layer * n * d,
+                                          1.7320508, 1, stream))
+            resident[layer] = hrows[b:e].clone() if e > b else hrows[:0].clone()
+        torch.cuda.synchronize()
 
     def timed(resident_mode, steps):
         dist.barrier()
@@ -249,7 +274,9 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                 "data": "synthetic (splitmix64 bf16 hidden states + random-init weights)",
                 "config": {"workload": args.config + " head-sharded", "layers": L,
                            "d_hidden": d, "kv_heads": kvh, "tokens": n,
-                           "parallelism": f"head-sharded x{world} + NCCL all-gather",
+                           "parallelism": f"head-sharded x{world} + " + (
+                               "all-gather fused into K1 over peer memory" if mode == "peer"
+                               else "NCCL all-gather"),
                            "l2": "inputs larger than L2"},
                 "restore_latency_ms": {"resident": ms_res, "e2e": ms_e2e},
                 "e2e": {"value": n / (ms_e2e * 1e-3), "unit": "tokens/s",
@@ -264,5 +291,133 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                 "note": "value: shards resident in HBM (all-gather + K1); e2e: each rank "
                         "fetches its 1/N over PCIe; times are max over ranks"}
         print(json.dumps(line), flush=True)
+    if isinstance(r, PeerShardedRestorer):
+        r.close()
     dist.barrier()
     dist.destroy_process_group()
+
+
+# ------------------------------------------- GPU path, all-gather in K1 (peer)
+def aligned_ranges(n_tokens: int, world: int, align: int = 128) -> List[Tuple[int, int]]:
+    """Contiguous token ranges per rank, boundaries multiples of `align` rows
+    (the K1 tile: one M tile reads one rank's range) and hence of the 64-token
+    chunk."""
+    if n_tokens < 1 or world < 1:
+        raise ValueError("aligned_ranges: n_tokens and world must be >= 1")
+    blocks = (n_tokens + align - 1) // align
+    per = (blocks + world - 1) // world
+    return [(min(n_tokens, r * per * align), min(n_tokens, (r + 1) * per * align))
+            for r in range(world)]
+
+
+class PeerShardedRestorer:
+    """Head-sharded restore with the all-gather fused into K1 over peer memory.
+
+    Rank r fetches only its token range of each layer (its own PCIe link) into
+    a slot of a small staging ring; every rank's K1 (hc_project_multi_source)
+    reads the A tiles of all ranges straight from the owners' slots, which are
+    mapped into each process with CUDA IPC (NVLink on a multi-GPU node). No
+    gathered n x d copy exists. Slot hand-off is stream-ordered through flags
+    in device memory: the owner stores the slot's epoch into every rank's
+    `ready` flag after the fetch; each consumer stores it into the owner's
+    `consumed` flag after its K1; each side waits on its own memory
+    (hc_stream_wait_flag). torch.distributed (any backend; gloo suffices) is
+    used once, to exchange the IPC handles."""
+
+    def __init__(self, store, sid: str, weights, kv, page_table, n_tokens: int, d: int,
+                 depth: int = 2, group=None):
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.torch = torch
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        if self.world > 8:
+            raise ValueError("peer all-gather: at most 8 ranks (K1 sources)")
+        self.store, self.sid, self.w, self.kv, self.table = store, sid, weights, kv, page_table
+        self.n, self.d, self.depth = n_tokens, d, max(1, depth)
+        self.ranges = aligned_ranges(n_tokens, self.world)
+        b, e = self.ranges[self.rank]
+        rows = max(1, e - b)
+        self.slots = [torch.empty((rows, d), dtype=torch.bfloat16, device="cuda")
+                      for _ in range(self.depth)]
+        # flags[0][src][slot]: epoch of src's slot ready; flags[1][c][slot]:
+        # epoch consumer c finished with MY slot
+        self.flags = torch.zeros((2, self.world, self.depth), dtype=torch.int32, device="cuda")
+        mine = [reduce_tensor(t) for t in self.slots + [self.flags]]
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self._peer = []  # keep the mapped tensors alive
+        self.peer_slots, self.peer_flags = [], []
+        for r in range(self.world):
+            if r == self.rank:
+                ts = self.slots + [self.flags]
+            else:
+                ts = [fn(*args) for fn, args in allh[r]]
+                self._peer.append(ts)
+            self.peer_slots.append(ts[:-1])
+            self.peer_flags.append(ts[-1])
+        self.copy = torch.cuda.Stream()
+        self.step = 0
+        dist.barrier(group=group)
+
+    def close(self, group=None):
+        """Unmap the peers' buffers (before any producer process exits)."""
+        import torch.distributed as dist
+        self.torch.cuda.synchronize()
+        self._peer.clear()
+        self.peer_slots, self.peer_flags = [], []
+        self.torch.cuda.ipc_collect()
+        dist.barrier(group=group)
+
+    def _flag_ptr(self, owner: int, kind: int, who: int, slot: int) -> int:
+        f = self.peer_flags[owner]
+        return f.data_ptr() + ((kind * self.world + who) * self.depth + slot) * 4
+
+    def restore(self, layers: List[int], resident_shards=None, stream=None):
+        """Enqueue the restore of `layers` on `stream` (default: current)."""
+        import ctypes as Cc
+        torch = self.torch
+        from .capi import check, lib
+        compute = stream or torch.cuda.current_stream()
+        b, e = self.ranges[self.rank]
+        row_begin = (Cc.c_int64 * (self.world + 1))(*([r[0] for r in self.ranges] + [self.n]))
+        start = torch.cuda.Event()
+        start.record(compute)
+        self.copy.wait_event(start)
+        P = Cc.c_void_p
+        for layer in layers:
+            g = self.step
+            self.step += 1
+            s, ep = g % self.depth, g // self.depth + 1
+            # IO lane: my slot is free once every consumer finished epoch ep-1
+            if ep > 1:
+                for c in range(self.world):
+                    check(lib().hc_stream_wait_flag(self.copy.cuda_stream,
+                                                    self._flag_ptr(self.rank, 1, c, s), ep - 1))
+            if e > b:
+                dst = self.slots[s]
+                if resident_shards is not None:
+                    with torch.cuda.stream(self.copy):
+                        dst[: e - b].copy_(resident_shards[layer][: e - b], non_blocking=True)
+                else:
+                    check(lib().hc_store_read_layer_range(
+                        self.store._h, self.sid.encode(), layer, 0, b, e, dst.data_ptr(),
+                        (e - b) * self.d * 2, 1, self.copy.cuda_stream))
+            ready = (P * self.world)(*[self._flag_ptr(r, 0, self.rank, s)
+                                       for r in range(self.world)])
+            check(lib().hc_stream_signal_flags(self.copy.cuda_stream, ready, self.world, ep))
+            # compute lane: every range of this layer is in place -> fused K1
+            for src in range(self.world):
+                check(lib().hc_stream_wait_flag(compute.cuda_stream,
+                                                self._flag_ptr(self.rank, 0, src, s), ep))
+            srcs = (P * self.world)(*[self.peer_slots[r][s].data_ptr()
+                                      for r in range(self.world)])
+            check(lib().hc_project_multi_source(self.w._h, layer, self.world, srcs, row_begin,
+                                                Cc.byref(self.kv.desc), self.table.data_ptr(), 0,
+                                                compute.cuda_stream))
+            done = (P * self.world)(*[self._flag_ptr(r, 1, self.rank, s)
+                                      for r in range(self.world)])
+            check(lib().hc_stream_signal_flags(compute.cuda_stream, done, self.world, ep))
+        end = torch.cuda.Event()
+        end.record(self.copy)
+        compute.wait_event(end)
