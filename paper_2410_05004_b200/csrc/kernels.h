@@ -153,6 +153,15 @@ cudaError_t launch_argmax_pairs(const float* logits, int vocab, int ld, int n_se
 cudaError_t launch_kv_gather(const KvOut& kv, int pos0, int64_t n_rows, void* rows,
                              cudaStream_t stream);
 
+// Decode-time save, stage 1: row b of a step's layer inputs (layers
+// [h0, h0+nh), row stride rows_in_step) -> dsts[b].dst + l * dsts[b].pitch.
+struct AppendDst {
+  void* dst;
+  int64_t pitch;  // bytes between layers in the request's round buffer
+};
+cudaError_t launch_append_rows(const void* step_rows, int rows_in_step, int h0, int nh, int d,
+                               const AppendDst* d_dsts, int n_rows, cudaStream_t stream);
+
 // Row statistics for the LayerNorm fold: mean and 1/sqrt(var+1e-5) per row,
 // mean/var accumulated in double like the reference (model.cpp:43-61).
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,

@@ -51,6 +51,15 @@ __global__ void wait_kernel(const uint32_t* addr, uint32_t value) {
   }
 }
 
+__global__ void append_rows_kernel(const uint4* __restrict__ step, int rows_in_step, int h0, int d,
+                                   const AppendDst* __restrict__ dsts) {
+  const int b = blockIdx.x, l = blockIdx.y;
+  const int vec = d / 8;
+  const uint4* src = step + (size_t(h0 + l) * rows_in_step + b) * vec;
+  uint4* dst = reinterpret_cast<uint4*>(static_cast<char*>(dsts[b].dst) + size_t(l) * dsts[b].pitch);
+  for (int i = threadIdx.x; i < vec; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
 using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
 WaitFn wait_value_fn() {
@@ -67,6 +76,15 @@ WaitFn wait_value_fn() {
 }
 
 }  // namespace
+
+cudaError_t launch_append_rows(const void* step_rows, int rows_in_step, int h0, int nh, int d,
+                               const AppendDst* d_dsts, int n_rows, cudaStream_t stream) {
+  if (n_rows <= 0 || nh <= 0) return cudaSuccess;
+  if (d % 8) return cudaErrorInvalidValue;
+  append_rows_kernel<<<dim3(unsigned(n_rows), unsigned(nh)), 128, 0, stream>>>(
+      static_cast<const uint4*>(step_rows), rows_in_step, h0, d, d_dsts);
+  return cudaGetLastError();
+}
 
 }  // namespace hc
 

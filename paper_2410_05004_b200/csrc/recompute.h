@@ -36,6 +36,15 @@ void forward_batch(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
                    const int32_t* d_page_tables, int table_stride, void* d_layer_inputs,
                    int32_t* d_next_tokens, cudaStream_t stream);
 
+// The same with the sequence metadata already on the device (d_cu [n_seqs+1]
+// row offsets, d_starts [n_seqs] first positions; positions validated by the
+// caller): no host->device traffic, so a decode step can be captured into a
+// CUDA graph.
+void forward_batch_dev(const hc_weights* w, const int32_t* d_tokens, int n_seqs, int64_t total,
+                       int max_new, const int32_t* d_cu, const int32_t* d_starts,
+                       const hc_kv_pages* pages, const int32_t* d_page_tables, int table_stride,
+                       void* d_layer_inputs, int32_t* d_next_tokens, cudaStream_t stream);
+
 // Measured seconds of one recompute layer over n tokens at the steady-state
 // clock (after warm_s seconds of back-to-back layers); 0 when the full block
 // weights are not set.

@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "common.h"
+#include "kernels.h"
 #include "recompute.h"
 #include "store.h"
 #include "weights.h"
@@ -220,9 +221,18 @@ class Engine {
   int32_t* h_tok_ = nullptr;    // pinned: tokens
   int32_t* h_table_ = nullptr;  // pinned: batch page tables
   int32_t* h_next_ = nullptr;   // pinned: next tokens
+  int32_t* h_meta_ = nullptr;   // pinned: decode cu_seqlens + positions
+  AppendDst* h_app_ = nullptr;  // pinned: per-sequence round-buffer rows (stage 1)
+  AppendDst* d_app_ = nullptr;
   int32_t* d_tok_ = nullptr;
   int32_t* d_table_ = nullptr;
   int32_t* d_next_ = nullptr;
+  int32_t* d_meta_ = nullptr;
+  // decode steps as CUDA graphs, one per batch size (launch-bound otherwise)
+  cudaStream_t cap_ = nullptr;
+  std::map<int, cudaGraphExec_t> graphs_;
+  std::map<int, int> eager_runs_;
+  bool use_graphs_ = true;
   void* d_step_ = nullptr;      // [L][max_rows][d] layer inputs of one step
   std::unique_ptr<PersistWorker> worker_;
   bool started_daemon_ = false;
@@ -304,7 +314,18 @@ void Engine::setup() {
   HC_CUDA(cudaMalloc(&d_table_, sizeof(int32_t) * size_t(max_batch_) * size_t(stride_)));
   HC_CUDA(cudaMalloc(&d_next_, sizeof(int32_t) * size_t(max_batch_)));
   HC_CUDA(cudaMalloc(&d_step_, size_t(L_) * size_t(max_rows_) * size_t(d_) * 2));
+  HC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_meta_),
+                        sizeof(int32_t) * size_t(2 * max_batch_ + 1), cudaHostAllocDefault));
+  HC_CUDA(cudaMalloc(&d_meta_, sizeof(int32_t) * size_t(2 * max_batch_ + 1)));
+  HC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_app_), sizeof(AppendDst) * size_t(max_batch_),
+                        cudaHostAllocDefault));
+  HC_CUDA(cudaMalloc(&d_app_, sizeof(AppendDst) * size_t(max_batch_)));
   HC_CUDA(cudaStreamCreateWithFlags(&save_, cudaStreamNonBlocking));
+  HC_CUDA(cudaStreamCreateWithFlags(&cap_, cudaStreamNonBlocking));
+  {
+    const char* e = getenv("HC_SERVE_GRAPHS");
+    use_graphs_ = !(e && atoi(e) == 0);
+  }
   per_.assign(size_t(n_), hc_request_metrics{});
   outs_.assign(size_t(n_), {});
   if (persisting()) {
@@ -338,6 +359,13 @@ void Engine::teardown() {
   cudaFree(d_table_);
   cudaFree(d_next_);
   cudaFree(d_step_);
+  cudaFreeHost(h_meta_);
+  cudaFree(d_meta_);
+  cudaFreeHost(h_app_);
+  cudaFree(d_app_);
+  for (auto& g : graphs_) cudaGraphExecDestroy(g.second);
+  graphs_.clear();
+  if (cap_) cudaStreamDestroy(cap_);
   if (save_) cudaStreamDestroy(save_);
 }
 
@@ -597,7 +625,7 @@ void Engine::decode_batch(std::vector<Active*>& batch) {
   // one batched decode step (harness.cpp:294-318): every member's pending token
   const auto t0 = Clock::now();
   const int B = int(batch.size());
-  std::vector<int32_t> ones(static_cast<size_t>(B), 1), starts(static_cast<size_t>(B));
+  std::vector<int32_t> starts(static_cast<size_t>(B));
   HC_CUDA(cudaStreamSynchronize(s_));  // pinned staging reuse
   for (int b = 0; b < B; ++b) {
     Active& a = *batch[size_t(b)];
@@ -606,14 +634,65 @@ void Engine::decode_batch(std::vector<Active*>& batch) {
     std::memcpy(h_table_ + size_t(b) * size_t(stride_), a.pages.data(),
                 a.pages.size() * sizeof(int32_t));
   }
+  for (int b = 0; b <= B; ++b) h_meta_[b] = b;  // one row per sequence
+  for (int b = 0; b < B; ++b) {
+    if (starts[size_t(b)] + 1 > w_->cfg.max_seq) fail(HC_EINVAL, "forward: sequence exceeds max_seq");
+    h_meta_[B + 1 + b] = starts[size_t(b)];
+  }
   HC_CUDA(cudaMemcpyAsync(d_tok_, h_tok_, sizeof(int32_t) * size_t(B), cudaMemcpyHostToDevice, s_));
   HC_CUDA(cudaMemcpyAsync(d_table_, h_table_, sizeof(int32_t) * size_t(B) * size_t(stride_),
                           cudaMemcpyHostToDevice, s_));
-  forward_batch(w_, d_tok_, B, ones.data(), starts.data(), &pages_, d_table_, stride_, d_step_,
-                d_next_, s_);
+  HC_CUDA(cudaMemcpyAsync(d_meta_, h_meta_, sizeof(int32_t) * size_t(2 * B + 1),
+                          cudaMemcpyHostToDevice, s_));
+  // stage 1 of the two-stage save rides inside the step: one kernel appends
+  // every sequence's new row of each HIDDEN layer to its round buffer
+  const bool fused_append = persisting() && hid_.count > 0 && o_.saving != HC_SAVING_DIRECT;
+  if (fused_append) {
+    const size_t rb = size_t(d_) * 2;
+    for (int b = 0; b < B; ++b) {
+      Active& a = *batch[size_t(b)];
+      h_app_[b].dst = static_cast<char*>(a.acc) + size_t(a.saved_rows) * rb;
+      h_app_[b].pitch = int64_t(a.cap) * int64_t(rb);
+    }
+    HC_CUDA(cudaMemcpyAsync(d_app_, h_app_, sizeof(AppendDst) * size_t(B), cudaMemcpyHostToDevice,
+                            s_));
+  }
+  auto step = [&](cudaStream_t st) {
+    forward_batch_dev(w_, d_tok_, B, B, 1, d_meta_, d_meta_ + B + 1, &pages_, d_table_, stride_,
+                      d_step_, d_next_, st);
+    if (fused_append)
+      HC_CUDA(launch_append_rows(d_step_, B, hid_.begin, hid_.count, d_, d_app_, B, st));
+  };
+  auto it = graphs_.find(B);
+  if (it != graphs_.end()) {
+    HC_CUDA(cudaGraphLaunch(it->second, s_));
+  } else if (use_graphs_ && eager_runs_[B] >= 1) {
+    // capture once per batch size (after one eager run set every kernel up)
+    cudaGraph_t graph = nullptr;
+    HC_CUDA(cudaStreamBeginCapture(cap_, cudaStreamCaptureModeThreadLocal));
+    try {
+      step(cap_);
+    } catch (...) {
+      cudaStreamEndCapture(cap_, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    HC_CUDA(cudaStreamEndCapture(cap_, &graph));
+    cudaGraphExec_t exec = nullptr;
+    HC_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    graphs_[B] = exec;
+    HC_CUDA(cudaGraphLaunch(exec, s_));
+  } else {
+    step(s_);
+    ++eager_runs_[B];
+  }
   HC_CUDA(cudaMemcpyAsync(h_next_, d_next_, sizeof(int32_t) * size_t(B), cudaMemcpyDeviceToHost,
                           s_));
-  for (int b = 0; b < B; ++b) append_rows(*batch[size_t(b)], d_step_, B, b, 1);
+  for (int b = 0; b < B; ++b) {
+    if (fused_append) ++batch[size_t(b)]->saved_rows;
+    else append_rows(*batch[size_t(b)], d_step_, B, b, 1);
+  }
   HC_CUDA(cudaStreamSynchronize(s_));
   charge(since(t0));
   ++steps_;
