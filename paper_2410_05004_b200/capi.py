@@ -11,7 +11,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libhcache_b200.so")
+LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(HERE, "lib", "libhcache_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "hcache_b200.h")
 
 HC_OK, HC_EINVAL, HC_ENOENT, HC_EINCOMPLETE, HC_EAGAIN, HC_ECUDA, HC_ENCCL, HC_ERUNTIME, \

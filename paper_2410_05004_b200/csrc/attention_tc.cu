@@ -97,7 +97,8 @@ struct AttnCfg {
 template <int DH>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK2,
+                   const __grid_constant__ CUtensorMap tmV2, AttnArgs a) {
   using Cfg = AttnCfg<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) asm volatile("trap;");  // SW128 operands need 1 KB alignment
@@ -130,6 +131,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmK2);
+    tma_prefetch_desc(&tmV2);
     mbar_init(q_full, 1);
     for (int s = 0; s < kAttnStages; ++s) {
       mbar_init(&k_full[s], 1);
@@ -169,6 +172,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_arrive_expect_tx(full, Cfg::kKVBytes);
         uint8_t* dst = sKV + st * Cfg::kStageBytes + (is_v ? Cfg::kKVBytes : 0);
         const CUtensorMap* map = is_v ? &tmV : &tmK;
+        if (a.page_table && a.box_rows < kAttnN) {
+          // pages of this tile consecutive in the pool (a freshly allocated
+          // session): one 128-row box per head half instead of one per page
+          const int last = (a.n - 1) / a.page_size;
+          const int pg0 = min(j * kAttnN / a.page_size, last);
+          const int per = kAttnN / a.page_size;
+          const int base = __ldg(a.page_table + pg0);
+          bool contig = pg0 + per - 1 <= last;
+          for (int c = 1; c < per && contig; ++c) contig = __ldg(a.page_table + pg0 + c) == base + c;
+          if (contig) {
+            const CUtensorMap* map2 = is_v ? &tmV2 : &tmK2;
+            for (int hb = 0; hb < DH / 64; ++hb)
+              tma_load_2d(dst + hb * Cfg::kHalf, map2, full, hk * DH + hb * 64, base * a.page_size);
+            return;
+          }
+        }
         for (int c = 0; c < kAttnN / a.box_rows; ++c) {
           const int key0 = j * kAttnN + c * a.box_rows;
           int row = key0;
@@ -375,7 +394,7 @@ template <int DH>
 cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, const KvOut& kv,
                            int64_t kv_rows, void* out, cudaStream_t stream) {
   const int box_rows = kv.page_table ? (kv.page_size < kAttnN ? kv.page_size : kAttnN) : kAttnN;
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, tk2, tv2;
   const uint64_t ldq = uint64_t(n_heads) * DH;
   if (!make_tmap_kmajor(&tq, q, ldq, uint64_t(n), ldq * 2, kAttnM)) return cudaErrorInvalidValue;
   // K/V maps cover the whole page pool (rows are gathered page by page) or,
@@ -384,7 +403,9 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
   if (!make_tmap_kmajor(&tk, kv.k_base, uint64_t(kv.d_kv), rows, uint64_t(kv.d_kv) * 2,
                         uint32_t(box_rows)) ||
       !make_tmap_kmajor(&tv, kv.v_base, uint64_t(kv.d_kv), rows, uint64_t(kv.d_kv) * 2,
-                        uint32_t(box_rows)))
+                        uint32_t(box_rows)) ||
+      !make_tmap_kmajor(&tk2, kv.k_base, uint64_t(kv.d_kv), rows, uint64_t(kv.d_kv) * 2, kAttnN) ||
+      !make_tmap_kmajor(&tv2, kv.v_base, uint64_t(kv.d_kv), rows, uint64_t(kv.d_kv) * 2, kAttnN))
     return cudaErrorInvalidValue;
   AttnArgs a;
   a.n = n;
@@ -406,7 +427,7 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
     attr_dev = dev;
   }
   const dim3 grid((n + kAttnM - 1) / kAttnM, n_heads);
-  attn_tc_kernel<DH><<<grid, kAttnThreads, AttnCfg<DH>::kSmem, stream>>>(tq, tk, tv, a);
+  attn_tc_kernel<DH><<<grid, kAttnThreads, AttnCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
   return cudaGetLastError();
 }
 

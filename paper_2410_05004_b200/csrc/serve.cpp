@@ -273,7 +273,7 @@ void Engine::setup() {
   hid_ = method_range(plan_, HC_METHOD_HIDDEN);
   kvr_ = method_range(plan_, HC_METHOD_KV_OFFLOAD);
   // request validation and staging sizes
-  int max_need = 1, max_rows = 1;
+  int max_need = 1, max_rows = 1, max_hist = 0;
   std::map<std::string, int> hist;
   for (int i = 0; i < n_; ++i) {
     const hc_request& r = reqs_[i];
@@ -283,6 +283,7 @@ void Engine::setup() {
       fail(HC_EINVAL, "serve: requests must be sorted by arrival");
     int& h = hist[r.session_id];
     if (r.n_context > 0 && h == 0) h = r.n_context;
+    max_hist = std::max(max_hist, h);
     const int need = h + r.n_prompt + r.output_budget;
     if (need > c.max_seq) fail(HC_EINVAL, "serve: request exceeds max_seq");
     max_need = std::max(max_need, need);
@@ -325,6 +326,21 @@ void Engine::setup() {
   {
     const char* e = getenv("HC_SERVE_GRAPHS");
     use_graphs_ = !(e && atoi(e) == 0);
+  }
+  // grow the stream-ordered pool once to what the largest restore stages
+  // (its ring of hidden-state layers + K/V rows), outside the clock, so the
+  // first large restore does not pay for the pool's growth
+  if (persisting() && max_hist > 0) {
+    const size_t warm = std::min<size_t>(size_t(16) << 30,
+                                         size_t(max_hist) * size_t(d_) * 2 * size_t(L_) +
+                                             size_t(max_hist) * size_t(4 * dkv_) * 2);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, warm, s_) == cudaSuccess) {
+      HC_CUDA(cudaFreeAsync(p, s_));
+      HC_CUDA(cudaStreamSynchronize(s_));
+    } else {
+      cudaGetLastError();
+    }
   }
   per_.assign(size_t(n_), hc_request_metrics{});
   outs_.assign(size_t(n_), {});
