@@ -162,6 +162,11 @@ struct AppendDst {
 cudaError_t launch_append_rows(const void* step_rows, int rows_in_step, int h0, int nh, int d,
                                const AppendDst* d_dsts, int n_rows, cudaStream_t stream);
 
+// Session rows in the reference's formats (HC_DTYPE_F32 / HC_DTYPE_F16) ->
+// bf16 (round to nearest even); dst may equal src for F16.
+cudaError_t launch_convert_to_bf16(const void* src, int src_dtype, void* dst, int64_t n,
+                                   cudaStream_t stream);
+
 // Row statistics for the LayerNorm fold: mean and 1/sqrt(var+1e-5) per row,
 // mean/var accumulated in double like the reference (model.cpp:43-61).
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,

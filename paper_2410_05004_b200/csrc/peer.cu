@@ -18,6 +18,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -60,6 +64,28 @@ __global__ void append_rows_kernel(const uint4* __restrict__ step, int rows_in_s
   for (int i = threadIdx.x; i < vec; i += blockDim.x) dst[i] = __ldg(src + i);
 }
 
+__global__ void convert_f32_kernel(const float4* __restrict__ src, uint2* __restrict__ dst,
+                                   int64_t n4) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = __ldg(src + i);
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    dst[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
+
+__global__ void convert_f16_kernel(const uint2* src, uint2* dst, int64_t n4) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint2 u = src[i];
+    const __half2 h0 = *reinterpret_cast<const __half2*>(&u.x);
+    const __half2 h1 = *reinterpret_cast<const __half2*>(&u.y);
+    const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+    __nv_bfloat162 a = __floats2bfloat162_rn(f0.x, f0.y), b = __floats2bfloat162_rn(f1.x, f1.y);
+    dst[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
+
 using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
 WaitFn wait_value_fn() {
@@ -76,6 +102,23 @@ WaitFn wait_value_fn() {
 }
 
 }  // namespace
+
+cudaError_t launch_convert_to_bf16(const void* src, int src_dtype, void* dst, int64_t n,
+                                   cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (n % 4) return cudaErrorInvalidValue;
+  const int64_t n4 = n / 4;
+  const unsigned grid = unsigned(std::min<int64_t>((n4 + 255) / 256, 148 * 16));
+  if (src_dtype == HC_DTYPE_F32)
+    convert_f32_kernel<<<grid, 256, 0, stream>>>(static_cast<const float4*>(src),
+                                                 static_cast<uint2*>(dst), n4);
+  else if (src_dtype == HC_DTYPE_F16)
+    convert_f16_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint2*>(src),
+                                                 static_cast<uint2*>(dst), n4);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_append_rows(const void* step_rows, int rows_in_step, int h0, int nh, int d,
                                const AppendDst* d_dsts, int n_rows, cudaStream_t stream) {

@@ -239,8 +239,14 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
   if (plan_serialize(plan) != plan_serialize(&m.plan))
     fail(HC_EINVAL, "restore: plan does not match session manifest");
   if (m.d_hidden != w->cfg.d_hidden) fail(HC_EINVAL, "restore: d_hidden mismatch");
-  if (m.elem_bytes != 2 || m.dtype != HC_DTYPE_BF16)
-    fail(HC_EINVAL, "restore: the device path restores bf16 sessions (elem_bytes 2)");
+  // persisted element type: bf16 (native), or the reference's own formats
+  // -- fp32 (ModelConfig::elem_bytes = 4, its default) and the fp16 codec --
+  // which arrive as stored over PCIe and are rounded to bf16 on the device
+  // right before their K1 / scatter
+  const int eb = m.elem_bytes;
+  const bool native = m.dtype == HC_DTYPE_BF16 && eb == 2;
+  if (!native && !(m.dtype == HC_DTYPE_F32 && eb == 4) && !(m.dtype == HC_DTYPE_F16 && eb == 2))
+    fail(HC_EINVAL, "restore: unsupported session element type");
   validate_pages(w, pages, w->d_kv);
   const int n = m.n_tokens;
   if (n <= 0) fail(HC_EINVAL, "restore: empty session");
@@ -263,8 +269,14 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
   if (n_kv && (m.d_kv != w->d_kv || w->d_kv != w->d_kv_all))
     fail(HC_EINVAL, "restore: KV-offload layers need all KV heads on this GPU");
 
-  const size_t h_bytes = size_t(n) * size_t(m.d_hidden) * 2;
-  const size_t kv_bytes = size_t(n) * size_t(2 * m.d_kv) * 2;
+  const size_t h_bytes = size_t(n) * size_t(m.d_hidden) * size_t(eb);
+  const size_t kv_bytes = size_t(n) * size_t(2 * m.d_kv) * size_t(eb);
+  // fp32 sessions: the bf16 copy K1 / K4 read (fp16 converts in place)
+  const size_t conv_bytes =
+      m.dtype == HC_DTYPE_F32
+          ? size_t(n) * size_t(std::max(n_hidden ? m.d_hidden : 0, n_kv ? 2 * m.d_kv : 0)) * 2
+          : 0;
+  StreamScratch conv(conv_bytes, stream);
   const int depth = auto_depth(std::max(n_hidden, 1), h_bytes, opts ? opts->prefetch_depth : 0);
   const int nbuf_h = std::min(std::max(n_hidden, 1), depth + 1);
   const int nbuf_kv = std::min(std::max(n_kv, 1), 2);
@@ -374,10 +386,17 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
     cudaEvent_t cs = timed ? evp.get() : nullptr;
     if (cs) HC_CUDA(cudaEventRecord(cs, stream));
     KvOut out = kv_out_pages(pages, f.job.layer, d_page_table, 0, nullptr, 1);
+    const void* rows = f.buf;
+    if (!native) {
+      const int64_t elems = int64_t(n) * (f.hid ? m.d_hidden : 2 * m.d_kv);
+      void* dst = m.dtype == HC_DTYPE_F32 ? conv.ptr : f.buf;
+      HC_CUDA(launch_convert_to_bf16(f.buf, m.dtype, dst, elems, stream));
+      rows = dst;
+    }
     if (f.hid) {
-      project_rows(w, f.job.layer, f.buf, n, out, stream);
+      project_rows(w, f.job.layer, rows, n, out, stream);
     } else {
-      HC_CUDA(launch_kv_scatter(f.buf, n, out, stream));
+      HC_CUDA(launch_kv_scatter(rows, n, out, stream));
     }
     cudaEvent_t done = evp.get();
     HC_CUDA(cudaEventRecord(done, stream));

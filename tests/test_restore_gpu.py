@@ -247,3 +247,44 @@ def test_token_wise_rejects_bad_splits(cuda):
     for bad in (-1, 101):
         with pytest.raises(ValueError):
             H.restore_token_wise(store, "tw2", w, bad, kv, table)
+
+
+@pytest.mark.parametrize("fmt", ["f32", "f16"])
+def test_restore_reference_element_formats(cuda, oracle, fmt):
+    """Sessions persisted in the reference's own formats -- fp32
+    (ModelConfig::elem_bytes = 4, its default) and the fp16 codec
+    (fp16.hpp) -- restore through the same device path: rows travel as stored
+    and are rounded to bf16 on the device. HIDDEN layers vs the oracle
+    projection of the bf16-rounded rows (REL_TOL); KV-offload layers equal the
+    bf16 rounding of the stored rows exactly."""
+    import torch
+    from oracle import bf16_round
+    from paper_2410_05004_b200 import capi
+    from paper_2410_05004_b200 import hcache as H
+    n = 450
+    cfg, w, kv, table = _setup(n=n)
+    store = H.StorageManager(H.DevicePool(2))
+    plan = H.RestorationPlan.make(4, 3, H.Complement.KV_OFFLOAD)
+    eb, dt = (4, capi.HC_DTYPE_F32) if fmt == "f32" else (2, capi.HC_DTYPE_F16)
+    store.create_session(H.SessionSeed("r", cfg.hash(), 4, 512, eb, plan, list(range(n)), d_kv=512,
+                                       dtype=dt))
+    rng = np.random.default_rng(5)
+    hid = [rng.standard_normal((n, 512)).astype(np.float32) for _ in range(3)]
+    kvrows = rng.standard_normal((n, 1024)).astype(np.float32)
+    for L in range(3):
+        assert store.snapshot("r", L, H.StateKind.HIDDEN, hid[L])  # host fp32 -> session codec
+    assert store.snapshot("r", 3, H.StateKind.KV, kvrows)
+    store.finalize("r")
+    H.restore(store, "r", w, plan, H.ThrottleConfig(), kv, table)
+    torch.cuda.synchronize()
+
+    def stored(x):  # what the session holds, as fp32
+        return x if fmt == "f32" else x.astype(np.float16).astype(np.float32)
+    for L in range(3):
+        kr, vr = oracle.project(bf16_round(stored(hid[L])), *cpu_wkv(oracle, 512, 512, L), 8)
+        k, v = kv.gather(L, table, n)
+        assert max_rel_err(k.float().cpu().numpy(), kr) < REL_TOL, L
+        assert max_rel_err(v.float().cpu().numpy(), vr) < REL_TOL, L
+    k, v = kv.gather(3, table, n)
+    want = torch.from_numpy(stored(kvrows)).bfloat16()
+    assert torch.equal(k.cpu(), want[:, :512]) and torch.equal(v.cpu(), want[:, 512:])
