@@ -18,6 +18,7 @@
 // backpressure and read_layer() returns std::nullopt for absent layers.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <optional>
@@ -530,6 +531,117 @@ inline ProfiledTimings profile_hardware(const DeviceWeights& w, int n_tokens) {
   hc_timings t{};
   check(hc_profile(w.get(), n_tokens, &t));
   return ProfiledTimings{t.io_h, t.io_kv, t.c_h, t.c_token, t.n_layers};
+}
+
+
+// restore_token_wise (restore.hpp:47-49), the token-wise partition ablation.
+inline RestoreResult restore_token_wise(StorageManager& store, const std::string& session_id,
+                                        const DeviceWeights& w, int hidden_tokens,
+                                        const KvPages& pages, const int32_t* d_page_table,
+                                        void* stream = nullptr) {
+  std::vector<hc_timeline> tl(1);
+  check(hc_restore_token_wise(store.get(), session_id.c_str(), w.get(), hidden_tokens,
+                              &pages.desc, d_page_table, stream, tl.data()));
+  RestoreResult r;
+  r.timeline = Timeline::from(tl[0]);
+  return r;
+}
+
+// forward_tokens / decode_step (model.hpp:115-120) for a batch of sequences
+// continuing their paged caches; next tokens stay on the device.
+inline void forward_batch(const DeviceWeights& w, const int32_t* d_tokens,
+                          const std::vector<int32_t>& new_lens,
+                          const std::vector<int32_t>& start_pos, const KvPages& pages,
+                          const int32_t* d_page_tables, int table_stride,
+                          void* d_layer_inputs, int32_t* d_next_tokens, void* stream = nullptr) {
+  if (new_lens.size() != start_pos.size())
+    throw std::invalid_argument("forward_batch: new_lens / start_pos size mismatch");
+  check(hc_forward_batch(w.get(), d_tokens, int32_t(new_lens.size()), new_lens.data(),
+                         start_pos.data(), &pages.desc, d_page_tables, table_stride,
+                         d_layer_inputs, d_next_tokens, stream));
+}
+
+// ---------------------------------------------------------------- serving
+// Strategy / SavingMode / Request / RequestMetrics / Metrics / RunOptions /
+// run (harness.hpp:14-72, trace.hpp:11-19) on the device engine.
+enum class Strategy { HCache = HC_STRATEGY_HCACHE, KvOffload = HC_STRATEGY_KV_OFFLOAD,
+                      Recompute = HC_STRATEGY_RECOMPUTE, Ideal = HC_STRATEGY_IDEAL };
+enum class SavingMode { TwoStage = HC_SAVING_TWO_STAGE, Direct = HC_SAVING_DIRECT,
+                        Off = HC_SAVING_OFF };
+
+struct Request {
+  std::string session_id;
+  int round = 1;
+  int history_tokens = 0;
+  std::vector<int32_t> context;
+  std::vector<int32_t> prompt;
+  int output_budget = 1;
+  double arrival_s = 0;
+};
+
+struct RequestMetrics {
+  std::string session_id;
+  int round = 1;
+  double arrival_s = 0;
+  int history_tokens = 0;
+  double restore_s = 0, ttft_s = 0, tbt_s = 0;
+  int generated = 0;
+};
+
+struct Metrics {
+  Strategy strategy = Strategy::Ideal;
+  std::vector<RequestMetrics> per_request;
+  std::vector<std::vector<int32_t>> outputs;
+  hc_serve_metrics agg{};  // ttft_p50/p95, tbt_mean/p50/p95, restore tok/s, bytes/token, ...
+};
+
+struct RunOptions {
+  Strategy strategy = Strategy::HCache;
+  SavingMode saving = SavingMode::TwoStage;
+  RestorationPlan hcache_plan;  // required for Strategy::HCache
+  int page_size = 64;
+  int num_pages = 0;  // KV page pool (all layers); 0: sized for the whole trace
+  int max_batch = 0;
+};
+
+inline Metrics run(const std::vector<Request>& trace, const DeviceWeights& w,
+                   StorageManager& store, const RunOptions& opt, void* stream = nullptr) {
+  std::vector<hc_request> reqs(trace.size());
+  long pages_needed = 0;
+  for (size_t i = 0; i < trace.size(); ++i) {
+    const Request& r = trace[i];
+    reqs[i] = hc_request{r.session_id.c_str(), r.round, int32_t(r.context.size()),
+                         r.context.data(), int32_t(r.prompt.size()), r.output_budget,
+                         r.prompt.data(), r.arrival_s};
+    pages_needed += (r.history_tokens + long(r.context.size()) + long(r.prompt.size()) +
+                     r.output_budget + opt.page_size - 1) / opt.page_size;
+  }
+  hc_serve_opts o{};
+  o.strategy = int32_t(opt.strategy);
+  o.saving = int32_t(opt.saving);
+  o.plan = opt.hcache_plan.raw;
+  o.page_size = opt.page_size;
+  o.num_pages = opt.num_pages > 0 ? opt.num_pages : int32_t(std::max(1L, pages_needed));
+  o.max_batch = opt.max_batch;
+  std::vector<hc_request_metrics> per(std::max<size_t>(1, trace.size()));
+  size_t total_out = 0;
+  for (const auto& r : trace) total_out += size_t(r.output_budget);
+  std::vector<int32_t> outs(std::max<size_t>(1, total_out));
+  Metrics m;
+  m.strategy = opt.strategy;
+  check(hc_serve_run(store.get(), w.get(), reqs.data(), int32_t(reqs.size()), &o, per.data(),
+                     outs.data(), &m.agg, stream));
+  size_t off = 0;
+  for (size_t i = 0; i < trace.size(); ++i) {
+    const hc_request_metrics& q = per[i];
+    m.per_request.push_back(RequestMetrics{trace[i].session_id, q.round, q.arrival_s,
+                                           q.history_tokens, q.restore_s, q.ttft_s, q.tbt_s,
+                                           q.generated});
+    m.outputs.emplace_back(outs.begin() + long(off),
+                           outs.begin() + long(off) + trace[i].output_budget);
+    off += size_t(trace[i].output_budget);
+  }
+  return m;
 }
 
 }  // namespace hcache_b200
