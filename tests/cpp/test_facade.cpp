@@ -281,6 +281,64 @@ static void gpu_tests() {
   cudaFree(d_table);
 }
 
+// serving loop through the facade (harness.hpp run): HCACHE and KV_OFFLOAD
+// rebuild the live K/V exactly, so they generate the same tokens; RECOMPUTE
+// and IDEAL both re-prefill and agree with each other.
+static void serve_tests() {
+  const int L = 2, d = 256, heads = 4, dffn = 1024, vocab = 512;
+  ModelConfig cfg;
+  cfg.n_layers = L;
+  cfg.d_hidden = d;
+  cfg.n_heads = heads;
+  cfg.d_ffn = dffn;
+  cfg.vocab_size = vocab;
+  cfg.max_seq = 1024;
+  cfg.elem_bytes = 2;
+  DeviceWeights w(cfg);
+  std::vector<void*> bufs;
+  auto fill = [&](size_t elems, uint64_t seed) {
+    void* p = nullptr;
+    cudaMalloc(&p, elems * 2);
+    check(hc_fill_symmetric(p, int64_t(elems), seed, 0, 0.0625f, HC_DTYPE_BF16, nullptr));
+    bufs.push_back(p);
+    return p;
+  };
+  w.set_embedding(fill(size_t(vocab) * d, 1));
+  for (int l = 0; l < L; ++l) {
+    void* wkv = fill(size_t(2 * d) * d, 10 + l);
+    w.set_layer_kv(l, wkv);
+    w.set_layer_full(l, fill(size_t(d) * d, 20 + l), wkv, fill(size_t(d) * d, 30 + l),
+                     fill(size_t(dffn) * d, 40 + l), fill(size_t(d) * dffn, 50 + l));
+  }
+  std::vector<Request> trace;
+  for (int r = 1; r <= 2; ++r)
+    for (int s = 0; s < 2; ++s) {
+      Request q;
+      q.session_id = "s" + std::to_string(s);
+      q.round = r;
+      for (int i = 0; i < 20; ++i) q.prompt.push_back((i * 7 + s * 13 + r) % vocab);
+      q.output_budget = 6;
+      q.arrival_s = (r - 1) * 1000.0 + s * 0.001;
+      trace.push_back(q);
+    }
+  auto one = [&](Strategy st) {
+    StorageManager store(DevicePool{2});
+    RunOptions o;
+    o.strategy = st;
+    o.hcache_plan = RestorationPlan::make(L, L, Complement::None);
+    return run(trace, w, store, o);
+  };
+  Metrics hc = one(Strategy::HCache), kvo = one(Strategy::KvOffload),
+          re = one(Strategy::Recompute), id = one(Strategy::Ideal);
+  CHECK(hc.outputs.size() == trace.size() && hc.outputs[0].size() == 6);
+  CHECK(hc.outputs == kvo.outputs);
+  CHECK(re.outputs == id.outputs);
+  CHECK(hc.per_request[2].history_tokens == 26 && hc.per_request[2].restore_s > 0);
+  CHECK(id.per_request[2].restore_s == 0);
+  CHECK(hc.agg.storage_bytes_per_token == double(L * d * 2));
+  for (void* p : bufs) cudaFree(p);
+}
+
 int main(int argc, char** argv) {
   const bool gpu = argc > 1 && std::string(argv[1]) == "gpu";
   planner_tests();
@@ -292,6 +350,7 @@ int main(int argc, char** argv) {
       return 2;
     }
     gpu_tests();
+    serve_tests();
   }
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
