@@ -21,6 +21,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -390,6 +391,431 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   }
 }
 
+// ============================================================================
+// Two-Q-tile kernel (default): one CTA per (256 queries, head). The two
+// 128-row Q tiles A and B share every K/V tile the TMA warp streams in, and
+// take turns on the tensor core: while the softmax warps of A turn S_A(j)
+// into P_A(j), the tensor core runs P_B(j-1) V and Q_B K(j)^T, and vice versa.
+//   TMEM (512 columns): S_A [0,128), S_B [128,256), O_A [256,256+DH),
+//   O_B [384,384+DH). P_t(j) (bf16, two keys per 32-bit column) overwrites
+//   the first 64 columns of S_t and is the A operand of O_t += P_t V straight
+//   from TMEM -- no smem round trip. QK_t(j+1) is issued after PV_t(j); the
+//   tensor pipe executes MMAs in issue order, so it never overwrites P_t(j)
+//   before PV_t(j) has read it.
+//   warp 0      TMA (Q_A, Q_B once; K(j), V(j-1) into two 2-stage rings)
+//   warp 1      TMEM owner + MMA issuer
+//   warps 2-9   softmax, two threads per query row (64 keys each, row max
+//               exchanged through smem), tile A then tile B every key step
+// Part of the exponentials run as a Cody-Waite + degree-3 polynomial on the
+// FMA pipe (rel. error 7.5e-5, far below bf16 P's 3.9e-3), the rest on MUFU:
+// with only MUFU the 16 ex2/clk/SM take exactly as long as the MMAs. The
+// softmax arithmetic is packed fp32x2 (FFMA2/FADD2) to halve its issue slots.
+// ============================================================================
+constexpr int kFaM = 128;       // rows per Q tile (two per CTA)
+constexpr int kFaThreads = 320;  // TMA, MMA, 8 softmax warps (two threads per query row)
+#ifndef HC_FA_EMU
+#define HC_FA_EMU 3
+#endif
+constexpr int kFaEmuPairs = HC_FA_EMU;  // of every 8 exponential pairs, this many on the FMA pipe
+
+template <int DH>
+struct FaCfg {
+  static constexpr uint32_t kQBytes = kFaM * DH * 2;        // one Q tile
+  static constexpr uint32_t kKVBytes = kAttnN * DH * 2;     // one K or V tile
+  static constexpr uint32_t kHalf = kFaM * 64 * 2;          // one 64-column block
+  // + barriers (256 B) + row max exchange [2 parity][2 tiles][2 halves][128] + row sums [2][2][128]
+  static constexpr size_t kSmem = 2 * size_t(kQBytes) + 4 * size_t(kKVBytes) + 256 + 8 * kFaM * 4 + 4 * kFaM * 4;
+};
+
+// packed fp32x2 arithmetic (FFMA2 / FADD2: two lanes per instruction)
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  return uint64_t(__float_as_uint(lo)) | (uint64_t(__float_as_uint(hi)) << 32);
+}
+__device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float(uint32_t(v)); }
+__device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float(uint32_t(v >> 32)); }
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for a pair, on the FMA pipe: Cody-Waite split x = j + f (j = round(x),
+// f in [-0.5, 0.5]) with the 1.5*2^23 trick, degree-3 minimax polynomial for
+// 2^f (max rel. error 7.5e-5), j added to the exponent field with one IMAD
+// (bits(t) << 23 == j << 23 mod 2^32). x is clamped at -126 so the result
+// stays a (possibly subnormal) positive float.
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
+  x = f2_pack(fmaxf(f2_lo(x), -126.0f), fmaxf(f2_hi(x), -126.0f));
+  const uint64_t magic = f2_pack(12582912.0f, 12582912.0f);
+  const uint64_t t = f2_add(x, magic);
+  const uint64_t f = f2_sub(x, f2_sub(t, magic));
+  uint64_t p = f2_fma(f2_pack(0.055170297622680664f, 0.055170297622680664f), f,
+                      f2_pack(0.24260802567005157f, 0.24260802567005157f));
+  p = f2_fma(p, f, f2_pack(0.693260908126831f, 0.693260908126831f));
+  p = f2_fma(p, f, f2_pack(0.9999282956123352f, 0.9999282956123352f));
+  uint32_t t_lo, t_hi, p_lo, p_hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(t_lo), "=r"(t_hi) : "l"(t));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(p_lo), "=r"(p_hi) : "l"(p));
+  asm("mad.lo.u32 %0, %0, 8388608, %1;" : "+r"(t_lo) : "r"(p_lo));  // one IMAD per lane
+  asm("mad.lo.u32 %0, %0, 8388608, %1;" : "+r"(t_hi) : "r"(p_hi));
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(t_lo), "r"(t_hi));
+  return r;
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem], kind::f16 (A K-major in TMEM: lane = row,
+// two 16-bit elements per 32-bit column).
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+#ifdef HC_FA_TRACE
+// per-event SM clocks of one CTA (blockIdx 0,0): [event][tile][j]
+__device__ unsigned long long g_fa_trace[10][2][64];
+#define FA_TRACE(ev, t, j)                                                                     \
+  do {                                                                                         \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) g_fa_trace[ev][t][j] = clock64();     \
+  } while (0)
+#else
+#define FA_TRACE(ev, t, j) \
+  do {                     \
+  } while (0)
+#endif
+
+template <int DH>
+__global__ void __launch_bounds__(kFaThreads, 1)
+    attn_fa_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK2,
+                   const __grid_constant__ CUtensorMap tmV2, AttnArgs a) {
+  using Cfg = FaCfg<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if (smem_u32(smem_raw) & 1023) asm volatile("trap;");
+  uint8_t* sQ = smem_raw;                       // Q_A, Q_B
+  uint8_t* sK = sQ + 2 * Cfg::kQBytes;          // K ring, 2 stages
+  uint8_t* sV = sK + 2 * Cfg::kKVBytes;         // V ring, 2 stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * Cfg::kKVBytes);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;      // [2]
+  uint64_t* k_empty = bars + 3;     // [2]
+  uint64_t* v_full = bars + 5;      // [2]
+  uint64_t* v_empty = bars + 7;     // [2]
+  uint64_t* s_full = bars + 9;      // [tile]
+  uint64_t* p_full = bars + 11;     // [tile]
+  uint64_t* o_done = bars + 13;     // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  float* xmax = reinterpret_cast<float*>(bars + 32);  // [j parity][tile][half][row]
+  float* xsum = xmax + 8 * kFaM;                      // [tile][half][row]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pt = int(gridDim.x) - 1 - int(blockIdx.x);  // heaviest causal tile pairs first
+  const int h = blockIdx.y, hk = h / a.group;
+  const int q0 = pt * 2 * kFaM;
+  const int kv_tiles = (a.n + kAttnN - 1) / kAttnN;
+  const int nt_a = min(2 * pt + 1, kv_tiles);
+  const int nt_b = min(2 * pt + 2, kv_tiles);  // == nt_a when tile B is past n
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmK2);
+    tma_prefetch_desc(&tmV2);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 8);
+      mbar_init(&o_done[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * Cfg::kQBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int hb = 0; hb < DH / 64; ++hb)
+          tma_load_2d(sQ + t * Cfg::kQBytes + hb * Cfg::kHalf, &tmQ, q_full, h * DH + hb * 64,
+                      q0 + t * kFaM);
+      auto load_tile = [&](int j, bool is_v) {
+        const int st = j & 1;
+        uint64_t* full = is_v ? &v_full[st] : &k_full[st];
+        mbar_wait(is_v ? &v_empty[st] : &k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(full, Cfg::kKVBytes);
+        uint8_t* dst = (is_v ? sV : sK) + st * Cfg::kKVBytes;
+        const CUtensorMap* map = is_v ? &tmV : &tmK;
+        if (a.page_table && a.box_rows < kAttnN) {
+          const int last = (a.n - 1) / a.page_size;
+          const int pg0 = min(j * kAttnN / a.page_size, last);
+          const int per = kAttnN / a.page_size;
+          const int base = __ldg(a.page_table + pg0);
+          bool contig = pg0 + per - 1 <= last;
+          for (int c = 1; c < per && contig; ++c) contig = __ldg(a.page_table + pg0 + c) == base + c;
+          if (contig) {
+            const CUtensorMap* map2 = is_v ? &tmV2 : &tmK2;
+            for (int hb = 0; hb < DH / 64; ++hb)
+              tma_load_2d(dst + hb * Cfg::kHalf, map2, full, hk * DH + hb * 64, base * a.page_size);
+            return;
+          }
+        }
+        for (int c = 0; c < kAttnN / a.box_rows; ++c) {
+          const int key0 = j * kAttnN + c * a.box_rows;
+          int row = key0;
+          if (a.page_table) {
+            const int last = (a.n - 1) / a.page_size;
+            const int pg = min(key0 / a.page_size, last);
+            row = __ldg(a.page_table + pg) * a.page_size + key0 % a.page_size;
+          }
+          for (int hb = 0; hb < DH / 64; ++hb)
+            tma_load_2d(dst + hb * Cfg::kHalf + c * a.box_rows * 128, map, full,
+                        hk * DH + hb * 64, row);
+        }
+      };
+      for (int j = 0; j <= nt_b; ++j) {
+        if (j < nt_b) load_tile(j, false);
+        if (j >= 1) load_tile(j - 1, true);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA
+    // warp-uniform loop; one elected lane issues (see elect_one)
+    const uint32_t id_qk = umma_idesc_f16(kFaM, kAttnN, true);
+    const uint32_t id_pv = umma_idesc_f16(kFaM, DH, true) | (1u << 16);  // B (V) MN-major
+    const uint64_t dq = umma_desc_sw128(smem_u32(sQ));
+    const uint64_t dk = umma_desc_sw128(smem_u32(sK));
+    const uint64_t dv = umma_desc_sw128_mn(smem_u32(sV), Cfg::kHalf);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    auto issue_qk = [&](int t, int j) {
+      const int st = j & 1;
+      FA_TRACE(4, t, j);
+      mbar_wait(&k_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      FA_TRACE(0, t, j);
+      if (elect_one()) {
+        const uint64_t q = dq + uint64_t(t * (Cfg::kQBytes >> 4));
+        const uint64_t k = dk + uint64_t(st * (Cfg::kKVBytes >> 4));
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint64_t off = uint64_t(((kk >> 2) * Cfg::kHalf + (kk & 3) * 32) >> 4);
+          umma_f16(tmem + uint32_t(t * 128), q + off, k + off, id_qk, kk != 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[t]);
+        if (t == 1) umma_commit(&k_empty[st]);  // tile B is the last reader of K(j)
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j) {
+      const int st = j & 1;
+      FA_TRACE(5, t, j);
+      mbar_wait(&p_full[t], j & 1);
+      mbar_wait(&v_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      FA_TRACE(1, t, j);
+      if (elect_one()) {
+        const uint64_t v = dv + uint64_t(st * (Cfg::kKVBytes >> 4));
+#pragma unroll
+        for (int kk = 0; kk < kAttnN / 16; ++kk)
+          umma_f16_ts(tmem + 256 + uint32_t(t * 128), tmem + uint32_t(t * 128 + kk * 8),
+                      v + uint64_t(kk * (2048 >> 4)), id_pv, (j | kk) != 0 ? 1u : 0u);
+        umma_commit(&o_done[t]);
+        if (t == 1) umma_commit(&v_empty[st]);
+      }
+      __syncwarp();
+    };
+    issue_qk(0, 0);
+    issue_qk(1, 0);
+    for (int j = 0; j < nt_b; ++j) {
+      if (j < nt_a) {
+        issue_pv(0, j);
+        if (j + 1 < nt_a) issue_qk(0, j + 1);
+      }
+      issue_pv(1, j);
+      if (j + 1 < nt_b) issue_qk(1, j + 1);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    // warps w and w+4 share a TMEM lane quadrant (32 query rows); `half`
+    // selects 64 of the 128 keys of a tile (and DH/2 of the O columns). Each
+    // step handles tile A then tile B (tile B's S is computed while A's
+    // softmax runs, and vice versa for the tensor core).
+    const int qd = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int rloc = qd * 32 + lane;
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const uint32_t bar_id = 1 + uint32_t(qd);  // named barrier of the quadrant's two warps
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    const uint64_t sc2 = f2_pack(a.scale_log2, a.scale_log2);
+    for (int j = 0; j < nt_b; ++j) {
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t) {
+        if (t == 0 && j >= nt_a) continue;
+        const int row = q0 + t * kFaM + rloc;
+        const int row_lim = min(row, a.n - 1);  // last visible key of this row
+        const uint32_t t_s = tmem + lane_off + uint32_t(t * 128);
+        const uint32_t t_o = tmem + lane_off + 256u + uint32_t(t * 128);
+        mbar_wait(&s_full[t], j & 1);
+        tc_fence_after();
+        if (rloc == 0 && half == 0) FA_TRACE(2, t, j);
+        uint32_t sv[64];
+        tmem_ld_32x32b_x32(t_s + uint32_t(half * 64), *reinterpret_cast<uint32_t(*)[32]>(sv));
+        tmem_ld_32x32b_x32(t_s + uint32_t(half * 64 + 32), *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+        tmem_wait_ld();
+        if (rloc == 0 && half == 0) FA_TRACE(6, t, j);
+        const int key0 = j * kAttnN + half * 64;
+        if (__any_sync(0xffffffffu, key0 + 63 > row_lim)) {  // diagonal / tail tile
+          const int lim = row_lim - key0;
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i > lim) sv[i] = __float_as_uint(-INFINITY);
+        }
+        float m8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m8[u] = fmaxf(__uint_as_float(sv[u]), __uint_as_float(sv[u + 8]));
+#pragma unroll
+        for (int i = 16; i < 64; i += 16)
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            m8[u] = fmaxf(m8[u], fmaxf(__uint_as_float(sv[i + u]), __uint_as_float(sv[i + 8 + u])));
+        float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                         fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        // row max across the two halves; after this barrier both threads have
+        // their S in registers, so P may overwrite any S column
+        float* xm = xmax + ((j & 1) * 4 + t * 2) * kFaM;
+        xm[half * kFaM + rloc] = mx;
+        pair_sync();
+        mx = fmaxf(mx, xm[(half ^ 1) * kFaM + rloc]) * a.scale_log2;
+        // lazy max: keep m_run unless the tile max exceeds it by > 8 (P <= 2^8)
+        const bool resc = mx > m_run[t] + 8.0f;
+        const float m_use = resc ? mx : m_run[t];
+        if (rloc == 0 && half == 0) FA_TRACE(7, t, j);
+        const uint64_t nm2 = f2_pack(-m_use, -m_use);
+        uint64_t sum2 = 0, sum2b = 0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int e = c * 32 + 2 * i;
+            const uint64_t x = f2_fma(uint64_t(sv[e]) | (uint64_t(sv[e + 1]) << 32), sc2, nm2);
+            uint64_t pv;
+            if ((i & 7) < kFaEmuPairs) {
+              pv = ex2_poly2(x);
+            } else {
+              pv = f2_pack(ex2_approx(f2_lo(x)), ex2_approx(f2_hi(x)));
+            }
+            if (i & 1) sum2b = f2_add(sum2b, pv);
+            else sum2 = f2_add(sum2, pv);
+            pk[i] = pack_bf16x2(f2_lo(pv), f2_hi(pv));
+          }
+          // keys half*64 + c*32 .. +31 -> P columns half*32 + c*16 .. +15
+          tmem_st_32x32b_x16(t_s + uint32_t(half * 32 + c * 16), pk);
+        }
+        sum2 = f2_add(sum2, sum2b);
+        if (rloc == 0 && half == 0) FA_TRACE(8, t, j);
+        // O_t rescale (rare with the lazy max): O_t must not be touched while
+        // PV_t(j-1) runs; PV_t(j) waits for p_full below
+        if (__any_sync(0xffffffffu, resc)) {
+          const float corr = resc ? ex2_approx(m_run[t] - m_use) : 1.0f;
+          l_run[t] *= corr;
+          if (j > 0) {
+            mbar_wait(&o_done[t], (j - 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < DH / 64; ++c) {
+              uint32_t v[32];
+              const uint32_t ta = t_o + uint32_t(half * (DH / 2) + c * 32);
+              tmem_ld_32x32b_x32(ta, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+              tmem_st_32x32b_x32(ta, v);
+            }
+          }
+          m_run[t] = m_use;
+        }
+        l_run[t] += f2_lo(sum2) + f2_hi(sum2);
+        tmem_wait_st();
+        if (rloc == 0 && half == 0) FA_TRACE(9, t, j);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+        if (rloc == 0 && half == 0) FA_TRACE(3, t, j);
+      }
+    }
+#pragma unroll 1
+    for (int t = 0; t < 2; ++t) {
+      const int nt = t == 0 ? nt_a : nt_b;
+      const int row = q0 + t * kFaM + rloc;
+      const uint32_t t_o = tmem + lane_off + 256u + uint32_t(t * 128);
+      xsum[(t * 2 + half) * kFaM + rloc] = l_run[t];
+      mbar_wait(&o_done[t], (nt - 1) & 1);
+      tc_fence_after();
+      pair_sync();
+      const float inv = 1.0f / (l_run[t] + xsum[(t * 2 + (half ^ 1)) * kFaM + rloc]);
+      __nv_bfloat16* dst = a.out + size_t(row) * size_t(a.n_heads * DH) + size_t(h) * DH;
+#pragma unroll 1
+      for (int c = 0; c < DH / 64; ++c) {
+        const int col = half * (DH / 2) + c * 32;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_o + uint32_t(col), v);
+        tmem_wait_ld();
+        if (row < a.n) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            d4[i] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * i + 0]) * inv, __uint_as_float(v[8 * i + 1]) * inv),
+                               pack_bf16x2(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv),
+                               pack_bf16x2(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv),
+                               pack_bf16x2(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 template <int DH>
 cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, const KvOut& kv,
                            int64_t kv_rows, void* out, cudaStream_t stream) {
@@ -416,6 +842,11 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
   a.page_table = kv.page_table;
   a.out = static_cast<__nv_bfloat16*>(out);
   a.scale_log2 = (1.0f / sqrtf(float(DH))) * 1.4426950408889634f;
+  // HC_ATTN_TC=1: the one-Q-tile kernel (kept for A/B measurements)
+  static const bool two_tile = [] {
+    const char* e = getenv("HC_ATTN_TC");
+    return !e || atoi(e) != 1;
+  }();
   static thread_local int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -423,11 +854,19 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
     cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<DH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(AttnCfg<DH>::kSmem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_fa_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(FaCfg<DH>::kSmem));
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  const dim3 grid((n + kAttnM - 1) / kAttnM, n_heads);
-  attn_tc_kernel<DH><<<grid, kAttnThreads, AttnCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
+  if (two_tile) {
+    const dim3 grid((n + 2 * kFaM - 1) / (2 * kFaM), n_heads);
+    attn_fa_kernel<DH><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
+  } else {
+    const dim3 grid((n + kAttnM - 1) / kAttnM, n_heads);
+    attn_tc_kernel<DH><<<grid, kAttnThreads, AttnCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
+  }
   return cudaGetLastError();
 }
 

@@ -123,6 +123,18 @@ __device__ __forceinline__ void cluster_sync_all() {
                    : "memory");
 }
 
+// One lane of a converged warp (elect.sync). Issuing tcgen05.mma from a
+// warp-uniform loop under elect_one() keeps descriptors and TMEM addresses in
+// uniform registers; issuing from a divergent `lane == 0` branch makes the
+// compiler wrap every MMA in an ELECT loop with R2UR moves (~100 clk each).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---------------------------------------------------------------- tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_slot, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

@@ -8,7 +8,10 @@ import torch
 from paper_2410_05004_b200.capi import check, lib
 
 s = torch.cuda.current_stream().cuda_stream
-for n, heads in ((4096, 32), (16384, 40), (1024, 32)):
+cases = ((4096, 32), (16384, 40), (1024, 32))
+if len(sys.argv) > 1:
+    cases = tuple(c for c in cases if c[0] == int(sys.argv[1]))
+for n, heads in cases:
     dh = 128
     q = torch.randn(n, heads * dh, device="cuda").bfloat16()
     k = torch.randn(n, heads * dh, device="cuda").bfloat16()
