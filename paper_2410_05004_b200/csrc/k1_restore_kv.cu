@@ -385,8 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (single thread) ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (warp-uniform loop, one elected lane issues) --
+    {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -399,20 +399,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint8_t* st = sA + size_t(stage) * stride;
-          const uint64_t adesc = umma_desc_sw128(smem_u32(st));
-          const uint64_t bdesc = umma_desc_sw128(smem_u32(st + a_bytes));
+          if (elect_one()) {
+            const uint8_t* st = sA + size_t(stage) * stride;
+            const uint64_t adesc = umma_desc_sw128(smem_u32(st));
+            const uint64_t bdesc = umma_desc_sw128(smem_u32(st + a_bytes));
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
-            umma_f16(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
-                     ((kb - kb0) | k) != 0 ? 1u : 0u);
-          umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+            for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+              umma_f16(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
+                       ((kb - kb0) | k) != 0 ? 1u : 0u);
+            umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+          }
+          __syncwarp();
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (elect_one()) umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -532,8 +536,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (leader CTA, one thread) ----------------
-    if (leader && lane == 0) {
+    // ---------------- MMA issuer (leader CTA; warp-uniform loop, one elected
+    // lane issues: a divergent lane-0 loop costs ~100 clk of R2UR/ELECT per MMA)
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -545,19 +550,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kPairHalfBytes));
-          const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * kPairHalfBytes));
+          if (elect_one()) {
+            const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kPairHalfBytes));
+            const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * kPairHalfBytes));
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            umma_f16_pair(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
-                          (kb | k) != 0 ? 1u : 0u);
-          umma_commit_pair(&empty[stage], 0x3);  // frees the slot in both CTAs
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_f16_pair(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
+                            (kb | k) != 0 ? 1u : 0u);
+            umma_commit_pair(&empty[stage], 0x3);  // frees the slot in both CTAs
+          }
+          __syncwarp();
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(&tfull[acc], 0x3);
+        if (elect_one()) umma_commit_pair(&tfull[acc], 0x3);
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -604,57 +613,78 @@ __device__ __forceinline__ void load8(const T* p, float (&x)[8]) {
   }
 }
 
-// One pass: sum and sum of squares in double (bf16 inputs have 8-bit
-// mantissas, so the double sums are exact or within 1 ulp of double and
-// var = E[x^2] - mean^2 matches the reference's two-pass double variance,
-// model.cpp:43-61, to far below float resolution). 16-byte loads, four in
-// flight per lane.
+// One pass over the row, shifted by its first element c (robust when
+// |mean| >> sigma): per 16-byte load the 8 values' sum and sum of squares of
+// (x - c) in fp32, accumulated across loads in double; mean = c + S/n,
+// var = Q/n - (S/n)^2 (the reference's two-pass double variance,
+// model.cpp:43-61, to ~1e-7 relative). FP64 only once per 8 elements: the
+// B200 FP64 / F2F.F64 rate made a per-element double accumulation the bound.
+// One warp per row, eight 16-byte loads in flight per lane, blockIdx.y
+// selects the matrix of a batch (every layer of a resident restore in one
+// launch). HBM-bound: 2 bytes per element read once.
+constexpr int kStatsMaxBatch = 128;
+struct StatsBatch {
+  const void* x[kStatsMaxBatch];
+  float* mean[kStatsMaxBatch];
+  float* rstd[kStatsMaxBatch];
+};
+
 template <typename T>
-__global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ x, int64_t rows,
-                                                        int cols, int64_t row_stride,
-                                                        float* __restrict__ mean_out,
-                                                        float* __restrict__ rstd_out) {
-  const int warps = blockDim.x >> 5;
-  const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const T* r = x + row * row_stride;
-  double s = 0.0, q = 0.0;
-  int c = lane * 8;
-  for (; c + 3 * 256 < cols; c += 4 * 256) {
-    float v[4][8];
+__device__ __forceinline__ void row_stats_row(const T* __restrict__ r, int cols, int lane,
+                                              float* mean_out, float* rstd_out) {
+  constexpr int U = 8;
+  const float c0 = __shfl_sync(0xffffffffu, lane == 0 ? float(r[0]) : 0.f, 0);
+  double s[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
+  auto acc8 = [&](const float (&v)[8], int k) {
+    float a = 0.f, b = 0.f;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) load8(r + c + u * 256, v[u]);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        s += double(v[u][i]);
-        q += double(v[u][i]) * double(v[u][i]);
-      }
+    for (int i = 0; i < 8; ++i) {
+      const float x = v[i] - c0;
+      a += x;
+      b = fmaf(x, x, b);
     }
+    s[k] += double(a);
+    q[k] += double(b);
+  };
+  int c = lane * 8;
+#pragma unroll 2
+  for (; c + (U - 1) * 256 < cols; c += U * 256) {
+    float v[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) load8(r + c + u * 256, v[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc8(v[u], u & 1);
   }
   for (; c < cols; c += 256) {
     float v[8];
     load8(r + c, v);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      s += double(v[i]);
-      q += double(v[i]) * double(v[i]);
-    }
+    acc8(v, 0);
   }
+  double ss = s[0] + s[1], qq = q[0] + q[1];
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    q += __shfl_xor_sync(0xffffffffu, q, o);
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    qq += __shfl_xor_sync(0xffffffffu, qq, o);
   }
   if (lane == 0) {
-    const double mean = s / double(cols);
-    double var = q / double(cols) - mean * mean;
+    const double mu = ss / double(cols);  // mean of x - c0
+    double var = qq / double(cols) - mu * mu;
     if (var < 0) var = 0;
-    mean_out[row] = float(mean);
-    rstd_out[row] = 1.0f / sqrtf(float(var) + 1e-5f);
+    *mean_out = float(double(c0) + mu);
+    *rstd_out = 1.0f / sqrtf(float(var) + 1e-5f);
   }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) row_stats_kernel(const __grid_constant__ StatsBatch b,
+                                                        int64_t rows, int cols,
+                                                        int64_t row_stride) {
+  const int warps = blockDim.x >> 5;
+  const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int m = blockIdx.y;
+  row_stats_row(static_cast<const T*>(b.x[m]) + row * row_stride, cols, threadIdx.x & 31,
+                b.mean[m] + row, b.rstd[m] + row);
 }
 
 template <typename T>
@@ -936,18 +966,31 @@ cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, in
                                 split_acc);
 }
 
+cudaError_t launch_row_stats_batch(const void* const* x, int n_mats, int64_t rows, int cols,
+                                   int64_t row_stride, bool bf16_in, float* const* mean,
+                                   float* const* rstd, cudaStream_t stream) {
+  if (rows <= 0 || n_mats <= 0) return cudaSuccess;
+  const int threads = 256, per_block = threads / 32;
+  for (int m0 = 0; m0 < n_mats; m0 += kStatsMaxBatch) {
+    const int nb = std::min(kStatsMaxBatch, n_mats - m0);
+    StatsBatch b;
+    for (int i = 0; i < nb; ++i) {
+      b.x[i] = x[m0 + i];
+      b.mean[i] = mean[m0 + i];
+      b.rstd[i] = rstd[m0 + i];
+    }
+    const dim3 grid(unsigned((rows + per_block - 1) / per_block), unsigned(nb));
+    if (bf16_in)
+      row_stats_kernel<__nv_bfloat16><<<grid, threads, 0, stream>>>(b, rows, cols, row_stride);
+    else
+      row_stats_kernel<__half><<<grid, threads, 0, stream>>>(b, rows, cols, row_stride);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,
                              bool bf16_in, float* mean, float* rstd, cudaStream_t stream) {
-  if (rows <= 0) return cudaSuccess;
-  const int threads = 256, per_block = threads / 32;
-  const unsigned grid = unsigned((rows + per_block - 1) / per_block);
-  if (bf16_in)
-    row_stats_kernel<__nv_bfloat16><<<grid, threads, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(x), rows, cols, row_stride, mean, rstd);
-  else
-    row_stats_kernel<__half><<<grid, threads, 0, stream>>>(static_cast<const __half*>(x), rows,
-                                                          cols, row_stride, mean, rstd);
-  return cudaGetLastError();
+  return launch_row_stats_batch(&x, 1, rows, cols, row_stride, bf16_in, &mean, &rstd, stream);
 }
 
 cudaError_t launch_colsum(const void* w, int64_t rows, int cols, bool bf16_in, float* out,

@@ -169,6 +169,10 @@ cudaError_t launch_convert_to_bf16(const void* src, int src_dtype, void* dst, in
 
 // Row statistics for the LayerNorm fold: mean and 1/sqrt(var+1e-5) per row,
 // mean/var accumulated in double like the reference (model.cpp:43-61).
+// Row statistics of n_mats matrices of identical shape in one launch.
+cudaError_t launch_row_stats_batch(const void* const* x, int n_mats, int64_t rows, int cols,
+                                   int64_t row_stride, bool bf16_in, float* const* mean,
+                                   float* const* rstd, cudaStream_t stream);
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,
                              bool bf16_in, float* mean, float* rstd, cudaStream_t stream);
 

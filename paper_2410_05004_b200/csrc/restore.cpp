@@ -49,6 +49,7 @@ int copy_streams() {
 struct Engine {
   cudaStream_t copy = nullptr;  // IO lane head: orders fetches, joins the helpers
   cudaStream_t helper[kCopyStreams - 1] = {};
+  cudaStream_t aux = nullptr;   // row statistics running ahead of the compute lane
   bool init = false;
 };
 
@@ -60,6 +61,7 @@ Engine& engine(int dev) {
   if (!e.init) {
     HC_CUDA(cudaStreamCreateWithFlags(&e.copy, cudaStreamNonBlocking));
     for (auto& h : e.helper) HC_CUDA(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking));
+    HC_CUDA(cudaStreamCreateWithFlags(&e.aux, cudaStreamNonBlocking));
     cudaMemPool_t pool;
     HC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thresh = UINT64_MAX;
@@ -622,20 +624,33 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
     DeviceGuard dg(w->device);
     cudaStream_t s = as_stream(stream);
     const int L = w->cfg.n_layers, d = w->cfg.d_hidden;
-    // every layer's rows are resident: all row statistics first (one buffer),
-    // then the K1 launches back to back
+    // every layer's rows are resident: the row statistics of layer l+1 run on
+    // a side stream while K1 projects layer l (K1 is tensor-bound and leaves
+    // HBM bandwidth and SM thread slots for the stats kernel)
     const bool norm = w->cfg.norm_enabled != 0;
     StreamScratch stats(norm ? size_t(L) * size_t(n_rows) * 2 * sizeof(float) : 0, s);
     float* st = static_cast<float*>(stats.ptr);
-    if (norm)
-      for (int l = 0; l < L; ++l)
-        HC_CUDA(launch_row_stats(d_hidden_layers[l], n_rows, d, d, true,
-                                 st + size_t(l) * 2 * size_t(n_rows),
-                                 st + size_t(l) * 2 * size_t(n_rows) + n_rows, s));
-    for (int l = 0; l < L; ++l)
+    EventPool evs(false);
+    std::vector<cudaEvent_t> ready;
+    if (norm) {
+      Engine& eng = engine(w->device);
+      cudaEvent_t start = evs.get();
+      HC_CUDA(cudaEventRecord(start, s));
+      HC_CUDA(cudaStreamWaitEvent(eng.aux, start, 0));
+      for (int l = 0; l < L; ++l) {
+        float* mean = st + size_t(l) * 2 * size_t(n_rows);
+        HC_CUDA(launch_row_stats(d_hidden_layers[l], n_rows, d, d, true, mean, mean + n_rows,
+                                 eng.aux));
+        ready.push_back(evs.get());
+        HC_CUDA(cudaEventRecord(ready.back(), eng.aux));
+      }
+    }
+    for (int l = 0; l < L; ++l) {
+      if (norm) HC_CUDA(cudaStreamWaitEvent(s, ready[size_t(l)], 0));
       project_rows(w, l, d_hidden_layers[l], n_rows,
                    kv_out_pages(pages, l, d_page_table, table_stride, d_cu_seqlens, n_seqs), s,
                    norm ? st + size_t(l) * 2 * size_t(n_rows) : nullptr);
+    }
   });
 }
 
