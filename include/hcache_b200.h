@@ -370,10 +370,13 @@ typedef struct hc_restore_opts {
 hc_status hc_restore(hc_store* s, const char* sid, const hc_weights* w, const hc_plan* plan,
                      const hc_restore_opts* opts, const hc_kv_pages* pages,
                      const int32_t* d_page_table, void* stream, hc_timeline* timeline);
-/* Several finalized sessions restored concurrently (config 4): per layer all
- * sessions' chunks land in one concatenated staging buffer and one grouped K1
- * launch projects them (per-row sequence/position/page indirection). Every
- * session's plan must be all-HIDDEN. d_page_tables: n_sessions x table_stride. */
+/* Several finalized sessions restored concurrently (config 4). The sessions
+ * must share one plan (HC_EINVAL otherwise); it is executed like hc_restore's:
+ * the RECOMPUTE prefix as one ragged forward over all sessions (each from
+ * position 0, token ids from the manifests), per HIDDEN layer all sessions'
+ * chunks land in one concatenated staging buffer and one grouped K1 launch
+ * projects them (per-row sequence/position/page indirection), per KV layer
+ * one K4 scatter. bf16 sessions only. d_page_tables: n_sessions x table_stride. */
 hc_status hc_restore_batch(hc_store* s, const char* const* sids, int32_t n_sessions,
                            const hc_weights* w, const hc_restore_opts* opts,
                            const hc_kv_pages* pages, const int32_t* d_page_tables,

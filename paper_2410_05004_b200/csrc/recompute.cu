@@ -265,6 +265,23 @@ void forward_batch_dev(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
                [](int, bool) {}, d_layer_inputs, nullptr, sb, d_next_tokens);
 }
 
+void forward_batch_layers(const hc_weights* w, const int32_t* d_tokens, int n_seqs, int64_t total,
+                          int max_new, const int32_t* d_cu, const int32_t* d_starts,
+                          const hc_kv_pages* pages, const int32_t* d_page_tables,
+                          int table_stride, int lb, int le, cudaStream_t stream,
+                          const std::function<void(int, bool)>& hook) {
+  if (!w || n_seqs < 1 || total < 1 || max_new < 1 || !d_cu || !d_starts)
+    fail(HC_EINVAL, "forward_batch: bad argument");
+  SeqBatch sb;
+  sb.n_seqs = n_seqs;
+  sb.cu = d_cu;
+  sb.seq_start = d_starts;
+  sb.max_new = max_new;
+  sb.table_stride = table_stride;
+  forward_impl(w, d_tokens, total, lb, le, pages, d_page_tables, stream, hook, nullptr, nullptr,
+               sb, nullptr);
+}
+
 void forward_batch(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
                    const int32_t* new_lens, const int32_t* start_pos, const hc_kv_pages* pages,
                    const int32_t* d_page_tables, int table_stride, void* d_layer_inputs,

@@ -45,6 +45,14 @@ void forward_batch_dev(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
                        const hc_kv_pages* pages, const int32_t* d_page_tables, int table_stride,
                        void* d_layer_inputs, int32_t* d_next_tokens, cudaStream_t stream);
 
+// Layers [lb, le) of forward_batch_dev (the RECOMPUTE prefix of a batched
+// restore: every sequence from position 0); hook as in prefill_layers_impl.
+void forward_batch_layers(const hc_weights* w, const int32_t* d_tokens, int n_seqs, int64_t total,
+                          int max_new, const int32_t* d_cu, const int32_t* d_starts,
+                          const hc_kv_pages* pages, const int32_t* d_page_tables,
+                          int table_stride, int lb, int le, cudaStream_t stream,
+                          const std::function<void(int, bool)>& hook);
+
 // Measured seconds of one recompute layer over n tokens at the steady-state
 // clock (after warm_s seconds of back-to-back layers); 0 when the full block
 // weights are not set.

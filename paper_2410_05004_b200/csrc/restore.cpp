@@ -227,20 +227,42 @@ int auto_depth(int n_staged, size_t buf_bytes, int requested) {
 }  // namespace
 
 // --------------------------------------------------------------- restore
-void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const hc_plan* plan,
-                     const hc_restore_opts* opts, const hc_kv_pages* pages,
-                     const int32_t* d_page_table, cudaStream_t stream, hc_timeline* tl) {
-  if (!st || !sid_c || !w || !plan || !pages || !d_page_table)
-    fail(HC_EINVAL, "restore: null argument");
+// One restore of a group of sessions sharing a plan: n_sessions == 1 is the
+// reference's restore (restore.cpp:133-235); more sessions are restored
+// concurrently (config 4) -- their rows are concatenated, each layer is one
+// fetch of every session's chunk runs, one K1 / K4 launch with per-row
+// (session, position, page) indirection, and the RECOMPUTE prefix one
+// ragged forward over all sessions.
+void restore_group(hc_store* st, const char* const* sids, int n_sessions, const hc_weights* w,
+                   const hc_plan* plan_arg, const hc_restore_opts* opts,
+                   const hc_kv_pages* pages, const int32_t* d_page_tables, int table_stride,
+                   cudaStream_t stream, hc_timeline* tl) {
+  const char* who = n_sessions > 1 ? "restore_batch" : "restore";
+  auto bad = [&](const std::string& msg) { fail(HC_EINVAL, std::string(who) + ": " + msg); };
+  if (!st || !sids || n_sessions < 1 || !w || !pages || !d_page_tables) bad("null argument");
   Store& store = st->impl;
-  const std::string sid(sid_c);
-  const hc_manifest m = store.open(sid);  // HC_ENOENT / HC_EINCOMPLETE
-  // restore.cpp:228-231
-  if (m.n_layers != w->cfg.n_layers || plan->n_layers != w->cfg.n_layers)
-    fail(HC_EINVAL, "restore: layer count mismatch");
-  if (plan_serialize(plan) != plan_serialize(&m.plan))
-    fail(HC_EINVAL, "restore: plan does not match session manifest");
-  if (m.d_hidden != w->cfg.d_hidden) fail(HC_EINVAL, "restore: d_hidden mismatch");
+  const bool batch = n_sessions > 1;
+  std::vector<hc_manifest> ms;
+  std::vector<int32_t> cu(size_t(n_sessions) + 1, 0);
+  for (int i = 0; i < n_sessions; ++i) {
+    if (!sids[i]) bad("null session id");
+    ms.push_back(store.open(sids[i]));  // HC_ENOENT / HC_EINCOMPLETE
+    const hc_manifest& m = ms.back();
+    // restore.cpp:228-231
+    if (m.n_layers != w->cfg.n_layers) bad("layer count mismatch");
+    if (m.d_hidden != w->cfg.d_hidden) bad("d_hidden mismatch");
+    if (m.n_tokens <= 0) bad("empty session");
+    if (plan_serialize(&m.plan) != plan_serialize(plan_arg ? plan_arg : &ms[0].plan))
+      bad(plan_arg ? "plan does not match session manifest"
+                   : "sessions of one batch must share a plan");
+    if (batch && (m.elem_bytes != 2 || m.dtype != HC_DTYPE_BF16)) bad("bf16 sessions required");
+    if (batch && int64_t(m.n_tokens) > int64_t(table_stride) * pages->page_size)
+      bad("page table too short");
+    cu[size_t(i) + 1] = cu[size_t(i)] + m.n_tokens;
+  }
+  const hc_manifest& m = ms[0];
+  const hc_plan& plan = m.plan;
+  if (plan.n_layers != w->cfg.n_layers) bad("layer count mismatch");
   // persisted element type: bf16 (native), or the reference's own formats
   // -- fp32 (ModelConfig::elem_bytes = 4, its default) and the fp16 codec --
   // which arrive as stored over PCIe and are rounded to bf16 on the device
@@ -248,12 +270,13 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
   const int eb = m.elem_bytes;
   const bool native = m.dtype == HC_DTYPE_BF16 && eb == 2;
   if (!native && !(m.dtype == HC_DTYPE_F32 && eb == 4) && !(m.dtype == HC_DTYPE_F16 && eb == 2))
-    fail(HC_EINVAL, "restore: unsupported session element type");
+    bad("unsupported session element type");
   validate_pages(w, pages, w->d_kv);
-  const int n = m.n_tokens;
-  if (n <= 0) fail(HC_EINVAL, "restore: empty session");
-  if (int64_t(n) > int64_t(pages->num_pages) * pages->page_size)
-    fail(HC_EINVAL, "restore: KV pages too small for the session");
+  const int64_t n = cu.back();
+  if (!batch && n > int64_t(pages->num_pages) * pages->page_size)
+    bad("KV pages too small for the session");
+  int max_len = 0;
+  for (const auto& mm : ms) max_len = std::max(max_len, mm.n_tokens);
 
   DeviceGuard dg(w->device);
   Engine& eng = engine(w->device);
@@ -261,7 +284,7 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
   EventPool evp(timed);
   std::vector<TimedOp> ops;
 
-  auto order = compute_order(*plan);
+  auto order = compute_order(plan);
   int n_hidden = 0, n_kv = 0, n_re = 0;
   for (auto& j : order) {
     if (j.method == HC_METHOD_HIDDEN) ++n_hidden;
@@ -269,10 +292,11 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
     else ++n_re;
   }
   if (n_kv && (m.d_kv != w->d_kv || w->d_kv != w->d_kv_all))
-    fail(HC_EINVAL, "restore: KV-offload layers need all KV heads on this GPU");
+    fail(HC_EINVAL, std::string(who) + ": KV-offload layers need all KV heads on this GPU");
 
-  const size_t h_bytes = size_t(n) * size_t(m.d_hidden) * size_t(eb);
-  const size_t kv_bytes = size_t(n) * size_t(2 * m.d_kv) * size_t(eb);
+  const size_t h_row = size_t(m.d_hidden) * size_t(eb), kv_row = size_t(2 * m.d_kv) * size_t(eb);
+  const size_t h_bytes = size_t(n) * h_row;
+  const size_t kv_bytes = size_t(n) * kv_row;
   // fp32 sessions: the bf16 copy K1 / K4 read (fp16 converts in place)
   const size_t conv_bytes =
       m.dtype == HC_DTYPE_F32
@@ -286,15 +310,31 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
   // staging rings (stream-ordered pool allocations, cached by the pool)
   StreamScratch ring_h(n_hidden ? h_bytes * size_t(nbuf_h) : 0, stream);
   StreamScratch ring_kv(n_kv ? kv_bytes * size_t(nbuf_kv) : 0, stream);
+  // batch: row offsets and (zero) first positions of the sessions
+  StreamScratch d_meta(batch ? sizeof(int32_t) * (cu.size() + size_t(n_sessions)) : 0, stream);
+  const int32_t* d_cu = nullptr;
+  const int32_t* d_starts = nullptr;
+  if (batch) {
+    std::vector<int32_t> meta(cu);
+    meta.resize(cu.size() + size_t(n_sessions), 0);
+    HC_CUDA(cudaMemcpyAsync(d_meta.ptr, meta.data(), sizeof(int32_t) * meta.size(),
+                            cudaMemcpyHostToDevice, stream));
+    d_cu = static_cast<const int32_t*>(d_meta.ptr);
+    d_starts = d_cu + cu.size();
+  }
 
-  // token ids for the RECOMPUTE prefix: async H2D from the store's pinned copy
+  // token ids for the RECOMPUTE prefix: async H2D from the store's pinned copies
   StreamScratch d_tok(n_re ? sizeof(int32_t) * size_t(n) : 0, stream);
   if (n_re) {
-    int64_t n_ids = 0;
-    const int32_t* toks = store.pinned_tokens(sid, &n_ids);
-    if (n_ids < n || !toks) fail(HC_EINVAL, "restore: manifest has fewer token ids than tokens");
-    HC_CUDA(cudaMemcpyAsync(d_tok.ptr, toks, sizeof(int32_t) * size_t(n), cudaMemcpyHostToDevice,
-                            stream));
+    for (int i = 0; i < n_sessions; ++i) {
+      int64_t n_ids = 0;
+      const int32_t* toks = store.pinned_tokens(sids[i], &n_ids);
+      if (n_ids < ms[size_t(i)].n_tokens || !toks)
+        bad("manifest has fewer token ids than tokens");
+      HC_CUDA(cudaMemcpyAsync(static_cast<int32_t*>(d_tok.ptr) + cu[size_t(i)], toks,
+                              sizeof(int32_t) * size_t(ms[size_t(i)].n_tokens),
+                              cudaMemcpyHostToDevice, stream));
+    }
   }
 
   cudaEvent_t t0 = evp.get();
@@ -328,11 +368,19 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
     f.reuses_slot = kind_idx >= (f.hid ? nbuf_h : nbuf_kv);
     f.buf = static_cast<uint8_t*>(f.hid ? ring_h.ptr : ring_kv.ptr) +
             (f.hid ? h_bytes : kv_bytes) * size_t(f.slot);
-    size_t got = 0;
-    f.segs = store.gather_plan(sid, j.layer, f.hid ? HC_STATE_HIDDEN : HC_STATE_KV, 0, -1,
-                               &got);  // HC_ENOENT if missing
-    if (got != (f.hid ? h_bytes : kv_bytes))
-      fail(HC_ERUNTIME, "restore: layer " + std::to_string(j.layer) + " has a short token count");
+    for (int i = 0; i < n_sessions; ++i) {
+      size_t got = 0;
+      auto segs = store.gather_plan(sids[i], j.layer, f.hid ? HC_STATE_HIDDEN : HC_STATE_KV, 0, -1,
+                                    &got);  // HC_ENOENT if missing
+      const size_t row = f.hid ? h_row : kv_row;
+      if (got != size_t(ms[size_t(i)].n_tokens) * row)
+        fail(HC_ERUNTIME, std::string(who) + ": layer " + std::to_string(j.layer) +
+                              " has a short token count");
+      for (auto& g : segs) {
+        g.dst_off += int64_t(cu[size_t(i)]) * int64_t(row);
+        f.segs.push_back(g);
+      }
+    }
     fetches.push_back(std::move(f));
   }
   std::vector<cudaEvent_t> consumed_h(size_t(nbuf_h), nullptr), consumed_kv(size_t(nbuf_kv), nullptr);
@@ -368,14 +416,20 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
   // lane prefetches hidden layers meanwhile.
   if (n_re) {
     std::vector<cudaEvent_t> marks;
-    prefill_layers_impl(w, static_cast<const int32_t*>(d_tok.ptr), n, 0, n_re, pages,
-                        d_page_table, stream, [&](int layer, bool start) {
-                          if (!timed) return;
-                          cudaEvent_t e = evp.get();
-                          HC_CUDA(cudaEventRecord(e, stream));
-                          if (start) marks.push_back(e);
-                          else ops.push_back({HC_LANE_COMPUTE, layer, HC_EV_RECOMPUTE, marks.back(), e});
-                        });
+    auto hook = [&](int layer, bool start) {
+      if (!timed) return;
+      cudaEvent_t e = evp.get();
+      HC_CUDA(cudaEventRecord(e, stream));
+      if (start) marks.push_back(e);
+      else ops.push_back({HC_LANE_COMPUTE, layer, HC_EV_RECOMPUTE, marks.back(), e});
+    };
+    if (batch)
+      forward_batch_layers(w, static_cast<const int32_t*>(d_tok.ptr), n_sessions, n, max_len,
+                           d_cu, d_starts, pages, d_page_tables, table_stride, 0, n_re, stream,
+                           hook);
+    else
+      prefill_layers_impl(w, static_cast<const int32_t*>(d_tok.ptr), n, 0, n_re, pages,
+                          d_page_tables, stream, hook);
   }
 
   issue_fetches(fetches.size());
@@ -387,10 +441,12 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
     HC_CUDA(cudaStreamWaitEvent(stream, f.fetched, 0));
     cudaEvent_t cs = timed ? evp.get() : nullptr;
     if (cs) HC_CUDA(cudaEventRecord(cs, stream));
-    KvOut out = kv_out_pages(pages, f.job.layer, d_page_table, 0, nullptr, 1);
+    KvOut out = batch ? kv_out_pages(pages, f.job.layer, d_page_tables, table_stride, d_cu,
+                                     n_sessions)
+                      : kv_out_pages(pages, f.job.layer, d_page_tables, 0, nullptr, 1);
     const void* rows = f.buf;
     if (!native) {
-      const int64_t elems = int64_t(n) * (f.hid ? m.d_hidden : 2 * m.d_kv);
+      const int64_t elems = n * (f.hid ? m.d_hidden : 2 * m.d_kv);
       void* dst = m.dtype == HC_DTYPE_F32 ? conv.ptr : f.buf;
       HC_CUDA(launch_convert_to_bf16(f.buf, m.dtype, dst, elems, stream));
       rows = dst;
@@ -419,87 +475,19 @@ void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const
   }
 }
 
+void restore_session(hc_store* st, const char* sid_c, const hc_weights* w, const hc_plan* plan,
+                     const hc_restore_opts* opts, const hc_kv_pages* pages,
+                     const int32_t* d_page_table, cudaStream_t stream, hc_timeline* tl) {
+  if (!plan) fail(HC_EINVAL, "restore: null argument");
+  restore_group(st, &sid_c, 1, w, plan, opts, pages, d_page_table, 0, stream, tl);
+}
+
 void restore_batch(hc_store* st, const char* const* sids, int n_sessions, const hc_weights* w,
                    const hc_restore_opts* opts, const hc_kv_pages* pages,
                    const int32_t* d_page_tables, int table_stride, cudaStream_t stream,
                    hc_timeline* tl) {
-  if (!st || !sids || n_sessions < 1 || !w || !pages || !d_page_tables)
-    fail(HC_EINVAL, "restore_batch: null argument");
-  Store& store = st->impl;
-  validate_pages(w, pages, w->d_kv);
-  const int L = w->cfg.n_layers, d = w->cfg.d_hidden;
-  std::vector<int32_t> cu(size_t(n_sessions) + 1, 0);
-  for (int s = 0; s < n_sessions; ++s) {
-    const hc_manifest m = store.open(sids[s]);
-    if (m.n_layers != L || m.d_hidden != d) fail(HC_EINVAL, "restore_batch: shape mismatch");
-    if (m.elem_bytes != 2 || m.dtype != HC_DTYPE_BF16)
-      fail(HC_EINVAL, "restore_batch: bf16 sessions required");
-    for (int l = 0; l < L; ++l)
-      if (m.plan.layer_assignment[l] != HC_METHOD_HIDDEN)
-        fail(HC_EINVAL, "restore_batch: every layer must be HIDDEN");
-    if (int64_t(m.n_tokens) > int64_t(table_stride) * pages->page_size)
-      fail(HC_EINVAL, "restore_batch: page table too short");
-    cu[size_t(s) + 1] = cu[size_t(s)] + m.n_tokens;
-  }
-  const int64_t total = cu.back();
-  if (total <= 0) fail(HC_EINVAL, "restore_batch: empty sessions");
-
-  DeviceGuard dg(w->device);
-  Engine& eng = engine(w->device);
-  const bool timed = tl != nullptr || (opts && opts->timeline);
-  EventPool evp(timed);
-  std::vector<TimedOp> ops;
-  const size_t h_bytes = size_t(total) * size_t(d) * 2;
-  const int depth = auto_depth(L, h_bytes, opts ? opts->prefetch_depth : 0);
-  const int nbuf = std::min(L, depth + 1);
-  StreamScratch ring(h_bytes * size_t(nbuf), stream);
-  StreamScratch d_cu(sizeof(int32_t) * cu.size(), stream);
-  HC_CUDA(cudaMemcpyAsync(d_cu.ptr, cu.data(), sizeof(int32_t) * cu.size(),
-                          cudaMemcpyHostToDevice, stream));
-  cudaEvent_t t0 = evp.get();
-  HC_CUDA(cudaEventRecord(t0, stream));
-  HC_CUDA(cudaStreamWaitEvent(eng.copy, t0, 0));
-  std::vector<cudaEvent_t> consumed(size_t(nbuf), nullptr);
-  std::vector<cudaEvent_t> joins;
-  for (int l = 0; l < L; ++l) {
-    const int slot = l % nbuf;
-    uint8_t* buf = static_cast<uint8_t*>(ring.ptr) + h_bytes * size_t(slot);
-    if (consumed[size_t(slot)]) HC_CUDA(cudaStreamWaitEvent(eng.copy, consumed[size_t(slot)], 0));
-    cudaEvent_t fs = timed ? evp.get() : nullptr;
-    if (fs) HC_CUDA(cudaEventRecord(fs, eng.copy));
-    {
-      std::vector<CopySeg> all;
-      for (int s = 0; s < n_sessions; ++s) {
-        auto segs = store.gather_plan(sids[s], l, HC_STATE_HIDDEN, 0, -1, nullptr);
-        for (auto g : segs) {
-          g.dst_off += int64_t(cu[size_t(s)]) * int64_t(d) * 2;
-          all.push_back(g);
-        }
-      }
-      issue_gather(all, buf, eng, joins, &EventPool::make, &evp);
-    }
-    cudaEvent_t fetched = evp.get();
-    HC_CUDA(cudaEventRecord(fetched, eng.copy));
-    if (timed) ops.push_back({HC_LANE_IO, l, HC_EV_FETCH_HIDDEN, fs, fetched});
-    HC_CUDA(cudaStreamWaitEvent(stream, fetched, 0));
-    cudaEvent_t cs = timed ? evp.get() : nullptr;
-    if (cs) HC_CUDA(cudaEventRecord(cs, stream));
-    project_rows(w, l, buf, total,
-                 kv_out_pages(pages, l, d_page_tables, table_stride,
-                              static_cast<const int32_t*>(d_cu.ptr), n_sessions),
-                 stream);
-    cudaEvent_t done = evp.get();
-    HC_CUDA(cudaEventRecord(done, stream));
-    consumed[size_t(slot)] = done;
-    if (timed) ops.push_back({HC_LANE_COMPUTE, l, HC_EV_PROJECT, cs, done});
-  }
-  cudaEvent_t io_done = evp.get();
-  HC_CUDA(cudaEventRecord(io_done, eng.copy));
-  HC_CUDA(cudaStreamWaitEvent(stream, io_done, 0));
-  if (timed) {
-    HC_CUDA(cudaStreamSynchronize(stream));
-    if (tl) fill_timeline(tl, t0, ops);
-  }
+  restore_group(st, sids, n_sessions, w, nullptr, opts, pages, d_page_tables, table_stride,
+                stream, tl);
 }
 
 // restore_token_wise (restore.cpp:237-301), the ablation: at every layer the

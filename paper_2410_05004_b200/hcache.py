@@ -585,8 +585,10 @@ def restore(store: StorageManager, session_id: str, w: Weights, p: RestorationPl
 
 def restore_batch(store: StorageManager, session_ids: Sequence[str], w: Weights,
                   throttle: ThrottleConfig, kv: KvCache, page_tables, stream=None):
-    """Concurrent all-HIDDEN restore of several sessions (config 4).
-    page_tables: (n_sessions x table_stride) int32 CUDA tensor."""
+    """Concurrent restore of several sessions sharing one plan (config 4):
+    RECOMPUTE prefix as one ragged forward, grouped K1 per HIDDEN layer, one
+    K4 scatter per KV layer. page_tables: (n_sessions x table_stride) int32
+    CUDA tensor."""
     ids = (C.c_char_p * len(session_ids))(*[s.encode() for s in session_ids])
     tc = capi.TimelineC() if throttle.timeline else None
     check(lib().hc_restore_batch(store._h, ids, len(session_ids), w._h, C.byref(throttle._c()),

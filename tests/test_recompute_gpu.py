@@ -205,3 +205,72 @@ def test_block_pieces_isolated(cuda, oracle, ablate):
                               vocab_size=vocab), flat, np.array(tokens, np.int32))
     err = norm_err(inputs[1].float().cpu().numpy(), ref["inputs"][1])
     assert err < RECOMPUTE_TOL, (ablate, err)
+
+
+@pytest.mark.parametrize("plan_name", ["1RE+2H+1KV", "2RE+2H", "4H"])
+def test_batch_restore_with_plan_is_lossless_vs_batched_forward(cuda, plan_name):
+    """Config 4 with the scheduler's plan types: several sessions share a plan
+    (RECOMPUTE prefix as one ragged forward, HIDDEN layers as one grouped K1,
+    KV-offload suffix as one K4 scatter). The restored pages equal the pages
+    the batched forward wrote, bit for bit."""
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    lens, page = [300, 1, 77, 530], 64
+    cfg, w = build(CONFIG1, 11)
+    toks = [[(i * 7 + 3 * s + 1) % 1024 for i in range(n)] for s, n in enumerate(lens)]
+    stride = max((n + page - 1) // page for n in lens)
+    tables = torch.randperm(len(lens) * stride, generator=torch.Generator().manual_seed(2)).to(
+        torch.int32).view(len(lens), stride).cuda()
+    kv_ref = H.KvCache(4, len(lens) * stride, page, w.d_kv)
+    total = sum(lens)
+    flat = torch.tensor([t for ts in toks for t in ts], dtype=torch.int32, device="cuda")
+    inputs = torch.empty((4, total, cfg.d_hidden), dtype=torch.bfloat16, device="cuda")
+    H.forward_batch(w, flat, lens, [0] * len(lens), kv_ref, tables, inputs)
+    torch.cuda.synchronize()
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    plan = {"1RE+2H+1KV": H.RestorationPlan.make_mixed(1, 2, 1),
+            "2RE+2H": H.RestorationPlan.make(4, 2, H.Complement.RECOMPUTE),
+            "4H": H.RestorationPlan.make(4, 4, H.Complement.NONE)}[plan_name]
+    store = H.StorageManager(H.DevicePool(3))
+    for s, n in enumerate(lens):
+        sid = f"b{s}"
+        store.create_session(H.SessionSeed(sid, cfg.hash(), 4, cfg.d_hidden, 2, plan, toks[s]))
+        for L, m in enumerate(plan.layer_assignment):
+            if m == H.LayerMethod.HIDDEN:
+                assert store.snapshot(sid, L, H.StateKind.HIDDEN, inputs[L, offs[s]:offs[s + 1]])
+            elif m == H.LayerMethod.KV_OFFLOAD:
+                k, v = kv_ref.gather(L, tables[s], n)
+                assert store.snapshot(sid, L, H.StateKind.KV, torch.cat([k, v], 1).contiguous())
+        store.finalize(sid)
+    kv = H.KvCache(4, len(lens) * stride, page, w.d_kv)
+    res = H.restore_batch(store, [f"b{s}" for s in range(len(lens))], w, H.ThrottleConfig(), kv,
+                          tables)
+    torch.cuda.synchronize()
+    for s, n in enumerate(lens):
+        for L in range(4):
+            k, v = kv.gather(L, tables[s], n)
+            kr, vr = kv_ref.gather(L, tables[s], n)
+            assert torch.equal(k, kr) and torch.equal(v, vr), (plan_name, s, L)
+    kinds = [e.kind for e in res.timeline.events]
+    assert kinds.count("recompute") == sum(m == H.LayerMethod.RECOMPUTE
+                                           for m in plan.layer_assignment)
+    assert kinds.count("scatter") == sum(m == H.LayerMethod.KV_OFFLOAD
+                                         for m in plan.layer_assignment)
+
+
+def test_batch_restore_rejects_mixed_plans(cuda):
+    from paper_2410_05004_b200 import hcache as H
+    cfg, w = build(CONFIG1, 11)
+    store = H.StorageManager(H.DevicePool(1))
+    for sid, plan in (("p0", H.RestorationPlan.make(4, 4, H.Complement.NONE)),
+                      ("p1", H.RestorationPlan.make(4, 3, H.Complement.RECOMPUTE))):
+        store.create_session(H.SessionSeed(sid, cfg.hash(), 4, cfg.d_hidden, 2, plan, [1] * 64))
+        for L, m in enumerate(plan.layer_assignment):
+            if m == H.LayerMethod.HIDDEN:
+                assert store.snapshot(sid, L, H.StateKind.HIDDEN, dev_symmetric(64 * 512, 5, L, 1.0).view(64, 512))
+        store.finalize(sid)
+    import torch
+    kv = H.KvCache(4, 4, 64, w.d_kv)
+    tables = torch.arange(4, dtype=torch.int32, device="cuda").view(2, 2)
+    with pytest.raises(ValueError, match="share a plan"):
+        H.restore_batch(store, ["p0", "p1"], w, H.ThrottleConfig(), kv, tables)
