@@ -80,6 +80,11 @@ struct AttnArgs {
   const int32_t* page_table;  // nullptr: dense rows
   __nv_bfloat16* out;         // [n][n_heads*dh]
   float scale_log2;
+  // ragged batch of sequences, each a prefill from position 0 (two-tile
+  // kernel only): sequence blockIdx.z owns query rows [cu[z], cu[z+1]) and
+  // page-table row z (stride table_stride); nullptr = one sequence of n rows
+  const int32_t* cu = nullptr;
+  int table_stride = 0;
 };
 
 template <int DH>
@@ -533,7 +538,16 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   float* xsum = xmax + 8 * kFaM;                      // [tile][half][row]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pt = int(gridDim.x) - 1 - int(blockIdx.x);  // heaviest causal tile pairs first
+  // ragged batch: this CTA's sequence, its length and its rows / page table
+  int row0 = 0;  // first query row of the sequence in q / out
+  if (a.cu) {
+    row0 = __ldg(a.cu + blockIdx.z);
+    a.n = __ldg(a.cu + blockIdx.z + 1) - row0;
+    if (a.page_table) a.page_table += size_t(blockIdx.z) * size_t(a.table_stride);
+  }
+  const int n_pairs = (a.n + 2 * kFaM - 1) / (2 * kFaM);
+  const int pt = n_pairs - 1 - int(blockIdx.x);  // heaviest causal tile pairs first
+  if (pt < 0) return;  // (ragged batch: a shorter sequence; uniform for the CTA)
   const int h = blockIdx.y, hk = h / a.group;
   const int q0 = pt * 2 * kFaM;
   const int kv_tiles = (a.n + kAttnN - 1) / kAttnN;
@@ -571,7 +585,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       for (int t = 0; t < 2; ++t)
         for (int hb = 0; hb < DH / 64; ++hb)
           tma_load_2d(sQ + t * Cfg::kQBytes + hb * Cfg::kHalf, &tmQ, q_full, h * DH + hb * 64,
-                      q0 + t * kFaM);
+                      row0 + q0 + t * kFaM);
       auto load_tile = [&](int j, bool is_v) {
         const int st = j & 1;
         uint64_t* full = is_v ? &v_full[st] : &k_full[st];
@@ -789,7 +803,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       tc_fence_after();
       pair_sync();
       const float inv = 1.0f / (l_run[t] + xsum[(t * 2 + (half ^ 1)) * kFaM + rloc]);
-      __nv_bfloat16* dst = a.out + size_t(row) * size_t(a.n_heads * DH) + size_t(h) * DH;
+      __nv_bfloat16* dst =
+          a.out + size_t(row0 + row) * size_t(a.n_heads * DH) + size_t(h) * DH;
 #pragma unroll 1
       for (int c = 0; c < DH / 64; ++c) {
         const int col = half * (DH / 2) + c * 32;
@@ -818,7 +833,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
 
 template <int DH>
 cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, const KvOut& kv,
-                           int64_t kv_rows, void* out, cudaStream_t stream) {
+                           int64_t kv_rows, void* out, cudaStream_t stream,
+                           const int32_t* cu = nullptr, int n_seqs = 1, int max_len = 0) {
   const int box_rows = kv.page_table ? (kv.page_size < kAttnN ? kv.page_size : kAttnN) : kAttnN;
   CUtensorMap tq, tk, tv, tk2, tv2;
   const uint64_t ldq = uint64_t(n_heads) * DH;
@@ -842,6 +858,8 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
   a.page_table = kv.page_table;
   a.out = static_cast<__nv_bfloat16*>(out);
   a.scale_log2 = (1.0f / sqrtf(float(DH))) * 1.4426950408889634f;
+  a.cu = cu;
+  a.table_stride = kv.table_stride;
   // HC_ATTN_TC=1: the one-Q-tile kernel (kept for A/B measurements)
   static const bool two_tile = [] {
     const char* e = getenv("HC_ATTN_TC");
@@ -860,7 +878,10 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  if (two_tile) {
+  if (cu) {  // ragged batch: (tile pairs of the longest sequence, heads, sequences)
+    const dim3 grid((max_len + 2 * kFaM - 1) / (2 * kFaM), n_heads, n_seqs);
+    attn_fa_kernel<DH><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
+  } else if (two_tile) {
     const dim3 grid((n + 2 * kFaM - 1) / (2 * kFaM), n_heads);
     attn_fa_kernel<DH><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
   } else {
@@ -880,6 +901,22 @@ cudaError_t launch_attention_tc(const void* q, int n, int n_heads, int n_kv_head
   if (kv.page_table && kv.page_size < 8) return cudaErrorInvalidValue;
   if (dh == 128) return launch_attn_tc<128>(q, n, n_heads, n_kv_heads, kv, kv_rows, out, stream);
   if (dh == 64) return launch_attn_tc<64>(q, n, n_heads, n_kv_heads, kv, kv_rows, out, stream);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_attention_tc_varlen(const void* q, int64_t total, int n_seqs, int max_len,
+                                       const int32_t* cu, int n_heads, int n_kv_heads, int dh,
+                                       const KvOut& kv, int64_t kv_rows, void* out,
+                                       cudaStream_t stream) {
+  if (total <= 0 || n_seqs <= 0 || max_len <= 0) return cudaSuccess;
+  if (!cu || !kv.page_table || kv.page_size < 8 || (kv.page_size & (kv.page_size - 1)) != 0)
+    return cudaErrorInvalidValue;
+  if (dh == 128)
+    return launch_attn_tc<128>(q, int(total), n_heads, n_kv_heads, kv, kv_rows, out, stream, cu,
+                               n_seqs, max_len);
+  if (dh == 64)
+    return launch_attn_tc<64>(q, int(total), n_heads, n_kv_heads, kv, kv_rows, out, stream, cu,
+                              n_seqs, max_len);
   return cudaErrorInvalidValue;
 }
 

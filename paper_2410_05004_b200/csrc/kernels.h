@@ -126,6 +126,15 @@ cudaError_t launch_attention_tc(const void* q, int n, int n_heads, int n_kv_head
                                 const KvOut& kv, int64_t kv_rows, void* out,
                                 cudaStream_t stream);
 
+// The tcgen05 attention for a ragged batch of prefills from position 0:
+// sequence s owns query rows [cu[s], cu[s+1]) (device) and page-table row s
+// (stride kv.table_stride), attending causally to its own keys 0..; max_len =
+// the longest sequence (grid extent).
+cudaError_t launch_attention_tc_varlen(const void* q, int64_t total, int n_seqs, int max_len,
+                                       const int32_t* cu, int n_heads, int n_kv_heads, int dh,
+                                       const KvOut& kv, int64_t kv_rows, void* out,
+                                       cudaStream_t stream);
+
 // Embedding gather (model.cpp:82-92): x[i] = E[tokens[i]] (fp32), xb = bf16.
 cudaError_t launch_embed(const int32_t* tokens, int64_t n, const void* emb, int d, float* x,
                          void* xb, cudaStream_t stream);

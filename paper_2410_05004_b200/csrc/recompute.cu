@@ -92,14 +92,18 @@ CUtensorMap wmap(const void* base, int k, int64_t rows, int box_rows) {
 
 // tcgen05 attention (default) or the mma.sync kernel (HC_ATTN_TC=0, or page
 // sizes the TMA gather cannot express)
-cudaError_t attention(const void* q, int n, int n_heads, int n_kv_heads, int dh, const KvOut& kv,
-                      int64_t kv_rows, void* out, cudaStream_t stream) {
+bool attention_tc_ok(const KvOut& kv) {
   static const int tc = [] {
     const char* e = getenv("HC_ATTN_TC");
     return e ? atoi(e) : 1;
   }();
   const bool pow2 = !kv.page_table || (kv.page_size >= 8 && (kv.page_size & (kv.page_size - 1)) == 0);
-  if (tc && pow2) return launch_attention_tc(q, n, n_heads, n_kv_heads, dh, kv, kv_rows, out, stream);
+  return tc && pow2;
+}
+
+cudaError_t attention(const void* q, int n, int n_heads, int n_kv_heads, int dh, const KvOut& kv,
+                      int64_t kv_rows, void* out, cudaStream_t stream) {
+  if (attention_tc_ok(kv)) return launch_attention_tc(q, n, n_heads, n_kv_heads, dh, kv, kv_rows, out, stream);
   return launch_attention(q, n, n_heads, n_kv_heads, dh, kv, out, stream);
 }
 
@@ -172,7 +176,12 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wq, d, d, bn_d), bn_d, int(n), d, d, true, qo,
                               epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true));
     pm.lap(5);
-    if (sb.cu)
+    if (sb.cu && sb.from_zero && attention_tc_ok(kv))
+      HC_CUDA(launch_attention_tc_varlen(q_buf.ptr, n, sb.n_seqs, sb.max_new, sb.cu, c.n_heads,
+                                         c.n_kv_heads, w->d_head, kv,
+                                         int64_t(pages->num_pages) * pages->page_size,
+                                         mix_buf.ptr, stream));
+    else if (sb.cu)
       HC_CUDA(launch_attention_extend(q_buf.ptr, sb.n_seqs, sb.max_new, sb.cu, sb.seq_start,
                                       c.n_heads, c.n_kv_heads, w->d_head, kv, mix_buf.ptr,
                                       stream));
@@ -278,6 +287,7 @@ void forward_batch_layers(const hc_weights* w, const int32_t* d_tokens, int n_se
   sb.seq_start = d_starts;
   sb.max_new = max_new;
   sb.table_stride = table_stride;
+  sb.from_zero = true;  // the RECOMPUTE prefix of a restore: every session from position 0
   forward_impl(w, d_tokens, total, lb, le, pages, d_page_tables, stream, hook, nullptr, nullptr,
                sb, nullptr);
 }
@@ -314,6 +324,7 @@ void forward_batch(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
   sb.seq_start = sb.cu + n_seqs + 1;
   sb.max_new = max_new;
   sb.table_stride = table_stride;
+  sb.from_zero = std::all_of(start_pos, start_pos + n_seqs, [](int32_t p) { return p == 0; });
   forward_impl(w, d_tokens, total, 0, w->cfg.n_layers, pages, d_page_tables, stream,
                [](int, bool) {}, d_layer_inputs, nullptr, sb, d_next_tokens);
 }

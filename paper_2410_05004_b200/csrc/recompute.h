@@ -25,6 +25,7 @@ struct SeqBatch {
   const int32_t* seq_start = nullptr;  // device [n_seqs] first positions
   int max_new = 0;
   int table_stride = 0;
+  bool from_zero = false;  // every sequence starts at position 0 (a ragged prefill)
 };
 
 // forward_tokens / decode_step (model.cpp:305-347) for a batch of sequences
