@@ -93,7 +93,8 @@ CUtensorMap weight_map(const hc_weights::Layer& L, int bn, int d, int rows) {
 }
 
 void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t n_rows,
-                  const KvOut& out, cudaStream_t stream, const float* pre_stats) {
+                  const KvOut& out, cudaStream_t stream, const float* pre_stats,
+                  const int32_t* pre_flag) {
   if (layer < 0 || layer >= w->cfg.n_layers) fail(HC_EINVAL, "project: layer out of range");
   const auto& L = w->layers[size_t(layer)];
   if (!L.ready) fail(HC_EINVAL, "project: layer weights not set");
@@ -105,21 +106,42 @@ void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t 
   const int N = 2 * w->d_kv;
   if (w->cfg.rope_enabled && !out.cu_seqlens && int64_t(out.start_pos) + n_rows > w->rope_rows)
     fail(HC_EINVAL, "project: positions exceed max_seq");
-  const bool need = w->cfg.norm_enabled && !pre_stats;
-  StreamScratch stats(need ? size_t(n_rows) * 2 * sizeof(float) : 0, stream);
-  const float* mean = need ? static_cast<float*>(stats.ptr) : pre_stats;
+  const bool norm = w->cfg.norm_enabled != 0;
+  const bool need = norm && !pre_stats;
+  if (!ln_center_enabled()) pre_flag = nullptr;
+  // statistics (+ the centering flag) unless the caller computed them
+  StreamScratch stats(need ? size_t(n_rows) * 2 * sizeof(float) + 16 : 0, stream);
+  float* mean = need ? static_cast<float*>(stats.ptr) : const_cast<float*>(pre_stats);
   const float* rstd = mean ? mean + n_rows : nullptr;
-  if (need)
-    HC_CUDA(launch_row_stats(d_hidden, n_rows, d, d, true, static_cast<float*>(stats.ptr),
-                             static_cast<float*>(stats.ptr) + n_rows, stream));
+  const int32_t* flag =
+      need && ln_center_enabled() ? reinterpret_cast<int32_t*>(mean + 2 * n_rows) : pre_flag;
+  if (need && flag) {
+    HC_CUDA(cudaMemsetAsync(const_cast<int32_t*>(flag), 0, sizeof(int32_t), stream));
+    HC_CUDA(launch_row_stats_flagged(d_hidden, n_rows, d, d, true, mean, mean + n_rows,
+                                     const_cast<int32_t*>(flag), stream));
+  } else if (need) {
+    HC_CUDA(launch_row_stats(d_hidden, n_rows, d, d, true, mean, mean + n_rows, stream));
+  }
+  const uint32_t abox = uint32_t(gemm_a_box(n_rows));
   CUtensorMap tmA;
-  if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2,
-                        uint32_t(gemm_a_box(n_rows))))
+  if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2, abox))
     fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the hidden-state operand");
+  // rows with |mean| >> sigma: K1 reads a mean-shifted copy (a no-op kernel
+  // and an unused map unless the statistics raised the flag)
+  StreamScratch centered(norm && flag ? size_t(n_rows) * size_t(d) * 2 : 0, stream);
+  AltA alt;
+  if (norm && flag) {
+    HC_CUDA(launch_center_rows(d_hidden, n_rows, d, d, mean, flag, centered.ptr, stream));
+    if (!make_tmap_kmajor(&alt.map, centered.ptr, uint64_t(d), uint64_t(n_rows),
+                          uint64_t(d) * 2, abox))
+      fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the centered operand");
+    alt.flag = flag;
+  }
   const int sms = device_sm_count(w->device);
   const int bn = gemm_pick_bn(n_rows, N, sms);
   HC_CUDA(launch_restore_kv(tmA, weight_map(L, bn, d, N), bn, int(n_rows), N, d, true, out,
-                            epi_for(w, L.colsum, mean, rstd), sms, stream));
+                            epi_for(w, L.colsum, mean, rstd), sms, stream, false,
+                            norm && flag ? &alt : nullptr));
 }
 
 KvOut kv_out_pages(const hc_kv_pages* pages, int layer, const int32_t* page_table,

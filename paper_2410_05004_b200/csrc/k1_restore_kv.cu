@@ -57,7 +57,12 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
 }
 
 // The tensor map holding A row `row` and the row's coordinate within it.
-__device__ __forceinline__ const CUtensorMap* amap(const AMaps& am, int row, int& local) {
+__device__ __forceinline__ const CUtensorMap* amap(const AMaps& am, int row, int& local,
+                                                   bool alt = false) {
+  if (alt) {  // single source, mean-shifted copy
+    local = row;
+    return &am.m[1];
+  }
   int s = 0;
   while (s + 1 < am.n && row >= am.row0[s + 1]) ++s;
   local = row - am.row0[s];
@@ -363,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
+      const bool alt = am.alt_flag && *reinterpret_cast<const volatile int32_t*>(am.alt_flag);
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -374,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_expect_tx(&full[stage], a_bytes + Cfg::kBBytes);
           uint8_t* st = sA + size_t(stage) * stride;
           int a_row;
-          const CUtensorMap* ma = amap(am, m_blk * kBM, a_row);
+          const CUtensorMap* ma = amap(am, m_blk * kBM, a_row, alt);
           tma_load_2d(st, ma, &full[stage], kb * kBK, a_row);
           tma_load_2d(st + a_bytes, &tmB, &full[stage], kb * kBK, n_blk * BN);
           if (++stage == S) {
@@ -515,6 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs; bytes counted on the leader) ----
     if (lane == 0) {
+      const bool alt = am.alt_flag && *reinterpret_cast<const volatile int32_t*>(am.alt_flag);
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
@@ -524,7 +531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
           int a_row;
-          const CUtensorMap* ma = amap(am, m_blk * 256 + int(rank) * 128, a_row);
+          const CUtensorMap* ma = amap(am, m_blk * 256 + int(rank) * 128, a_row, alt);
           tma_load_2d_pair(sA + stage * kPairHalfBytes, ma, &full[stage], kb * kBK, a_row);
           tma_load_2d_pair(sB + stage * kPairHalfBytes, &tmB, &full[stage], kb * kBK,
                            n_blk * BN + int(rank) * 128);
@@ -627,11 +634,12 @@ struct StatsBatch {
   const void* x[kStatsMaxBatch];
   float* mean[kStatsMaxBatch];
   float* rstd[kStatsMaxBatch];
+  int32_t* flag[kStatsMaxBatch];  // nullable: raised when a row needs centering
 };
 
 template <typename T>
 __device__ __forceinline__ void row_stats_row(const T* __restrict__ r, int cols, int lane,
-                                              float* mean_out, float* rstd_out) {
+                                              float* mean_out, float* rstd_out, int32_t* flag) {
   constexpr int U = 8;
   const float c0 = __shfl_sync(0xffffffffu, lane == 0 ? float(r[0]) : 0.f, 0);
   double s[2] = {0.0, 0.0}, q[2] = {0.0, 0.0};
@@ -670,8 +678,10 @@ __device__ __forceinline__ void row_stats_row(const T* __restrict__ r, int cols,
     const double mu = ss / double(cols);  // mean of x - c0
     double var = qq / double(cols) - mu * mu;
     if (var < 0) var = 0;
-    *mean_out = float(double(c0) + mu);
-    *rstd_out = 1.0f / sqrtf(float(var) + 1e-5f);
+    const float mean = float(double(c0) + mu), rstd = 1.0f / sqrtf(float(var) + 1e-5f);
+    *mean_out = mean;
+    *rstd_out = rstd;
+    if (flag && fabsf(mean) * rstd > kCenterRatio) atomicOr(flag, 1);
   }
 }
 
@@ -684,7 +694,35 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const __grid_constant__ 
   if (row >= rows) return;
   const int m = blockIdx.y;
   row_stats_row(static_cast<const T*>(b.x[m]) + row * row_stride, cols, threadIdx.x & 31,
-                b.mean[m] + row, b.rstd[m] + row);
+                b.mean[m] + row, b.rstd[m] + row, b.flag[m]);
+}
+
+// launch_center_rows: one warp per row, 16-byte vectors; a no-op (every CTA
+// returns at once) unless the statistics raised the matrix's flag.
+__global__ void __launch_bounds__(256) center_rows_kernel(const __nv_bfloat16* __restrict__ x,
+                                                          int64_t rows, int cols,
+                                                          int64_t row_stride, float* mean,
+                                                          const int32_t* flag,
+                                                          __nv_bfloat16* __restrict__ out) {
+  if (*reinterpret_cast<const volatile int32_t*>(flag) == 0) return;
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5); row < rows;
+       row += int64_t(gridDim.x) * warps) {
+    const float m = mean[row];
+    const float c = __bfloat162float(__float2bfloat16_rn(m));
+    const uint4* src = reinterpret_cast<const uint4*>(x + row * row_stride);
+    uint4* dst = reinterpret_cast<uint4*>(out + row * int64_t(cols));
+    for (int i = lane; i < cols / 8; i += 32) {
+      uint4 u = __ldg(src + i);
+      __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&u);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) h[e] = __float2bfloat16_rn(__bfloat162float(h[e]) - c);
+      dst[i] = u;
+    }
+    __syncwarp();
+    if (lane == 0) mean[row] = m - c;
+  }
 }
 
 template <typename T>
@@ -923,12 +961,23 @@ cudaError_t launch_tc_bn(int bn, const AMaps& tmA, const CUtensorMap& tmB, int M
 
 }  // namespace
 
+namespace {
+AMaps amaps_with_alt(const CUtensorMap& tmA, const AltA* alt) {
+  AMaps am = single_amap(tmA);
+  if (alt) {
+    am.m[1] = alt->map;
+    am.alt_flag = alt->flag;
+  }
+  return am;
+}
+}  // namespace
+
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream, bool split_acc) {
+                              int num_sms, cudaStream_t stream, bool split_acc, const AltA* alt) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   GemmOut g;
-  const AMaps am = single_amap(tmA);
+  const AMaps am = amaps_with_alt(tmA, alt);
   if (bn == 128 && use_pair(M, N, num_sms))  // tmB has the 128-row box the pair needs
     return launch_pair<kEpiKv>(am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
   return launch_tc_bn<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream,
@@ -951,10 +1000,10 @@ cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int
 
 cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,
                               int M, int N, int K, const GemmOut& g, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream, bool split_acc) {
+                              int num_sms, cudaStream_t stream, bool split_acc, const AltA* alt) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   KvOut o;
-  const AMaps am = single_amap(tmA);
+  const AMaps am = amaps_with_alt(tmA, alt);
   if (bn == 128 && use_pair(M, N, num_sms))
     return mode == kEpiResid
                ? launch_pair<kEpiResid>(am, tmB, M, N, K, true, o, g, epi, num_sms, stream)
@@ -968,7 +1017,8 @@ cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, in
 
 cudaError_t launch_row_stats_batch(const void* const* x, int n_mats, int64_t rows, int cols,
                                    int64_t row_stride, bool bf16_in, float* const* mean,
-                                   float* const* rstd, cudaStream_t stream) {
+                                   float* const* rstd, cudaStream_t stream,
+                                   int32_t* const* flags) {
   if (rows <= 0 || n_mats <= 0) return cudaSuccess;
   const int threads = 256, per_block = threads / 32;
   for (int m0 = 0; m0 < n_mats; m0 += kStatsMaxBatch) {
@@ -978,6 +1028,7 @@ cudaError_t launch_row_stats_batch(const void* const* x, int n_mats, int64_t row
       b.x[i] = x[m0 + i];
       b.mean[i] = mean[m0 + i];
       b.rstd[i] = rstd[m0 + i];
+      b.flag[i] = flags ? flags[m0 + i] : nullptr;
     }
     const dim3 grid(unsigned((rows + per_block - 1) / per_block), unsigned(nb));
     if (bf16_in)
@@ -990,7 +1041,35 @@ cudaError_t launch_row_stats_batch(const void* const* x, int n_mats, int64_t row
 
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,
                              bool bf16_in, float* mean, float* rstd, cudaStream_t stream) {
-  return launch_row_stats_batch(&x, 1, rows, cols, row_stride, bf16_in, &mean, &rstd, stream);
+  return launch_row_stats_batch(&x, 1, rows, cols, row_stride, bf16_in, &mean, &rstd, stream,
+                                nullptr);
+}
+
+cudaError_t launch_row_stats_flagged(const void* x, int64_t rows, int cols, int64_t row_stride,
+                                     bool bf16_in, float* mean, float* rstd, int32_t* flag,
+                                     cudaStream_t stream) {
+  return launch_row_stats_batch(&x, 1, rows, cols, row_stride, bf16_in, &mean, &rstd, stream,
+                                &flag);
+}
+
+bool ln_center_enabled() {
+  static const bool on = [] {  // HC_LN_CENTER=0: never center (A/B measurements only)
+    const char* e = getenv("HC_LN_CENTER");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+cudaError_t launch_center_rows(const void* x, int64_t rows, int cols, int64_t row_stride,
+                               float* mean, const int32_t* flag, void* out, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (cols % 8 != 0 || row_stride % 8 != 0) return cudaErrorInvalidValue;
+  const int threads = 256, per_block = threads / 32;
+  const int64_t blocks = std::min<int64_t>((rows + per_block - 1) / per_block, 148 * 2);
+  center_rows_kernel<<<unsigned(blocks), threads, 0, stream>>>(
+      static_cast<const __nv_bfloat16*>(x), rows, cols, row_stride, mean, flag,
+      static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_colsum(const void* w, int64_t rows, int cols, bool bf16_in, float* out,

@@ -58,6 +58,10 @@ struct AMaps {
   CUtensorMap m[kMaxASrc];
   int row0[kMaxASrc + 1];
   int n;
+  // single source only: when *alt_flag != 0 (set on the device by the row
+  // statistics) the A operand is read through m[1], the mean-shifted copy
+  // written by launch_center_rows, instead of m[0]
+  const int32_t* alt_flag = nullptr;
 };
 inline AMaps single_amap(const CUtensorMap& t) {
   AMaps a;
@@ -90,9 +94,15 @@ int gemm_a_box(int64_t M);
 // reduced in a fixed order; a different summation order than the fused path).
 // Off for every K/V projection, so restored K/V stay bit-identical to the K/V
 // a forward wrote.
+// The mean-shifted A copy of launch_center_rows and its device flag.
+struct AltA {
+  CUtensorMap map;
+  const int32_t* flag;
+};
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream, bool split_acc = false);
+                              int num_sms, cudaStream_t stream, bool split_acc = false,
+                              const AltA* alt = nullptr);
 // K1 with a multi-source A (AMaps): the peer-memory all-gather fused in.
 cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int bn, int M, int N,
                                     int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
@@ -101,7 +111,8 @@ cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int
 // The same GEMM with a dense epilogue (mode kEpiResid or kEpiGelu).
 cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,
                               int M, int N, int K, const GemmOut& g, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream, bool split_acc = false);
+                              int num_sms, cudaStream_t stream, bool split_acc = false,
+                              const AltA* alt = nullptr);
 
 // Causal attention over the paged cache for a prefill from position 0
 // (attention_forward, model.cpp:237-288): q [n x n_heads*dh] bf16 (RoPE
@@ -178,10 +189,28 @@ cudaError_t launch_convert_to_bf16(const void* src, int src_dtype, void* dst, in
 
 // Row statistics for the LayerNorm fold: mean and 1/sqrt(var+1e-5) per row,
 // mean/var accumulated in double like the reference (model.cpp:43-61).
+// Rows whose |mean| exceeds this many standard deviations make the LayerNorm
+// fold lose precision (H W^T ~ mean * colsum(W) cancels in fp32): the row
+// statistics raise a per-matrix flag and the GEMM reads a shifted copy.
+constexpr float kCenterRatio = 16.0f;
+
+// Row statistics of n_mats matrices of identical shape in one launch;
+// flags[i] (nullable, zeroed by the caller) is set when a row of matrix i
+// has |mean| * rstd > kCenterRatio.
+cudaError_t launch_row_stats_flagged(const void* x, int64_t rows, int cols, int64_t row_stride,
+                                     bool bf16_in, float* mean, float* rstd, int32_t* flag,
+                                     cudaStream_t stream);
+// When *flag (device) is set: out[r] = bf16(x[r] - c_r), c_r = bf16(mean[r])
+// (exact for |x - c| small against c, Sterbenz), and mean[r] -= c_r in place,
+// so the LayerNorm fold over `out` is well conditioned. A no-op otherwise.
+bool ln_center_enabled();
+cudaError_t launch_center_rows(const void* x, int64_t rows, int cols, int64_t row_stride,
+                               float* mean, const int32_t* flag, void* out, cudaStream_t stream);
 // Row statistics of n_mats matrices of identical shape in one launch.
 cudaError_t launch_row_stats_batch(const void* const* x, int n_mats, int64_t rows, int cols,
                                    int64_t row_stride, bool bf16_in, float* const* mean,
-                                   float* const* rstd, cudaStream_t stream);
+                                   float* const* rstd, cudaStream_t stream,
+                                   int32_t* const* flags = nullptr);
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,
                              bool bf16_in, float* mean, float* rstd, cudaStream_t stream);
 

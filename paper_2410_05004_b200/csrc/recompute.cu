@@ -135,16 +135,36 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
   const size_t nd = size_t(n) * size_t(d);
   StreamScratch x_buf(nd * 4, stream), xb_buf(nd * 2, stream), q_buf(nd * 2, stream),
       mix_buf(nd * 2, stream), h1_buf(size_t(n) * size_t(dffn) * 2, stream),
-      stats(size_t(n) * 2 * 4, stream);
+      stats(size_t(n) * 2 * 4 + 16, stream), xc_buf(c.norm_enabled ? nd * 2 : 0, stream);
   float* x = static_cast<float*>(x_buf.ptr);
   float* mean = static_cast<float*>(stats.ptr);
   float* rstd = mean + n;
+  int32_t* flag = reinterpret_cast<int32_t*>(mean + 2 * n);
   pm.lap(0);
   HC_CUDA(launch_embed(d_tokens, n, w->embedding, d, x, xb_buf.ptr, stream));
   const int abox = gemm_a_box(n);
   const CUtensorMap tm_xb = tmap(xb_buf.ptr, d, n, abox);
   const CUtensorMap tm_mix = tmap(mix_buf.ptr, d, n, abox);
   const CUtensorMap tm_h1 = tmap(h1_buf.ptr, dffn, n, abox);
+  // LayerNorm statistics of xb + the mean-shifted operand for rows with
+  // |mean| >> sigma (launch_center_rows; a no-op unless flagged)
+  AltA alt;
+  const AltA* altp = nullptr;
+  const bool center = c.norm_enabled && ln_center_enabled();
+  if (center) {
+    alt.map = tmap(xc_buf.ptr, d, n, abox);
+    alt.flag = flag;
+    altp = &alt;
+  }
+  auto ln_stats = [&]() {
+    if (!center) {
+      HC_CUDA(launch_row_stats(xb_buf.ptr, n, d, d, true, mean, rstd, stream));
+      return;
+    }
+    HC_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), stream));
+    HC_CUDA(launch_row_stats_flagged(xb_buf.ptr, n, d, d, true, mean, rstd, flag, stream));
+    HC_CUDA(launch_center_rows(xb_buf.ptr, n, d, d, mean, flag, xc_buf.ptr, stream));
+  };
   // K/V: the exact path (restores must reproduce these K/V bit for bit); the
   // other projections may split K when n is decode-sized
   const int bn_kv = pick_bn(n, 2 * w->d_kv_all, sms), bn_d = gemm_pick_bn_skinny(n, d, sms),
@@ -158,13 +178,13 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
                               nd * 2, cudaMemcpyDeviceToDevice, stream));
     // attention block: LN(x) -> K/V (paged) and Q
     pm.lap(2);
-    HC_CUDA(launch_row_stats(xb_buf.ptr, n, d, d, true, mean, rstd, stream));
+    ln_stats();
     pm.lap(3);
     KvOut kv = kv_out_pages(pages, L, d_page_table, sb.table_stride, sb.cu, sb.n_seqs);
     kv.seq_start = sb.seq_start;
     HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wkv_all, d, 2 * w->d_kv_all, bn_kv), bn_kv, int(n),
                               2 * w->d_kv_all, d, true, kv, epi_for(w, lw.colsum_all, mean, rstd),
-                              sms, stream));
+                              sms, stream, false, altp));
     pm.lap(4);
     KvOut qo;
     qo.k_base = q_buf.ptr;
@@ -174,7 +194,7 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     qo.n_seqs = sb.cu ? sb.n_seqs : 1;
     qo.seq_start = sb.seq_start;
     HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wq, d, d, bn_d), bn_d, int(n), d, d, true, qo,
-                              epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true));
+                              epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true, altp));
     pm.lap(5);
     if (sb.cu && sb.from_zero && attention_tc_ok(kv))
       HC_CUDA(launch_attention_tc_varlen(q_buf.ptr, n, sb.n_seqs, sb.max_new, sb.cu, c.n_heads,
@@ -197,7 +217,7 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
                               resid, EpiArgs{}, sms, stream, true));
     pm.lap(7);
     // FFN block (ffn_forward, model.cpp:290-303)
-    HC_CUDA(launch_row_stats(xb_buf.ptr, n, d, d, true, mean, rstd, stream));
+    ln_stats();
     pm.lap(8);
     GemmOut g1;
     g1.xb = h1_buf.ptr;
@@ -209,7 +229,7 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
       fold.colsum = lw.colsum_fc1;
     }
     HC_CUDA(launch_gemm_dense(tm_xb, wmap(lw.fc1, d, dffn, bn_f), bn_f, kEpiGelu, int(n), dffn,
-                              d, g1, fold, sms, stream, true));
+                              d, g1, fold, sms, stream, true, altp));
     pm.lap(9);
     HC_CUDA(launch_gemm_dense(tm_h1, wmap(lw.fc2, dffn, d, bn_d), bn_d, kEpiResid, int(n), d,
                               dffn, resid, EpiArgs{}, sms, stream, true));

@@ -617,18 +617,21 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
     // HBM bandwidth and SM thread slots for the stats kernel)
     const bool norm = w->cfg.norm_enabled != 0;
     StreamScratch stats(norm ? size_t(L) * size_t(n_rows) * 2 * sizeof(float) : 0, s);
+    StreamScratch flags(norm ? size_t(L) * sizeof(int32_t) : 0, s);
     float* st = static_cast<float*>(stats.ptr);
+    int32_t* fl = static_cast<int32_t*>(flags.ptr);
     EventPool evs(false);
     std::vector<cudaEvent_t> ready;
     if (norm) {
       Engine& eng = engine(w->device);
+      HC_CUDA(cudaMemsetAsync(fl, 0, size_t(L) * sizeof(int32_t), s));
       cudaEvent_t start = evs.get();
       HC_CUDA(cudaEventRecord(start, s));
       HC_CUDA(cudaStreamWaitEvent(eng.aux, start, 0));
       for (int l = 0; l < L; ++l) {
         float* mean = st + size_t(l) * 2 * size_t(n_rows);
-        HC_CUDA(launch_row_stats(d_hidden_layers[l], n_rows, d, d, true, mean, mean + n_rows,
-                                 eng.aux));
+        HC_CUDA(launch_row_stats_flagged(d_hidden_layers[l], n_rows, d, d, true, mean,
+                                         mean + n_rows, fl + l, eng.aux));
         ready.push_back(evs.get());
         HC_CUDA(cudaEventRecord(ready.back(), eng.aux));
       }
@@ -637,7 +640,7 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
       if (norm) HC_CUDA(cudaStreamWaitEvent(s, ready[size_t(l)], 0));
       project_rows(w, l, d_hidden_layers[l], n_rows,
                    kv_out_pages(pages, l, d_page_table, table_stride, d_cu_seqlens, n_seqs), s,
-                   norm ? st + size_t(l) * 2 * size_t(n_rows) : nullptr);
+                   norm ? st + size_t(l) * 2 * size_t(n_rows) : nullptr, norm ? fl + l : nullptr);
     }
   });
 }

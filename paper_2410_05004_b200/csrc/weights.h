@@ -47,9 +47,12 @@ EpiArgs epi_for(const hc_weights* w, const float* colsum, const float* mean, con
 // Runs K1 for rows [0, n_rows) of a K-major bf16 hidden matrix (row stride
 // d_hidden) of `layer` into `out`. Computes the row statistics itself.
 // With `stats` (mean[n_rows] then rstd[n_rows], from launch_row_stats) the
-// row-statistics launch is skipped.
+// row-statistics launch is skipped; `flag` (from launch_row_stats_flagged)
+// then enables the mean-shifted operand (the means may be adjusted in place).
+// Without them the statistics and the flag are computed here.
 void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t n_rows,
-                  const KvOut& out, cudaStream_t stream, const float* stats = nullptr);
+                  const KvOut& out, cudaStream_t stream, const float* stats = nullptr,
+                  const int32_t* flag = nullptr);
 
 // KvOut for a layer of a paged cache.
 KvOut kv_out_pages(const hc_kv_pages* pages, int layer, const int32_t* page_table,

@@ -178,3 +178,25 @@ def test_config4_opt30b_no_rope_sampled(cuda, oracle):
     cfg = H.ModelConfig(n_layers=48, d_hidden=7168, n_heads=56, d_ffn=28672, max_seq=4096,
                         rope_enabled=False)
     _sampled_slices_check(oracle, cfg, 3338, 0, [(0, 20), (3338 - 17, 17)])
+
+
+@pytest.mark.parametrize("offset", [8.0, -40.0])
+def test_k1_layernorm_large_mean(cuda, oracle, offset):
+    """Rows whose mean dwarfs their spread (|mean| / sigma ~ 80-400): the row
+    statistics must not cancel (the reference takes mean and variance in
+    double, model.cpp:43-61; K1's statistics use sums of x - x0 per row)."""
+    import torch
+    from oracle import bf16_round
+    from paper_2410_05004_b200 import hcache as H
+    n, d, nh = 300, 1024, 8
+    cfg = H.ModelConfig(n_layers=1, d_hidden=d, n_heads=nh, d_ffn=4 * d, max_seq=4096)
+    w = _weights(cfg, None)
+    hc = bf16_round(np.float32(offset) + np.float32(0.1) * cpu_hidden(oracle, n, d))
+    h = torch.from_numpy(hc).cuda().bfloat16()
+    assert np.array_equal(h.float().cpu().numpy(), hc)  # exactly the oracle's input
+    k16, v16 = H.project_hidden_to_kv(w, 0, h, 0, torch.bfloat16)
+    torch.cuda.synchronize()
+    wk, wv = cpu_wkv(oracle, d, d, 0)
+    kr, vr = oracle.project(hc, wk, wv, nh, 0, True, True)
+    assert max_rel_err(k16.float().cpu().numpy(), kr) < REL_TOL
+    assert max_rel_err(v16.float().cpu().numpy(), vr) < REL_TOL
