@@ -409,15 +409,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 //   before PV_t(j) has read it.
 //   warp 0      TMA (Q_A, Q_B once; K(j), V(j-1) into two 2-stage rings)
 //   warp 1      TMEM owner + MMA issuer
-//   warps 2-9   softmax, two threads per query row (64 keys each, row max
-//               exchanged through smem), tile A then tile B every key step
+//   warps 2-9   softmax of tile A, warps 10-17 of tile B (the two overlap on
+//               every SM sub-partition): two threads per query row (64 keys
+//               each, row max exchanged through smem)
 // Part of the exponentials run as a Cody-Waite + degree-3 polynomial on the
 // FMA pipe (rel. error 7.5e-5, far below bf16 P's 3.9e-3), the rest on MUFU:
 // with only MUFU the 16 ex2/clk/SM take exactly as long as the MMAs. The
 // softmax arithmetic is packed fp32x2 (FFMA2/FADD2) to halve its issue slots.
 // ============================================================================
 constexpr int kFaM = 128;       // rows per Q tile (two per CTA)
-constexpr int kFaThreads = 320;  // TMA, MMA, 8 softmax warps (two threads per query row)
+constexpr int kFaThreads = 576;  // TMA, MMA, 8 softmax warps per Q tile (two threads per row)
 #ifndef HC_FA_EMU
 #define HC_FA_EMU 3
 #endif
@@ -567,7 +568,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 8);
+      mbar_init(&p_full[s], 8);  // the tile's 8 softmax warps
       mbar_init(&o_done[s], 1);
     }
     fence_barrier_init();
@@ -665,7 +666,10 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         const uint64_t v = dv + uint64_t(st * (Cfg::kKVBytes >> 4));
 #pragma unroll
         for (int kk = 0; kk < kAttnN / 16; ++kk)
-          umma_f16_ts(tmem + 256 + uint32_t(t * 128), tmem + uint32_t(t * 128 + kk * 8),
+          // P of keys 16kk..: key half kk/4 wrote its 32 columns at the start
+          // of its own 64-column S half
+          umma_f16_ts(tmem + 256 + uint32_t(t * 128),
+                      tmem + uint32_t(t * 128 + (kk >> 2) * 64 + (kk & 3) * 8),
                       v + uint64_t(kk * (2048 >> 4)), id_pv, (j | kk) != 0 ? 1u : 0u);
         umma_commit(&o_done[t]);
         if (t == 1) umma_commit(&v_empty[st]);
@@ -684,142 +688,147 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax
-    // warps w and w+4 share a TMEM lane quadrant (32 query rows); `half`
-    // selects 64 of the 128 keys of a tile (and DH/2 of the O columns). Each
-    // step handles tile A then tile B (tile B's S is computed while A's
-    // softmax runs, and vice versa for the tensor core).
+    // warps 2-9 own Q tile A, 10-17 tile B, so the two tiles' softmax
+    // overlap on every SM sub-partition. In a tile's group warps w and w+4
+    // share a TMEM lane quadrant (32 query rows); `half` selects 64 of the
+    // 128 keys (and DH/2 of the O columns). S is read from TMEM in 32-column
+    // chunks, twice (row max, then exponentials), to keep registers for
+    // instruction-level parallelism; a thread writes the bf16 P of its 64 keys
+    // into the first 32 columns of its own S half, so it never overwrites
+    // scores its partner has not read.
+    const int t = (warp - 2) >> 3;  // Q tile
     const int qd = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int half = ((warp - 2) >> 2) & 1;
     const int rloc = qd * 32 + lane;
+    const int row = q0 + t * kFaM + rloc;
+    const int nt = t == 0 ? nt_a : nt_b;
+    const int row_lim = min(row, a.n - 1);  // last visible key of this row
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
-    const uint32_t bar_id = 1 + uint32_t(qd);  // named barrier of the quadrant's two warps
+    const uint32_t t_s = tmem + lane_off + uint32_t(t * 128 + half * 64);  // my S half
+    const uint32_t t_o = tmem + lane_off + 256u + uint32_t(t * 128);
+    const uint32_t bar_id = 1 + uint32_t(t * 4 + qd);  // named barrier of the row pair
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
-    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    float m_run = -INFINITY, l_run = 0.f;
     const uint64_t sc2 = f2_pack(a.scale_log2, a.scale_log2);
-    for (int j = 0; j < nt_b; ++j) {
-#pragma unroll 1
-      for (int t = 0; t < 2; ++t) {
-        if (t == 0 && j >= nt_a) continue;
-        const int row = q0 + t * kFaM + rloc;
-        const int row_lim = min(row, a.n - 1);  // last visible key of this row
-        const uint32_t t_s = tmem + lane_off + uint32_t(t * 128);
-        const uint32_t t_o = tmem + lane_off + 256u + uint32_t(t * 128);
-        mbar_wait(&s_full[t], j & 1);
-        tc_fence_after();
-        if (rloc == 0 && half == 0) FA_TRACE(2, t, j);
-        uint32_t sv[64];
-        tmem_ld_32x32b_x32(t_s + uint32_t(half * 64), *reinterpret_cast<uint32_t(*)[32]>(sv));
-        tmem_ld_32x32b_x32(t_s + uint32_t(half * 64 + 32), *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+    for (int j = 0; j < nt; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      if (rloc == 0 && half == 0) FA_TRACE(2, t, j);
+      const int key0 = j * kAttnN + half * 64;
+      const bool diag = __any_sync(0xffffffffu, key0 + 63 > row_lim);  // diagonal / tail
+      const int lim = row_lim - key0;
+      // pass 1: row max of my 64 scores
+      float m8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_s + uint32_t(c * 32), v);
         tmem_wait_ld();
-        if (rloc == 0 && half == 0) FA_TRACE(6, t, j);
-        const int key0 = j * kAttnN + half * 64;
-        if (__any_sync(0xffffffffu, key0 + 63 > row_lim)) {  // diagonal / tail tile
-          const int lim = row_lim - key0;
+        if (diag) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (i > lim) sv[i] = __float_as_uint(-INFINITY);
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i > lim) v[i] = __float_as_uint(-INFINITY);
         }
-        float m8[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) m8[u] = fmaxf(__uint_as_float(sv[u]), __uint_as_float(sv[u + 8]));
-#pragma unroll
-        for (int i = 16; i < 64; i += 16)
+        for (int i = 0; i < 32; i += 16)
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            m8[u] = fmaxf(m8[u], fmaxf(__uint_as_float(sv[i + u]), __uint_as_float(sv[i + 8 + u])));
-        float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                         fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-        // row max across the two halves; after this barrier both threads have
-        // their S in registers, so P may overwrite any S column
-        float* xm = xmax + ((j & 1) * 4 + t * 2) * kFaM;
-        xm[half * kFaM + rloc] = mx;
-        pair_sync();
-        mx = fmaxf(mx, xm[(half ^ 1) * kFaM + rloc]) * a.scale_log2;
-        // lazy max: keep m_run unless the tile max exceeds it by > 8 (P <= 2^8)
-        const bool resc = mx > m_run[t] + 8.0f;
-        const float m_use = resc ? mx : m_run[t];
-        if (rloc == 0 && half == 0) FA_TRACE(7, t, j);
-        const uint64_t nm2 = f2_pack(-m_use, -m_use);
-        uint64_t sum2 = 0, sum2b = 0;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int e = c * 32 + 2 * i;
-            const uint64_t x = f2_fma(uint64_t(sv[e]) | (uint64_t(sv[e + 1]) << 32), sc2, nm2);
-            uint64_t pv;
-            if ((i & 7) < kFaEmuPairs) {
-              pv = ex2_poly2(x);
-            } else {
-              pv = f2_pack(ex2_approx(f2_lo(x)), ex2_approx(f2_hi(x)));
-            }
-            if (i & 1) sum2b = f2_add(sum2b, pv);
-            else sum2 = f2_add(sum2, pv);
-            pk[i] = pack_bf16x2(f2_lo(pv), f2_hi(pv));
-          }
-          // keys half*64 + c*32 .. +31 -> P columns half*32 + c*16 .. +15
-          tmem_st_32x32b_x16(t_s + uint32_t(half * 32 + c * 16), pk);
-        }
-        sum2 = f2_add(sum2, sum2b);
-        if (rloc == 0 && half == 0) FA_TRACE(8, t, j);
-        // O_t rescale (rare with the lazy max): O_t must not be touched while
-        // PV_t(j-1) runs; PV_t(j) waits for p_full below
-        if (__any_sync(0xffffffffu, resc)) {
-          const float corr = resc ? ex2_approx(m_run[t] - m_use) : 1.0f;
-          l_run[t] *= corr;
-          if (j > 0) {
-            mbar_wait(&o_done[t], (j - 1) & 1);
-            tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < DH / 64; ++c) {
-              uint32_t v[32];
-              const uint32_t ta = t_o + uint32_t(half * (DH / 2) + c * 32);
-              tmem_ld_32x32b_x32(ta, v);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
-              tmem_st_32x32b_x32(ta, v);
-            }
-          }
-          m_run[t] = m_use;
-        }
-        l_run[t] += f2_lo(sum2) + f2_hi(sum2);
-        tmem_wait_st();
-        if (rloc == 0 && half == 0) FA_TRACE(9, t, j);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[t]);
-        if (rloc == 0 && half == 0) FA_TRACE(3, t, j);
+            m8[u] = fmaxf(m8[u], fmaxf(__uint_as_float(v[i + u]), __uint_as_float(v[i + 8 + u])));
       }
-    }
-#pragma unroll 1
-    for (int t = 0; t < 2; ++t) {
-      const int nt = t == 0 ? nt_a : nt_b;
-      const int row = q0 + t * kFaM + rloc;
-      const uint32_t t_o = tmem + lane_off + 256u + uint32_t(t * 128);
-      xsum[(t * 2 + half) * kFaM + rloc] = l_run[t];
-      mbar_wait(&o_done[t], (nt - 1) & 1);
-      tc_fence_after();
+      if (rloc == 0 && half == 0) FA_TRACE(6, t, j);
+      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      float* xm = xmax + ((j & 1) * 4 + t * 2) * kFaM;
+      xm[half * kFaM + rloc] = mx;
       pair_sync();
-      const float inv = 1.0f / (l_run[t] + xsum[(t * 2 + (half ^ 1)) * kFaM + rloc]);
-      __nv_bfloat16* dst =
-          a.out + size_t(row0 + row) * size_t(a.n_heads * DH) + size_t(h) * DH;
-#pragma unroll 1
-      for (int c = 0; c < DH / 64; ++c) {
-        const int col = half * (DH / 2) + c * 32;
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_o + uint32_t(col), v);
-        tmem_wait_ld();
-        if (row < a.n) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+      mx = fmaxf(mx, xm[(half ^ 1) * kFaM + rloc]) * a.scale_log2;
+      // lazy max: keep m_run unless the tile max exceeds it by > 8 (P <= 2^8)
+      const bool resc = mx > m_run + 8.0f;
+      const float m_use = resc ? mx : m_run;
+      if (rloc == 0 && half == 0) FA_TRACE(7, t, j);
+      // pass 2: P = 2^(s * scale_log2 - m), 32 keys -> 16 columns at a time
+      const uint64_t nm2 = f2_pack(-m_use, -m_use);
+      uint64_t sum2 = 0, sum2b = 0;
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            d4[i] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * i + 0]) * inv, __uint_as_float(v[8 * i + 1]) * inv),
-                               pack_bf16x2(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv),
-                               pack_bf16x2(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv),
-                               pack_bf16x2(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv));
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_s + uint32_t(c * 32), v);
+        tmem_wait_ld();
+        if (diag) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i > lim) v[i] = __float_as_uint(-INFINITY);
         }
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint64_t x = f2_fma(uint64_t(v[2 * i]) | (uint64_t(v[2 * i + 1]) << 32), sc2, nm2);
+          uint64_t pv;
+          if ((i & 7) < kFaEmuPairs) {
+            pv = ex2_poly2(x);
+          } else {
+            pv = f2_pack(ex2_approx(f2_lo(x)), ex2_approx(f2_hi(x)));
+          }
+          if (i & 1) sum2b = f2_add(sum2b, pv);
+          else sum2 = f2_add(sum2, pv);
+          pk[i] = pack_bf16x2(f2_lo(pv), f2_hi(pv));
+        }
+        // columns c*16.. of my half: scores already read (chunk 0)
+        tmem_st_32x32b_x16(t_s + uint32_t(c * 16), pk);
+      }
+      sum2 = f2_add(sum2, sum2b);
+      if (rloc == 0 && half == 0) FA_TRACE(8, t, j);
+      // O_t rescale (rare with the lazy max): O_t must not be touched while
+      // PV_t(j-1) runs; PV_t(j) waits for p_full below
+      if (__any_sync(0xffffffffu, resc)) {
+        const float corr = resc ? ex2_approx(m_run - m_use) : 1.0f;
+        l_run *= corr;
+        if (j > 0) {
+          mbar_wait(&o_done[t], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < DH / 64; ++c) {
+            uint32_t v[32];
+            const uint32_t ta = t_o + uint32_t(half * (DH / 2) + c * 32);
+            tmem_ld_32x32b_x32(ta, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st_32x32b_x32(ta, v);
+          }
+        }
+        m_run = m_use;
+      }
+      l_run += f2_lo(sum2) + f2_hi(sum2);
+      tmem_wait_st();
+      if (rloc == 0 && half == 0) FA_TRACE(9, t, j);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
+      if (rloc == 0 && half == 0) FA_TRACE(3, t, j);
+    }
+    xsum[(t * 2 + half) * kFaM + rloc] = l_run;
+    mbar_wait(&o_done[t], (nt - 1) & 1);
+    tc_fence_after();
+    pair_sync();
+    const float inv = 1.0f / (l_run + xsum[(t * 2 + (half ^ 1)) * kFaM + rloc]);
+    __nv_bfloat16* dst = a.out + size_t(row0 + row) * size_t(a.n_heads * DH) + size_t(h) * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 64; ++c) {
+      const int col = half * (DH / 2) + c * 32;
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(t_o + uint32_t(col), v);
+      tmem_wait_ld();
+      if (row < a.n) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          d4[i] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * i + 0]) * inv, __uint_as_float(v[8 * i + 1]) * inv),
+                             pack_bf16x2(__uint_as_float(v[8 * i + 2]) * inv, __uint_as_float(v[8 * i + 3]) * inv),
+                             pack_bf16x2(__uint_as_float(v[8 * i + 4]) * inv, __uint_as_float(v[8 * i + 5]) * inv),
+                             pack_bf16x2(__uint_as_float(v[8 * i + 6]) * inv, __uint_as_float(v[8 * i + 7]) * inv));
       }
     }
   }

@@ -291,6 +291,14 @@ void Engine::setup() {
     h = need;
   }
   stride_ = (max_need + page_ - 1) / page_;
+  if (persisting()) {
+    // the run's save volume (every session's final token count x the plan's
+    // bytes per token, x2 for extent slack), page-locked outside the clock
+    size_t tokens = 0;
+    for (const auto& kv : hist) tokens += size_t(kv.second);
+    const size_t per_token = size_t(hid_.count) * size_t(d_) * 2 + size_t(kvr_.count) * size_t(2 * dkv_) * 2;
+    st_.reserve_pinned(std::min<size_t>(size_t(64) << 30, 2 * tokens * per_token));
+  }
   max_batch_ = o_.max_batch > 0 ? std::min(o_.max_batch, n_) : n_;
   max_rows_ = std::max(max_rows, max_batch_);
   // page pool: per layer K and V [num_pages][page][d_kv] bf16

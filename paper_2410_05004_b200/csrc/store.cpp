@@ -108,14 +108,16 @@ size_t PinnedPool::size_class(size_t bytes) {
   return c;
 }
 
-void* PinnedPool::alloc_raw(size_t bytes) {
-  std::lock_guard<std::mutex> lk(mu_);
+void PinnedPool::probe() {
   if (!probed_) {
     int n = 0;
     pinned_ = cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
     if (!pinned_) cudaGetLastError();
     probed_ = true;
   }
+}
+
+uint8_t* PinnedPool::new_block(size_t bytes) {
   void* p = nullptr;
   if (pinned_) {
     if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
@@ -124,12 +126,50 @@ void* PinnedPool::alloc_raw(size_t bytes) {
     }
     blocks_.push_back({p, true});
   } else {
-    size_t r = (bytes + 4095) & ~size_t(4095);
-    p = std::aligned_alloc(4096, r ? r : 4096);
+    p = std::aligned_alloc(4096, bytes);
     if (!p) fail(HC_ENOMEM, "host allocation failed");
     blocks_.push_back({p, false});
   }
+  return static_cast<uint8_t*>(p);
+}
+
+namespace {
+constexpr size_t kSlabBytes = size_t(256) << 20;
+}
+
+void* PinnedPool::alloc_raw(size_t bytes) {
+  std::lock_guard<std::mutex> lk(mu_);
+  probe();
+  const size_t r = std::max<size_t>(4096, (bytes + 4095) & ~size_t(4095));
+  if (r > left_) {
+    // the next reserved slab that fits, else a new one
+    auto it = std::find_if(slabs_.begin(), slabs_.end(),
+                           [&](const std::pair<uint8_t*, size_t>& sl) { return sl.second >= r; });
+    if (it != slabs_.end()) {
+      cur_ = it->first;
+      left_ = it->second;
+      slabs_.erase(it);
+    } else {
+      const size_t sz = std::max(r, kSlabBytes);
+      cur_ = new_block(sz);
+      left_ = sz;
+    }
+  }
+  void* p = cur_;
+  cur_ += r;
+  left_ -= r;
   return p;
+}
+
+void PinnedPool::reserve(size_t bytes) {
+  std::lock_guard<std::mutex> lk(mu_);
+  probe();
+  size_t have = left_;
+  for (const auto& sl : slabs_) have += sl.second;
+  while (have < bytes) {
+    slabs_.push_back({new_block(kSlabBytes), kSlabBytes});
+    have += kSlabBytes;
+  }
 }
 
 void* PinnedPool::alloc(size_t bytes) {

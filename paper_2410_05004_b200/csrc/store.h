@@ -32,14 +32,24 @@ class PinnedPool {
   ~PinnedPool();
   void* alloc(size_t bytes);
   void release(void* p, size_t bytes);
-  void* alloc_raw(size_t bytes);  // never returned before destruction
+  // Never returned before destruction: carved from 256 MiB page-locked slabs
+  // (cudaHostAlloc pins page by page -- tens of ms per slab -- and is
+  // best kept off a restore's critical path).
+  void* alloc_raw(size_t bytes);
+  // Page-lock slabs for `bytes` of future alloc_raw calls now.
+  void reserve(size_t bytes);
   bool pinned() const { return pinned_; }
 
  private:
   static size_t size_class(size_t bytes);
+  void probe();
+  uint8_t* new_block(size_t bytes);
   std::mutex mu_;
   std::map<size_t, std::vector<void*>> free_;
   std::vector<std::pair<void*, bool>> blocks_;  // (ptr, is_cuda_host)
+  std::vector<std::pair<uint8_t*, size_t>> slabs_;  // reserved, not yet in use
+  uint8_t* cur_ = nullptr;  // bump pointer into the current slab
+  size_t left_ = 0;
   bool pinned_ = false;
   bool probed_ = false;
 };
@@ -117,6 +127,9 @@ class Store {
   void chunk_info(const std::string& sid, int layer, int kind, int c, int* dev,
                   const void** payload, int64_t* bytes) const;
   std::vector<int64_t> device_chunk_counts() const;
+  // Page-lock `bytes` of chunk arena now (e.g. a serving run's whole save
+  // volume at start-up), so later extents are carved without cudaHostAlloc.
+  void reserve_pinned(size_t bytes) { pool_mem_.reserve(bytes); }
   void start_daemon();
   bool daemon_running() const;
   void stop_daemon();
