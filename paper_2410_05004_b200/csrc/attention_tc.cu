@@ -502,11 +502,14 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
 }
 
 #ifdef HC_FA_TRACE
-// per-event SM clocks of one CTA (blockIdx 0,0): [event][tile][j]
-__device__ unsigned long long g_fa_trace[10][2][64];
+// per-event SM clocks of one CTA (blockIdx 0,0): [event][tile][j], written to
+// host-mapped memory (readable even after the kernel traps)
+__device__ unsigned long long* g_fa_trace;
 #define FA_TRACE(ev, t, j)                                                                     \
   do {                                                                                         \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) g_fa_trace[ev][t][j] = clock64();     \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64)                                        \
+      *reinterpret_cast<volatile unsigned long long*>(g_fa_trace + ((ev) * 2 + (t)) * 64 + (j)) = \
+          clock64();                                                                           \
   } while (0)
 #else
 #define FA_TRACE(ev, t, j) \

@@ -32,22 +32,28 @@ int main(int argc, char** argv) {
   kv.k_base = k;
   kv.v_base = v;
   kv.d_kv = heads * dh;
+  unsigned long long* h_tr = nullptr;
+  cudaHostAlloc(&h_tr, sizeof(unsigned long long) * 10 * 2 * 64, cudaHostAllocMapped);
+  memset(h_tr, 0, sizeof(unsigned long long) * 10 * 2 * 64);
+  unsigned long long* d_tr = nullptr;
+  cudaHostGetDevicePointer(&d_tr, h_tr, 0);
+  cudaMemcpyToSymbol(hc::g_fa_trace, &d_tr, sizeof(d_tr));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int i = 0; i < 3; ++i) hc::launch_attention_tc(q, n, heads, heads, dh, kv, n, o, 0);
+  const int reps = argc > 3 ? atoi(argv[3]) : 10;
+  for (int i = 0; i < (reps > 1 ? 3 : 0); ++i) hc::launch_attention_tc(q, n, heads, heads, dh, kv, n, o, 0);
   cudaEventRecord(e0);
-  for (int i = 0; i < 10; ++i) hc::launch_attention_tc(q, n, heads, heads, dh, kv, n, o, 0);
+  for (int i = 0; i < reps; ++i) hc::launch_attention_tc(q, n, heads, heads, dh, kv, n, o, 0);
   cudaEventRecord(e1);
   cudaError_t err = cudaDeviceSynchronize();
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  printf("status %s, %.1f us/launch\n", cudaGetErrorString(err), ms * 100);
-  unsigned long long tr[10][2][64];
-  cudaMemcpyFromSymbol(tr, hc::g_fa_trace, sizeof(tr));
+  printf("status %s, %.1f us/launch\n", cudaGetErrorString(err), ms * 1e3 / reps);
+  unsigned long long(&tr)[10][2][64] = *reinterpret_cast<unsigned long long(*)[10][2][64]>(h_tr);
   const unsigned long long t0 = tr[4][0][0];
   const char* names[10] = {"QKi", "PVi", "S", "P", "QKw", "PVw", "Sld", "max", "exp", "st"};
-  const int nt = (n + 127) / 128;
+  const int nt = argc > 2 ? atoi(argv[2]) : (n + 127) / 128;
   for (int j = 0; j < nt; ++j)
     for (int t = 0; t < 2; ++t) {
       printf("j=%2d t=%d", j, t);
