@@ -94,7 +94,7 @@ CUtensorMap weight_map(const hc_weights::Layer& L, int bn, int d, int rows) {
 
 void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t n_rows,
                   const KvOut& out, cudaStream_t stream, const float* pre_stats,
-                  const int32_t* pre_flag) {
+                  const int32_t* pre_flag, const void* pre_centered) {
   if (layer < 0 || layer >= w->cfg.n_layers) fail(HC_EINVAL, "project: layer out of range");
   const auto& L = w->layers[size_t(layer)];
   if (!L.ready) fail(HC_EINVAL, "project: layer weights not set");
@@ -128,12 +128,14 @@ void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t 
     fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the hidden-state operand");
   // rows with |mean| >> sigma: K1 reads a mean-shifted copy (a no-op kernel
   // and an unused map unless the statistics raised the flag)
-  StreamScratch centered(norm && flag ? size_t(n_rows) * size_t(d) * 2 : 0, stream);
+  const bool own_center = norm && flag && !(pre_flag && pre_centered);
+  StreamScratch centered(own_center ? size_t(n_rows) * size_t(d) * 2 : 0, stream);
   AltA alt;
   if (norm && flag) {
-    HC_CUDA(launch_center_rows(d_hidden, n_rows, d, d, mean, flag, centered.ptr, stream));
-    if (!make_tmap_kmajor(&alt.map, centered.ptr, uint64_t(d), uint64_t(n_rows),
-                          uint64_t(d) * 2, abox))
+    const void* cbuf = own_center ? centered.ptr : pre_centered;
+    if (own_center)
+      HC_CUDA(launch_center_rows(d_hidden, n_rows, d, d, mean, flag, centered.ptr, stream));
+    if (!make_tmap_kmajor(&alt.map, cbuf, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2, abox))
       fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the centered operand");
     alt.flag = flag;
   }

@@ -50,6 +50,7 @@ struct Engine {
   cudaStream_t copy = nullptr;  // IO lane head: orders fetches, joins the helpers
   cudaStream_t helper[kCopyStreams - 1] = {};
   cudaStream_t aux = nullptr;   // row statistics running ahead of the compute lane
+  cudaStream_t aux2 = nullptr;  // second K1 lane of a resident restore
   bool init = false;
 };
 
@@ -62,6 +63,7 @@ Engine& engine(int dev) {
     HC_CUDA(cudaStreamCreateWithFlags(&e.copy, cudaStreamNonBlocking));
     for (auto& h : e.helper) HC_CUDA(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking));
     HC_CUDA(cudaStreamCreateWithFlags(&e.aux, cudaStreamNonBlocking));
+    HC_CUDA(cudaStreamCreateWithFlags(&e.aux2, cudaStreamNonBlocking));
     cudaMemPool_t pool;
     HC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thresh = UINT64_MAX;
@@ -612,35 +614,75 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
     DeviceGuard dg(w->device);
     cudaStream_t s = as_stream(stream);
     const int L = w->cfg.n_layers, d = w->cfg.d_hidden;
-    // every layer's rows are resident: the row statistics of layer l+1 run on
-    // a side stream while K1 projects layer l (K1 is tensor-bound and leaves
-    // HBM bandwidth and SM thread slots for the stats kernel)
+    // every layer's rows are resident: the row statistics (and the
+    // mean-shift check, launch_center_rows, into a ring of two buffers) of
+    // layer l+1 run on a side stream while K1 projects layer l (K1 is
+    // tensor-bound and leaves HBM bandwidth and SM thread slots for them)
     const bool norm = w->cfg.norm_enabled != 0;
+    const bool center = norm && ln_center_enabled();
     StreamScratch stats(norm ? size_t(L) * size_t(n_rows) * 2 * sizeof(float) : 0, s);
     StreamScratch flags(norm ? size_t(L) * sizeof(int32_t) : 0, s);
+    const size_t cbytes = size_t(n_rows) * size_t(d) * 2;
+    StreamScratch cring(center ? 2 * cbytes : 0, s);
     float* st = static_cast<float*>(stats.ptr);
     int32_t* fl = static_cast<int32_t*>(flags.ptr);
     EventPool evs(false);
-    std::vector<cudaEvent_t> ready;
-    if (norm) {
-      Engine& eng = engine(w->device);
-      HC_CUDA(cudaMemsetAsync(fl, 0, size_t(L) * sizeof(int32_t), s));
-      cudaEvent_t start = evs.get();
-      HC_CUDA(cudaEventRecord(start, s));
-      HC_CUDA(cudaStreamWaitEvent(eng.aux, start, 0));
-      for (int l = 0; l < L; ++l) {
-        float* mean = st + size_t(l) * 2 * size_t(n_rows);
+    Engine& eng = engine(w->device);
+    // the layers' K1 launches are independent: alternate two streams so the
+    // next layer's CTAs start on the SMs the current one's last wave leaves
+    // idle (HC_RESIDENT_STREAMS=1: one stream)
+    static const int lanes = [] {
+      const char* e = std::getenv("HC_RESIDENT_STREAMS");
+      return e && std::atoi(e) == 1 ? 1 : 2;
+    }();
+    cudaStream_t cs[2] = {s, eng.aux2};
+    cudaEvent_t fork = evs.get();
+    if (norm) HC_CUDA(cudaMemsetAsync(fl, 0, size_t(L) * sizeof(int32_t), s));
+    HC_CUDA(cudaEventRecord(fork, s));
+    if (norm) HC_CUDA(cudaStreamWaitEvent(eng.aux, fork, 0));
+    if (lanes == 2) HC_CUDA(cudaStreamWaitEvent(eng.aux2, fork, 0));
+    std::vector<cudaEvent_t> ready(size_t(L), nullptr), consumed(size_t(L), nullptr);
+    auto stats_of = [&](int l) {  // enqueue layer l's statistics (+ check) on aux
+      float* mean = st + size_t(l) * 2 * size_t(n_rows);
+      if (center && l >= 2) HC_CUDA(cudaStreamWaitEvent(eng.aux, consumed[size_t(l - 2)], 0));
+      if (center) {
         HC_CUDA(launch_row_stats_flagged(d_hidden_layers[l], n_rows, d, d, true, mean,
                                          mean + n_rows, fl + l, eng.aux));
-        ready.push_back(evs.get());
-        HC_CUDA(cudaEventRecord(ready.back(), eng.aux));
+        HC_CUDA(launch_center_rows(d_hidden_layers[l], n_rows, d, d, mean, fl + l,
+                                   static_cast<uint8_t*>(cring.ptr) + size_t(l & 1) * cbytes,
+                                   eng.aux));
+      } else {
+        HC_CUDA(launch_row_stats(d_hidden_layers[l], n_rows, d, d, true, mean, mean + n_rows,
+                                 eng.aux));
       }
+      ready[size_t(l)] = evs.get();
+      HC_CUDA(cudaEventRecord(ready[size_t(l)], eng.aux));
+    };
+    if (norm) {
+      stats_of(0);
+      if (L > 1) stats_of(1);
     }
     for (int l = 0; l < L; ++l) {
-      if (norm) HC_CUDA(cudaStreamWaitEvent(s, ready[size_t(l)], 0));
+      cudaStream_t c = cs[lanes == 2 ? (l & 1) : 0];
+      if (norm) HC_CUDA(cudaStreamWaitEvent(c, ready[size_t(l)], 0));
       project_rows(w, l, d_hidden_layers[l], n_rows,
-                   kv_out_pages(pages, l, d_page_table, table_stride, d_cu_seqlens, n_seqs), s,
-                   norm ? st + size_t(l) * 2 * size_t(n_rows) : nullptr, norm ? fl + l : nullptr);
+                   kv_out_pages(pages, l, d_page_table, table_stride, d_cu_seqlens, n_seqs), c,
+                   norm ? st + size_t(l) * 2 * size_t(n_rows) : nullptr,
+                   center ? fl + l : nullptr,
+                   center ? static_cast<uint8_t*>(cring.ptr) + size_t(l & 1) * cbytes : nullptr);
+      consumed[size_t(l)] = evs.get();
+      HC_CUDA(cudaEventRecord(consumed[size_t(l)], c));
+      if (norm && l + 2 < L) stats_of(l + 2);
+    }
+    if (lanes == 2) {
+      cudaEvent_t join = evs.get();
+      HC_CUDA(cudaEventRecord(join, eng.aux2));
+      HC_CUDA(cudaStreamWaitEvent(s, join, 0));
+    }
+    if (norm) {  // the stats lane's last work is ordered before the buffers are released
+      cudaEvent_t join = evs.get();
+      HC_CUDA(cudaEventRecord(join, eng.aux));
+      HC_CUDA(cudaStreamWaitEvent(s, join, 0));
     }
   });
 }

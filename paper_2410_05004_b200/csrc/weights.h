@@ -50,9 +50,11 @@ EpiArgs epi_for(const hc_weights* w, const float* colsum, const float* mean, con
 // row-statistics launch is skipped; `flag` (from launch_row_stats_flagged)
 // then enables the mean-shifted operand (the means may be adjusted in place).
 // Without them the statistics and the flag are computed here.
+// With `centered` as well, the caller has already run launch_center_rows into
+// it (n_rows x d_hidden bf16) and K1 only reads it when the flag is set.
 void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t n_rows,
                   const KvOut& out, cudaStream_t stream, const float* stats = nullptr,
-                  const int32_t* flag = nullptr);
+                  const int32_t* flag = nullptr, const void* centered = nullptr);
 
 // KvOut for a layer of a paged cache.
 KvOut kv_out_pages(const hc_kv_pages* pages, int layer, const int32_t* page_table,
