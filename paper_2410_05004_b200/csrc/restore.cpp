@@ -631,10 +631,13 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
     // the layers' K1 launches are independent: alternate two streams so the
     // next layer's CTAs start on the SMs the current one's last wave leaves
     // idle (HC_RESIDENT_STREAMS=1: one stream)
-    static const int lanes = [] {
+    // (a K1 of many waves -- a large ragged batch -- has no tail worth
+    // overlapping and its persistent CTAs are better started together)
+    static const int env_lanes = [] {
       const char* e = std::getenv("HC_RESIDENT_STREAMS");
-      return e && std::atoi(e) == 1 ? 1 : 2;
+      return e ? std::atoi(e) : 0;
     }();
+    const int lanes = env_lanes == 1 || env_lanes == 2 ? env_lanes : (n_rows <= 16384 ? 2 : 1);
     cudaStream_t cs[2] = {s, eng.aux2};
     cudaEvent_t fork = evs.get();
     if (norm) HC_CUDA(cudaMemsetAsync(fl, 0, size_t(L) * sizeof(int32_t), s));
