@@ -641,17 +641,8 @@ __device__ __forceinline__ void load8(const T* p, float (&x)[8]) {
 // var = Q/n - (S/n)^2 (the reference's two-pass double variance,
 // model.cpp:43-61, to ~1e-7 relative). FP64 only once per 8 elements: the
 // B200 FP64 / F2F.F64 rate made a per-element double accumulation the bound.
-// One warp per row, eight 16-byte loads in flight per lane, blockIdx.y
-// selects the matrix of a batch (every layer of a resident restore in one
-// launch). HBM-bound: 2 bytes per element read once.
-constexpr int kStatsMaxBatch = 128;
-struct StatsBatch {
-  const void* x[kStatsMaxBatch];
-  float* mean[kStatsMaxBatch];
-  float* rstd[kStatsMaxBatch];
-  int32_t* flag[kStatsMaxBatch];  // nullable: raised when a row needs centering
-};
-
+// One warp per row, eight 16-byte loads in flight per lane. HBM-bound: 2
+// bytes per element read once.
 template <typename T>
 __device__ __forceinline__ void row_stats_row(const T* __restrict__ r, int cols, int lane,
                                               float* mean_out, float* rstd_out, int32_t* flag) {
@@ -701,15 +692,16 @@ __device__ __forceinline__ void row_stats_row(const T* __restrict__ r, int cols,
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) row_stats_kernel(const __grid_constant__ StatsBatch b,
-                                                        int64_t rows, int cols,
-                                                        int64_t row_stride) {
+__global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ x, int64_t rows,
+                                                        int cols, int64_t row_stride,
+                                                        float* __restrict__ mean_out,
+                                                        float* __restrict__ rstd_out,
+                                                        int32_t* flag) {
   const int warps = blockDim.x >> 5;
   const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
   if (row >= rows) return;
-  const int m = blockIdx.y;
-  row_stats_row(static_cast<const T*>(b.x[m]) + row * row_stride, cols, threadIdx.x & 31,
-                b.mean[m] + row, b.rstd[m] + row, b.flag[m]);
+  row_stats_row(x + row * row_stride, cols, threadIdx.x & 31, mean_out + row, rstd_out + row,
+                flag);
 }
 
 // launch_center_rows: one warp per row, 16-byte vectors; a no-op (every CTA
@@ -1030,41 +1022,25 @@ cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, in
                                 split_acc);
 }
 
-cudaError_t launch_row_stats_batch(const void* const* x, int n_mats, int64_t rows, int cols,
-                                   int64_t row_stride, bool bf16_in, float* const* mean,
-                                   float* const* rstd, cudaStream_t stream,
-                                   int32_t* const* flags) {
-  if (rows <= 0 || n_mats <= 0) return cudaSuccess;
+cudaError_t launch_row_stats_flagged(const void* x, int64_t rows, int cols, int64_t row_stride,
+                                     bool bf16_in, float* mean, float* rstd, int32_t* flag,
+                                     cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
   const int threads = 256, per_block = threads / 32;
-  for (int m0 = 0; m0 < n_mats; m0 += kStatsMaxBatch) {
-    const int nb = std::min(kStatsMaxBatch, n_mats - m0);
-    StatsBatch b;
-    for (int i = 0; i < nb; ++i) {
-      b.x[i] = x[m0 + i];
-      b.mean[i] = mean[m0 + i];
-      b.rstd[i] = rstd[m0 + i];
-      b.flag[i] = flags ? flags[m0 + i] : nullptr;
-    }
-    const dim3 grid(unsigned((rows + per_block - 1) / per_block), unsigned(nb));
-    if (bf16_in)
-      row_stats_kernel<__nv_bfloat16><<<grid, threads, 0, stream>>>(b, rows, cols, row_stride);
-    else
-      row_stats_kernel<__half><<<grid, threads, 0, stream>>>(b, rows, cols, row_stride);
-  }
+  const unsigned grid = unsigned((rows + per_block - 1) / per_block);
+  if (bf16_in)
+    row_stats_kernel<__nv_bfloat16><<<grid, threads, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(x), rows, cols, row_stride, mean, rstd, flag);
+  else
+    row_stats_kernel<__half><<<grid, threads, 0, stream>>>(static_cast<const __half*>(x), rows,
+                                                          cols, row_stride, mean, rstd, flag);
   return cudaGetLastError();
 }
 
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,
                              bool bf16_in, float* mean, float* rstd, cudaStream_t stream) {
-  return launch_row_stats_batch(&x, 1, rows, cols, row_stride, bf16_in, &mean, &rstd, stream,
-                                nullptr);
-}
-
-cudaError_t launch_row_stats_flagged(const void* x, int64_t rows, int cols, int64_t row_stride,
-                                     bool bf16_in, float* mean, float* rstd, int32_t* flag,
-                                     cudaStream_t stream) {
-  return launch_row_stats_batch(&x, 1, rows, cols, row_stride, bf16_in, &mean, &rstd, stream,
-                                &flag);
+  return launch_row_stats_flagged(x, rows, cols, row_stride, bf16_in, mean, rstd, nullptr,
+                                  stream);
 }
 
 bool ln_center_enabled() {

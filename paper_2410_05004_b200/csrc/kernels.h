@@ -187,30 +187,26 @@ cudaError_t launch_append_rows(const void* step_rows, int rows_in_step, int h0, 
 cudaError_t launch_convert_to_bf16(const void* src, int src_dtype, void* dst, int64_t n,
                                    cudaStream_t stream);
 
-// Row statistics for the LayerNorm fold: mean and 1/sqrt(var+1e-5) per row,
-// mean/var accumulated in double like the reference (model.cpp:43-61).
+// Row statistics for the LayerNorm fold: mean and 1/sqrt(var+1e-5) per row
+// (the reference's double statistics, model.cpp:43-61, to ~1e-7).
 // Rows whose |mean| exceeds this many standard deviations make the LayerNorm
 // fold lose precision (H W^T ~ mean * colsum(W) cancels in fp32): the row
 // statistics raise a per-matrix flag and the GEMM reads a shifted copy.
 constexpr float kCenterRatio = 16.0f;
 
-// Row statistics of n_mats matrices of identical shape in one launch;
-// flags[i] (nullable, zeroed by the caller) is set when a row of matrix i
-// has |mean| * rstd > kCenterRatio.
+// Row statistics; flag (nullable, zeroed by the caller) is set when a row has
+// |mean| * rstd > kCenterRatio.
 cudaError_t launch_row_stats_flagged(const void* x, int64_t rows, int cols, int64_t row_stride,
                                      bool bf16_in, float* mean, float* rstd, int32_t* flag,
                                      cudaStream_t stream);
+// HC_LN_CENTER=0 disables the mean shift (A/B measurements only).
+bool ln_center_enabled();
 // When *flag (device) is set: out[r] = bf16(x[r] - c_r), c_r = bf16(mean[r])
 // (exact for |x - c| small against c, Sterbenz), and mean[r] -= c_r in place,
 // so the LayerNorm fold over `out` is well conditioned. A no-op otherwise.
-bool ln_center_enabled();
 cudaError_t launch_center_rows(const void* x, int64_t rows, int cols, int64_t row_stride,
                                float* mean, const int32_t* flag, void* out, cudaStream_t stream);
-// Row statistics of n_mats matrices of identical shape in one launch.
-cudaError_t launch_row_stats_batch(const void* const* x, int n_mats, int64_t rows, int cols,
-                                   int64_t row_stride, bool bf16_in, float* const* mean,
-                                   float* const* rstd, cudaStream_t stream,
-                                   int32_t* const* flags = nullptr);
+// The same without the flag.
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,
                              bool bf16_in, float* mean, float* rstd, cudaStream_t stream);
 
