@@ -199,7 +199,10 @@ def run_reference_arm(args, cfg, rank, world):
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * n / v, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "tokens": n, "layers": L},
+            "config": {"workload": args.config + " (configs[1])" if args.config == "llama2-7b"
+                       else args.config, "tokens": n, "layers": L,
+                       "note": "the reference's project_hidden_to_kv on the host cores, "
+                               "sampled and extrapolated to the whole context"},
             "cpu_baseline": dict(desc, value=v, unit="tokens/s"),
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
