@@ -262,6 +262,13 @@ def run_ours(args, cfg, rank, world):
         # the planner splits between hidden states and KV offload only
         prof.c_token = 1e9
     plan, plan_ms = H.plan_three_way(prof, L)
+    # B200 extension: split the first hidden layer between the recompute
+    # prefix and the link where that balances the two lanes
+    # (opt-in, HC_SPLIT=1: interleaved A/B runs on B200 did not separate it
+    # from run-to-run noise, scripts/ab_split.sh)
+    split, split_ms = 0, plan_ms
+    if full and os.environ.get("HC_SPLIT") == "1":
+        split, split_ms = H.plan_token_split(prof, plan, n, L)
     all_h = H.RestorationPlan.make(L, L, H.Complement.NONE)
     all_kv = H.RestorationPlan.make(L, 0, H.Complement.KV_OFFLOAD)
 
@@ -288,11 +295,12 @@ def run_ours(args, cfg, rank, world):
         check(lib().hc_restore_resident(w._h, hptrs, n, None, 1, C.byref(kv.desc),
                                         table.data_ptr(), 0, stream))
 
-    opts = capi.RestoreOptsC(0, 0)
+    opts = capi.RestoreOptsC(0, 0, 0)
+    opts_plan = capi.RestoreOptsC(0, 0, split)
     host_ck = torch.empty(16 * d_kv, dtype=torch.bfloat16, pin_memory=True)
 
-    def restore_step(sid, p):
-        check(lib().hc_restore(store._h, sid, w._h, C.byref(p._c), C.byref(opts),
+    def restore_step(sid, p, o=opts):
+        check(lib().hc_restore(store._h, sid, w._h, C.byref(p._c), C.byref(o),
                                C.byref(kv.desc), table.data_ptr(), stream, None))
         # device->host read of the step's result: 16 restored K rows of the last layer
         host_ck.copy_(kv.k[L - 1].view(-1)[: 16 * d_kv], non_blocking=True)
@@ -316,7 +324,7 @@ def run_ours(args, cfg, rank, world):
     sid_allh = b"hcache" if plan.serialize() == all_h.serialize() else b"all_hidden"
 
     def e2e_step():
-        restore_step(sid_plan, plan)
+        restore_step(sid_plan, plan, opts_plan)
 
     def timed(fn, steps):
         torch.cuda.synchronize()
@@ -349,7 +357,7 @@ def run_ours(args, cfg, rank, world):
     ms_kv = timed(lambda: restore_step(b"kv_offload", all_kv), max(3, args.steps // 2))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    restore_step(sid_plan, plan)
+    restore_step(sid_plan, plan, opts_plan)
     enqueue_ms = (time.perf_counter() - t0) * 1e3  # host time to enqueue one restore
     torch.cuda.synchronize()
     ms_re = None
@@ -367,13 +375,15 @@ def run_ours(args, cfg, rank, world):
     h2d = H.measure_h2d(256 << 20, 5, dev)
 
     # restore timeline of one e2e step (fill / bubble / lane busy)
-    res = H.restore(store, sid_plan.decode(), w, plan, H.ThrottleConfig(0, True), kv, table)
+    res = H.restore(store, sid_plan.decode(), w, plan, H.ThrottleConfig(0, True, split), kv,
+                    table)
     tl = res.timeline
     if os.environ.get("HC_DUMP_TIMELINE"):
         with open(os.environ["HC_DUMP_TIMELINE"], "w") as f:
             f.write(tl.export_text())
     h_bytes = L * n * d * 2
-    h_bytes_plan = plan.l_h * n * d * 2 + plan.l_kv * n * 2 * d_kv * 2 + (4 * n if plan.l_re else 0)
+    h_bytes_plan = (plan.l_h * n - split) * d * 2 + plan.l_kv * n * 2 * d_kv * 2 + \
+        (4 * n if plan.l_re or split else 0)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tpath):
@@ -395,7 +405,8 @@ def run_ours(args, cfg, rank, world):
                    else args.config, "layers": L, "d_hidden": d, "heads": heads,
                    "kv_heads": kvh, "tokens": n, "page_size": page,
                    "l2": "inputs larger than L2 (1 GiB hidden + 2 GiB weights per step)",
-                   "plan": plan.serialize(), "planner": "hc_plan_three_way on hc_profile"},
+                   "plan": plan.serialize(), "split_tokens": split,
+                   "planner": "hc_plan_three_way + hc_plan_token_split on hc_profile"},
         "restore_latency_ms": {"resident": ms_resident, "e2e": ms_e2e, "e2e_wall": wall_e2e,
                                "all_hidden": ms_allh, "kv_offload": ms_kv,
                                "host_enqueue": enqueue_ms,
@@ -406,7 +417,9 @@ def run_ours(args, cfg, rank, world):
         "planner": {"profiled": {"io_h_ms": prof.io_h * 1e3, "io_kv_ms": prof.io_kv * 1e3,
                                  "c_h_ms": prof.c_h * 1e3, "c_token_ms": prof.c_token * 1e3},
                     "plan": plan.serialize(),
-                    "predicted_ms": plan_ms * 1e3 if plan_ms else None},
+                    "predicted_ms": plan_ms * 1e3 if plan_ms else None,
+                    "split_tokens": split,
+                    "predicted_with_split_ms": split_ms * 1e3 if split_ms else None},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h_bytes_plan,
                 "d2h_bytes_per_step": int(host_ck.numel() * 2),
                 "roofline": {"bound": "pcie", "unit": "GB/s",

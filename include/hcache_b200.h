@@ -198,6 +198,11 @@ hc_status hc_brute_force_plan(const hc_timings* t, hc_plan* out);
  * bubble-free under the executor's real buffer bound. */
 hc_status hc_plan_three_way(const hc_timings* t, int32_t prefetch_depth, hc_plan* out,
                             double* makespan_out);
+/* B200 extension: the token split of the plan's first layer after the
+ * recompute prefix (hc_restore_opts.split_tokens) that minimises the pipeline
+ * makespan; 0 when no split helps or the layer is not HIDDEN. */
+hc_status hc_plan_token_split(const hc_timings* t, int32_t prefetch_depth, const hc_plan* plan,
+                              int32_t n_tokens, int32_t* split_out, double* makespan_out);
 
 /* --------------------------------------------------------------- timeline */
 typedef enum hc_lane { HC_LANE_IO = 0, HC_LANE_COMPUTE = 1 } hc_lane;
@@ -357,7 +362,12 @@ double hc_store_simulated_read_seconds_tokens(hc_store* s, int32_t n_tokens, int
 typedef struct hc_restore_opts {
   int32_t prefetch_depth; /* staged hidden layers in flight beyond the one in use (>=1) */
   int32_t timeline;       /* 1: record per-layer CUDA events into the timeline */
-  int32_t pad_[2];
+  /* B200 extension (0 = off): the first layer after the RECOMPUTE prefix must be
+   * HIDDEN; its first split_tokens tokens (a multiple of 64) are recomputed
+   * with the prefix and only tokens [split_tokens, n) are fetched and
+   * projected (hc_plan_token_split picks the value that balances the lanes). */
+  int32_t split_tokens;
+  int32_t pad_;
 } hc_restore_opts;
 
 /* restore (restore.hpp:40-42): executes the plan over a finalized session

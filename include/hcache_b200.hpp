@@ -517,7 +517,7 @@ inline RestoreResult restore(StorageManager& store, const std::string& session_i
                              const DeviceWeights& w, const RestorationPlan& plan,
                              const ThrottleConfig& throttle, const KvPages& pages,
                              const int32_t* d_page_table, void* stream = nullptr) {
-  hc_restore_opts o{throttle.prefetch_depth, throttle.timeline ? 1 : 0, {0, 0}};
+  hc_restore_opts o{throttle.prefetch_depth, throttle.timeline ? 1 : 0, 0, 0};
   std::vector<hc_timeline> tl(1);
   check(hc_restore(store.get(), session_id.c_str(), w.get(), &plan.raw, &o, &pages.desc,
                    d_page_table, stream, throttle.timeline ? tl.data() : nullptr));

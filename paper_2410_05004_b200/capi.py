@@ -88,7 +88,7 @@ class ManifestC(C.Structure):
 
 
 class RestoreOptsC(C.Structure):
-    _fields_ = [("prefetch_depth", i32), ("timeline", i32), ("pad_", i32 * 2)]
+    _fields_ = [("prefetch_depth", i32), ("timeline", i32), ("split_tokens", i32), ("pad_", i32)]
 
 
 class RequestC(C.Structure):
@@ -143,6 +143,7 @@ _PROTOS = {
     "hc_makespan": (i32, [P(PlanC), P(TimingsC), P(f64)]),
     "hc_brute_force_plan": (i32, [P(TimingsC), P(PlanC)]),
     "hc_plan_three_way": (i32, [P(TimingsC), i32, P(PlanC), P(f64)]),
+    "hc_plan_token_split": (i32, [P(TimingsC), i32, P(PlanC), i32, P(i32), P(f64)]),
     "hc_timeline_lane_busy": (f64, [P(TimelineC), i32]),
     "hc_timeline_bubble_fraction": (i32, [P(TimelineC), P(f64)]),
     "hc_simulate_pipeline": (i32, [P(PipelineJobC), i32, i32, P(TimelineC)]),

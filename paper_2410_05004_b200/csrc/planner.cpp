@@ -364,6 +364,59 @@ hc_status hc_plan_three_way(const hc_timings* t, int32_t prefetch_depth, hc_plan
   });
 }
 
+hc_status hc_plan_token_split(const hc_timings* t, int32_t prefetch_depth, const hc_plan* plan,
+                              int32_t n_tokens, int32_t* split_out, double* makespan_out) {
+  return guard([&] {
+    check_timings(t);
+    if (!plan || !split_out) fail(HC_EINVAL, "plan_token_split: null argument");
+    if (prefetch_depth < 1) fail(HC_EINVAL, "prefetch_depth < 1");
+    if (n_tokens < 1) fail(HC_EINVAL, "plan_token_split: n_tokens < 1");
+    if (plan->n_layers != t->n_layers) fail(HC_EINVAL, "plan_token_split: layer count mismatch");
+    const auto base = plan_jobs(plan, t);
+    // the first job after the recompute prefix, if it is the HIDDEN layer l_re
+    size_t at = 0;
+    while (at < base.size() && base[at].compute_kind == HC_EV_RECOMPUTE && !base[at].has_io) ++at;
+    const bool ok = at < base.size() && base[at].io_kind == HC_EV_FETCH_HIDDEN &&
+                    base[at].layer == int(at);
+    hc_timeline* tl = new hc_timeline;
+    int best_s = 0;
+    double best = 0;
+    try {
+      simulate(base.data(), int(base.size()), prefetch_depth, tl);
+      best = tl->total_s;
+      // split s: the layer's first s tokens join the prefix (recompute cost
+      // linear in s -- the attention part is sub-linear, so this errs high),
+      // the rest is fetched and projected
+      for (int sp = HC_CHUNK_TOKENS; ok && sp < n_tokens; sp += HC_CHUNK_TOKENS) {
+        const double x = double(sp) / double(n_tokens);
+        std::vector<hc_pipeline_job> jobs(base.begin(), base.begin() + long(at));
+        hc_pipeline_job re{};
+        re.layer = base[at].layer;
+        re.has_compute = 1;
+        re.compute_s = t->c_token * x;
+        re.compute_kind = HC_EV_RECOMPUTE;
+        jobs.push_back(re);
+        hc_pipeline_job h = base[at];
+        h.io_s *= 1.0 - x;
+        h.compute_s *= 1.0 - x;
+        jobs.push_back(h);
+        jobs.insert(jobs.end(), base.begin() + long(at) + 1, base.end());
+        simulate(jobs.data(), int(jobs.size()), prefetch_depth, tl);
+        if (tl->total_s < best * (1 - 1e-9)) {
+          best = tl->total_s;
+          best_s = sp;
+        }
+      }
+    } catch (...) {
+      delete tl;
+      throw;
+    }
+    delete tl;
+    *split_out = best_s;
+    if (makespan_out) *makespan_out = best;
+  });
+}
+
 double hc_timeline_lane_busy(const hc_timeline* tl, int32_t lane) {
   // Timeline::lane_busy (pipeline.cpp:9-14)
   if (!tl) return 0;

@@ -112,11 +112,14 @@ cudaError_t attention(const void* q, int n, int n_heads, int n_kv_heads, int dh,
 void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int lb, int le,
                   const hc_kv_pages* pages, const int32_t* d_page_table, cudaStream_t stream,
                   const std::function<void(int, bool)>& hook, void* d_layer_inputs,
-                  int32_t* next_token, const SeqBatch& sb, int32_t* d_next_tokens) {
+                  int32_t* next_token, const SeqBatch& sb, int32_t* d_next_tokens,
+                  int64_t n_last = 0) {
   if (!w || !d_tokens || !pages || !d_page_table) fail(HC_EINVAL, "prefill_layers: null argument");
   const auto& c = w->cfg;
   if (lb < 0 || le > c.n_layers || lb > le) fail(HC_EINVAL, "prefill_layers: bad layer range");
   if (n < 1) fail(HC_EINVAL, "forward: empty sequence");
+  if (n_last < 0 || n_last > n || (n_last > 0 && (sb.cu || next_token || d_next_tokens)))
+    fail(HC_EINVAL, "forward: bad last-layer row count");
   if (!sb.cu && n > c.max_seq) fail(HC_EINVAL, "forward: sequence exceeds max_seq");
   if (!w->embedding) fail(HC_EINVAL, "prefill_layers: embedding not set");
   if (w->d_kv != w->d_kv_all) fail(HC_EINVAL, "prefill_layers: needs all KV heads on this GPU");
@@ -143,9 +146,9 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
   pm.lap(0);
   HC_CUDA(launch_embed(d_tokens, n, w->embedding, d, x, xb_buf.ptr, stream));
   const int abox = gemm_a_box(n);
-  const CUtensorMap tm_xb = tmap(xb_buf.ptr, d, n, abox);
-  const CUtensorMap tm_mix = tmap(mix_buf.ptr, d, n, abox);
-  const CUtensorMap tm_h1 = tmap(h1_buf.ptr, dffn, n, abox);
+  CUtensorMap tm_xb = tmap(xb_buf.ptr, d, n, abox);
+  CUtensorMap tm_mix = tmap(mix_buf.ptr, d, n, abox);
+  CUtensorMap tm_h1 = tmap(h1_buf.ptr, dffn, n, abox);
   // LayerNorm statistics of xb + the mean-shifted operand for rows with
   // |mean| >> sigma (launch_center_rows; a no-op unless flagged)
   AltA alt;
@@ -156,33 +159,47 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     alt.flag = flag;
     altp = &alt;
   }
-  auto ln_stats = [&]() {
+  auto ln_stats = [&](int64_t rows) {
     if (!center) {
-      HC_CUDA(launch_row_stats(xb_buf.ptr, n, d, d, true, mean, rstd, stream));
+      HC_CUDA(launch_row_stats(xb_buf.ptr, rows, d, d, true, mean, rstd, stream));
       return;
     }
     HC_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), stream));
-    HC_CUDA(launch_row_stats_flagged(xb_buf.ptr, n, d, d, true, mean, rstd, flag, stream));
-    HC_CUDA(launch_center_rows(xb_buf.ptr, n, d, d, mean, flag, xc_buf.ptr, stream));
+    HC_CUDA(launch_row_stats_flagged(xb_buf.ptr, rows, d, d, true, mean, rstd, flag, stream));
+    HC_CUDA(launch_center_rows(xb_buf.ptr, rows, d, d, mean, flag, xc_buf.ptr, stream));
   };
   // K/V: the exact path (restores must reproduce these K/V bit for bit); the
   // other projections may split K when n is decode-sized
-  const int bn_kv = pick_bn(n, 2 * w->d_kv_all, sms), bn_d = gemm_pick_bn_skinny(n, d, sms),
-            bn_f = gemm_pick_bn_skinny(n, dffn, sms);
+  int bn_kv = pick_bn(n, 2 * w->d_kv_all, sms), bn_d = gemm_pick_bn_skinny(n, d, sms),
+      bn_f = gemm_pick_bn_skinny(n, dffn, sms);
   pm.lap(1);
   for (int L = lb; L < le; ++L) {
     const auto& lw = w->layers[size_t(L)];
+    // rows of this layer: all n, or only the first n_last tokens of the last
+    // layer (a restore recomputing part of its first hidden layer)
+    const int64_t m = (L == le - 1 && n_last > 0) ? n_last : n;
+    if (m != n) {
+      // the GEMMs of a shorter last layer pick their own tiles and A boxes
+      const int ab = gemm_a_box(m);
+      tm_xb = tmap(xb_buf.ptr, d, n, ab);
+      tm_mix = tmap(mix_buf.ptr, d, n, ab);
+      tm_h1 = tmap(h1_buf.ptr, dffn, n, ab);
+      if (center) alt.map = tmap(xc_buf.ptr, d, n, ab);
+      bn_kv = pick_bn(m, 2 * w->d_kv_all, sms);
+      bn_d = gemm_pick_bn_skinny(m, d, sms);
+      bn_f = gemm_pick_bn_skinny(m, dffn, sms);
+    }
     hook(L, true);
     if (d_layer_inputs)
       HC_CUDA(cudaMemcpyAsync(static_cast<char*>(d_layer_inputs) + size_t(L) * nd * 2, xb_buf.ptr,
                               nd * 2, cudaMemcpyDeviceToDevice, stream));
     // attention block: LN(x) -> K/V (paged) and Q
     pm.lap(2);
-    ln_stats();
+    ln_stats(m);
     pm.lap(3);
     KvOut kv = kv_out_pages(pages, L, d_page_table, sb.table_stride, sb.cu, sb.n_seqs);
     kv.seq_start = sb.seq_start;
-    HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wkv_all, d, 2 * w->d_kv_all, bn_kv), bn_kv, int(n),
+    HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wkv_all, d, 2 * w->d_kv_all, bn_kv), bn_kv, int(m),
                               2 * w->d_kv_all, d, true, kv, epi_for(w, lw.colsum_all, mean, rstd),
                               sms, stream, false, altp));
     pm.lap(4);
@@ -193,7 +210,7 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     qo.cu_seqlens = sb.cu;
     qo.n_seqs = sb.cu ? sb.n_seqs : 1;
     qo.seq_start = sb.seq_start;
-    HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wq, d, d, bn_d), bn_d, int(n), d, d, true, qo,
+    HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wq, d, d, bn_d), bn_d, int(m), d, d, true, qo,
                               epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true, altp));
     pm.lap(5);
     if (sb.cu && sb.from_zero && attention_tc_ok(kv))
@@ -206,18 +223,18 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
                                       c.n_heads, c.n_kv_heads, w->d_head, kv, mix_buf.ptr,
                                       stream));
     else
-      HC_CUDA(attention(q_buf.ptr, int(n), c.n_heads, c.n_kv_heads, w->d_head, kv,
+      HC_CUDA(attention(q_buf.ptr, int(m), c.n_heads, c.n_kv_heads, w->d_head, kv,
                         int64_t(pages->num_pages) * pages->page_size, mix_buf.ptr, stream));
     pm.lap(6);
     GemmOut resid;
     resid.x = x;
     resid.xb = xb_buf.ptr;
     resid.ldo = d;
-    HC_CUDA(launch_gemm_dense(tm_mix, wmap(lw.wo, d, d, bn_d), bn_d, kEpiResid, int(n), d, d,
+    HC_CUDA(launch_gemm_dense(tm_mix, wmap(lw.wo, d, d, bn_d), bn_d, kEpiResid, int(m), d, d,
                               resid, EpiArgs{}, sms, stream, true));
     pm.lap(7);
     // FFN block (ffn_forward, model.cpp:290-303)
-    ln_stats();
+    ln_stats(m);
     pm.lap(8);
     GemmOut g1;
     g1.xb = h1_buf.ptr;
@@ -228,10 +245,10 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
       fold.row_rstd = rstd;
       fold.colsum = lw.colsum_fc1;
     }
-    HC_CUDA(launch_gemm_dense(tm_xb, wmap(lw.fc1, d, dffn, bn_f), bn_f, kEpiGelu, int(n), dffn,
+    HC_CUDA(launch_gemm_dense(tm_xb, wmap(lw.fc1, d, dffn, bn_f), bn_f, kEpiGelu, int(m), dffn,
                               d, g1, fold, sms, stream, true, altp));
     pm.lap(9);
-    HC_CUDA(launch_gemm_dense(tm_h1, wmap(lw.fc2, dffn, d, bn_d), bn_d, kEpiResid, int(n), d,
+    HC_CUDA(launch_gemm_dense(tm_h1, wmap(lw.fc2, dffn, d, bn_d), bn_d, kEpiResid, int(m), d,
                               dffn, resid, EpiArgs{}, sms, stream, true));
     hook(L, false);
     pm.lap(10);
@@ -273,9 +290,9 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
 void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int lb, int le,
                          const hc_kv_pages* pages, const int32_t* d_page_table,
                          cudaStream_t stream, const std::function<void(int, bool)>& hook,
-                         void* d_layer_inputs, int32_t* next_token) {
+                         void* d_layer_inputs, int32_t* next_token, int64_t n_last) {
   forward_impl(w, d_tokens, n, lb, le, pages, d_page_table, stream, hook, d_layer_inputs,
-               next_token, SeqBatch{}, nullptr);
+               next_token, SeqBatch{}, nullptr, n_last);
 }
 
 void forward_batch_dev(const hc_weights* w, const int32_t* d_tokens, int n_seqs, int64_t total,

@@ -9,14 +9,16 @@
 namespace hc {
 
 // prefill_layers (proj/src/model.cpp:349-356): embed d_tokens, run layers
-// [lb, le) from position 0, writing each layer's K/V into the pages.
+// [lb, le) from position 0, writing each layer's K/V into the pages. With
+// n_last in (0, n) the last layer runs only for the first n_last tokens.
 // hook(layer, start) is called on the host around each layer's enqueue (for
 // CUDA-event timelines). d_layer_inputs (optional, L x n x d bf16) receives
 // each layer's input hidden state (prefill's layer_inputs, model.cpp:316).
 void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int lb, int le,
                          const hc_kv_pages* pages, const int32_t* d_page_table,
                          cudaStream_t stream, const std::function<void(int, bool)>& hook,
-                         void* d_layer_inputs = nullptr, int32_t* next_token = nullptr);
+                         void* d_layer_inputs = nullptr, int32_t* next_token = nullptr,
+                         int64_t n_last = 0);
 
 // Sequences of a batched forward: nullptr cu = one sequence from position 0.
 struct SeqBatch {

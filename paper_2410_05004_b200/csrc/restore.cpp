@@ -295,6 +295,18 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
   }
   if (n_kv && (m.d_kv != w->d_kv || w->d_kv != w->d_kv_all))
     fail(HC_EINVAL, std::string(who) + ": KV-offload layers need all KV heads on this GPU");
+  // token split of the first layer after the recompute prefix (layer n_re,
+  // HIDDEN): its first `split` tokens are recomputed with the prefix and only
+  // tokens [split, n) are fetched and projected -- a continuous knob that
+  // balances the IO and compute lanes between whole-layer plans
+  const int split = opts ? opts->split_tokens : 0;
+  if (split != 0) {
+    if (batch) bad("split_tokens applies to a single session");
+    if (split < 0 || split >= n || split % HC_CHUNK_TOKENS != 0)
+      bad("split_tokens must be a multiple of 64 below the session's token count");
+    if (n_re >= plan.n_layers || plan.layer_assignment[n_re] != HC_METHOD_HIDDEN)
+      bad("split_tokens needs a HIDDEN layer right after the recompute prefix");
+  }
 
   const size_t h_row = size_t(m.d_hidden) * size_t(eb), kv_row = size_t(2 * m.d_kv) * size_t(eb);
   const size_t h_bytes = size_t(n) * h_row;
@@ -326,8 +338,9 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
   }
 
   // token ids for the RECOMPUTE prefix: async H2D from the store's pinned copies
-  StreamScratch d_tok(n_re ? sizeof(int32_t) * size_t(n) : 0, stream);
-  if (n_re) {
+  const bool prefix = n_re > 0 || split > 0;
+  StreamScratch d_tok(prefix ? sizeof(int32_t) * size_t(n) : 0, stream);
+  if (prefix) {
     for (int i = 0; i < n_sessions; ++i) {
       int64_t n_ids = 0;
       const int32_t* toks = store.pinned_tokens(sids[i], &n_ids);
@@ -352,6 +365,7 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
   struct Fetch {
     LayerJob job;
     bool hid;
+    int row0 = 0;  // first token fetched (the split layer: split)
     int slot;
     bool reuses_slot;  // an earlier fetch of this kind used the slot
     uint8_t* buf;
@@ -370,12 +384,13 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
     f.reuses_slot = kind_idx >= (f.hid ? nbuf_h : nbuf_kv);
     f.buf = static_cast<uint8_t*>(f.hid ? ring_h.ptr : ring_kv.ptr) +
             (f.hid ? h_bytes : kv_bytes) * size_t(f.slot);
+    if (split && j.layer == n_re) f.row0 = split;
     for (int i = 0; i < n_sessions; ++i) {
       size_t got = 0;
-      auto segs = store.gather_plan(sids[i], j.layer, f.hid ? HC_STATE_HIDDEN : HC_STATE_KV, 0, -1,
-                                    &got);  // HC_ENOENT if missing
+      auto segs = store.gather_plan(sids[i], j.layer, f.hid ? HC_STATE_HIDDEN : HC_STATE_KV,
+                                    f.row0, -1, &got);  // HC_ENOENT if missing
       const size_t row = f.hid ? h_row : kv_row;
-      if (got != size_t(ms[size_t(i)].n_tokens) * row)
+      if (got != size_t(ms[size_t(i)].n_tokens - f.row0) * row)
         fail(HC_ERUNTIME, std::string(who) + ": layer " + std::to_string(j.layer) +
                               " has a short token count");
       for (auto& g : segs) {
@@ -416,7 +431,7 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
 
   // RECOMPUTE prefix first on the compute lane (restore.cpp:177-182); the IO
   // lane prefetches hidden layers meanwhile.
-  if (n_re) {
+  if (prefix) {
     std::vector<cudaEvent_t> marks;
     auto hook = [&](int layer, bool start) {
       if (!timed) return;
@@ -430,8 +445,8 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
                            d_cu, d_starts, pages, d_page_tables, table_stride, 0, n_re, stream,
                            hook);
     else
-      prefill_layers_impl(w, static_cast<const int32_t*>(d_tok.ptr), n, 0, n_re, pages,
-                          d_page_tables, stream, hook);
+      prefill_layers_impl(w, static_cast<const int32_t*>(d_tok.ptr), n, 0, n_re + (split ? 1 : 0),
+                          pages, d_page_tables, stream, hook, nullptr, nullptr, split);
   }
 
   issue_fetches(fetches.size());
@@ -447,16 +462,18 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
                                      n_sessions)
                       : kv_out_pages(pages, f.job.layer, d_page_tables, 0, nullptr, 1);
     const void* rows = f.buf;
+    const int64_t rows_n = n - f.row0;
+    out.start_pos = f.row0;
     if (!native) {
-      const int64_t elems = n * (f.hid ? m.d_hidden : 2 * m.d_kv);
+      const int64_t elems = rows_n * (f.hid ? m.d_hidden : 2 * m.d_kv);
       void* dst = m.dtype == HC_DTYPE_F32 ? conv.ptr : f.buf;
       HC_CUDA(launch_convert_to_bf16(f.buf, m.dtype, dst, elems, stream));
       rows = dst;
     }
     if (f.hid) {
-      project_rows(w, f.job.layer, rows, n, out, stream);
+      project_rows(w, f.job.layer, rows, rows_n, out, stream);
     } else {
-      HC_CUDA(launch_kv_scatter(rows, n, out, stream));
+      HC_CUDA(launch_kv_scatter(rows, rows_n, out, stream));
     }
     cudaEvent_t done = evp.get();
     HC_CUDA(cudaEventRecord(done, stream));

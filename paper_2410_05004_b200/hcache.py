@@ -152,6 +152,18 @@ def plan_three_way(t: ProfiledTimings, prefetch_depth: int = 1):
     return RestorationPlan(p), out.value
 
 
+def plan_token_split(t: ProfiledTimings, plan: "RestorationPlan", n_tokens: int,
+                     prefetch_depth: int = 1):
+    """B200 extension: (split_tokens, makespan) -- how many tokens of the
+    plan's first layer after the recompute prefix to recompute instead of
+    fetching (ThrottleConfig.split_tokens); 0 when no split helps."""
+    sp = C.c_int32()
+    out = C.c_double()
+    check(lib().hc_plan_token_split(C.byref(t._c()), prefetch_depth, C.byref(plan._c), n_tokens,
+                                    C.byref(sp), C.byref(out)))
+    return sp.value, out.value
+
+
 # -------------------------------------------------------------------- timeline
 @dataclass
 class TimelineEvent:
@@ -562,9 +574,10 @@ class ThrottleConfig:
     staged hidden layers (0 = auto: stage every hidden layer within 8 GiB)."""
     prefetch_depth: int = 0
     timeline: bool = True
+    split_tokens: int = 0  # B200 extension (hc_restore_opts.split_tokens)
 
     def _c(self):
-        return capi.RestoreOptsC(self.prefetch_depth, int(self.timeline))
+        return capi.RestoreOptsC(self.prefetch_depth, int(self.timeline), self.split_tokens)
 
 
 @dataclass

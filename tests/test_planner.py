@@ -236,3 +236,26 @@ def test_end_to_end_ratio_criterion6():
         assert 1.33 <= r <= 2.66
         if devices == 4:
             assert L * t.c_token / H.makespan(H.plan(t), t) >= 5.0
+
+
+def test_token_split_balances_the_lanes():
+    """B200 extension: splitting the first hidden layer between the recompute
+    prefix and the IO lane never loses and, at a lane imbalance smaller than
+    one layer, wins (7B-like timings)."""
+    t = T(0.61e-3, 1.21e-3, 0.20e-3, 1.31e-3, 32)
+    for l_re in (0, 6, 7, 8):
+        p = H.RestorationPlan.make(32, 32 - l_re, C.RECOMPUTE if l_re else C.NONE)
+        base = H.simulate_pipeline(_jobs(p, t.io_h, t.io_kv, t.c_h, t.c_token), 32).total_s
+        s, ms = H.plan_token_split(t, p, 4096, 32)
+        assert s % 64 == 0 and 0 <= s < 4096
+        assert ms <= base + 1e-12
+    p7 = H.RestorationPlan.make(32, 25, C.RECOMPUTE)
+    s, ms = H.plan_token_split(t, p7, 4096, 32)
+    best_whole = min(H.simulate_pipeline(_jobs(H.RestorationPlan.make(32, 32 - r, C.RECOMPUTE if r
+                                                                       else C.NONE),
+                                               t.io_h, t.io_kv, t.c_h, t.c_token), 32).total_s
+                     for r in range(0, 12))
+    assert s > 0 and ms < best_whole
+    # no HIDDEN layer right after the prefix (KV-offload-only plan): no split
+    pk = H.RestorationPlan.make(32, 0, C.KV_OFFLOAD)
+    assert H.plan_token_split(t, pk, 4096, 32)[0] == 0

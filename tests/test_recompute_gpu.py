@@ -310,3 +310,62 @@ def test_ragged_prefill_batch_equals_single_prefills(cuda):
                 for a, b in ((k, k1), (v, v1), (x, x1)):
                     assert norm_err(a.float().cpu().numpy(), b.float().cpu().numpy()) < 1e-2
         assert 0 <= int(nxt[s]) < cfg.vocab_size
+
+
+@pytest.mark.parametrize("plan_name,split", [("4H", 320), ("1RE+3H", 64), ("1RE+3H", 704),
+                                             ("1RE+2H+1KV", 448)])
+def test_split_layer_restore_is_lossless_vs_gpu_prefill(cuda, plan_name, split):
+    """B200 extension hc_restore_opts.split_tokens: the first layer after the
+    recompute prefix recomputes its first `split` tokens and projects only the
+    rest from hidden states; the restored pages still equal the prefill's."""
+    import torch
+    from paper_2410_05004_b200 import hcache as H
+    n = 777
+    tokens = [(i * 17 + 3) % 1024 for i in range(n)]
+    cfg, w = build(CONFIG1, 13)
+    kv_ref, table, inputs, _ = gpu_prefill(w, cfg, tokens)
+    plan = {"4H": H.RestorationPlan.make(4, 4, H.Complement.NONE),
+            "1RE+3H": H.RestorationPlan.make(4, 3, H.Complement.RECOMPUTE),
+            "1RE+2H+1KV": H.RestorationPlan.make_mixed(1, 2, 1)}[plan_name]
+    store = H.StorageManager(H.DevicePool(2))
+    store.create_session(H.SessionSeed("sp", cfg.hash(), 4, cfg.d_hidden, 2, plan, tokens))
+    for L, m in enumerate(plan.layer_assignment):
+        if m == H.LayerMethod.HIDDEN:
+            assert store.snapshot("sp", L, H.StateKind.HIDDEN, inputs[L])
+        elif m == H.LayerMethod.KV_OFFLOAD:
+            k, v = kv_ref.gather(L, table, n)
+            assert store.snapshot("sp", L, H.StateKind.KV, torch.cat([k, v], 1).contiguous())
+    store.finalize("sp")
+    kv = H.KvCache(4, kv_ref.num_pages, kv_ref.page_size, w.d_kv)
+    res = H.restore(store, "sp", w, plan, H.ThrottleConfig(split_tokens=split), kv, table)
+    torch.cuda.synchronize()
+    for L in range(4):
+        k, v = kv.gather(L, table, n)
+        kr, vr = kv_ref.gather(L, table, n)
+        assert torch.equal(k, kr) and torch.equal(v, vr), (plan_name, split, L)
+    n_re = sum(m == H.LayerMethod.RECOMPUTE for m in plan.layer_assignment)
+    assert sum(e.kind == "recompute" for e in res.timeline.events) == n_re + 1
+
+
+def test_split_layer_rejects_bad_splits(cuda):
+    import torch
+    from paper_2410_05004_b200 import capi
+    from paper_2410_05004_b200 import hcache as H
+    n = 256
+    tokens = list(range(n))
+    cfg, w = build(CONFIG1, 13)
+    kv_ref, table, inputs, _ = gpu_prefill(w, cfg, tokens)
+    plan = H.RestorationPlan.make(4, 3, H.Complement.KV_OFFLOAD)  # layer 0 HIDDEN, KV suffix
+    store = H.StorageManager(H.DevicePool(1))
+    store.create_session(H.SessionSeed("b", cfg.hash(), 4, cfg.d_hidden, 2, plan, tokens))
+    for L, m in enumerate(plan.layer_assignment):
+        if m == H.LayerMethod.HIDDEN:
+            assert store.snapshot("b", L, H.StateKind.HIDDEN, inputs[L])
+        else:
+            k, v = kv_ref.gather(L, table, n)
+            assert store.snapshot("b", L, H.StateKind.KV, torch.cat([k, v], 1).contiguous())
+    store.finalize("b")
+    kv = H.KvCache(4, kv_ref.num_pages, kv_ref.page_size, w.d_kv)
+    for bad in (-64, 100, n, 1024):
+        with pytest.raises(capi.InvalidArgument):
+            H.restore(store, "b", w, plan, H.ThrottleConfig(split_tokens=bad), kv, table)
