@@ -46,12 +46,14 @@ __global__ void signal_kernel(uint32_t* const* addrs, int n, uint32_t value) {
 
 __global__ void wait_kernel(const uint32_t* addr, uint32_t value) {
   uint32_t v = 0;
-  uint64_t spins = 0;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
     asm volatile("ld.global.acquire.sys.u32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
     if (v >= value) break;
     __nanosleep(200);
-    if (++spins == (1ull << 34)) asm volatile("trap;");  // watchdog (~1 h)
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 60000000000ull) asm volatile("trap;");  // watchdog: a peer gone for 60 s
   }
 }
 

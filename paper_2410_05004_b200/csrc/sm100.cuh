@@ -30,10 +30,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
   uint32_t spins = 0;
+  uint64_t t0 = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -42,9 +49,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(done)
         : "r"(addr), "r"(parity)
         : "memory");
-    // watchdog: a pipeline that never completes traps (launch error) instead
-    // of hanging the GPU
-    if (!done && ++spins == (1u << 28)) asm volatile("trap;");
+    // watchdog: a pipeline that never completes traps (a launch error the
+    // host sees) after ~10 s instead of hanging the GPU
+    if (!done && (++spins & 0xFFFFu) == 0) {
+      const uint64_t now = global_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 10000000000ull) asm volatile("trap;");
+    }
   } while (!done);
 }
 
