@@ -124,7 +124,8 @@ void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t 
   }
   const uint32_t abox = uint32_t(gemm_a_box(n_rows));
   CUtensorMap tmA;
-  if (!make_tmap_kmajor(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2, abox))
+  if (!make_tmap_kmajor_cached(&tmA, d_hidden, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2,
+                               abox))
     fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the hidden-state operand");
   // rows with |mean| >> sigma: K1 reads a mean-shifted copy (a no-op kernel
   // and an unused map unless the statistics raised the flag)
@@ -135,7 +136,8 @@ void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t 
     const void* cbuf = own_center ? centered.ptr : pre_centered;
     if (own_center)
       HC_CUDA(launch_center_rows(d_hidden, n_rows, d, d, mean, flag, centered.ptr, stream));
-    if (!make_tmap_kmajor(&alt.map, cbuf, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2, abox))
+    if (!make_tmap_kmajor_cached(&alt.map, cbuf, uint64_t(d), uint64_t(n_rows), uint64_t(d) * 2,
+                                 abox))
       fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the centered operand");
     alt.flag = flag;
   }

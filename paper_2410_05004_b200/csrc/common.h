@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
+
 #include <stdexcept>
 #include <string>
 
@@ -72,11 +75,31 @@ void require_sm100(int dev);
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // Stream-ordered scratch (cudaMallocAsync pool), released on the same stream.
+// The current device's stream-ordered pool keeps freed memory (release
+// threshold = max) so per-call scratch -- e.g. a 32 MB mean-shift buffer per
+// projection -- is recycled instead of being unmapped and remapped at every
+// synchronisation (that doubled a back-to-back K1 loop). Once per device.
+inline void retain_pool_once() {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  if (done.load(std::memory_order_relaxed) & (1ull << dev)) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thresh = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+  }
+  done.fetch_or(1ull << dev);
+}
+
 struct StreamScratch {
   void* ptr = nullptr;
   cudaStream_t stream = nullptr;
   StreamScratch(size_t bytes, cudaStream_t s) : stream(s) {
-    if (bytes) HC_CUDA(cudaMallocAsync(&ptr, bytes, s));
+    if (bytes) {
+      retain_pool_once();
+      HC_CUDA(cudaMallocAsync(&ptr, bytes, s));
+    }
   }
   ~StreamScratch() {
     if (ptr) cudaFreeAsync(ptr, stream);

@@ -76,6 +76,9 @@ inline AMaps single_amap(const CUtensorMap& t) {
 // 128-byte swizzle (the K1 operand layout). Returns false on failure.
 bool make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows,
                       uint64_t row_stride_bytes, uint32_t box_rows);
+// The same, memoised on (address, shape, stride, box) (bounded cache).
+bool make_tmap_kmajor_cached(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows,
+                             uint64_t row_stride_bytes, uint32_t box_rows);
 
 // Box rows of the B tensor map for an M x N GEMM (32, 64, 128 or 256). 128
 // selects the CTA-pair kernel when the problem fills the SM pairs; 32/64 only

@@ -3,7 +3,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "kernels.h"
 
@@ -42,6 +44,37 @@ bool make_tmap_kmajor(CUtensorMap* map, const void* base, uint64_t k, uint64_t r
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+bool make_tmap_kmajor_cached(CUtensorMap* map, const void* base, uint64_t k, uint64_t rows,
+                             uint64_t row_stride_bytes, uint32_t box_rows) {
+  // a tensor map is a pure function of (address, shape, stride, box): maps of
+  // reused buffers (staging-ring slots, pool allocations) are encoded once
+  struct Key {
+    const void* base;
+    uint64_t k, rows, stride;
+    uint32_t box;
+    bool operator<(const Key& o) const {
+      return std::tie(base, k, rows, stride, box) <
+             std::tie(o.base, o.k, o.rows, o.stride, o.box);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, CUtensorMap> cache;
+  const Key key{base, k, rows, row_stride_bytes, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *map = it->second;
+      return true;
+    }
+  }
+  if (!make_tmap_kmajor(map, base, k, rows, row_stride_bytes, box_rows)) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 8192) cache.clear();  // bounded
+  cache.emplace(key, *map);
+  return true;
 }
 
 }  // namespace hc
