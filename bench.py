@@ -441,7 +441,9 @@ def run_ours(args, cfg, rank, world):
                      "io_busy_ms": tl.lane_busy(H.Lane.IO) * 1e3,
                      "compute_busy_ms": tl.lane_busy(H.Lane.COMPUTE) * 1e3,
                      "bubble_fraction": tl.bubble_fraction()},
-        "gpu_launches": args.steps * 2 * L,
+        # the resident leg's launches: per layer row statistics, the mean-shift
+        # check (launch_center_rows) and K1
+        "gpu_launches": args.steps * 3 * L,
         "clocks": clocks,
     }
     if cpu_tok_s is not None:
@@ -651,7 +653,7 @@ def run_ours_batch(args, cfg, rank, world):
                      "io_busy_ms": tl.lane_busy(H.Lane.IO) * 1e3,
                      "compute_busy_ms": tl.lane_busy(H.Lane.COMPUTE) * 1e3,
                      "bubble_fraction": tl.bubble_fraction()},
-        "gpu_launches": None,
+        "gpu_launches": args.steps * 3 * L,
         "clocks": clocks,
     }
     if cpu_tok_s is not None:

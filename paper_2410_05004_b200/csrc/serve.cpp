@@ -292,12 +292,20 @@ void Engine::setup() {
   }
   stride_ = (max_need + page_ - 1) / page_;
   if (persisting()) {
-    // the run's save volume (every session's final token count x the plan's
-    // bytes per token, x2 for extent slack), page-locked outside the clock
-    size_t tokens = 0;
-    for (const auto& kv : hist) tokens += size_t(kv.second);
-    const size_t per_token = size_t(hid_.count) * size_t(d_) * 2 + size_t(kvr_.count) * size_t(2 * dkv_) * 2;
-    st_.reserve_pinned(std::min<size_t>(size_t(64) << 30, 2 * tokens * per_token));
+    // the run's save volume, page-locked outside the clock: per session and
+    // stored layer the chunk extents it can grow to (first extent >= 8 slots
+    // per arena, later ones doubling: <= 2x the final chunk count) -- an
+    // under-estimate would pin a new slab (~0.1 s of cudaHostAlloc) under the
+    // store lock in the middle of a restore
+    const size_t ch = size_t(HC_CHUNK_TOKENS);
+    const size_t cb_h = ch * size_t(d_) * 2, cb_kv = ch * size_t(2 * dkv_) * 2;
+    size_t bytes = 0;
+    for (const auto& kv : hist) {
+      const size_t chunks = (size_t(kv.second) + ch - 1) / ch;
+      const size_t slots = std::max(2 * chunks, size_t(8) * size_t(st_.device_count())) + size_t(st_.device_count());
+      bytes += slots * (size_t(hid_.count) * cb_h + size_t(kvr_.count) * cb_kv);
+    }
+    st_.reserve_pinned(std::min<size_t>(size_t(96) << 30, bytes));
   }
   max_batch_ = o_.max_batch > 0 ? std::min(o_.max_batch, n_) : n_;
   max_rows_ = std::max(max_rows, max_batch_);

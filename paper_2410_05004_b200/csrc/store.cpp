@@ -343,6 +343,37 @@ uint8_t* Store::new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx) 
   return p;
 }
 
+int64_t Store::flush_record(Record& rec) {
+  // one stage-1 record into its chunk slots (the body of drain_locked)
+  fifo_bytes_ -= rec.bytes;
+  if (rec.ready) {
+    check_cuda(cudaEventSynchronize(rec.ready), "snapshot D2H wait");
+    cudaEventDestroy(rec.ready);
+  }
+  int64_t flushed = 0;
+  Session& s = sessions_.at(rec.sid);
+  LayerStream& ls = s.streams[{rec.layer, rec.kind}];
+  ls.kind = rec.kind;
+  const size_t cb = s.chunk_bytes(rec.kind), tb = s.token_bytes(rec.kind);
+  size_t off = 0;
+  while (off < rec.bytes) {
+    if (ls.partial_bytes == 0 && int(ls.chunks.size()) == ls.next_chunk_idx)
+      new_slot(s, ls, rec.layer, ls.next_chunk_idx);
+    const size_t take = std::min(cb - ls.partial_bytes, rec.bytes - off);
+    std::memcpy(ls.chunks[size_t(ls.next_chunk_idx)].ptr + ls.partial_bytes, rec.buf + off, take);
+    off += take;
+    ls.partial_bytes += take;
+    ls.n_tokens += int(take / tb);
+    if (ls.partial_bytes == cb) {
+      ls.partial_bytes = 0;
+      ++ls.next_chunk_idx;
+      ++flushed;
+    }
+  }
+  pool_mem_.release(rec.buf, rec.bytes ? rec.bytes : 1);
+  return flushed;
+}
+
 int64_t Store::drain_locked(int64_t max_chunks, bool block) {
   // drain_locked (storage.cpp:162-191)
   int64_t flushed = 0;
@@ -351,32 +382,7 @@ int64_t Store::drain_locked(int64_t max_chunks, bool block) {
       break;
     Record rec = fifo_.front();
     fifo_.pop_front();
-    fifo_bytes_ -= rec.bytes;
-    if (rec.ready) {
-      check_cuda(cudaEventSynchronize(rec.ready), "snapshot D2H wait");
-      cudaEventDestroy(rec.ready);
-    }
-    Session& s = sessions_.at(rec.sid);
-    LayerStream& ls = s.streams[{rec.layer, rec.kind}];
-    ls.kind = rec.kind;
-    const size_t cb = s.chunk_bytes(rec.kind), tb = s.token_bytes(rec.kind);
-    size_t off = 0;
-    while (off < rec.bytes) {
-      if (ls.partial_bytes == 0 && int(ls.chunks.size()) == ls.next_chunk_idx)
-        new_slot(s, ls, rec.layer, ls.next_chunk_idx);
-      const size_t take = std::min(cb - ls.partial_bytes, rec.bytes - off);
-      std::memcpy(ls.chunks[size_t(ls.next_chunk_idx)].ptr + ls.partial_bytes, rec.buf + off,
-                  take);
-      off += take;
-      ls.partial_bytes += take;
-      ls.n_tokens += int(take / tb);
-      if (ls.partial_bytes == cb) {
-        ls.partial_bytes = 0;
-        ++ls.next_chunk_idx;
-        ++flushed;
-      }
-    }
-    pool_mem_.release(rec.buf, rec.bytes ? rec.bytes : 1);
+    flushed += flush_record(rec);
   }
   return flushed;
 }
@@ -390,7 +396,21 @@ void Store::finalize(const std::string& sid) {
   // finalize (storage.cpp:200-217): drains first; idempotent; partial tails
   // are already in place (length implies token count)
   std::lock_guard<std::mutex> lk(mu_);
-  drain_locked(INT64_MAX);
+  // every record whose copy has landed, then this session's own records in
+  // order (the serving engine finalizes after its last D2H completed, so these
+  // do not block). Records of other sessions still in flight stay queued for
+  // the daemon / the next drain: waiting on them here would hold the store
+  // lock across unrelated D2H copies and stall concurrent restores.
+  drain_locked(INT64_MAX, false);
+  for (auto it = fifo_.begin(); it != fifo_.end();) {
+    if (it->sid == sid) {
+      Record rec = *it;
+      it = fifo_.erase(it);
+      flush_record(rec);
+    } else {
+      ++it;
+    }
+  }
   Session& s = find_open(sid);
   if (s.finalized) return;
   if (!s.tokens.empty()) {

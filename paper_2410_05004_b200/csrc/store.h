@@ -153,6 +153,7 @@ class Store {
   // block=false stops at the first record whose device->host copy is still
   // in flight (the daemon never waits on the GPU while holding mu_).
   int64_t drain_locked(int64_t max_chunks, bool block = true);
+  int64_t flush_record(Record& rec);
   uint8_t* new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx);
   Session& find_open(const std::string& sid);
 
