@@ -174,6 +174,10 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     from .capi import check, lib
 
     if not dist.is_initialized():
+        # a plain `python bench.py --sharded` (no torchrun): a world of one
+        for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"),
+                     ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517")):
+            os.environ.setdefault(k, v)
         backend = os.environ.get("HC_DIST_BACKEND", "nccl")  # gloo: 2 ranks on one GPU (tests)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
@@ -238,6 +242,8 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
             resident[layer] = hrows[b:e].clone() if e > b else hrows[:0].clone()
         torch.cuda.synchronize()
 
+    host_ck = torch.empty(16 * w.d_kv, dtype=torch.bfloat16, pin_memory=True)
+
     def timed(resident_mode, steps):
         dist.barrier()
         torch.cuda.synchronize()
@@ -245,6 +251,8 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
         a.record()
         for _ in range(steps):
             r.restore(list(range(L)), resident if resident_mode else None)
+            if not resident_mode:  # e2e: device->host read of the step's result
+                host_ck.copy_(kv.k[L - 1].view(-1)[: 16 * w.d_kv], non_blocking=True)
         z.record()
         torch.cuda.synchronize()
         ms = torch.tensor([a.elapsed_time(z) / steps], device="cuda")
@@ -280,8 +288,9 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                            "l2": "inputs larger than L2"},
                 "restore_latency_ms": {"resident": ms_res, "e2e": ms_e2e},
                 "e2e": {"value": n / (ms_e2e * 1e-3), "unit": "tokens/s",
-                        "h2d_bytes_per_step": h_bytes // world, "d2h_bytes_per_step": 0},
-                "gpu_launches": args.steps * 2 * L,
+                        "h2d_bytes_per_step": h_bytes // world,
+                        "d2h_bytes_per_step": int(host_ck.numel() * 2)},
+                "gpu_launches": args.steps * 2 * L,  # resident leg: row statistics + K1 per layer
                 "clocks": clocks,
                 "roofline": {"bound": "pcie", "unit": "GB/s",
                              "achieved": h_bytes / world / (ms_e2e * 1e-3) / 1e9,
