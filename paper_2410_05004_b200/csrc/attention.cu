@@ -10,6 +10,9 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
+
+#include <algorithm>
 #include <cmath>
 
 #include "kernels.h"
@@ -511,9 +514,15 @@ cudaError_t launch_attention_extend(const void* q, int n_seqs, int max_new, cons
   if (n_seqs <= 0 || max_new <= 0) return cudaSuccess;
   if (!cu_q || !seq_start) return cudaErrorInvalidValue;
   if (max_new == 1 && (dh == 128 || dh == 64)) {
-    // decode: split the keys so ~2 CTAs per SM stream K/V
+    // decode: split the keys so ~4 CTAs (16 warps) per SM stream K/V -- at 2
+    // per SM the kernel was latency-bound at 41 % of HBM bandwidth (ncu), at 8
+    // the per-split merge overhead dominates (B=16: 5.8 TB/s at 4K context)
     const int group = n_heads / n_kv_heads;
-    int splits = (2 * 148 + n_kv_heads * n_seqs - 1) / (n_kv_heads * n_seqs);
+    static const int per_sm = [] {
+      const char* e = getenv("HC_DECODE_CTAS_PER_SM");
+      return e ? std::max(1, atoi(e)) : 4;
+    }();
+    int splits = (per_sm * 148 + n_kv_heads * n_seqs - 1) / (n_kv_heads * n_seqs);
     splits = splits < 1 ? 1 : splits > 64 ? 64 : splits;
     float* part = nullptr;
     const size_t pb = size_t(n_seqs) * n_heads * splits * (dh + 2) * sizeof(float);
