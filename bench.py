@@ -328,13 +328,16 @@ def run_ours(args, cfg, rank, world):
 
     def timed(fn, steps):
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev[0].record()
+        for i in range(steps):
             fn()
-        b.record()
+            ev[i + 1].record()
         torch.cuda.synchronize()
-        return a.elapsed_time(b) / steps
+        if os.environ.get("HC_STEP_TIMES"):  # per-step device times (diagnostics)
+            print("step_ms", [round(ev[i].elapsed_time(ev[i + 1]), 3) for i in range(steps)],
+                  file=sys.stderr)
+        return ev[0].elapsed_time(ev[-1]) / steps
 
     for _ in range(args.warmup):
         resident_step()
@@ -510,13 +513,16 @@ def run_ours_batch(args, cfg, rank, world):
 
     def timed(fn, steps):
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(steps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev[0].record()
+        for i in range(steps):
             fn()
-        b.record()
+            ev[i + 1].record()
         torch.cuda.synchronize()
-        return a.elapsed_time(b) / steps
+        if os.environ.get("HC_STEP_TIMES"):  # per-step device times (diagnostics)
+            print("step_ms", [round(ev[i].elapsed_time(ev[i + 1]), 3) for i in range(steps)],
+                  file=sys.stderr)
+        return ev[0].elapsed_time(ev[-1]) / steps
 
     host_ck = torch.empty(16 * d_kv, dtype=torch.bfloat16, pin_memory=True)
 

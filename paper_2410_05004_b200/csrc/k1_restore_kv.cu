@@ -300,11 +300,17 @@ __global__ void splitk_epilogue_kernel(const float* __restrict__ part, int split
 // whatever follows (the stage's B rows, the next stage, or the tail pad) --
 // they only feed accumulator rows >= M, which the epilogue never stores. A
 // decode-sized GEMM thus keeps 3-4x more weight bytes in flight per SM.
+// There, `kbs` consecutive k-block slots share one full/empty barrier pair
+// (one expect_tx, one commit): a weight-streaming CTA moves >= 32 KB per
+// barrier round trip. Measured (scripts/tma_stream.cu, 148 CTAs, 200 KB
+// ring): 8 KB per barrier streams 4.6 TB/s, 16 KB 6.5, 32 KB 6.8-7.1. The
+// MMA order over K is unchanged, so results are bit-identical.
 constexpr size_t kMaxRingSmem = 227 * 1024;
 
 struct RingCfg {
-  int stages;
-  uint32_t stride;  // bytes per stage
+  int stages;       // slots (a multiple of kbs)
+  int kbs;          // k-block slots per barrier group
+  uint32_t stride;  // bytes per slot
   uint32_t a_bytes;
   size_t smem;      // dynamic smem incl. tail pad, barriers, alignment slack
 };
@@ -317,6 +323,10 @@ RingCfg ring_cfg(int a_rows) {
   const uint32_t pad = K1Cfg<BN>::kABytes - r.a_bytes;  // garbage rows past the last stage
   r.stages = a_rows == kBM ? K1Cfg<BN>::kStages
                            : int(std::min<size_t>(32, (size_t(200) * 1024 - pad) / r.stride));
+  r.kbs = a_rows == kBM ? 1 : std::max(1, int((32u << 10) / r.stride));
+  if (const char* e = getenv("HC_RING_KBS")) r.kbs = std::max(1, atoi(e));  // experiments
+  r.kbs = std::max(1, std::min(r.kbs, r.stages / 2));
+  r.stages -= r.stages % r.kbs;
   r.smem = size_t(r.stages) * r.stride + pad + 1024 /*bars*/ + 1024 /*align*/;
   return r;
 }
@@ -325,7 +335,7 @@ template <int BN, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ AMaps am,
                    const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
-                   GemmOut gout, EpiArgs epi, uint32_t idesc, int S, uint32_t stride,
+                   GemmOut gout, EpiArgs epi, uint32_t idesc, int S, int kbs, uint32_t stride,
                    uint32_t a_bytes, int k_splits, float* part) {
   using Cfg = K1Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
@@ -333,8 +343,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem;  // stage s: A at s*stride, B at s*stride + a_bytes
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(S) * stride +
                                                (Cfg::kABytes - a_bytes));
-  uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
+  const int G = S / kbs;  // barrier groups of kbs slots
+  uint64_t* empty = full + G;
+  uint64_t* tfull = empty + G;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -350,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < am.n; ++i) tma_prefetch_desc(&am.m[i]);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < S; ++s) {
+    for (int s = 0; s < G; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -373,22 +384,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       // select between maps cost 6 % of tensor-pipe activity (ncu A/B)
       auto produce = [&](auto alt_tag) {
         constexpr bool kAlt = decltype(alt_tag)::value;
-        int stage = 0;
+        int grp = 0;
         uint32_t phase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
           int m_blk, n_blk;
           tile_coords(tile % num_mn, num_m, num_n, m_blk, n_blk);
           const int kb0 = (tile / num_mn) * kb_per, kb1 = min(num_kb, kb0 + kb_per);
-          for (int kb = kb0; kb < kb1; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], a_bytes + Cfg::kBBytes);
-            uint8_t* st = sA + size_t(stage) * stride;
-            int a_row;
-            const CUtensorMap* ma = amap(am, m_blk * kBM, a_row, kAlt);
-            tma_load_2d(st, ma, &full[stage], kb * kBK, a_row);
-            tma_load_2d(st + a_bytes, &tmB, &full[stage], kb * kBK, n_blk * BN);
-            if (++stage == S) {
-              stage = 0;
+          int a_row;
+          const CUtensorMap* ma = amap(am, m_blk * kBM, a_row, kAlt);
+          for (int kb = kb0; kb < kb1; kb += kbs) {
+            const int nk = min(kbs, kb1 - kb);
+            mbar_wait(&empty[grp], phase ^ 1);
+            mbar_arrive_expect_tx(&full[grp], uint32_t(nk) * (a_bytes + Cfg::kBBytes));
+            for (int i = 0; i < nk; ++i) {
+              uint8_t* st = sA + size_t(grp * kbs + i) * stride;
+              tma_load_2d(st, ma, &full[grp], (kb + i) * kBK, a_row);
+              tma_load_2d(st + a_bytes, &tmB, &full[grp], (kb + i) * kBK, n_blk * BN);
+            }
+            if (++grp == G) {
+              grp = 0;
               phase ^= 1;
             }
           }
@@ -402,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (warp-uniform loop, one elected lane issues) --
     {
-      int stage = 0;
+      int grp = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
@@ -411,22 +425,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
         const int kb0 = (tile / num_mn) * kb_per, kb1 = min(num_kb, kb0 + kb_per);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
+        for (int kb = kb0; kb < kb1; kb += kbs) {
+          const int nk = min(kbs, kb1 - kb);
+          mbar_wait(&full[grp], phase);
           tc_fence_after();
           if (elect_one()) {
-            const uint8_t* st = sA + size_t(stage) * stride;
-            const uint64_t adesc = umma_desc_sw128(smem_u32(st));
-            const uint64_t bdesc = umma_desc_sw128(smem_u32(st + a_bytes));
+            for (int i = 0; i < nk; ++i) {
+              const uint8_t* st = sA + size_t(grp * kbs + i) * stride;
+              const uint64_t adesc = umma_desc_sw128(smem_u32(st));
+              const uint64_t bdesc = umma_desc_sw128(smem_u32(st + a_bytes));
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
-              umma_f16(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
-                       ((kb - kb0) | k) != 0 ? 1u : 0u);
-            umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+              for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+                umma_f16(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
+                         ((kb + i - kb0) | k) != 0 ? 1u : 0u);
+            }
+            umma_commit(&empty[grp]);  // frees the group's slots when these MMAs retire
           }
           __syncwarp();
-          if (++stage == S) {
-            stage = 0;
+          if (++grp == G) {
+            grp = 0;
             phase ^= 1;
           }
         }
@@ -895,7 +912,7 @@ cudaError_t launch_tc(const AMaps& tmA, const CUtensorMap& tmB, int M, int N, in
   }
   const int grid_k = std::min(num_sms, tiles * k_splits);
   tc_gemm_kernel<BN, MODE><<<grid_k, kThreads, r.smem, stream>>>(
-      tmA, tmB, M, N, K, out, g, epi, idesc, r.stages, r.stride, r.a_bytes, k_splits, part);
+      tmA, tmB, M, N, K, out, g, epi, idesc, r.stages, r.kbs, r.stride, r.a_bytes, k_splits, part);
   if (k_splits > 1) {
     const int64_t threads = int64_t(M) * (N / 32) * 32;
     splitk_epilogue_kernel<MODE><<<unsigned((threads + 255) / 256), 256, 0, stream>>>(
