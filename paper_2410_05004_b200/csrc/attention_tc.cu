@@ -81,10 +81,13 @@ struct AttnArgs {
   __nv_bfloat16* out;         // [n][n_heads*dh]
   float scale_log2;
   // ragged batch of sequences, each a prefill from position 0 (two-tile
-  // kernel only): sequence blockIdx.z owns query rows [cu[z], cu[z+1]) and
-  // page-table row z (stride table_stride); nullptr = one sequence of n rows
+  // kernel only): sequence blockIdx.y owns query rows [cu[y], cu[y+1]) and
+  // page-table row y (stride table_stride); nullptr = one sequence of n rows
   const int32_t* cu = nullptr;
   int table_stride = 0;
+  // two-tile kernel grid order: true = (heads, sequences, pair rank), false =
+  // (pair rank, heads, sequences); see launch_attn_tc
+  bool rank_major = false;
 };
 
 template <int DH>
@@ -505,15 +508,26 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
 // per-event SM clocks of one CTA (blockIdx 0,0): [event][tile][j], written to
 // host-mapped memory (readable even after the kernel traps)
 __device__ unsigned long long* g_fa_trace;
+// per CTA (linear block id): globaltimer at entry and exit, SM id, steps
+__device__ unsigned long long* g_fa_cta;
+#define FA_CTA(slot, v)                                                                         \
+  do {                                                                                          \
+    if (g_fa_cta && threadIdx.x == 0)                                                           \
+      g_fa_cta[(size_t(blockIdx.z) * gridDim.y * gridDim.x + size_t(blockIdx.y) * gridDim.x +   \
+                blockIdx.x) * 4 + (slot)] = (v);                                                \
+  } while (0)
 #define FA_TRACE(ev, t, j)                                                                     \
   do {                                                                                         \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64)                                        \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64)                     \
       *reinterpret_cast<volatile unsigned long long*>(g_fa_trace + ((ev) * 2 + (t)) * 64 + (j)) = \
           clock64();                                                                           \
   } while (0)
 #else
 #define FA_TRACE(ev, t, j) \
   do {                     \
+  } while (0)
+#define FA_CTA(slot, v) \
+  do {                  \
   } while (0)
 #endif
 
@@ -525,6 +539,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   using Cfg = FaCfg<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) asm volatile("trap;");
+  FA_CTA(0, global_ns());
   uint8_t* sQ = smem_raw;                       // Q_A, Q_B
   uint8_t* sK = sQ + 2 * Cfg::kQBytes;          // K ring, 2 stages
   uint8_t* sV = sK + 2 * Cfg::kKVBytes;         // V ring, 2 stages
@@ -535,24 +550,28 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   uint64_t* v_full = bars + 5;      // [2]
   uint64_t* v_empty = bars + 7;     // [2]
   uint64_t* s_full = bars + 9;      // [tile]
-  uint64_t* p_full = bars + 11;     // [tile]
-  uint64_t* o_done = bars + 13;     // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* p_full = bars + 11;     // [tile][key chunk]
+  uint64_t* o_done = bars + 15;     // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
   float* xmax = reinterpret_cast<float*>(bars + 32);  // [j parity][tile][half][row]
   float* xsum = xmax + 8 * kFaM;                      // [tile][half][row]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // ragged batch: this CTA's sequence, its length and its rows / page table
+  const int b_head = a.rank_major ? blockIdx.x : blockIdx.y;
+  const int b_seq = a.rank_major ? blockIdx.y : blockIdx.z;
+  const int b_rank = a.rank_major ? blockIdx.z : blockIdx.x;
   int row0 = 0;  // first query row of the sequence in q / out
   if (a.cu) {
-    row0 = __ldg(a.cu + blockIdx.z);
-    a.n = __ldg(a.cu + blockIdx.z + 1) - row0;
-    if (a.page_table) a.page_table += size_t(blockIdx.z) * size_t(a.table_stride);
+    row0 = __ldg(a.cu + b_seq);
+    a.n = __ldg(a.cu + b_seq + 1) - row0;
+    if (a.page_table) a.page_table += size_t(b_seq) * size_t(a.table_stride);
   }
   const int n_pairs = (a.n + 2 * kFaM - 1) / (2 * kFaM);
-  const int pt = n_pairs - 1 - int(blockIdx.x);  // heaviest causal tile pairs first
+  const int pt = n_pairs - 1 - b_rank;  // heaviest causal tile pairs first
   if (pt < 0) return;  // (ragged batch: a shorter sequence; uniform for the CTA)
-  const int h = blockIdx.y, hk = h / a.group;
+  FA_CTA(3, uint64_t(2 * pt + 2));
+  const int h = b_head, hk = h / a.group;
   const int q0 = pt * 2 * kFaM;
   const int kv_tiles = (a.n + kAttnN - 1) / kAttnN;
   const int nt_a = min(2 * pt + 1, kv_tiles);
@@ -571,7 +590,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 8);  // the tile's 8 softmax warps
+      mbar_init(&p_full[2 * s], 8);  // the tile's 8 softmax warps, per 32-key chunk
+      mbar_init(&p_full[2 * s + 1], 8);
       mbar_init(&o_done[s], 1);
     }
     fence_barrier_init();
@@ -661,23 +681,32 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     auto issue_pv = [&](int t, int j) {
       const int st = j & 1;
       FA_TRACE(5, t, j);
-      mbar_wait(&p_full[t], j & 1);
       mbar_wait(&v_full[st], (j >> 1) & 1);
-      tc_fence_after();
-      FA_TRACE(1, t, j);
-      if (elect_one()) {
-        const uint64_t v = dv + uint64_t(st * (Cfg::kKVBytes >> 4));
+      // P arrives in two 32-key chunks per key half; the first chunk's MMAs
+      // run while the softmax warps still compute the second
 #pragma unroll
-        for (int kk = 0; kk < kAttnN / 16; ++kk)
-          // P of keys 16kk..: key half kk/4 wrote its 32 columns at the start
-          // of its own 64-column S half
-          umma_f16_ts(tmem + 256 + uint32_t(t * 128),
-                      tmem + uint32_t(t * 128 + (kk >> 2) * 64 + (kk & 3) * 8),
-                      v + uint64_t(kk * (2048 >> 4)), id_pv, (j | kk) != 0 ? 1u : 0u);
-        umma_commit(&o_done[t]);
-        if (t == 1) umma_commit(&v_empty[st]);
+      for (int c = 0; c < 2; ++c) {
+        mbar_wait(&p_full[2 * t + c], j & 1);
+        tc_fence_after();
+        if (c == 0) FA_TRACE(1, t, j);
+        if (elect_one()) {
+          const uint64_t v = dv + uint64_t(st * (Cfg::kKVBytes >> 4));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            // P of keys 16kk..: key half kk/4 wrote its 32 columns at the
+            // start of its own 64-column S half, chunk c in columns 16c..
+            const int kk = (u >> 1) * 4 + c * 2 + (u & 1);
+            umma_f16_ts(tmem + 256 + uint32_t(t * 128),
+                        tmem + uint32_t(t * 128 + (kk >> 2) * 64 + (kk & 3) * 8),
+                        v + uint64_t(kk * (2048 >> 4)), id_pv, (j | kk) != 0 ? 1u : 0u);
+          }
+          if (c == 1) {
+            umma_commit(&o_done[t]);
+            if (t == 1) umma_commit(&v_empty[st]);
+          }
+        }
+        __syncwarp();
       }
-      __syncwarp();
     };
     issue_qk(0, 0);
     issue_qk(1, 0);
@@ -751,7 +780,30 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       const bool resc = mx > m_run + 8.0f;
       const float m_use = resc ? mx : m_run;
       if (rloc == 0 && half == 0) FA_TRACE(7, t, j);
-      // pass 2: P = 2^(s * scale_log2 - m), 32 keys -> 16 columns at a time
+      // O_t rescale (rare with the lazy max), before any P of this step is
+      // published: PV_t(j-1) has retired (QK_t(j), whose S we hold, was
+      // issued after it), and PV_t(j) waits for p_full below
+      if (__any_sync(0xffffffffu, resc)) {
+        const float corr = resc ? ex2_approx(m_run - m_use) : 1.0f;
+        l_run *= corr;
+        if (j > 0) {
+          mbar_wait(&o_done[t], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < DH / 64; ++c) {
+            uint32_t v[32];
+            const uint32_t ta = t_o + uint32_t(half * (DH / 2) + c * 32);
+            tmem_ld_32x32b_x32(ta, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st_32x32b_x32(ta, v);
+          }
+        }
+        m_run = m_use;
+      }
+      // pass 2: P = 2^(s * scale_log2 - m), 32 keys -> 16 columns at a time,
+      // each chunk published as soon as it is in TMEM
       const uint64_t nm2 = f2_pack(-m_use, -m_use);
       uint64_t sum2 = 0, sum2b = 0;
 #pragma unroll
@@ -780,36 +832,15 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         }
         // columns c*16.. of my half: scores already read (chunk 0)
         tmem_st_32x32b_x16(t_s + uint32_t(c * 16), pk);
+        tmem_wait_st();
+        if (c == 1 && rloc == 0 && half == 0) FA_TRACE(9, t, j);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[2 * t + c]);
       }
       sum2 = f2_add(sum2, sum2b);
       if (rloc == 0 && half == 0) FA_TRACE(8, t, j);
-      // O_t rescale (rare with the lazy max): O_t must not be touched while
-      // PV_t(j-1) runs; PV_t(j) waits for p_full below
-      if (__any_sync(0xffffffffu, resc)) {
-        const float corr = resc ? ex2_approx(m_run - m_use) : 1.0f;
-        l_run *= corr;
-        if (j > 0) {
-          mbar_wait(&o_done[t], (j - 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < DH / 64; ++c) {
-            uint32_t v[32];
-            const uint32_t ta = t_o + uint32_t(half * (DH / 2) + c * 32);
-            tmem_ld_32x32b_x32(ta, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
-            tmem_st_32x32b_x32(ta, v);
-          }
-        }
-        m_run = m_use;
-      }
       l_run += f2_lo(sum2) + f2_hi(sum2);
-      tmem_wait_st();
-      if (rloc == 0 && half == 0) FA_TRACE(9, t, j);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
       if (rloc == 0 && half == 0) FA_TRACE(3, t, j);
     }
     xsum[(t * 2 + half) * kFaM + rloc] = l_run;
@@ -840,6 +871,12 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+  FA_CTA(1, global_ns());
+  if (threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    FA_CTA(2, uint64_t(smid));
   }
 }
 
@@ -890,11 +927,19 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  if (cu) {  // ragged batch: (tile pairs of the longest sequence, heads, sequences)
-    const dim3 grid((max_len + 2 * kFaM - 1) / (2 * kFaM), n_heads, n_seqs);
-    attn_fa_kernel<DH><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
-  } else if (two_tile) {
-    const dim3 grid((n + 2 * kFaM - 1) / (2 * kFaM), n_heads);
+  if (cu || two_tile) {
+    // Block order. The scheduler dispatches x fastest. Rank-major (heads,
+    // sequences, pair rank) hands out every head's heaviest causal tile pair
+    // before any lighter one -- longest-first over the launch; head-major
+    // (pair rank, heads, sequences) left the heaviest pairs of the last heads
+    // running alone at the end (7B 4K: SMs 76 % busy, 176 us; rank-major 94 %,
+    // 145 us). Head-major keeps one head's K/V hot in L2 while its pairs run,
+    // which wins once the launch's K/V outgrows L2 (16K x 40 heads: 2.37 vs
+    // 2.42 ms), so rank-major is used while K/V fits in 80 MB.
+    const int pairs = ((cu ? max_len : n) + 2 * kFaM - 1) / (2 * kFaM);
+    const double kv_bytes = double(n) * double(n_kv_heads) * DH * 2 * 2;  // n = total rows
+    a.rank_major = kv_bytes <= 80.0 * (1 << 20);
+    const dim3 grid = a.rank_major ? dim3(n_heads, n_seqs, pairs) : dim3(pairs, n_heads, n_seqs);
     attn_fa_kernel<DH><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
   } else {
     const dim3 grid((n + kAttnM - 1) / kAttnM, n_heads);

@@ -23,12 +23,19 @@ for n, heads in cases:
         f()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
+    reps = int(os.environ.get("REPS", 10))
+    clk = None
+    if os.environ.get("CLOCKS"):  # median SM clock over the loop (nvml)
+        from bench import ClockSampler
+        clk = ClockSampler(torch.cuda.current_device()).__enter__()
     e0.record()
     for _ in range(reps):
         f()
     e1.record()
     torch.cuda.synchronize()
+    if clk is not None:
+        clk.__exit__()
+        print(clk.summary())
     us = e0.elapsed_time(e1) / reps * 1e3
     flops = 4.0 * n * n * heads * dh / 2
     print(f"n={n:6d} heads={heads}: {us:8.1f} us  {flops / us / 1e6:7.1f} TFLOP/s (causal)")

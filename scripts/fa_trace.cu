@@ -6,6 +6,7 @@
 #include "../paper_2410_05004_b200/csrc/attention_tc.cu"
 
 #include <cstdio>
+#include <algorithm>
 #include <vector>
 
 int main(int argc, char** argv) {
@@ -38,6 +39,13 @@ int main(int argc, char** argv) {
   unsigned long long* d_tr = nullptr;
   cudaHostGetDevicePointer(&d_tr, h_tr, 0);
   cudaMemcpyToSymbol(hc::g_fa_trace, &d_tr, sizeof(d_tr));
+  const int n_ctas = ((n + 255) / 256) * heads;
+  unsigned long long* h_cta = nullptr;
+  cudaHostAlloc(&h_cta, sizeof(unsigned long long) * 4 * n_ctas, cudaHostAllocMapped);
+  memset(h_cta, 0, sizeof(unsigned long long) * 4 * n_ctas);
+  unsigned long long* d_cta = nullptr;
+  cudaHostGetDevicePointer(&d_cta, h_cta, 0);
+  cudaMemcpyToSymbol(hc::g_fa_cta, &d_cta, sizeof(d_cta));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -60,5 +68,26 @@ int main(int argc, char** argv) {
       for (int ev = 0; ev < 10; ++ev) printf(" %s %6lld", names[ev], (long long)(tr[ev][t][j] - t0));
       printf("\n");
     }
+  // per-CTA spans of the last launch: duration = a + b * steps (least squares),
+  // SM occupancy = sum of CTA spans / (SMs x kernel span)
+  unsigned long long t_lo = ~0ull, t_hi = 0;
+  double sx = 0, sy = 0, sxx = 0, sxy = 0, busy = 0;
+  int sm_max = 0;
+  for (int c = 0; c < n_ctas; ++c) {
+    const unsigned long long* r = h_cta + 4 * c;
+    t_lo = std::min(t_lo, r[0]);
+    t_hi = std::max(t_hi, r[1]);
+    const double d = double(r[1] - r[0]), x = double(r[3]);
+    sx += x; sy += d; sxx += x * x; sxy += x * d; busy += d;
+    sm_max = std::max(sm_max, int(r[2]));
+  }
+  const double b = (n_ctas * sxy - sx * sy) / (n_ctas * sxx - sx * sx), a = (sy - b * sx) / n_ctas;
+  printf("kernel span %.1f us; CTA span = %.2f us + %.3f us/step; SM busy %.1f %%\n",
+         (t_hi - t_lo) * 1e-3, a * 1e-3, b * 1e-3, 100.0 * busy / ((sm_max + 1) * double(t_hi - t_lo)));
+  for (int c = 0; c < n_ctas; c += n_ctas / 16) {
+    const unsigned long long* r = h_cta + 4 * c;
+    printf("cta %3d sm %3llu steps %2llu start %7.1f end %7.1f us\n", c, r[2], r[3],
+           (r[0] - t_lo) * 1e-3, (r[1] - t_lo) * 1e-3);
+  }
   return 0;
 }
