@@ -226,6 +226,19 @@ int auto_depth(int n_staged, size_t buf_bytes, int requested) {
   return std::max(1, std::min(n_staged, fit) - 1);
 }
 
+// K1 launches of consecutive hidden layers are independent: alternating two
+// streams lets the next layer's CTAs start on the SMs the current one's last
+// wave leaves idle (HC_RESIDENT_STREAMS=1: one stream). A K1 of many waves --
+// a large ragged batch -- has no tail worth overlapping and its persistent
+// CTAs are better started together.
+int k1_lanes(int64_t rows) {
+  static const int env_lanes = [] {
+    const char* e = std::getenv("HC_RESIDENT_STREAMS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return env_lanes == 1 || env_lanes == 2 ? env_lanes : (rows <= 16384 ? 2 : 1);
+}
+
 }  // namespace
 
 // --------------------------------------------------------------- restore
@@ -352,9 +365,27 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
     }
   }
 
+  // HIDDEN layers off the compute lane's critical path (as in
+  // hc_restore_resident): a fetched layer's LayerNorm statistics and
+  // mean-shift check run on a side stream as soon as its copy lands,
+  // overlapping the previous layer's K1, and consecutive K1 launches
+  // alternate two streams. Serialised on one stream, statistics + check +
+  // launch gaps added ~25-40 us to each 0.2 ms K1 (7B, 4096 tokens).
+  const bool norm = w->cfg.norm_enabled != 0;
+  const bool side = native && n_hidden > 0;
+  const bool side_stats = side && norm;
+  const bool center = side_stats && ln_center_enabled();
+  const int lanes = side ? k1_lanes(n) : 1;
+  StreamScratch hstats(side_stats ? size_t(n_hidden) * 2 * size_t(n) * sizeof(float) : 0, stream);
+  StreamScratch hflags(center ? size_t(n_hidden) * sizeof(int32_t) : 0, stream);
+  const size_t cbytes = size_t(n) * size_t(m.d_hidden) * 2;
+  StreamScratch hcring(center ? 2 * cbytes : 0, stream);
+  if (center) HC_CUDA(cudaMemsetAsync(hflags.ptr, 0, size_t(n_hidden) * sizeof(int32_t), stream));
+
   cudaEvent_t t0 = evp.get();
   HC_CUDA(cudaEventRecord(t0, stream));
   HC_CUDA(cudaStreamWaitEvent(eng.copy, t0, 0));  // IO lane starts with the restore
+  if (side_stats) HC_CUDA(cudaStreamWaitEvent(eng.aux, t0, 0));
 
   // IO lane: every fetch in compute order. A fetch whose staging slot is
   // still in use waits (cudaStreamWaitEvent) for the consume event of the
@@ -450,11 +481,57 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
   }
 
   issue_fetches(fetches.size());
+  if (lanes == 2) {  // the second K1 lane starts after the RECOMPUTE prefix
+    cudaEvent_t pre = evp.get();
+    HC_CUDA(cudaEventRecord(pre, stream));
+    HC_CUDA(cudaStreamWaitEvent(eng.aux2, pre, 0));
+  }
+  int k_hid = 0;  // hidden layers consumed so far
+  std::vector<cudaEvent_t> hid_done;
   // compute lane consumes in order
   for (size_t i = 0; i < fetches.size(); ++i) {
     issue_fetches(fetches.size());
     Fetch& f = fetches[i];
     if (!f.fetched) fail(HC_ERUNTIME, "restore: internal fetch ordering error");
+    if (f.hid && side) {
+      const int k = k_hid++;
+      const int64_t rows_n = n - f.row0;
+      float* mean = side_stats ? static_cast<float*>(hstats.ptr) + size_t(k) * 2 * size_t(n)
+                               : nullptr;
+      int32_t* flag = center ? static_cast<int32_t*>(hflags.ptr) + k : nullptr;
+      uint8_t* cbuf = center ? static_cast<uint8_t*>(hcring.ptr) + size_t(k & 1) * cbytes : nullptr;
+      cudaEvent_t ready = f.fetched;
+      if (side_stats) {
+        HC_CUDA(cudaStreamWaitEvent(eng.aux, f.fetched, 0));
+        if (center && k >= 2) HC_CUDA(cudaStreamWaitEvent(eng.aux, hid_done[size_t(k - 2)], 0));
+        if (center) {
+          HC_CUDA(launch_row_stats_flagged(f.buf, rows_n, m.d_hidden, m.d_hidden, true, mean,
+                                           mean + rows_n, flag, eng.aux));
+          HC_CUDA(launch_center_rows(f.buf, rows_n, m.d_hidden, m.d_hidden, mean, flag, cbuf,
+                                     eng.aux));
+        } else {
+          HC_CUDA(launch_row_stats(f.buf, rows_n, m.d_hidden, m.d_hidden, true, mean,
+                                   mean + rows_n, eng.aux));
+        }
+        ready = evp.get();
+        HC_CUDA(cudaEventRecord(ready, eng.aux));
+      }
+      cudaStream_t c = lanes == 2 && (k & 1) ? eng.aux2 : stream;
+      HC_CUDA(cudaStreamWaitEvent(c, ready, 0));
+      cudaEvent_t cs = timed ? evp.get() : nullptr;
+      if (cs) HC_CUDA(cudaEventRecord(cs, c));
+      KvOut out = batch ? kv_out_pages(pages, f.job.layer, d_page_tables, table_stride, d_cu,
+                                       n_sessions)
+                        : kv_out_pages(pages, f.job.layer, d_page_tables, 0, nullptr, 1);
+      out.start_pos = f.row0;
+      project_rows(w, f.job.layer, f.buf, rows_n, out, c, mean, flag, cbuf);
+      cudaEvent_t done = evp.get();
+      HC_CUDA(cudaEventRecord(done, c));
+      hid_done.push_back(done);
+      consumed_h[size_t(f.slot)] = done;
+      if (timed) ops.push_back({HC_LANE_COMPUTE, f.job.layer, HC_EV_PROJECT, cs, done});
+      continue;
+    }
     HC_CUDA(cudaStreamWaitEvent(stream, f.fetched, 0));
     cudaEvent_t cs = timed ? evp.get() : nullptr;
     if (cs) HC_CUDA(cudaEventRecord(cs, stream));
@@ -481,7 +558,14 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
     if (timed) ops.push_back({HC_LANE_COMPUTE, f.job.layer, f.hid ? HC_EV_PROJECT : HC_EV_SCATTER, cs, done});
   }
   issue_fetches(fetches.size());
-  // join the IO lane into the caller stream before the ring is released
+  // join the side lanes (K1, statistics) and the IO lane into the caller
+  // stream before the rings and statistics buffers are released
+  for (cudaStream_t lane : {lanes == 2 ? eng.aux2 : nullptr, side_stats ? eng.aux : nullptr}) {
+    if (!lane) continue;
+    cudaEvent_t j = evp.get();
+    HC_CUDA(cudaEventRecord(j, lane));
+    HC_CUDA(cudaStreamWaitEvent(stream, j, 0));
+  }
   cudaEvent_t io_done = evp.get();
   HC_CUDA(cudaEventRecord(io_done, eng.copy));
   HC_CUDA(cudaStreamWaitEvent(stream, io_done, 0));
@@ -650,11 +734,7 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
     // idle (HC_RESIDENT_STREAMS=1: one stream)
     // (a K1 of many waves -- a large ragged batch -- has no tail worth
     // overlapping and its persistent CTAs are better started together)
-    static const int env_lanes = [] {
-      const char* e = std::getenv("HC_RESIDENT_STREAMS");
-      return e ? std::atoi(e) : 0;
-    }();
-    const int lanes = env_lanes == 1 || env_lanes == 2 ? env_lanes : (n_rows <= 16384 ? 2 : 1);
+    const int lanes = k1_lanes(n_rows);
     cudaStream_t cs[2] = {s, eng.aux2};
     cudaEvent_t fork = evs.get();
     if (norm) HC_CUDA(cudaMemsetAsync(fl, 0, size_t(L) * sizeof(int32_t), s));
