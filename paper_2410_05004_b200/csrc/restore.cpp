@@ -870,10 +870,18 @@ hc_status hc_profile(const hc_weights* w, int32_t n_tokens, hc_timings* out) {
     HC_CUDA(cudaMalloc(&dma_d, dma_bytes));
     project_rows(w, layer, h, n_tokens, o, nullptr);  // warm-up
     // c_token first: one K6 layer (full weights present) at the steady-state
-    // clock, under the same DMA load (~0.4 s of copies queued)
-    for (int i = 0; i < 320; ++i)
+    // clock, under the same DMA load. The warm-up is long enough for the
+    // power-capped clock of a long restore to settle: after 0.2 s the 13B
+    // profile still ran ~10 % faster than back-to-back restores did, and the
+    // plan it picked was compute-bound (HC_PROFILE_WARM_S overrides, seconds)
+    static const double warm_s = [] {
+      const char* e = std::getenv("HC_PROFILE_WARM_S");
+      return e ? std::max(0.0, std::atof(e)) : 1.0;
+    }();
+    const int n_dma = int((warm_s + 0.4) * 900);  // 64 MiB copies at ~55 GB/s
+    for (int i = 0; i < n_dma; ++i)
       HC_CUDA(cudaMemcpyAsync(dma_d, dma_h, dma_bytes, cudaMemcpyHostToDevice, dma));
-    out->c_token = recompute_layer_seconds(w, n_tokens);
+    out->c_token = recompute_layer_seconds(w, n_tokens, warm_s);
     // c_h right after, still at that clock: mean of back-to-back K1 launches
     (void)best;
     HC_CUDA(cudaEventRecord(a.e, nullptr));
