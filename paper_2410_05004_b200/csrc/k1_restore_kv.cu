@@ -723,11 +723,13 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ x,
 
 // launch_center_rows: one warp per row, 16-byte vectors; a no-op (every CTA
 // returns at once) unless the statistics raised the matrix's flag.
-__global__ void __launch_bounds__(256) center_rows_kernel(const __nv_bfloat16* __restrict__ x,
+// out may alias x (in-place centering: every element is read, then written,
+// by the same thread)
+__global__ void __launch_bounds__(256) center_rows_kernel(const __nv_bfloat16* x,
                                                           int64_t rows, int cols,
                                                           int64_t row_stride, float* mean,
                                                           const int32_t* flag,
-                                                          __nv_bfloat16* __restrict__ out) {
+                                                          __nv_bfloat16* out) {
   if (*reinterpret_cast<const volatile int32_t*>(flag) == 0) return;
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -738,7 +740,7 @@ __global__ void __launch_bounds__(256) center_rows_kernel(const __nv_bfloat16* _
     const uint4* src = reinterpret_cast<const uint4*>(x + row * row_stride);
     uint4* dst = reinterpret_cast<uint4*>(out + row * int64_t(cols));
     for (int i = lane; i < cols / 8; i += 32) {
-      uint4 u = __ldg(src + i);
+      uint4 u = src[i];
       __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(&u);
 #pragma unroll
       for (int e = 0; e < 8; ++e) h[e] = __float2bfloat16_rn(__bfloat162float(h[e]) - c);

@@ -372,14 +372,22 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
   // alternate two streams. Serialised on one stream, statistics + check +
   // launch gaps added ~25-40 us to each 0.2 ms K1 (7B, 4096 tokens).
   const bool norm = w->cfg.norm_enabled != 0;
-  const bool side = native && n_hidden > 0;
+  static const bool side_env = [] {  // HC_RESTORE_SIDE=0: serial statistics (experiments)
+    const char* e = std::getenv("HC_RESTORE_SIDE");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool side = side_env && native && n_hidden > 0;
   const bool side_stats = side && norm;
+  // (rows with |mean| >> sigma are mean-shifted in place in their staging
+  // slot -- only K1 reads it -- so K1 needs no second operand map)
   const bool center = side_stats && ln_center_enabled();
-  const int lanes = side ? k1_lanes(n) : 1;
+  static const int restore_lanes = [] {  // HC_RESTORE_LANES: 1 or 2 K1 streams (experiments)
+    const char* e = std::getenv("HC_RESTORE_LANES");
+    return e ? std::atoi(e) : 2;
+  }();
+  const int lanes = side && restore_lanes == 2 ? k1_lanes(n) : 1;
   StreamScratch hstats(side_stats ? size_t(n_hidden) * 2 * size_t(n) * sizeof(float) : 0, stream);
   StreamScratch hflags(center ? size_t(n_hidden) * sizeof(int32_t) : 0, stream);
-  const size_t cbytes = size_t(n) * size_t(m.d_hidden) * 2;
-  StreamScratch hcring(center ? 2 * cbytes : 0, stream);
   if (center) HC_CUDA(cudaMemsetAsync(hflags.ptr, 0, size_t(n_hidden) * sizeof(int32_t), stream));
 
   cudaEvent_t t0 = evp.get();
@@ -487,7 +495,6 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
     HC_CUDA(cudaStreamWaitEvent(eng.aux2, pre, 0));
   }
   int k_hid = 0;  // hidden layers consumed so far
-  std::vector<cudaEvent_t> hid_done;
   // compute lane consumes in order
   for (size_t i = 0; i < fetches.size(); ++i) {
     issue_fetches(fetches.size());
@@ -499,15 +506,13 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
       float* mean = side_stats ? static_cast<float*>(hstats.ptr) + size_t(k) * 2 * size_t(n)
                                : nullptr;
       int32_t* flag = center ? static_cast<int32_t*>(hflags.ptr) + k : nullptr;
-      uint8_t* cbuf = center ? static_cast<uint8_t*>(hcring.ptr) + size_t(k & 1) * cbytes : nullptr;
       cudaEvent_t ready = f.fetched;
       if (side_stats) {
         HC_CUDA(cudaStreamWaitEvent(eng.aux, f.fetched, 0));
-        if (center && k >= 2) HC_CUDA(cudaStreamWaitEvent(eng.aux, hid_done[size_t(k - 2)], 0));
         if (center) {
           HC_CUDA(launch_row_stats_flagged(f.buf, rows_n, m.d_hidden, m.d_hidden, true, mean,
                                            mean + rows_n, flag, eng.aux));
-          HC_CUDA(launch_center_rows(f.buf, rows_n, m.d_hidden, m.d_hidden, mean, flag, cbuf,
+          HC_CUDA(launch_center_rows(f.buf, rows_n, m.d_hidden, m.d_hidden, mean, flag, f.buf,
                                      eng.aux));
         } else {
           HC_CUDA(launch_row_stats(f.buf, rows_n, m.d_hidden, m.d_hidden, true, mean,
@@ -524,10 +529,9 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
                                        n_sessions)
                         : kv_out_pages(pages, f.job.layer, d_page_tables, 0, nullptr, 1);
       out.start_pos = f.row0;
-      project_rows(w, f.job.layer, f.buf, rows_n, out, c, mean, flag, cbuf);
+      project_rows(w, f.job.layer, f.buf, rows_n, out, c, mean, nullptr, nullptr);
       cudaEvent_t done = evp.get();
       HC_CUDA(cudaEventRecord(done, c));
-      hid_done.push_back(done);
       consumed_h[size_t(f.slot)] = done;
       if (timed) ops.push_back({HC_LANE_COMPUTE, f.job.layer, HC_EV_PROJECT, cs, done});
       continue;

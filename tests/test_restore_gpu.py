@@ -67,6 +67,34 @@ def test_restore_all_hidden_matches_oracle(cuda, oracle, devices):
             assert e.start_s >= fetch_end[e.layer] - 1e-6
 
 
+@pytest.mark.parametrize("offset", [8.0, -40.0])
+def test_restore_layernorm_large_mean(cuda, oracle, offset):
+    """Hidden rows whose mean dwarfs their spread, restored through the store:
+    the restore centres them in their staging slot (side stream) before K1;
+    odd layers are ordinary rows, so flagged and unflagged layers alternate
+    on the two K1 lanes."""
+    import torch
+    from oracle import bf16_round
+    from paper_2410_05004_b200 import hcache as H
+    n = 640
+    cfg, w, kv, table = _setup(n=n)
+    store = H.StorageManager(H.DevicePool(2))
+    plan = H.RestorationPlan.make(4, 4, H.Complement.NONE)
+
+    def rows(L):
+        base = cpu_hidden(oracle, n, 512, seed=7 + L)
+        return bf16_round(np.float32(offset) + np.float32(0.1) * base) if L % 2 == 0 else base
+    _store_hidden(H, store, "s", cfg, n, plan,
+                  lambda L: torch.from_numpy(rows(L)).cuda().bfloat16())
+    H.restore(store, "s", w, plan, H.ThrottleConfig(), kv, table)
+    torch.cuda.synchronize()
+    for L in range(4):
+        kr, vr = oracle.project(rows(L), *cpu_wkv(oracle, 512, 512, L), 8)
+        k, v = kv.gather(L, table, n)
+        assert max_rel_err(k.float().cpu().numpy(), kr) < REL_TOL
+        assert max_rel_err(v.float().cpu().numpy(), vr) < REL_TOL
+
+
 def test_restore_is_deterministic_and_equals_resident_path(cuda):
     import ctypes as C
 
