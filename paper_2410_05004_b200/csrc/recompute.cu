@@ -375,6 +375,10 @@ double recompute_layer_seconds(const hc_weights* w, int n, double warm_s) {
       break;
     }
   if (layer < 0 || (w->d_head != 64 && w->d_head != 128)) return 0.0;
+  // up to 4 consecutive layers per call, as a restore's prefix runs them:
+  // the per-call embedding and setup are not part of a layer's cost
+  int nl = 1;
+  while (nl < 4 && layer + nl < w->cfg.n_layers && w->layers[size_t(layer + nl)].full) ++nl;
   DeviceGuard dg(w->device);
   cudaStream_t s = nullptr;
   const size_t kvb = size_t(n) * size_t(w->d_kv_all) * 2;
@@ -388,7 +392,7 @@ double recompute_layer_seconds(const hc_weights* w, int n, double warm_s) {
   HC_CUDA(cudaEventCreate(&a));
   HC_CUDA(cudaEventCreate(&b));
   auto one = [&] {
-    prefill_layers_impl(w, static_cast<int32_t*>(tok.ptr), n, layer, layer + 1, &pages,
+    prefill_layers_impl(w, static_cast<int32_t*>(tok.ptr), n, layer, layer + nl, &pages,
                         static_cast<int32_t*>(table.ptr), s, [](int, bool) {});
   };
   auto timed = [&](int reps) {
@@ -407,7 +411,7 @@ double recompute_layer_seconds(const hc_weights* w, int n, double warm_s) {
   double warm = 0;
   while (warm < warm_s) warm += timed(8);
   const int reps = 16;
-  const double sec = timed(reps) / reps;
+  const double sec = timed(reps) / reps / nl;
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   return sec;
