@@ -41,6 +41,30 @@ def test_attention_dense_vs_torch(cuda, n, heads, kvh, dh):
     assert err < 2e-2, err
 
 
+@pytest.mark.parametrize("n,heads", [(4096, 16), (4608, 40)])
+def test_attention_block_orders_vs_torch(cuda, n, heads):
+    """Both block orders of the two-tile kernel: rank-major (every head's
+    heaviest tile pair first; K/V of 4096 x 16 heads = 32 MB) and head-major
+    (K/V of 4608 x 40 heads = 94 MB > the 80 MB L2 budget)."""
+    import torch
+    from paper_2410_05004_b200 import capi
+    dh = 128
+    g = torch.Generator(device="cuda").manual_seed(n + heads)
+    q = torch.randn(n, heads * dh, device="cuda", generator=g).bfloat16()
+    k = torch.randn(n, heads * dh, device="cuda", generator=g).bfloat16()
+    v = torch.randn(n, heads * dh, device="cuda", generator=g).bfloat16()
+    out = torch.empty(n, heads * dh, device="cuda", dtype=torch.bfloat16)
+    capi.check(capi.lib().hc_attention_dense(q.data_ptr(), n, heads, heads, dh, k.data_ptr(),
+                                             v.data_ptr(), heads * dh, out.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    for h0 in range(0, heads, 8):  # the fp32 reference eight heads at a time
+        sl = slice(h0 * dh, (h0 + 8) * dh)
+        ref = _attn_ref(q[:, sl], k[:, sl], v[:, sl], 8, 8, dh)
+        err = (out[:, sl].float() - ref).abs().max().item() / ref.abs().max().item()
+        assert err < 2e-2, (h0, err)
+
+
 @pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("m,n,k,split", [
     (200, 256, 512, 0), (1024, 512, 2048, 0), (130, 4096, 256, 0),
