@@ -415,15 +415,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 //   warps 2-9   softmax of tile A, warps 10-17 of tile B (the two overlap on
 //               every SM sub-partition): two threads per query row (64 keys
 //               each, row max exchanged through smem)
-// Part of the exponentials run as a Cody-Waite + degree-3 polynomial on the
-// FMA pipe (rel. error 7.5e-5, far below bf16 P's 3.9e-3), the rest on MUFU:
-// with only MUFU the 16 ex2/clk/SM take exactly as long as the MMAs. The
-// softmax arithmetic is packed fp32x2 (FFMA2/FADD2) to halve its issue slots.
+// HC_FA_EMU of every 8 exponential pairs can run as a Cody-Waite + degree-3
+// polynomial on the FMA pipe (rel. error 7.5e-5, far below bf16 P's 3.9e-3)
+// instead of MUFU. With the SMs 76 % busy (head-major block order) 3 of 8 was
+// best; once the launch kept them 94 % busy, all-MUFU won (7B layer 150 ->
+// 143 us, 16K x 40 heads 2.44 -> 2.29 ms; scripts/ab_fa_emu.sh), so the
+// default is 0. The softmax arithmetic is packed fp32x2 (FFMA2/FADD2) to
+// halve its issue slots.
 // ============================================================================
 constexpr int kFaM = 128;       // rows per Q tile (two per CTA)
 constexpr int kFaThreads = 576;  // TMA, MMA, 8 softmax warps per Q tile (two threads per row)
 #ifndef HC_FA_EMU
-#define HC_FA_EMU 3
+#define HC_FA_EMU 0
 #endif
 constexpr int kFaEmuPairs = HC_FA_EMU;  // of every 8 exponential pairs, this many on the FMA pipe
 
