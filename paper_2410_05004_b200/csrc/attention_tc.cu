@@ -428,6 +428,9 @@ constexpr int kFaThreads = 576;  // TMA, MMA, 8 softmax warps per Q tile (two th
 #ifndef HC_FA_EMU
 #define HC_FA_EMU 0
 #endif
+#ifndef HC_FA_PCHUNK  // 1: P published per 32-key chunk, 0: once per tile (experiments)
+#define HC_FA_PCHUNK 1
+#endif
 constexpr int kFaEmuPairs = HC_FA_EMU;  // of every 8 exponential pairs, this many on the FMA pipe
 
 template <int DH>
@@ -835,11 +838,23 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         }
         // columns c*16.. of my half: scores already read (chunk 0)
         tmem_st_32x32b_x16(t_s + uint32_t(c * 16), pk);
+#if HC_FA_PCHUNK
         tmem_wait_st();
         if (c == 1 && rloc == 0 && half == 0) FA_TRACE(9, t, j);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[2 * t + c]);
+#else
+        if (c == 1) {  // both chunks published together (experiments)
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&p_full[2 * t]);
+            mbar_arrive(&p_full[2 * t + 1]);
+          }
+        }
+#endif
       }
       sum2 = f2_add(sum2, sum2b);
       if (rloc == 0 && half == 0) FA_TRACE(8, t, j);
