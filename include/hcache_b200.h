@@ -315,6 +315,16 @@ hc_status hc_store_reopen_for_append(hc_store* s, const char* sid, const int32_t
 hc_status hc_store_snapshot(hc_store* s, const char* sid, int32_t layer, int32_t kind,
                             const void* rows, int64_t n_rows, int32_t row_width,
                             int32_t src_dtype, int32_t src_on_device, void* stream);
+/* snapshot of tokens [tok_begin, tok_begin + n_rows) of a layer (tok_begin
+ * a multiple of 64): the save path of a head-sharded context, where every
+ * rank persists only its own token range of each hidden layer (chunk index,
+ * striping and payload stay the reference's; chunks below tok_begin are held
+ * by the other ranks' stores). Further rows of the layer append after it.
+ * B200 extension of snapshot (storage.hpp:96-97). */
+hc_status hc_store_snapshot_range(hc_store* s, const char* sid, int32_t layer, int32_t kind,
+                                  int64_t tok_begin, const void* rows, int64_t n_rows,
+                                  int32_t row_width, int32_t src_dtype, int32_t src_on_device,
+                                  void* stream);
 /* drain / drain_all (storage.hpp:101-102): stage 2, chunk assembly. */
 hc_status hc_store_drain(hc_store* s, int64_t max_chunks, int64_t* flushed);
 hc_status hc_store_drain_all(hc_store* s);
@@ -489,6 +499,50 @@ hc_status hc_project_multi_source(const hc_weights* w, int32_t layer, int32_t n_
 hc_status hc_stream_wait_flag(void* stream, const uint32_t* d_flag, uint32_t value);
 hc_status hc_stream_signal_flags(void* stream, uint32_t* const* d_flag_ptrs, int32_t n,
                                  uint32_t value);
+
+/* ------------------------------------- multi-GPU: head-sharded restore */
+/* restore (restore.hpp:40-42) of a context whose KV heads are sharded over
+ * `world` GPUs, one process per GPU (north star (4)). Rank r owns
+ * KV heads hc_shard_heads(r) and the 128-row aligned token range
+ * hc_shard_range(r) of every HIDDEN layer: it fetches only that range over
+ * its own PCIe link into a small ring of HBM slots that every other rank has
+ * mapped (CUDA IPC over NVLink / NVSwitch), computes the range's LayerNorm
+ * statistics (and the mean shift of rows with |mean| >> sigma) in place,
+ * and announces the slot through flags in the peers' memory. Every rank's
+ * K1 then reads all ranges' A tiles straight from the owners' slots -- the
+ * all-gather fused into the GEMM, no gathered n x d copy -- and projects
+ * only its own heads into its paged cache; it reads the owners' statistics
+ * (8 B per row), not their rows. KV_OFFLOAD layers fetch this rank's heads'
+ * [K|V] rows only. RECOMPUTE layers need the whole model on one GPU: with
+ * world > 1 they are rejected (HC_EINVAL); with world == 1 the call is
+ * hc_restore. Every rank must call with the same session plan, in the same
+ * order of calls. */
+typedef struct hc_peer_group hc_peer_group;
+/* Chunk-aligned (128-row) contiguous token range [*begin, *end) of `rank`. */
+hc_status hc_shard_range(int64_t n_tokens, int32_t world, int32_t rank, int64_t* begin,
+                         int64_t* end);
+/* KV heads [*begin, *begin + *count) of `rank` (n_kv_heads % world == 0). */
+hc_status hc_shard_heads(int32_t n_kv_heads, int32_t world, int32_t rank, int32_t* begin,
+                         int32_t* count);
+/* This rank's member: `depth` staging slots of max_rows x d_hidden bf16 rows
+ * (+ their statistics) and the flag arrays, on `device`. */
+hc_status hc_peer_group_create(int32_t world, int32_t rank, int32_t device, int32_t d_hidden,
+                               int64_t max_rows, int32_t depth, hc_peer_group** out);
+void hc_peer_group_destroy(hc_peer_group* g);
+/* The member's CUDA IPC handles as an opaque blob of hc_peer_group_blob_size()
+ * bytes, to be handed to every other rank by any transport (MPI, sockets,
+ * torch.distributed). */
+size_t hc_peer_group_blob_size(void);
+hc_status hc_peer_group_export(const hc_peer_group* g, void* blob, size_t cap);
+/* Maps every peer: blobs[r] = rank r's blob (blobs[rank] is ignored). */
+hc_status hc_peer_group_import(hc_peer_group* g, const void* const* blobs);
+/* Reads back the peers' view of this rank after import (tests): 1 when every
+ * peer is mapped. */
+int32_t hc_peer_group_ready(const hc_peer_group* g);
+hc_status hc_restore_sharded(hc_peer_group* g, hc_store* s, const char* sid,
+                             const hc_weights* w, const hc_plan* plan,
+                             const hc_restore_opts* opts, const hc_kv_pages* pages,
+                             const int32_t* d_page_table, void* stream, hc_timeline* timeline);
 
 /* ---------------------------------------------------------- serving loop */
 /* Strategy / SavingMode (harness.hpp:14-17). */

@@ -92,6 +92,8 @@ class Oracle:
         L.hco_symmetric_at.restype = C.c_float
         L.hco_symmetric_at.argtypes = [C.c_uint64, C.c_uint64, C.c_float]
         L.hco_fill_symmetric.argtypes = [_f32p, C.c_size_t, C.c_uint64, C.c_uint64, C.c_float]
+        L.hco_fill_symmetric_bf16.argtypes = [_f32p, C.c_size_t, C.c_uint64, C.c_uint64,
+                                              C.c_float, C.c_int]
         L.hco_init_model.restype = C.c_size_t
         L.hco_init_model.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
         L.hco_float_to_half.restype = C.c_uint16
@@ -114,6 +116,8 @@ class Oracle:
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         L.hco_prefill_layers.argtypes = [C.POINTER(_Config), _f32p, _i32p, C.c_int64, C.c_int,
                                          C.c_int, _f32p, _f32p, C.c_int]
+        L.hco_block_forward.argtypes = [C.POINTER(_Config), _f32p, _f32p, _f32p, _f32p, _f32p,
+                                        _f32p, _f32p, C.c_int64, _f32p, _f32p, C.c_int]
         L.hco_device_for_chunk.restype = C.c_int
         L.hco_device_for_chunk.argtypes = [C.c_int, C.c_int, C.c_int]
         L.hco_num_chunks.restype = C.c_int
@@ -135,6 +139,12 @@ class Oracle:
     def symmetric(self, n, seed, offset=0, bound=1.0):
         out = np.empty(int(n), np.float32)
         self.lib.hco_fill_symmetric(out, out.size, seed, offset, bound)
+        return out
+
+    def symmetric_bf16(self, n, seed, offset=0, bound=1.0, nthreads=None):
+        """bf16_round(symmetric(...)), generated on all host threads."""
+        out = np.empty(int(n), np.float32)
+        self.lib.hco_fill_symmetric_bf16(out, out.size, seed, offset, bound, _nthreads(nthreads))
         return out
 
     def init_model(self, n_layers, d, d_ffn, vocab, seed):
@@ -226,6 +236,22 @@ class Oracle:
         v = np.zeros((L, n, d), np.float32)
         self.lib.hco_prefill_layers(C.byref(c), np.ascontiguousarray(weights, np.float32), tokens,
                                     n, lb, le, k, v, _nthreads(nthreads))
+        return k, v
+
+    def block_forward(self, cfg: dict, lw: dict, x, nthreads=None):
+        """block_forward (model.cpp:102-115) of one layer with explicit
+        weights lw = {wq, wk, wv, wo, fc1, fc2}; x (n x d float32) is updated
+        in place; returns the layer's (K, V)."""
+        c = _Config(1, cfg["d_hidden"], cfg["n_heads"], cfg["d_ffn"], cfg.get("vocab_size", 1),
+                    cfg.get("max_seq", 4096), int(cfg.get("norm", 1)), int(cfg.get("rope", 1)))
+        assert x.dtype == np.float32 and x.flags["C_CONTIGUOUS"]
+        n = x.shape[0]
+        k = np.empty_like(x)
+        v = np.empty_like(x)
+        w = {key: np.ascontiguousarray(lw[key], np.float32)
+             for key in ("wq", "wk", "wv", "wo", "fc1", "fc2")}
+        self.lib.hco_block_forward(C.byref(c), w["wq"], w["wk"], w["wv"], w["wo"], w["fc1"],
+                                   w["fc2"], x, n, k, v, _nthreads(nthreads))
         return k, v
 
     # indexing / planner / pipeline

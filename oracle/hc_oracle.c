@@ -347,10 +347,9 @@ static float gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654
 
 /* block_forward (model.cpp:102-115) with start_pos 0 and an empty cache, so
  * the layer's cache is exactly the fresh projection. x is updated in place. */
-static void block_forward(const hco_config* cfg, const float* weights, int L,
-                          float* x, int64_t n, float* k, float* v, int nthreads) {
+static void block_forward_view(const hco_config* cfg, layer_view lw, float* x, int64_t n,
+                               float* k, float* v, int nthreads) {
   int d = cfg->d_hidden, dh = d / cfg->n_heads;
-  layer_view lw = view_layer(cfg, weights, L);
   size_t nd = (size_t)n * d;
   hco_project_hidden_to_kv(x, n, d, lw.wk, lw.wv, d, cfg->n_heads, 0,
                            cfg->norm_enabled, cfg->rope_enabled, k, v, nthreads);
@@ -379,6 +378,19 @@ static void block_forward(const hco_config* cfg, const float* weights, int L,
   free(mix);
   free(q);
   free(a);
+}
+
+static void block_forward(const hco_config* cfg, const float* weights, int L,
+                          float* x, int64_t n, float* k, float* v, int nthreads) {
+  block_forward_view(cfg, view_layer(cfg, weights, L), x, n, k, v, nthreads);
+}
+
+void hco_block_forward(const hco_config* cfg, const float* wq, const float* wk,
+                       const float* wv, const float* wo, const float* fc1,
+                       const float* fc2, float* x, int64_t n, float* k_out,
+                       float* v_out, int nthreads) {
+  layer_view lw = {NULL, wq, wk, wv, wo, fc1, fc2};
+  block_forward_view(cfg, lw, x, n, k_out, v_out, nthreads);
 }
 
 static void embed(const hco_config* cfg, const float* weights, const int* tokens,
@@ -436,6 +448,25 @@ void hco_prefill_layers(const hco_config* cfg, const float* weights,
     block_forward(cfg, weights, L, x, n, k_out + (size_t)L * nd,
                   v_out + (size_t)L * nd, nthreads);
   free(x);
+}
+
+typedef struct {
+  float* out;
+  uint64_t seed, offset;
+  float bound;
+} fill_ctx;
+
+static void fill_bf16_range(void* p, int64_t b, int64_t e) {
+  fill_ctx* c = (fill_ctx*)p;
+  for (int64_t i = b; i < e; ++i)
+    c->out[i] = hco_bf16_to_float(
+        hco_float_to_bf16(hco_symmetric_at(c->seed, c->offset + (uint64_t)i, c->bound)));
+}
+
+void hco_fill_symmetric_bf16(float* out, size_t n, uint64_t seed, uint64_t offset,
+                             float bound, int nthreads) {
+  fill_ctx c = {out, seed, offset, bound};
+  parallel_for((int64_t)n, nthreads, fill_bf16_range, &c);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -89,6 +89,20 @@ void hco_prefill_layers(const hco_config* cfg, const float* weights,
                         int layer_end, float* k_out, float* v_out,
                         int nthreads);
 
+/* block_forward (model.cpp:102-115) of one layer from explicit weights
+ * (row-major out x in), start_pos 0 and an empty cache: x (n x d) is updated
+ * in place, the layer's K/V (n x d) written. Lets a parity check walk a
+ * large model layer by layer without materialising the whole weight set. */
+void hco_block_forward(const hco_config* cfg, const float* wq, const float* wk,
+                       const float* wv, const float* wo, const float* fc1,
+                       const float* fc2, float* x, int64_t n, float* k_out,
+                       float* v_out, int nthreads);
+
+/* hco_fill_symmetric rounded to bf16 (RNE) and widened back, rows split over
+ * nthreads (the draws are counter based, so the values do not depend on it). */
+void hco_fill_symmetric_bf16(float* out, size_t n, uint64_t seed, uint64_t offset,
+                             float bound, int nthreads);
+
 /* ---- chunk indexing: include/hcache/storage.hpp:20, src/storage.cpp:29-31 */
 int hco_chunk_tokens(void);
 int hco_device_for_chunk(int layer, int chunk_idx, int device_count);

@@ -175,6 +175,17 @@ _PROTOS = {
                                P(TimelineC)]),
     "hc_project_multi_source": (i32, [vp, i32, i32, P(vp), P(i64), P(KvPagesC), vp, i32, vp]),
     "hc_stream_wait_flag": (i32, [vp, vp, C.c_uint32]),
+    "hc_store_snapshot_range": (i32, [vp, cp, i32, i32, i64, vp, i64, i32, i32, i32, vp]),
+    "hc_shard_range": (i32, [i64, i32, i32, P(i64), P(i64)]),
+    "hc_shard_heads": (i32, [i32, i32, i32, P(i32), P(i32)]),
+    "hc_peer_group_create": (i32, [i32, i32, i32, i32, i64, i32, P(vp)]),
+    "hc_peer_group_destroy": (None, [vp]),
+    "hc_peer_group_blob_size": (C.c_size_t, []),
+    "hc_peer_group_export": (i32, [vp, vp, C.c_size_t]),
+    "hc_peer_group_import": (i32, [vp, P(vp)]),
+    "hc_peer_group_ready": (i32, [vp]),
+    "hc_restore_sharded": (i32, [vp, vp, cp, vp, P(PlanC), P(RestoreOptsC), P(KvPagesC), vp, vp,
+                                 P(TimelineC)]),
     "hc_stream_signal_flags": (i32, [vp, P(vp), i32, C.c_uint32]),
     "hc_serve_run": (i32, [vp, vp, P(RequestC), i32, P(ServeOptsC), P(RequestMetricsC), vp,
                            P(ServeMetricsC), vp]),

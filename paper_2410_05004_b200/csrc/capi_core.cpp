@@ -358,6 +358,28 @@ hc_status hc_project_hidden_to_kv(const hc_weights* w, int32_t layer, const void
   });
 }
 
+}  // extern "C"
+
+namespace hc {
+// Ragged batches restart positions at 0 per sequence, so K1's RoPE rows are
+// bounded by the longest sequence. Only when the concatenated rows exceed the
+// table can a sequence do so; then the offsets are read back (synchronously)
+// and checked, so no launch reads past the RoPE table.
+void check_seq_positions(const hc_weights* w, const int32_t* d_cu_seqlens, int n_seqs,
+                         int64_t n_rows, cudaStream_t stream) {
+  if (!w->cfg.rope_enabled || !d_cu_seqlens || n_rows <= w->rope_rows) return;
+  std::vector<int32_t> cu(size_t(n_seqs) + 1);
+  HC_CUDA(cudaMemcpyAsync(cu.data(), d_cu_seqlens, sizeof(int32_t) * cu.size(),
+                          cudaMemcpyDeviceToHost, stream));
+  HC_CUDA(cudaStreamSynchronize(stream));
+  for (int i = 0; i < n_seqs; ++i)
+    if (cu[size_t(i) + 1] - cu[size_t(i)] > w->rope_rows)
+      fail(HC_EINVAL, "project: a sequence exceeds max_seq (RoPE table)");
+}
+}  // namespace hc
+
+extern "C" {
+
 hc_status hc_project_to_pages(const hc_weights* w, int32_t layer, const void* d_hidden,
                               int64_t n_rows, const int32_t* d_cu_seqlens, int32_t n_seqs,
                               const hc_kv_pages* pages, const int32_t* d_page_table,
@@ -367,6 +389,7 @@ hc_status hc_project_to_pages(const hc_weights* w, int32_t layer, const void* d_
     validate_pages(w, pages, w->d_kv);
     if (d_cu_seqlens && n_seqs < 1) fail(HC_EINVAL, "project_to_pages: n_seqs < 1");
     DeviceGuard dg(w->device);
+    check_seq_positions(w, d_cu_seqlens, n_seqs, n_rows, as_stream(stream));
     project_rows(w, layer, d_hidden, n_rows,
                  kv_out_pages(pages, layer, d_page_table, table_stride, d_cu_seqlens, n_seqs),
                  as_stream(stream));

@@ -1,6 +1,9 @@
 // common.h -- internal error plumbing and device helpers for the C ABI.
 #pragma once
 
+#include <exception>
+#include <initializer_list>
+
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -106,6 +109,34 @@ struct StreamScratch {
   }
   StreamScratch(const StreamScratch&) = delete;
   StreamScratch& operator=(const StreamScratch&) = delete;
+};
+
+// Error-path guard: when the scope unwinds by an exception, makes `stream`
+// wait for everything already queued on the side lanes, so stream-ordered
+// frees of scratch buffers on `stream` cannot overtake copies or kernels
+// still using them. A no-op on normal exit (the code joins explicitly).
+struct LaneJoin {
+  cudaStream_t stream;
+  cudaStream_t lanes[4] = {nullptr, nullptr, nullptr, nullptr};
+  int entered;
+  LaneJoin(cudaStream_t s, std::initializer_list<cudaStream_t> ls)
+      : stream(s), entered(std::uncaught_exceptions()) {
+    int i = 0;
+    for (cudaStream_t l : ls)
+      if (i < 4) lanes[i++] = l;
+  }
+  ~LaneJoin() {
+    if (std::uncaught_exceptions() <= entered) return;
+    for (cudaStream_t l : lanes) {
+      if (!l || l == stream) continue;
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) continue;
+      if (cudaEventRecord(e, l) == cudaSuccess) cudaStreamWaitEvent(stream, e, 0);
+      cudaEventDestroy(e);
+    }
+  }
+  LaneJoin(const LaneJoin&) = delete;
+  LaneJoin& operator=(const LaneJoin&) = delete;
 };
 
 }  // namespace hc

@@ -60,9 +60,9 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
 // The tensor map holding A row `row` and the row's coordinate within it.
 __device__ __forceinline__ const CUtensorMap* amap(const AMaps& am, int row, int& local,
                                                    bool alt = false) {
-  if (alt) {  // single source, mean-shifted copy
+  if (alt) {  // the mean-shifted copy of the whole matrix, after the sources
     local = row;
-    return &am.m[1];
+    return &am.m[am.n];
   }
   int s = 0;
   while (s + 1 < am.n && row >= am.row0[s + 1]) ++s;

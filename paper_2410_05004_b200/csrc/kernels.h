@@ -55,12 +55,12 @@ struct GemmOut {
 // one CTA's half of a CTA-pair tile, reads one source).
 constexpr int kMaxASrc = 8;
 struct AMaps {
-  CUtensorMap m[kMaxASrc];
+  CUtensorMap m[kMaxASrc + 1];
   int row0[kMaxASrc + 1];
   int n;
-  // single source only: when *alt_flag != 0 (set on the device by the row
-  // statistics) the A operand is read through m[1], the mean-shifted copy
-  // written by launch_center_rows, instead of m[0]
+  // when *alt_flag != 0 (set on the device by the row statistics) every A
+  // tile is read through m[n] -- the mean-shifted copy of the whole matrix
+  // written by launch_center_rows -- instead of the source maps m[0..n)
   const int32_t* alt_flag = nullptr;
 };
 inline AMaps single_amap(const CUtensorMap& t) {
@@ -106,6 +106,24 @@ cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, in
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
                               int num_sms, cudaStream_t stream, bool split_acc = false,
                               const AltA* alt = nullptr);
+// Per-source LayerNorm statistics of a head-sharded layer (the owners'
+// slots, mapped over NVLink): rows [row0[s], row0[s+1]) come from
+// mean[s] / rstd[s].
+struct StatSources {
+  const float* mean[kMaxASrc];
+  const float* rstd[kMaxASrc];
+  int64_t row0[kMaxASrc + 1];
+  int n;
+};
+cudaError_t launch_gather_stats(const StatSources& src, int64_t max_rows, float* mean, float* rstd,
+                                cudaStream_t stream);
+// Stream-ordered cross-GPU flags: store `value` (system-scope release) into
+// each of n flags whose addresses are in device memory; wait until a flag in
+// this GPU's memory is >= value (cuStreamWaitValue32 or a polling kernel).
+cudaError_t launch_signal_flags(uint32_t* const* d_flag_ptrs, int n, uint32_t value,
+                                cudaStream_t stream);
+cudaError_t wait_flag_geq(cudaStream_t stream, const uint32_t* d_flag, uint32_t value);
+
 // K1 with a multi-source A (AMaps): the peer-memory all-gather fused in.
 cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int bn, int M, int N,
                                     int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,

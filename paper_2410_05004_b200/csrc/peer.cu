@@ -88,6 +88,24 @@ __global__ void convert_f16_kernel(const uint2* src, uint2* dst, int64_t n4) {
   }
 }
 
+// LayerNorm statistics of a head-sharded layer: every owner computed the
+// mean/rstd of its own token range into its staging slot; a consumer copies
+// them (8 B per row, over NVLink) into one contiguous array for K1's
+// epilogue instead of re-reading the owners' rows.
+__global__ void gather_stats_kernel(StatSources src, float* __restrict__ mean,
+                                    float* __restrict__ rstd) {
+  const int s = blockIdx.y;
+  if (s >= src.n) return;
+  const int64_t b = src.row0[s], rows = src.row0[s + 1] - b;
+  const float* m = src.mean[s];
+  const float* r = src.rstd[s];
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    mean[b + i] = m[i];
+    rstd[b + i] = r[i];
+  }
+}
+
 using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
 WaitFn wait_value_fn() {
@@ -122,6 +140,31 @@ cudaError_t launch_convert_to_bf16(const void* src, int src_dtype, void* dst, in
   return cudaGetLastError();
 }
 
+cudaError_t launch_signal_flags(uint32_t* const* d_flag_ptrs, int n, uint32_t value,
+                                cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  signal_kernel<<<1, 32, 0, stream>>>(d_flag_ptrs, n, value);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_stats(const StatSources& src, int64_t max_rows, float* mean, float* rstd,
+                                cudaStream_t stream) {
+  if (src.n <= 0 || max_rows <= 0) return cudaSuccess;
+  const unsigned gx = unsigned(std::min<int64_t>((max_rows + 255) / 256, 64));
+  gather_stats_kernel<<<dim3(gx, unsigned(src.n)), 256, 0, stream>>>(src, mean, rstd);
+  return cudaGetLastError();
+}
+
+cudaError_t wait_flag_geq(cudaStream_t stream, const uint32_t* d_flag, uint32_t value) {
+  static const bool use_kernel = getenv("HC_WAIT_KERNEL") != nullptr;
+  WaitFn fn = use_kernel ? nullptr : wait_value_fn();
+  if (fn && fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value,
+               CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS)
+    return cudaSuccess;
+  wait_kernel<<<1, 1, 0, stream>>>(d_flag, value);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_append_rows(const void* step_rows, int rows_in_step, int h0, int nh, int d,
                                const AppendDst* d_dsts, int n_rows, cudaStream_t stream) {
   if (n_rows <= 0 || nh <= 0) return cudaSuccess;
@@ -140,15 +183,7 @@ extern "C" {
 hc_status hc_stream_wait_flag(void* stream, const uint32_t* d_flag, uint32_t value) {
   return guard([&] {
     if (!d_flag) fail(HC_EINVAL, "wait_flag: null flag");
-    static const bool use_kernel = getenv("HC_WAIT_KERNEL") != nullptr;
-    WaitFn fn = use_kernel ? nullptr : wait_value_fn();
-    if (fn) {
-      const CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag),
-                            value, CU_STREAM_WAIT_VALUE_GEQ);
-      if (r == CUDA_SUCCESS) return;
-    }
-    wait_kernel<<<1, 1, 0, as_stream(stream)>>>(d_flag, value);
-    HC_CUDA(cudaGetLastError());
+    HC_CUDA(wait_flag_geq(as_stream(stream), d_flag, value));
   });
 }
 
@@ -191,16 +226,29 @@ hc_status hc_project_multi_source(const hc_weights* w, int32_t layer, int32_t n_
     DeviceGuard dg(w->device);
     cudaStream_t s = as_stream(stream);
     const int d = w->cfg.d_hidden, N = 2 * w->d_kv;
-    StreamScratch stats(size_t(n) * 2 * sizeof(float), s);
+    const bool norm = w->cfg.norm_enabled != 0;
+    const bool center = norm && ln_center_enabled();
+    StreamScratch stats(size_t(n) * 2 * sizeof(float) + 16, s);
     float* mean = static_cast<float*>(stats.ptr);
     float* rstd = mean + n;
+    int32_t* flag = reinterpret_cast<int32_t*>(rstd + n);
+    // the LayerNorm fold's guard for rows with |mean| >> sigma, as in the
+    // single-GPU path: the statistics raise one flag for the matrix, and the
+    // mean-shifted rows of every source are written into a local copy that K1
+    // reads instead (the sources are other GPUs' buffers: never written here;
+    // the copy is only touched when the flag is set)
+    StreamScratch centered(center ? size_t(n) * size_t(d) * 2 : 0, s);
+    if (center) HC_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
     AMaps am;
     am.n = 0;
     const uint32_t abox = uint32_t(gemm_a_box(n));
     for (int i = 0; i < n_src; ++i) {
       const int64_t rows = row_begin[i + 1] - row_begin[i];
       if (rows == 0) continue;  // empty range (more ranks than row blocks)
-      if (w->cfg.norm_enabled)
+      if (center)
+        HC_CUDA(launch_row_stats_flagged(d_src[i], rows, d, d, true, mean + row_begin[i],
+                                         rstd + row_begin[i], flag, s));
+      else if (norm)
         HC_CUDA(launch_row_stats(d_src[i], rows, d, d, true, mean + row_begin[i],
                                  rstd + row_begin[i], s));
       if (!make_tmap_kmajor(&am.m[am.n], d_src[i], uint64_t(d), uint64_t(rows), uint64_t(d) * 2,
@@ -210,13 +258,27 @@ hc_status hc_project_multi_source(const hc_weights* w, int32_t layer, int32_t n_
       ++am.n;
     }
     am.row0[am.n] = 0x7fffffff;
+    if (center) {
+      // (after every statistics launch: the flag is final)
+      for (int i = 0; i < n_src; ++i) {
+        const int64_t rows = row_begin[i + 1] - row_begin[i];
+        if (rows == 0) continue;
+        HC_CUDA(launch_center_rows(d_src[i], rows, d, d, mean + row_begin[i], flag,
+                                   static_cast<char*>(centered.ptr) + size_t(row_begin[i]) * d * 2,
+                                   s));
+      }
+      if (!make_tmap_kmajor(&am.m[am.n], centered.ptr, uint64_t(d), uint64_t(n), uint64_t(d) * 2,
+                            abox))
+        fail(HC_ECUDA, "cuTensorMapEncodeTiled failed (centered rows)");
+      am.alt_flag = flag;
+    }
     const int sms = device_sm_count(w->device);
     const int bn = gemm_pick_bn(n, N, sms);
     KvOut out = kv_out_pages(pages, layer, d_page_table, 0, nullptr, 1);
     out.start_pos = start_pos;
     HC_CUDA(launch_restore_kv_multi(am, weight_map(L, bn, d, N), bn, int(n), N, d, true, out,
-                                    epi_for(w, L.colsum, w->cfg.norm_enabled ? mean : nullptr,
-                                            w->cfg.norm_enabled ? rstd : nullptr),
+                                    epi_for(w, L.colsum, norm ? mean : nullptr,
+                                            norm ? rstd : nullptr),
                                     sms, s));
   });
 }

@@ -418,11 +418,32 @@ hc_status hc_plan_token_split(const hc_timings* t, int32_t prefetch_depth, const
 }
 
 double hc_timeline_lane_busy(const hc_timeline* tl, int32_t lane) {
-  // Timeline::lane_busy (pipeline.cpp:9-14)
+  // Timeline::lane_busy (pipeline.cpp:9-14) sums event durations: the
+  // reference's lanes are strictly serial, so that is the time the lane was
+  // busy. The device executor's compute lane is not (consecutive K1 launches
+  // alternate two streams, row statistics run on a side stream), so busy time
+  // is the length of the union of the lane's intervals -- identical to the
+  // sum whenever events do not overlap (every simulated timeline).
   if (!tl) return 0;
-  double b = 0;
+  std::vector<std::pair<double, double>> iv;
+  iv.reserve(size_t(std::max(0, tl->n_events)));
   for (int i = 0; i < tl->n_events; ++i)
-    if (tl->events[i].lane == lane) b += tl->events[i].end_s - tl->events[i].start_s;
+    if (tl->events[i].lane == lane && tl->events[i].end_s > tl->events[i].start_s)
+      iv.emplace_back(tl->events[i].start_s, tl->events[i].end_s);
+  std::sort(iv.begin(), iv.end());
+  double b = 0, cur_s = 0, cur_e = 0;
+  bool open = false;
+  for (const auto& [s, e] : iv) {
+    if (open && s < cur_e) {
+      cur_e = std::max(cur_e, e);
+      continue;
+    }
+    if (open) b += cur_e - cur_s;
+    cur_s = s;
+    cur_e = e;
+    open = true;
+  }
+  if (open) b += cur_e - cur_s;
   return b;
 }
 

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "common.h"
+#include "engine.h"
 #include "kernels.h"
 #include "recompute.h"
 #include "store.h"
@@ -33,10 +34,6 @@ std::string plan_serialize(const hc_plan* p);
 
 namespace {
 
-// Per-device engine state: the IO lane's copy streams (a layer's gather is
-// split over kCopyStreams so several copy engines share the PCIe link) and a
-// memory pool that keeps the staging ring cached across restores.
-constexpr int kCopyStreams = 4;
 // IO-lane width actually used (HC_COPY_STREAMS, 1..kCopyStreams; default 1)
 int copy_streams() {
   static int v = [] {
@@ -45,32 +42,6 @@ int copy_streams() {
     return std::max(1, std::min(kCopyStreams, x));
   }();
   return v;
-}
-struct Engine {
-  cudaStream_t copy = nullptr;  // IO lane head: orders fetches, joins the helpers
-  cudaStream_t helper[kCopyStreams - 1] = {};
-  cudaStream_t aux = nullptr;   // row statistics running ahead of the compute lane
-  cudaStream_t aux2 = nullptr;  // second K1 lane of a resident restore
-  bool init = false;
-};
-
-Engine& engine(int dev) {
-  static std::mutex mu;
-  static std::vector<Engine> engines(64);
-  std::lock_guard<std::mutex> lk(mu);
-  Engine& e = engines[size_t(dev)];
-  if (!e.init) {
-    HC_CUDA(cudaStreamCreateWithFlags(&e.copy, cudaStreamNonBlocking));
-    for (auto& h : e.helper) HC_CUDA(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking));
-    HC_CUDA(cudaStreamCreateWithFlags(&e.aux, cudaStreamNonBlocking));
-    HC_CUDA(cudaStreamCreateWithFlags(&e.aux2, cudaStreamNonBlocking));
-    cudaMemPool_t pool;
-    HC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t thresh = UINT64_MAX;
-    HC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
-    e.init = true;
-  }
-  return e;
 }
 
 struct Ev {
@@ -83,10 +54,6 @@ struct Ev {
   Ev& operator=(const Ev&) = delete;
 };
 
-struct TimedOp {
-  int lane, layer, kind;
-  cudaEvent_t start, end;
-};
 
 void copy_seg(const CopySeg& g, uint8_t* dst, cudaStream_t s) {
   cudaError_t e;
@@ -133,8 +100,27 @@ std::vector<std::vector<CopySeg>> split_gather(const std::vector<CopySeg>& segs,
   return out;
 }
 
-// Gather on the IO lane: the head stream forks to the helper streams and
-// joins them again, so the lane stays one ordered sequence of layer fetches.
+}  // namespace
+
+Engine& engine(int dev) {
+  static std::mutex mu;
+  static std::vector<Engine> engines(64);
+  std::lock_guard<std::mutex> lk(mu);
+  Engine& e = engines[size_t(dev)];
+  if (!e.init) {
+    HC_CUDA(cudaStreamCreateWithFlags(&e.copy, cudaStreamNonBlocking));
+    for (auto& h : e.helper) HC_CUDA(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking));
+    HC_CUDA(cudaStreamCreateWithFlags(&e.aux, cudaStreamNonBlocking));
+    HC_CUDA(cudaStreamCreateWithFlags(&e.aux2, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    HC_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thresh = UINT64_MAX;
+    HC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    e.init = true;
+  }
+  return e;
+}
+
 void issue_gather(const std::vector<CopySeg>& segs, uint8_t* dst, Engine& eng,
                   std::vector<cudaEvent_t>& scratch_events, cudaEvent_t (*make)(void*), void* ctx) {
   const int width = copy_streams();
@@ -159,28 +145,6 @@ void issue_gather(const std::vector<CopySeg>& segs, uint8_t* dst, Engine& eng,
   scratch_events.clear();
 }
 
-// Lazily created CUDA events, destroyed with the object.
-struct EventPool {
-  std::vector<cudaEvent_t> all;
-  bool timing;
-  explicit EventPool(bool t) : timing(t) {}
-  cudaEvent_t get() {
-    cudaEvent_t e;
-    HC_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
-    all.push_back(e);
-    return e;
-  }
-  ~EventPool() {
-    for (auto e : all) cudaEventDestroy(e);
-  }
-  static cudaEvent_t make(void* self) {
-    EventPool* p = static_cast<EventPool*>(self);
-    cudaEvent_t e;
-    HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    p->all.push_back(e);
-    return e;
-  }
-};
 
 void fill_timeline(hc_timeline* tl, cudaEvent_t t0, const std::vector<TimedOp>& ops) {
   std::memset(tl, 0, sizeof(*tl));
@@ -204,10 +168,6 @@ void fill_timeline(hc_timeline* tl, cudaEvent_t t0, const std::vector<TimedOp>& 
     }
 }
 
-struct LayerJob {
-  int layer;
-  int method;
-};
 
 std::vector<LayerJob> compute_order(const hc_plan& p) {
   // restore.cpp:50-63: recompute prefix, hidden, KV suffix
@@ -238,8 +198,6 @@ int k1_lanes(int64_t rows) {
   }();
   return env_lanes == 1 || env_lanes == 2 ? env_lanes : (rows <= 16384 ? 2 : 1);
 }
-
-}  // namespace
 
 // --------------------------------------------------------------- restore
 // One restore of a group of sessions sharing a plan: n_sessions == 1 is the
@@ -321,6 +279,24 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
       bad("split_tokens needs a HIDDEN layer right after the recompute prefix");
   }
 
+  // Every argument check the launches below would make runs here, before the
+  // first H2D copy is queued: a throw after that point would unwind with
+  // copies still in flight into the staging rings.
+  for (const auto& mm : ms)
+    if (w->cfg.rope_enabled && mm.n_tokens > w->rope_rows)
+      bad("session longer than max_seq (RoPE table)");
+  if (n_kv && pages->dtype != HC_DTYPE_BF16) bad("KV-offload layers need bf16 pages");
+  if (n_re > 0 || split > 0) {
+    if (!w->embedding) bad("RECOMPUTE prefix needs the embedding");
+    if (w->d_kv != w->d_kv_all) bad("RECOMPUTE prefix needs all KV heads on this GPU");
+    if (pages->dtype != HC_DTYPE_BF16) bad("RECOMPUTE prefix needs bf16 pages");
+    for (int l = 0; l < n_re + (split ? 1 : 0); ++l)
+      if (!w->layers[size_t(l)].full) bad("RECOMPUTE prefix needs full block weights");
+  }
+  for (const auto& j : order)
+    if (j.method == HC_METHOD_HIDDEN && !w->layers[size_t(j.layer)].ready)
+      bad("layer weights not set for a HIDDEN layer");
+
   const size_t h_row = size_t(m.d_hidden) * size_t(eb), kv_row = size_t(2 * m.d_kv) * size_t(eb);
   const size_t h_bytes = size_t(n) * h_row;
   const size_t kv_bytes = size_t(n) * kv_row;
@@ -389,6 +365,11 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
   StreamScratch hstats(side_stats ? size_t(n_hidden) * 2 * size_t(n) * sizeof(float) : 0, stream);
   StreamScratch hflags(center ? size_t(n_hidden) * sizeof(int32_t) : 0, stream);
   if (center) HC_CUDA(cudaMemsetAsync(hflags.ptr, 0, size_t(n_hidden) * sizeof(int32_t), stream));
+
+  // On an exception after work was queued on the side lanes, join them into
+  // the caller stream before the scratch buffers above are released
+  // (destroyed first: declared after them).
+  LaneJoin unwind_join(stream, {eng.copy, eng.aux, eng.aux2});
 
   cudaEvent_t t0 = evp.get();
   HC_CUDA(cudaEventRecord(t0, stream));
@@ -619,6 +600,12 @@ void restore_token_wise(hc_store* st, const char* sid_c, const hc_weights* w, in
   if (s_tok < n && (m.d_kv != w->d_kv || w->d_kv != w->d_kv_all))
     fail(HC_EINVAL, "restore_token_wise: KV rows need all KV heads on this GPU");
   validate_pages(w, pages, w->d_kv);
+  if (s_tok < n && pages->dtype != HC_DTYPE_BF16)
+    fail(HC_EINVAL, "restore_token_wise: spliced KV rows need bf16 pages");
+  if (w->cfg.rope_enabled && n > w->rope_rows)
+    fail(HC_EINVAL, "restore_token_wise: session longer than max_seq (RoPE table)");
+  for (int layer = 0; layer < L && s_tok > 0; ++layer)
+    if (!w->layers[size_t(layer)].ready) fail(HC_EINVAL, "restore_token_wise: layer weights not set");
   DeviceGuard dg(w->device);
   Engine& eng = engine(w->device);
   const bool timed = tl != nullptr;
@@ -630,6 +617,7 @@ void restore_token_wise(hc_store* st, const char* sid_c, const hc_weights* w, in
   const int nbuf = std::min(L, 2);
   StreamScratch ring_h(s_tok > 0 ? h_bytes * size_t(nbuf) : 0, stream);
   StreamScratch ring_kv(s_tok < n ? kv_bytes * size_t(nbuf) : 0, stream);
+  LaneJoin unwind_join(stream, {eng.copy});
   cudaEvent_t t0 = evp.get();
   HC_CUDA(cudaEventRecord(t0, stream));
   HC_CUDA(cudaStreamWaitEvent(eng.copy, t0, 0));
@@ -716,8 +704,10 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
     if (!w || !d_hidden_layers || !pages || !d_page_table)
       fail(HC_EINVAL, "restore_resident: null argument");
     validate_pages(w, pages, w->d_kv);
+    if (d_cu_seqlens && n_seqs < 1) fail(HC_EINVAL, "restore_resident: n_seqs < 1");
     DeviceGuard dg(w->device);
     cudaStream_t s = as_stream(stream);
+    check_seq_positions(w, d_cu_seqlens, n_seqs, n_rows, s);
     const int L = w->cfg.n_layers, d = w->cfg.d_hidden;
     // every layer's rows are resident: the row statistics (and the
     // mean-shift check, launch_center_rows, into a ring of two buffers) of

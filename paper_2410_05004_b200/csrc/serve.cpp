@@ -480,6 +480,23 @@ void Engine::persist(const std::string& sid, bool exists, const std::vector<int3
     seed.n_tokens = int64_t(round_tokens.size());
     st_.create_session(seed);
   }
+  // KV-offload layers: gather the rows out of the pages on the compute
+  // stream, so the gather is ordered before any later work on s_ that
+  // reuses these pages (complete() returns them to the free list right after
+  // this call); the save stream then only reads the private gathered buffer.
+  void* kvbuf = nullptr;
+  const size_t kvb = size_t(n_rows) * size_t(2 * dkv_) * 2;
+  if (kvr_.count > 0) {
+    HC_CUDA(cudaMallocAsync(&kvbuf, kvb * size_t(kvr_.count), s_));
+    StreamScratch table(a.pages.size() * sizeof(int32_t), s_);
+    HC_CUDA(cudaMemcpyAsync(table.ptr, a.pages.data(), a.pages.size() * sizeof(int32_t),
+                            cudaMemcpyHostToDevice, s_));
+    // (pageable source: staged by the driver before the call returns)
+    for (int l = 0; l < kvr_.count; ++l)
+      if (hc_kv_gather_rows(&pages_, kvr_.begin + l, static_cast<int32_t*>(table.ptr), row_begin,
+                            n_rows, static_cast<char*>(kvbuf) + kvb * size_t(l), s_) != HC_OK)
+        fail(HC_ECUDA, std::string("serve: kv gather: ") + hc_last_error());
+  }
   // the save stream picks up everything the compute stream produced so far
   cudaEvent_t produced;
   HC_CUDA(cudaEventCreateWithFlags(&produced, cudaEventDisableTiming));
@@ -507,22 +524,8 @@ void Engine::persist(const std::string& sid, bool exists, const std::vector<int3
               size_t(l) * size_t(dev_hidden_rows ? hid_pitch : a.cap) * rb,
           true, d_);
   }
-  void* kvbuf = nullptr;
-  if (kvr_.count > 0) {
-    const size_t kvb = size_t(n_rows) * size_t(2 * dkv_) * 2;
-    HC_CUDA(cudaMallocAsync(&kvbuf, kvb * size_t(kvr_.count), save_));
-    StreamScratch table(a.pages.size() * sizeof(int32_t), save_);
-    HC_CUDA(cudaMemcpyAsync(table.ptr, a.pages.data(), a.pages.size() * sizeof(int32_t),
-                            cudaMemcpyHostToDevice, save_));
-    // (pageable source: staged by the driver before the call returns)
-    for (int l = 0; l < kvr_.count; ++l) {
-      void* dst = static_cast<char*>(kvbuf) + kvb * size_t(l);
-      if (hc_kv_gather_rows(&pages_, kvr_.begin + l, static_cast<int32_t*>(table.ptr), row_begin,
-                            n_rows, dst, save_) != HC_OK)
-        fail(HC_ECUDA, std::string("serve: kv gather: ") + hc_last_error());
-      put(kvr_.begin + l, HC_STATE_KV, dst, true, 2 * dkv_);
-    }
-  }
+  for (int l = 0; l < kvr_.count; ++l)
+    put(kvr_.begin + l, HC_STATE_KV, static_cast<char*>(kvbuf) + kvb * size_t(l), true, 2 * dkv_);
   if (kvbuf) HC_CUDA(cudaFreeAsync(kvbuf, save_));
   if (a.acc) {
     HC_CUDA(cudaFreeAsync(a.acc, save_));

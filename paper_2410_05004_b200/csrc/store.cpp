@@ -269,10 +269,14 @@ void Store::reopen_for_append(const std::string& sid, const int32_t* toks, int64
 
 bool Store::snapshot(const std::string& sid, int layer, int kind, const void* rows,
                      int64_t n_rows, int row_width, int src_dtype, bool src_on_device,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, int64_t tok_begin) {
   // snapshot (storage.cpp:129-149)
   std::lock_guard<std::mutex> lk(mu_);
   Session& s = find_open(sid);
+  if (tok_begin >= 0 && tok_begin % HC_CHUNK_TOKENS != 0)
+    fail(HC_EINVAL, "snapshot_range: tok_begin must be a multiple of 64");
+  if (tok_begin > int64_t(s.tokens.size()))
+    fail(HC_EINVAL, "snapshot_range: tok_begin beyond the session's tokens");
   if (s.finalized) fail(HC_ERUNTIME, "snapshot after finalize: " + sid);
   if (kind != HC_STATE_HIDDEN && kind != HC_STATE_KV) fail(HC_EINVAL, "snapshot: bad kind");
   if (row_width != s.width(kind)) fail(HC_EINVAL, "snapshot: bad row width");
@@ -291,6 +295,7 @@ bool Store::snapshot(const std::string& sid, int layer, int kind, const void* ro
   rec.layer = layer;
   rec.kind = kind;
   rec.bytes = bytes;
+  rec.tok_begin = tok_begin;
   rec.buf = static_cast<uint8_t*>(pool_mem_.alloc(bytes ? bytes : 1));
   if (src_on_device) {
     if (src_dtype != s.dtype) {
@@ -312,7 +317,8 @@ bool Store::snapshot(const std::string& sid, int layer, int kind, const void* ro
   return true;
 }
 
-uint8_t* Store::new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx) {
+uint8_t* Store::new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx,
+                         int expect_chunks) {
   const int dev = (layer + chunk_idx) % ndev_;  // device_for_chunk (storage.cpp:29-31)
   if (ls.extents.empty()) ls.extents.resize(size_t(ndev_));
   auto& ex = ls.extents[size_t(dev)];
@@ -325,8 +331,6 @@ uint8_t* Store::new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx) 
     const int max_slots = std::max<int>(1, int((size_t(256) << 20) / cb));
     int cap;
     if (ex.cap == 0) {
-      const int expect_tokens = int(s.tokens.size());
-      const int expect_chunks = (expect_tokens + HC_CHUNK_TOKENS - 1) / HC_CHUNK_TOKENS;
       cap = std::max(8, (expect_chunks + ndev_ - 1) / ndev_);
     } else {
       cap = ex.cap * 2;
@@ -355,10 +359,29 @@ int64_t Store::flush_record(Record& rec) {
   LayerStream& ls = s.streams[{rec.layer, rec.kind}];
   ls.kind = rec.kind;
   const size_t cb = s.chunk_bytes(rec.kind), tb = s.token_bytes(rec.kind);
+  // first extent per device: sized for the chunks this stream will hold -- a
+  // whole session, or (range snapshots) this record's own chunks
+  int expect_chunks =
+      int((s.tokens.size() + HC_CHUNK_TOKENS - 1) / HC_CHUNK_TOKENS);
+  if (rec.tok_begin >= 0) {
+    if (rec.tok_begin != ls.n_tokens) {
+      if (ls.n_tokens != 0 || !ls.chunks.empty()) {
+        pool_mem_.release(rec.buf, rec.bytes ? rec.bytes : 1);
+        fail(HC_EINVAL, "snapshot_range: tokens must continue the layer's stored range");
+      }
+      // a shard stream: chunks [0, tok_begin/64) are held by other ranks
+      const int c0 = int(rec.tok_begin / HC_CHUNK_TOKENS);
+      for (int c = 0; c < c0; ++c)
+        ls.chunks.push_back(ChunkRef{(rec.layer + c) % ndev_, nullptr, -1});
+      ls.next_chunk_idx = ls.first_stored = c0;
+      ls.n_tokens = int(rec.tok_begin);
+    }
+    expect_chunks = int((rec.bytes + cb - 1) / cb);
+  }
   size_t off = 0;
   while (off < rec.bytes) {
     if (ls.partial_bytes == 0 && int(ls.chunks.size()) == ls.next_chunk_idx)
-      new_slot(s, ls, rec.layer, ls.next_chunk_idx);
+      new_slot(s, ls, rec.layer, ls.next_chunk_idx, expect_chunks);
     const size_t take = std::min(cb - ls.partial_bytes, rec.bytes - off);
     std::memcpy(ls.chunks[size_t(ls.next_chunk_idx)].ptr + ls.partial_bytes, rec.buf + off, take);
     off += take;
@@ -491,6 +514,10 @@ std::vector<CopySeg> Store::gather_plan(const std::string& sid, int layer, int k
   if (e < 0) e = ls.n_tokens;
   if (b < 0 || b >= e || e > ls.n_tokens || b % HC_CHUNK_TOKENS != 0)
     fail(HC_EINVAL, "read_layer: bad token range");
+  if (b < ls.first_stored * HC_CHUNK_TOKENS)
+    fail(HC_ENOENT, "layer " + std::to_string(layer) + ": tokens below " +
+                        std::to_string(ls.first_stored * HC_CHUNK_TOKENS) +
+                        " are not held by this shard");
   const int64_t cb = int64_t(s.chunk_bytes(kind)), tb = int64_t(s.token_bytes(kind));
   const int c_first = b / HC_CHUNK_TOKENS, c_last = (e - 1) / HC_CHUNK_TOKENS;
   auto chunk_len = [&](int c) {  // tokens of chunk c inside [b, e)
@@ -531,7 +558,8 @@ void Store::chunk_info(const std::string& sid, int layer, int kind, int c, int* 
   if (it == s.streams.end()) fail(HC_ENOENT, "chunk_info: layer not stored");
   const LayerStream& ls = it->second;
   const int n_chunks = ls.next_chunk_idx + (ls.partial_bytes ? 1 : 0);
-  if (c < 0 || c >= n_chunks) fail(HC_ENOENT, "chunk_info: no such chunk");
+  if (c < 0 || c >= n_chunks || !ls.chunks[size_t(c)].ptr)
+    fail(HC_ENOENT, "chunk_info: no such chunk");
   if (dev) *dev = ls.chunks[size_t(c)].device;
   if (payload) *payload = ls.chunks[size_t(c)].ptr;
   if (bytes)
@@ -546,7 +574,7 @@ std::vector<int64_t> Store::device_chunk_counts() const {
   for (const auto& kv : sessions_)
     for (const auto& st : kv.second.streams) {
       const LayerStream& ls = st.second;
-      for (int c = 0; c < int(ls.chunks.size()); ++c)
+      for (int c = ls.first_stored; c < int(ls.chunks.size()); ++c)
         if (c < ls.next_chunk_idx || kv.second.finalized || kv.second.ever_finalized)
           ++out[size_t(ls.chunks[size_t(c)].device)];
     }
@@ -664,6 +692,21 @@ hc_status hc_store_snapshot(hc_store* s, const char* sid, int32_t layer, int32_t
   hc_status g = guard([&] {
     if (!S(s).snapshot(SID(sid), layer, kind, rows, n_rows, row_width, src_dtype,
                        src_on_device != 0, as_stream(stream)))
+      st = HC_EAGAIN;
+  });
+  if (g == HC_OK && st == HC_EAGAIN) set_last_error("snapshot: buffer full (backpressure)");
+  return g != HC_OK ? g : st;
+}
+
+hc_status hc_store_snapshot_range(hc_store* s, const char* sid, int32_t layer, int32_t kind,
+                                  int64_t tok_begin, const void* rows, int64_t n_rows,
+                                  int32_t row_width, int32_t src_dtype, int32_t src_on_device,
+                                  void* stream) {
+  hc_status st = HC_OK;
+  hc_status g = guard([&] {
+    if (tok_begin < 0) fail(HC_EINVAL, "snapshot_range: negative tok_begin");
+    if (!S(s).snapshot(SID(sid), layer, kind, rows, n_rows, row_width, src_dtype,
+                       src_on_device != 0, as_stream(stream), tok_begin))
       st = HC_EAGAIN;
   });
   if (g == HC_OK && st == HC_EAGAIN) set_last_error("snapshot: buffer full (backpressure)");

@@ -64,6 +64,7 @@ struct LayerStream {
   int kind = 0;
   int n_tokens = 0;         // tokens stored so far
   int next_chunk_idx = 0;   // index of the chunk being filled (== full chunks)
+  int first_stored = 0;     // shard streams: chunks [0, first_stored) are held elsewhere
   size_t partial_bytes = 0; // bytes in the chunk being filled
   std::vector<ChunkRef> chunks;  // every started chunk, in chunk order
   // per device: current extent (consecutive slots)
@@ -110,8 +111,12 @@ class Store {
 
   void create_session(const hc_session_seed& seed);
   void reopen_for_append(const std::string& sid, const int32_t* toks, int64_t n);
+  // tok_begin >= 0 (chunk aligned): the rows are tokens [tok_begin, ..) of
+  // the layer -- a head-sharded rank stores only its own token range; the
+  // stream's earlier chunks then belong to other ranks. -1: append.
   bool snapshot(const std::string& sid, int layer, int kind, const void* rows, int64_t n_rows,
-                int row_width, int src_dtype, bool src_on_device, cudaStream_t stream);
+                int row_width, int src_dtype, bool src_on_device, cudaStream_t stream,
+                int64_t tok_begin = -1);
   int64_t drain(int64_t max_chunks);
   void finalize(const std::string& sid);
   hc_manifest open(const std::string& sid) const;
@@ -149,12 +154,13 @@ class Store {
     uint8_t* buf = nullptr;
     size_t bytes = 0;
     cudaEvent_t ready = nullptr;  // D2H completion (device-sourced rows)
+    int64_t tok_begin = -1;       // range snapshot (shard sessions)
   };
   // block=false stops at the first record whose device->host copy is still
   // in flight (the daemon never waits on the GPU while holding mu_).
   int64_t drain_locked(int64_t max_chunks, bool block = true);
   int64_t flush_record(Record& rec);
-  uint8_t* new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx);
+  uint8_t* new_slot(Session& s, LayerStream& ls, int layer, int chunk_idx, int expect_chunks);
   Session& find_open(const std::string& sid);
 
   int ndev_;

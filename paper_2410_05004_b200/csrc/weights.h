@@ -62,4 +62,9 @@ KvOut kv_out_pages(const hc_kv_pages* pages, int layer, const int32_t* page_tabl
 
 void validate_pages(const hc_weights* w, const hc_kv_pages* pages, int d_kv_expected);
 
+// Fails with HC_EINVAL when a sequence of a ragged batch (device offsets
+// d_cu_seqlens) is longer than the RoPE table (may read the offsets back).
+void check_seq_positions(const hc_weights* w, const int32_t* d_cu_seqlens, int n_seqs,
+                         int64_t n_rows, cudaStream_t stream);
+
 }  // namespace hc

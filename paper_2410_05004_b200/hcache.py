@@ -144,8 +144,24 @@ def makespan(p: RestorationPlan, t: ProfiledTimings) -> float:
     return out.value
 
 
-def plan_three_way(t: ProfiledTimings, prefetch_depth: int = 1):
-    """B200 planner: (plan, bounded-staging makespan)."""
+def executor_depth(n_layers: int, layer_bytes: Optional[int] = None) -> int:
+    """The staging depth restore() uses by default (ThrottleConfig
+    prefetch_depth 0, restore.cpp auto_depth): every hidden layer staged, up
+    to an 8 GiB ring; without `layer_bytes` (one layer's staged hidden bytes)
+    the budget is assumed to hold all of them."""
+    if not layer_bytes:
+        return max(1, n_layers)
+    fit = max(2, (8 << 30) // max(1, int(layer_bytes)))
+    return max(1, min(n_layers, fit) - 1)
+
+
+def plan_three_way(t: ProfiledTimings, prefetch_depth: Optional[int] = None,
+                   layer_bytes: Optional[int] = None):
+    """B200 planner: (plan, bounded-staging makespan). prefetch_depth
+    defaults to the executor's own (executor_depth), so the plan is costed
+    under the staging bound restore() will actually run with."""
+    if prefetch_depth is None:
+        prefetch_depth = executor_depth(t.n_layers, layer_bytes)
     p = capi.PlanC()
     out = C.c_double()
     check(lib().hc_plan_three_way(C.byref(t._c()), prefetch_depth, C.byref(p), C.byref(out)))
@@ -153,10 +169,12 @@ def plan_three_way(t: ProfiledTimings, prefetch_depth: int = 1):
 
 
 def plan_token_split(t: ProfiledTimings, plan: "RestorationPlan", n_tokens: int,
-                     prefetch_depth: int = 1):
+                     prefetch_depth: Optional[int] = None, layer_bytes: Optional[int] = None):
     """B200 extension: (split_tokens, makespan) -- how many tokens of the
     plan's first layer after the recompute prefix to recompute instead of
     fetching (ThrottleConfig.split_tokens); 0 when no split helps."""
+    if prefetch_depth is None:
+        prefetch_depth = executor_depth(t.n_layers, layer_bytes)
     sp = C.c_int32()
     out = C.c_double()
     check(lib().hc_plan_token_split(C.byref(t._c()), prefetch_depth, C.byref(plan._c), n_tokens,
@@ -189,7 +207,21 @@ class Timeline:
         return Timeline(ev, tc.total_s, tc.fill_s, tc)
 
     def lane_busy(self, lane: Lane) -> float:
-        return sum(e.end_s - e.start_s for e in self.events if e.lane == lane)
+        """Time the lane was busy: the union of its event intervals (the
+        reference's sum, pipeline.cpp:9-14, whenever events do not overlap)."""
+        if self._c is not None:
+            return lib().hc_timeline_lane_busy(C.byref(self._c), int(lane))
+        iv = sorted((e.start_s, e.end_s) for e in self.events
+                    if e.lane == lane and e.end_s > e.start_s)
+        busy, cur = 0.0, None
+        for a, b in iv:
+            if cur is not None and a < cur[1]:
+                cur[1] = max(cur[1], b)
+                continue
+            if cur is not None:
+                busy += cur[1] - cur[0]
+            cur = [a, b]
+        return busy + (cur[1] - cur[0] if cur is not None else 0.0)
 
     def bubble_fraction(self) -> float:
         out = C.c_double()
@@ -324,18 +356,19 @@ class StorageManager:
         check(lib().hc_store_reopen_for_append(self._h, sid.encode(), toks, len(new_tokens)))
 
     def snapshot(self, sid: str, layer: int, kind: StateKind, rows, dtype: int = None,
-                 stream=None) -> bool:
+                 stream=None, tok_begin: Optional[int] = None) -> bool:
         """Host numpy rows (float32, or uint16 bf16 bits with dtype) or a CUDA
         torch tensor (session dtype; copied D2H on `stream`). False on
-        backpressure, like the reference."""
+        backpressure, like the reference. tok_begin: the rows are tokens
+        [tok_begin, ...) of the layer (hc_store_snapshot_range: a head-sharded
+        rank's own token range)."""
         if hasattr(rows, "is_cuda") and rows.is_cuda:
             import torch
             assert rows.is_contiguous()
             src_dtype = {torch.bfloat16: capi.HC_DTYPE_BF16, torch.float16: capi.HC_DTYPE_F16,
                          torch.float32: capi.HC_DTYPE_F32}[rows.dtype]
             s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
-            st = lib().hc_store_snapshot(self._h, sid.encode(), layer, int(kind), rows.data_ptr(),
-                                         rows.shape[0], rows.shape[1], src_dtype, 1, s)
+            args = (rows.data_ptr(), rows.shape[0], rows.shape[1], src_dtype, 1, s)
         else:
             rows = np.ascontiguousarray(rows)
             if dtype is None:
@@ -343,9 +376,12 @@ class StorageManager:
                 src_dtype = capi.HC_DTYPE_F32
             else:
                 src_dtype = dtype
-            st = lib().hc_store_snapshot(self._h, sid.encode(), layer, int(kind),
-                                         rows.ctypes.data, rows.shape[0], rows.shape[1],
-                                         src_dtype, 0, None)
+            args = (rows.ctypes.data, rows.shape[0], rows.shape[1], src_dtype, 0, None)
+        if tok_begin is None:
+            st = lib().hc_store_snapshot(self._h, sid.encode(), layer, int(kind), *args)
+        else:
+            st = lib().hc_store_snapshot_range(self._h, sid.encode(), layer, int(kind),
+                                               int(tok_begin), *args)
         if st == capi.HC_EAGAIN:
             return False
         check(st)
@@ -566,6 +602,80 @@ class KvCache:
         pages = pt[pos // self.page_size]
         slots = pos % self.page_size
         return self.k[layer][pages, slots], self.v[layer][pages, slots]
+
+
+# ------------------------------------------------- multi-GPU (head sharded)
+def shard_range(n_tokens: int, world: int, rank: int):
+    """[begin, end) token range rank `rank` fetches (128-row aligned)."""
+    b, e = C.c_int64(), C.c_int64()
+    check(lib().hc_shard_range(n_tokens, world, rank, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def shard_heads(n_kv_heads: int, world: int, rank: int):
+    """(first KV head, count) projected by `rank`."""
+    b, c = C.c_int32(), C.c_int32()
+    check(lib().hc_shard_heads(n_kv_heads, world, rank, C.byref(b), C.byref(c)))
+    return b.value, c.value
+
+
+class PeerGroup:
+    """This rank's member of a head-sharded restore (hc_peer_group): staging
+    slots + flags in HBM, exported with CUDA IPC. `exchange(blob) -> list of
+    every rank's blob` is any all-gather of bytes (torch.distributed
+    all_gather_object on gloo or NCCL here; MPI / sockets in a C++ host)."""
+
+    def __init__(self, world: int, rank: int, d_hidden: int, max_rows: int, depth: int = 2,
+                 device: int = 0, exchange=None):
+        self.world, self.rank, self.device = world, rank, device
+        h = C.c_void_p()
+        check(lib().hc_peer_group_create(world, rank, device, d_hidden, max_rows, depth,
+                                         C.byref(h)))
+        self._h = h
+        if world > 1:
+            n = lib().hc_peer_group_blob_size()
+            buf = C.create_string_buffer(n)
+            check(lib().hc_peer_group_export(self._h, buf, n))
+            blobs = exchange(bytes(buf.raw))
+            keep = [C.create_string_buffer(b, len(b)) for b in blobs]
+            arr = (C.c_void_p * world)(*[C.cast(k, C.c_void_p) for k in keep])
+            check(lib().hc_peer_group_import(self._h, arr))
+
+    @staticmethod
+    def torch_exchange(group=None):
+        import torch.distributed as dist
+
+        def ex(blob: bytes):
+            out = [None] * dist.get_world_size(group)
+            dist.all_gather_object(out, blob, group=group)
+            return out
+        return ex
+
+    def close(self):
+        if self._h:
+            lib().hc_peer_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def restore_sharded(group: PeerGroup, store: "StorageManager", sid: str, w: "Weights",
+                    plan: "RestorationPlan", throttle: "ThrottleConfig", kv: "KvCache",
+                    page_table, stream=None, timeline: bool = False):
+    """hc_restore_sharded: this rank's share of a head-sharded restore (all
+    ranks call it with the same session plan). Returns a Timeline when
+    `timeline`, else the work is queued on `stream`."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    tl = capi.TimelineC() if timeline else None
+    check(lib().hc_restore_sharded(group._h, store._h, sid.encode(), w._h, C.byref(plan._c),
+                                   C.byref(throttle._c()), C.byref(kv.desc),
+                                   page_table.data_ptr(), s, C.byref(tl) if tl else None))
+    return Timeline.from_c(tl) if tl else None
 
 
 @dataclass

@@ -1,27 +1,34 @@
-"""Head-sharded multi-GPU restoration (north star (4)).
+"""Head-sharded multi-GPU restoration (north star (4)) -- host side.
 
 Every GPU needs the full [n x d] hidden state of a layer (each KV head
-contracts over all of d), while the projection output shards by KV head. So,
-per layer, on each of the N ranks (one process per GPU):
+contracts over all of d), while the projection output shards by KV head. The
+data path is the C ABI's ``hc_restore_sharded`` (csrc/sharded.cpp): rank r of
+N fetches its 128-row aligned token range of each HIDDEN layer over its own
+PCIe link into an HBM slot every other rank has mapped (CUDA IPC over
+NVLink), publishes the range's LayerNorm statistics, and every rank's K1
+reads all ranges' A tiles straight from the owners' slots (the all-gather
+fused into the GEMM) for its own KV heads. KV_OFFLOAD layers fetch only the
+rank's heads' [K|V] rows. Chunk indexing is the reference's (chunk c = tokens
+[64c, 64c+64), device (L + c) % ndev, storage.cpp:29-31).
 
-  IO      fetch this rank's chunk-aligned 1/N of the layer's tokens over its
-          own PCIe link (hc_store_read_layer_range on the copy stream);
-  gather  all-gather the N shards over NVLink (NCCL, torch.distributed) into
-          the full hidden matrix;
-  compute K1 for this rank's KV heads only (hc_project_to_pages).
+This module holds what sits around that call:
 
-The three stages run on three streams and are pipelined across layers
-(fetch L+1 || all-gather L || K1 L-1) with a bounded staging ring. Chunk
-indexing is the reference's (chunk c = tokens [64c, 64c+64), device
-(L + c) % ndev, storage.cpp:29-31); shards are whole chunks so ranks never
-split one. Timing is device time, max over ranks.
-
-The stages are functions so the same orchestration runs on gloo + CPU in the
-tests (host reads, gloo all-gather, oracle projection).
+* ``save_shard``  -- one rank's save path: its token range of each HIDDEN
+  layer (hc_store_snapshot_range) and its heads' KV rows of each KV layer;
+* ``plan_sharded`` -- the bubble-free planner at N GPUs: per-rank costs
+  (PCIe measured with every rank copying at once, K1 on the rank's heads),
+  the three-way planner without RECOMPUTE (the prefix would need the whole
+  model on one GPU), one plan agreed by all ranks;
+* ``restore_layers`` -- the orchestration in plain host terms (fetch own
+  range, all-gather, project own heads), which the gloo CPU test runs with
+  the oracle as the projection;
+* ``bench`` -- ``bench.py --gpus N``: one process per GPU, timing = max over
+  ranks.
 """
 from __future__ import annotations
 
 import ctypes as C
+import json
 import os
 import time
 from dataclasses import dataclass
@@ -32,7 +39,8 @@ from .capi import HC_CHUNK_TOKENS
 
 def shard_ranges(n_tokens: int, world: int) -> Tuple[List[Tuple[int, int]], int]:
     """Chunk-aligned contiguous token ranges per rank and the padded shard
-    size (tokens) every rank contributes to the all-gather."""
+    size (tokens) every rank contributes to an all-gather (host reference of
+    the partition; the device path uses the 128-row aligned hc_shard_range)."""
     if n_tokens < 1 or world < 1:
         raise ValueError("shard_ranges: n_tokens and world must be >= 1")
     chunks = (n_tokens + HC_CHUNK_TOKENS - 1) // HC_CHUNK_TOKENS
@@ -76,7 +84,8 @@ def restore_layers(layers: List[int], plan: ShardPlan,
                    project: Callable[[int, object], None],
                    alloc_full: Callable[[], object], shard_view: Callable[[object, int], object],
                    depth: int = 2):
-    """Host-side orchestration shared by the CPU (gloo) and GPU (NCCL) paths.
+    """Host-side orchestration of one rank (the CPU reference of what
+    hc_restore_sharded does on the device).
 
     fetch(layer, tok_begin, tok_end, dst_shard) fills this rank's shard;
     allgather(shard, full) assembles [world * shard_tokens x d] in `full`;
@@ -93,79 +102,50 @@ def restore_layers(layers: List[int], plan: ShardPlan,
         project(layer, full)
 
 
-# ------------------------------------------------------------------ GPU path
-class GpuShardedRestorer:
-    """NCCL + copy engine + K1 pipeline for one rank (torch.distributed must
-    be initialised with the nccl backend; one process per GPU)."""
+def save_shard(store, sid: str, seed, plan, rank: int, world: int,
+               hidden_rows: Callable[[int, int, int], object],
+               kv_rows: Callable[[int], object]):
+    """One rank's save path (storage.cpp:129-149 per rank): the session
+    (every token id, so positions and chunk indices are the context's) with
+    this rank's token range [b, e) of each HIDDEN layer -- hidden_rows(layer,
+    b, e) -> rows -- and its own heads' [K|V] rows of each KV layer --
+    kv_rows(layer) -> n x 2*d_kv_local rows."""
+    from . import hcache as H
+    n = len(seed.tokens)
+    b, e = H.shard_range(n, world, rank)
+    store.create_session(seed)
+    for layer, m in enumerate(plan.layer_assignment):
+        if m == H.LayerMethod.HIDDEN:
+            if e > b:
+                rows = hidden_rows(layer, b, e)
+                while not store.snapshot(sid, layer, H.StateKind.HIDDEN, rows, tok_begin=b):
+                    store.drain()
+        elif m == H.LayerMethod.KV_OFFLOAD:
+            rows = kv_rows(layer)
+            while not store.snapshot(sid, layer, H.StateKind.KV, rows):
+                store.drain()
+        else:
+            raise ValueError("save_shard: RECOMPUTE layers are not restored per rank")
+    store.finalize(sid)
 
-    def __init__(self, store, sid: str, weights, kv, page_table, n_tokens: int, d: int,
-                 depth: int = 3):
-        import torch
-        import torch.distributed as dist
-        self.torch, self.dist = torch, dist
-        self.world, self.rank = dist.get_world_size(), dist.get_rank()
-        self.store, self.sid, self.w, self.kv, self.table = store, sid, weights, kv, page_table
-        self.n, self.d = n_tokens, d
-        self.plan = ShardPlan.make(n_tokens, self.world, self.rank)
-        rows = self.plan.shard_tokens * self.world
-        self.ring = [torch.empty((rows, d), dtype=torch.bfloat16, device="cuda")
-                     for _ in range(max(2, depth))]
-        self.copy = torch.cuda.Stream()
-        self.comm = torch.cuda.Stream()
-        self.compute = torch.cuda.current_stream()
 
-    def _shard(self, full):
-        s = self.plan.shard_tokens
-        return full[self.rank * s:(self.rank + 1) * s]
-
-    def restore(self, layers: List[int], resident_shards=None):
-        """Enqueue the pipelined restore of `layers`. resident_shards: optional
-        per-layer HBM tensors holding this rank's shard (skips PCIe)."""
-        import ctypes as Cc
-        torch = self.torch
-        from .capi import check, lib
-        b, e = self.plan.mine
-        consumed = [None] * len(self.ring)
-        start = torch.cuda.Event()
-        start.record(self.compute)
-        self.copy.wait_event(start)
-        for i, layer in enumerate(layers):
-            slot = i % len(self.ring)
-            full = self.ring[slot]
-            mine = self._shard(full)
-            if consumed[slot] is not None:
-                self.copy.wait_event(consumed[slot])
-            with torch.cuda.stream(self.copy):
-                if e > b:
-                    if resident_shards is not None:
-                        mine[: e - b].copy_(resident_shards[layer][: e - b], non_blocking=True)
-                    else:
-                        check(lib().hc_store_read_layer_range(
-                            self.store._h, self.sid.encode(), layer, 0, b, e, mine.data_ptr(),
-                            (e - b) * self.d * 2, 1, self.copy.cuda_stream))
-                fetched = torch.cuda.Event()
-                fetched.record(self.copy)
-            self.comm.wait_event(fetched)
-            with torch.cuda.stream(self.comm):
-                self.dist.all_gather_into_tensor(full, mine)
-                gathered = torch.cuda.Event()
-                gathered.record(self.comm)
-            self.compute.wait_event(gathered)
-            check(lib().hc_project_to_pages(self.w._h, layer, full.data_ptr(), self.n, None, 1,
-                                            Cc.byref(self.kv.desc), self.table.data_ptr(), 0,
-                                            self.compute.cuda_stream))
-            done = torch.cuda.Event()
-            done.record(self.compute)
-            consumed[slot] = done
+def plan_sharded(io_h_rank: List[float], io_kv_rank: List[float], c_h_rank: List[float],
+                 n_layers: int, depth: int = 2):
+    """The three-way planner at N GPUs: every rank's lanes must finish, so a
+    layer costs the slowest rank's fetch (io_h: its token range, io_kv: its
+    heads' KV rows, both measured with all ranks copying at once) and K1
+    (its heads over all n rows). RECOMPUTE is unavailable (c_token = inf).
+    Deterministic in its inputs, so ranks that share them agree."""
+    from . import hcache as H
+    t = H.ProfiledTimings(io_h=max(io_h_rank), io_kv=max(io_kv_rank), c_h=max(c_h_rank),
+                          c_token=1e9, n_layers=n_layers)
+    return H.plan_three_way(t, prefetch_depth=max(1, depth - 1)) + (t,)
 
 
 def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
-    """bench.py --gpus N (torchrun): head-sharded restore of one context
-    (strong scaling). Prints the JSON line on rank 0. clock_sampler: context
-    manager class sampling nvidia-smi clocks (bench.ClockSampler); peaks: the
-    measured-peaks dict."""
-    import json
-
+    """bench.py --gpus N: head-sharded restore of one context over N ranks
+    (strong scaling), every rank calling hc_restore_sharded. Prints the JSON
+    line on rank 0."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -174,259 +154,272 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     from .capi import check, lib
 
     if not dist.is_initialized():
-        # a plain `python bench.py --sharded` (no torchrun): a world of one
         for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"),
                      ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517")):
             os.environ.setdefault(k, v)
-        backend = os.environ.get("HC_DIST_BACKEND", "nccl")  # gloo: 2 ranks on one GPU (tests)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-        else:
-            dist.init_process_group(backend)
+        # the control plane only (handle exchange, barriers, max over ranks):
+        # the data path is peer memory, no collective library call
+        dist.init_process_group("gloo")
     L, d, heads, kvh, dffn, n, rope = cfg
+    torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream().cuda_stream
-    hb, hc = head_range(kvh, world, rank)
+    hb, hc = H.shard_heads(kvh, world, rank)
+    dh = d // heads
+    d_kv_all = kvh * dh
     mc = H.ModelConfig(n_layers=L, d_hidden=d, n_heads=heads, n_kv_heads=kvh, d_ffn=dffn,
                        max_seq=max(n, 4096), rope_enabled=rope)
     w = H.Weights(mc, hb, hc, dev)
-    dh = d // heads
     bound = float(np.float32(1) / np.sqrt(np.float32(d)))
+    a, c = hb * dh, (hb + hc) * dh
+    keep = []
     for layer in range(L):
-        full_w = torch.empty((2 * kvh * dh, d), dtype=torch.bfloat16, device="cuda")
+        full_w = torch.empty((2 * d_kv_all, d), dtype=torch.bfloat16, device="cuda")
         check(lib().hc_fill_symmetric(full_w.data_ptr(), full_w.numel(), 1234 + layer, 0, bound,
                                       1, stream))
-        a, c = hb * dh, (hb + hc) * dh
-        w.set_layer_kv(layer, torch.cat([full_w[a:c], full_w[kvh * dh + a: kvh * dh + c]]).contiguous())
+        mine = torch.cat([full_w[a:c], full_w[d_kv_all + a: d_kv_all + c]]).contiguous()
+        w.set_layer_kv(layer, mine)
+        keep.append(mine)
+        del full_w
     page = 64
     n_pages = (n + page - 1) // page
     kv = H.KvCache(L, n_pages, page, w.d_kv)
     table = torch.arange(n_pages, dtype=torch.int32, device="cuda")
-    # every rank's store holds the session (stand-in for shared storage); each
-    # rank reads only its chunk-aligned token range
-    store = H.StorageManager(H.DevicePool(1), buffer_capacity_bytes=4 << 30)
-    plan = H.RestorationPlan.make(L, L, H.Complement.NONE)
-    store.create_session(H.SessionSeed("bench", mc.hash(), L, d, 2, plan, list(range(n)),
-                                       d_kv=kvh * dh))
-    shard = ShardPlan.make(n, world, rank)
-    b, e = shard.mine
-    resident = []
-    for layer in range(L):
-        hrows = torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
-        check(lib().hc_fill_symmetric(hrows.data_ptr(), hrows.numel(), 7, layer * n * d,
-                                      1.7320508, 1, stream))
-        while not store.snapshot("bench", layer, H.StateKind.HIDDEN, hrows):
-            store.drain()
-        resident.append(hrows[b:e].clone() if e > b else hrows[:0].clone())
-    store.finalize("bench")
-    torch.cuda.synchronize()
-    # default: the all-gather fused into K1 over peer memory (CUDA IPC over
-    # NVLink); HC_SHARD_MODE=nccl selects the NCCL all-gather pipeline
-    mode = os.environ.get("HC_SHARD_MODE", "peer")
-    if mode == "peer":
-        try:
-            r = PeerShardedRestorer(store, "bench", w, kv, table, n, d)
-        except Exception as exc:  # noqa: BLE001  (IPC mapping unavailable)
-            print(f"[rank {rank}] peer mapping failed ({exc}); using the NCCL all-gather",
-                  flush=True)
-            mode = "nccl"
-    if mode != "peer":
-        r = GpuShardedRestorer(store, "bench", w, kv, table, n, d)
-    if mode == "peer":
-        # resident shards live in this rank's range of the aligned split
-        b, e = r.ranges[rank]
-        resident = [None] * L
-        for layer in range(L):
-            hrows = torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
-            check(lib().hc_fill_symmetric(hrows.data_ptr(), hrows.numel(), 7, layer * n * d,
-                                          1.7320508, 1, stream))
-            resident[layer] = hrows[b:e].clone() if e > b else hrows[:0].clone()
-        torch.cuda.synchronize()
+    ranges = [H.shard_range(n, world, r) for r in range(world)]
+    b, e = ranges[rank]
+    rows_max = max(1, max(y - x for x, y in ranges))
+    depth = 2
+    group = H.PeerGroup(world, rank, d, rows_max, depth=depth, device=dev,
+                        exchange=H.PeerGroup.torch_exchange())
+    tokens = [(i * 11 + 1) % 32000 for i in range(n)]
 
+    def layer_hidden(layer):  # the synthetic layer input of every token (bench.py seeds)
+        h = torch.empty((n, d), dtype=torch.bfloat16, device="cuda")
+        check(lib().hc_fill_symmetric(h.data_ptr(), h.numel(), 7, layer * n * d, 1.7320508, 1,
+                                      stream))
+        return h
+
+    def max_over_ranks(x):
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- per-rank costs for the planner
+    # PCIe with every rank copying at once (ranks share host memory / PCIe
+    # switches: the aggregate, not N x one GPU's), per-rank bytes of a layer
+    def concurrent_h2d(nbytes, reps=5):
+        dist.barrier()
+        torch.cuda.synchronize()
+        bw = H.measure_h2d(nbytes, reps, dev)
+        t = nbytes / bw
+        slowest = max_over_ranks(t)
+        return bw, world * nbytes / slowest  # this rank's, aggregate
+    probe = max(64 << 20, rows_max * d * 2)
+    bw_rank, bw_agg = concurrent_h2d(probe)
+    bw_min = -max_over_ranks(-bw_rank)
+    io_h = rows_max * d * 2 / bw_min
+    io_kv = n * 2 * w.d_kv * 2 / bw_min
+    hb_probe = layer_hidden(0)
+    stats_ms, k1_ms = C.c_double(), C.c_double()
+    check(lib().hc_bench_project(w._h, 0, hb_probe.data_ptr(), n, 10, stream, C.byref(stats_ms),
+                                 C.byref(k1_ms)))
+    del hb_probe
+    c_h = max_over_ranks(k1_ms.value * 1e-3)
+    plan, plan_s, prof = plan_sharded([io_h], [io_kv], [c_h], L, depth)
+    # every rank computed the same plan from the same maxima; check it
+    plans = [None] * world
+    dist.all_gather_object(plans, plan.serialize())
+    if len(set(plans)) != 1:
+        raise RuntimeError(f"ranks disagree on the plan: {plans}")
+    all_h = H.RestorationPlan.make(L, L, H.Complement.NONE)
+    all_kv = H.RestorationPlan.make(L, 0, H.Complement.KV_OFFLOAD)
+
+    # ---- this rank's share of the sessions (pinned host store)
+    store = H.StorageManager(H.DevicePool(1), buffer_capacity_bytes=2 << 30)
+    kv_saved = {}
+
+    def kv_rows(layer):
+        k_, v_ = H.project_hidden_to_kv(w, layer, layer_hidden(layer), 0)
+        return torch.cat([k_, v_], 1).contiguous()
+
+    def save(sid, p, keep_kv=False):
+        def kvr(layer):
+            r = kv_rows(layer)
+            if keep_kv:
+                kv_saved[layer] = r
+            return r
+        save_shard(store, sid, H.SessionSeed(sid, mc.hash(), L, d, 2, p, tokens, d_kv=w.d_kv),
+                   p, rank, world, lambda layer, x, y: layer_hidden(layer)[x:y].contiguous(), kvr)
+    save("hcache", plan, keep_kv=True)
+    sids = {"hcache": plan}
+    if plan.serialize() != all_h.serialize():
+        save("all_hidden", all_h)
+        sids["all_hidden"] = all_h
+    if plan.serialize() != all_kv.serialize():
+        save("kv_offload", all_kv)
+        sids["kv_offload"] = all_kv
+    torch.cuda.synchronize()
+    throttle = H.ThrottleConfig(0, False)
     host_ck = torch.empty(16 * w.d_kv, dtype=torch.bfloat16, pin_memory=True)
 
-    def timed(resident_mode, steps):
+    def step(sid):
+        H.restore_sharded(group, store, sid, w, sids[sid], throttle, kv, table, stream)
+        host_ck.copy_(kv.k[L - 1].view(-1)[: 16 * w.d_kv], non_blocking=True)
+
+    def timed(sid, steps):
         dist.barrier()
         torch.cuda.synchronize()
-        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
         for _ in range(steps):
-            r.restore(list(range(L)), resident if resident_mode else None)
-            if not resident_mode:  # e2e: device->host read of the step's result
-                host_ck.copy_(kv.k[L - 1].view(-1)[: 16 * w.d_kv], non_blocking=True)
-        z.record()
+            step(sid)
+        ev1.record()
         torch.cuda.synchronize()
-        ms = torch.tensor([a.elapsed_time(z) / steps], device="cuda")
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms = ev0.elapsed_time(ev1) / steps
         dist.barrier()
-        return float(ms.item())
+        return max_over_ranks(ms)
+
+    def latency(sid, steps):
+        out = []
+        for _ in range(steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            step(sid)
+            torch.cuda.synchronize()
+            out.append(max_over_ranks((time.perf_counter() - t) * 1e3))
+        return float(np.mean(out))
 
     for _ in range(args.warmup):
-        r.restore(list(range(L)), resident)
-        r.restore(list(range(L)))
+        for sid in sids:
+            step(sid)
+    torch.cuda.synchronize()
     clk = clock_sampler(dev) if clock_sampler else None
     if clk:
         clk.__enter__()
-    ms_e2e = timed(False, args.steps)
-    ms_res = timed(True, args.steps)
+    ms = timed("hcache", args.steps)
+    ms_e2e = latency("hcache", args.steps)
     if clk:
         clk.__exit__(None, None, None)
-    clocks = clk.summary() if clk else {"sm_mhz": None, "sm_max_mhz": None,
-                                        "reasons": ["unsampled"]}
-    h2d = H.measure_h2d(256 << 20, 5, dev) / 1e9
+    clocks = clk.summary() if clk else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+    legs = {}
+    for sid in ("all_hidden", "kv_offload"):
+        legs[sid] = timed(sid, max(3, args.steps // 2)) if sid in sids else ms
+    # parity of this rank's heads after one more restore of the plan
+    step("hcache")
+    torch.cuda.synchronize()
+    par = _verify_shard(kv, table, plan, cfg, hb, hc, kv_saved, w.d_kv)
+    pars = [None] * world
+    dist.all_gather_object(pars, par)
+    tl = H.restore_sharded(group, store, "hcache", w, plan, H.ThrottleConfig(0, True), kv, table,
+                           stream, timeline=True)
+    tl_total = max_over_ranks(tl.total_s * 1e3)
     if rank == 0:
-        h_bytes = L * n * d * 2
-        line = {"metric": "restored_kv_tokens_per_s", "value": n / (ms_res * 1e-3),
-                "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms_res, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (splitmix64 bf16 hidden states + random-init weights)",
-                "config": {"workload": args.config + " head-sharded", "layers": L,
-                           "d_hidden": d, "kv_heads": kvh, "tokens": n,
-                           "parallelism": f"head-sharded x{world} + " + (
-                               "all-gather fused into K1 over peer memory" if mode == "peer"
-                               else "NCCL all-gather"),
-                           "l2": "inputs larger than L2"},
-                "restore_latency_ms": {"resident": ms_res, "e2e": ms_e2e},
-                "e2e": {"value": n / (ms_e2e * 1e-3), "unit": "tokens/s",
-                        "h2d_bytes_per_step": h_bytes // world,
-                        "d2h_bytes_per_step": int(host_ck.numel() * 2)},
-                "gpu_launches": args.steps * 2 * L,  # resident leg: row statistics + K1 per layer
-                "clocks": clocks,
-                "roofline": {"bound": "pcie", "unit": "GB/s",
-                             "achieved": h_bytes / world / (ms_e2e * 1e-3) / 1e9,
-                             "peak": h2d, "peak_source": "measured pinned H2D 256 MiB (this rank)",
-                             "frac": h_bytes / world / (ms_e2e * 1e-3) / 1e9 / h2d,
-                             "traffic": None},
-                "note": "value: shards resident in HBM (all-gather + K1); e2e: each rank "
-                        "fetches its 1/N over PCIe; times are max over ranks"}
+        pk = peaks or {"bf16_tflops": 1617.3, "_source": "fallback"}
+        flop = 4.0 * n * d * w.d_kv
+        k1_tflops = flop / (c_h) / 1e12
+        h_bytes = L * n * d * 2  # the context's hidden states, all ranks together
+        plan_bytes = (plan.l_h * n * d * 2 + plan.l_kv * n * 2 * d_kv_all * 2)
+        roof_pcie_s = h_bytes / bw_agg
+        roof_gemm_s = L * 4.0 * n * d * d_kv_all / (world * pk["bf16_tflops"] * 1e12)
+        roof_s = max(roof_pcie_s, roof_gemm_s)
+        parity = {"ranks": pars,
+                  "hidden_max_rel": max(p_["hidden_max_rel"] for p_ in pars),
+                  "kv_bitexact": (all(p_["kv_bitexact"] for p_ in pars)
+                                  if pars[0]["kv_bitexact"] is not None else None),
+                  "ok": all(p_["ok"] for p_ in pars),
+                  "tolerances": {"hidden_max_rel": 1e-2, "kv": "bit-exact"}}
+        line = {
+            "metric": "restored_kv_tokens_per_s", "value": n / (ms * 1e-3), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (splitmix64 bf16 hidden states + random-init weights)",
+            "config": args.workload_config,
+            "measures": "value: hc_restore_sharded on every rank from its pinned-host share of "
+                        "the session (its token range of each hidden layer, its heads' KV rows; "
+                        "H2D inside), steps back to back, CUDA events, max over ranks; e2e: per "
+                        "step the call + a D2H read + sync, host clock, max over ranks",
+            "restore_latency_ms": {"restore": ms, "e2e": ms_e2e, "all_hidden": legs["all_hidden"],
+                                   "kv_offload": legs["kv_offload"], "timeline_total": tl_total},
+            "speedup": {"hcache_vs_kv_offload": legs["kv_offload"] / ms,
+                        "hcache_vs_all_hidden": legs["all_hidden"] / ms,
+                        "hcache_vs_recompute": None},
+            "planner": {"plan": plan.serialize(),
+                        "per_rank_ms": {"io_h": io_h * 1e3, "io_kv": io_kv * 1e3,
+                                        "c_h": c_h * 1e3},
+                        "predicted_ms": plan_s * 1e3,
+                        "how": "hc_plan_three_way on the slowest rank's measured costs (PCIe "
+                               "with all ranks copying at once); RECOMPUTE unavailable at N>1"},
+            "pcie": {"per_rank_gbs": bw_rank / 1e9, "slowest_rank_gbs": bw_min / 1e9,
+                     "aggregate_gbs": bw_agg / 1e9, "probe_bytes": probe,
+                     "how": f"hc_measure_h2d on every rank at once after a barrier; aggregate = "
+                            f"{world} x bytes / slowest rank's time"},
+            "parity": parity,
+            "e2e": {"value": n / (ms_e2e * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(plan_bytes),
+                    "d2h_bytes_per_step": int(world * host_ck.numel() * 2)},
+            "path_roofline": {"bound": "pcie" if roof_pcie_s >= roof_gemm_s else "tensor",
+                              "all_hidden_roofline_ms": roof_s * 1e3,
+                              "frac_vs_all_hidden_roofline": roof_s / (ms * 1e-3),
+                              "achieved_pcie_gbs": plan_bytes / (ms * 1e-3) / 1e9,
+                              "frac_of_aggregate_pcie": plan_bytes / (ms * 1e-3) / bw_agg,
+                              "note": "north-star roofline max(hidden bytes / aggregate PCIe, "
+                                      "FLOPs / (N x tensor peak))"},
+            "roofline": {"bound": "tensor", "kernel": "k1_restore_kv (this rank's heads)",
+                         "achieved": k1_tflops, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                         "frac": k1_tflops / pk["bf16_tflops"], "peak_source": pk["_source"],
+                         "traffic": None, "flop_per_launch": flop, "k1_ms": c_h * 1e3},
+            # per step and rank: per HIDDEN layer statistics, mean-shift check,
+            # two flag signals, statistics gather and K1; per KV layer the scatter
+            "gpu_launches": 2 * args.steps * world * (plan.l_h * 6 + plan.l_kv),
+            "clocks": clocks,
+        }
+        if not args.no_cpu_baseline:
+            from bench import cpu_reference_sample
+            tok_s, desc = cpu_reference_sample(cfg)
+            line["cpu_baseline"] = dict(desc, value=tok_s, unit="tokens/s")
         print(json.dumps(line), flush=True)
-    if isinstance(r, PeerShardedRestorer):
-        r.close()
+    dist.barrier()
+    group.close()
     dist.barrier()
     dist.destroy_process_group()
 
 
-# ------------------------------------------- GPU path, all-gather in K1 (peer)
-def aligned_ranges(n_tokens: int, world: int, align: int = 128) -> List[Tuple[int, int]]:
-    """Contiguous token ranges per rank, boundaries multiples of `align` rows
-    (the K1 tile: one M tile reads one rank's range) and hence of the 64-token
-    chunk."""
-    if n_tokens < 1 or world < 1:
-        raise ValueError("aligned_ranges: n_tokens and world must be >= 1")
-    blocks = (n_tokens + align - 1) // align
-    per = (blocks + world - 1) // world
-    return [(min(n_tokens, r * per * align), min(n_tokens, (r + 1) * per * align))
-            for r in range(world)]
+def _verify_shard(kv, table, plan, cfg, hb, hc, kv_saved, d_kv_local, m=32):
+    """This rank's heads after the benchmarked restore: HIDDEN layers on
+    token slices vs the oracle's project_hidden_to_kv (north-star metric),
+    KV layers bit-exact against the stored rows (oracle/parity.py seeds)."""
+    import numpy as np
+    import torch
 
+    from oracle import Oracle
+    from oracle import parity as P
 
-class PeerShardedRestorer:
-    """Head-sharded restore with the all-gather fused into K1 over peer memory.
-
-    Rank r fetches only its token range of each layer (its own PCIe link) into
-    a slot of a small staging ring; every rank's K1 (hc_project_multi_source)
-    reads the A tiles of all ranges straight from the owners' slots, which are
-    mapped into each process with CUDA IPC (NVLink on a multi-GPU node). No
-    gathered n x d copy exists. Slot hand-off is stream-ordered through flags
-    in device memory: the owner stores the slot's epoch into every rank's
-    `ready` flag after the fetch; each consumer stores it into the owner's
-    `consumed` flag after its K1; each side waits on its own memory
-    (hc_stream_wait_flag). torch.distributed (any backend; gloo suffices) is
-    used once, to exchange the IPC handles."""
-
-    def __init__(self, store, sid: str, weights, kv, page_table, n_tokens: int, d: int,
-                 depth: int = 2, group=None):
-        import torch
-        import torch.distributed as dist
-        from torch.multiprocessing.reductions import reduce_tensor
-        self.torch = torch
-        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
-        if self.world > 8:
-            raise ValueError("peer all-gather: at most 8 ranks (K1 sources)")
-        self.store, self.sid, self.w, self.kv, self.table = store, sid, weights, kv, page_table
-        self.n, self.d, self.depth = n_tokens, d, max(1, depth)
-        self.ranges = aligned_ranges(n_tokens, self.world)
-        b, e = self.ranges[self.rank]
-        rows = max(1, e - b)
-        self.slots = [torch.empty((rows, d), dtype=torch.bfloat16, device="cuda")
-                      for _ in range(self.depth)]
-        # flags[0][src][slot]: epoch of src's slot ready; flags[1][c][slot]:
-        # epoch consumer c finished with MY slot
-        self.flags = torch.zeros((2, self.world, self.depth), dtype=torch.int32, device="cuda")
-        mine = [reduce_tensor(t) for t in self.slots + [self.flags]]
-        allh = [None] * self.world
-        dist.all_gather_object(allh, mine, group=group)
-        self._peer = []  # keep the mapped tensors alive
-        self.peer_slots, self.peer_flags = [], []
-        for r in range(self.world):
-            if r == self.rank:
-                ts = self.slots + [self.flags]
-            else:
-                ts = [fn(*args) for fn, args in allh[r]]
-                self._peer.append(ts)
-            self.peer_slots.append(ts[:-1])
-            self.peer_flags.append(ts[-1])
-        self.copy = torch.cuda.Stream()
-        self.step = 0
-        dist.barrier(group=group)
-
-    def close(self, group=None):
-        """Unmap the peers' buffers (before any producer process exits)."""
-        import torch.distributed as dist
-        self.torch.cuda.synchronize()
-        self._peer.clear()
-        self.peer_slots, self.peer_flags = [], []
-        self.torch.cuda.ipc_collect()
-        dist.barrier(group=group)
-
-    def _flag_ptr(self, owner: int, kind: int, who: int, slot: int) -> int:
-        f = self.peer_flags[owner]
-        return f.data_ptr() + ((kind * self.world + who) * self.depth + slot) * 4
-
-    def restore(self, layers: List[int], resident_shards=None, stream=None):
-        """Enqueue the restore of `layers` on `stream` (default: current)."""
-        import ctypes as Cc
-        torch = self.torch
-        from .capi import check, lib
-        compute = stream or torch.cuda.current_stream()
-        b, e = self.ranges[self.rank]
-        row_begin = (Cc.c_int64 * (self.world + 1))(*([r[0] for r in self.ranges] + [self.n]))
-        start = torch.cuda.Event()
-        start.record(compute)
-        self.copy.wait_event(start)
-        P = Cc.c_void_p
-        for layer in layers:
-            g = self.step
-            self.step += 1
-            s, ep = g % self.depth, g // self.depth + 1
-            # IO lane: my slot is free once every consumer finished epoch ep-1
-            if ep > 1:
-                for c in range(self.world):
-                    check(lib().hc_stream_wait_flag(self.copy.cuda_stream,
-                                                    self._flag_ptr(self.rank, 1, c, s), ep - 1))
-            if e > b:
-                dst = self.slots[s]
-                if resident_shards is not None:
-                    with torch.cuda.stream(self.copy):
-                        dst[: e - b].copy_(resident_shards[layer][: e - b], non_blocking=True)
-                else:
-                    check(lib().hc_store_read_layer_range(
-                        self.store._h, self.sid.encode(), layer, 0, b, e, dst.data_ptr(),
-                        (e - b) * self.d * 2, 1, self.copy.cuda_stream))
-            ready = (P * self.world)(*[self._flag_ptr(r, 0, self.rank, s)
-                                       for r in range(self.world)])
-            check(lib().hc_stream_signal_flags(self.copy.cuda_stream, ready, self.world, ep))
-            # compute lane: every range of this layer is in place -> fused K1
-            for src in range(self.world):
-                check(lib().hc_stream_wait_flag(compute.cuda_stream,
-                                                self._flag_ptr(self.rank, 0, src, s), ep))
-            srcs = (P * self.world)(*[self.peer_slots[r][s].data_ptr()
-                                      for r in range(self.world)])
-            check(lib().hc_project_multi_source(self.w._h, layer, self.world, srcs, row_begin,
-                                                Cc.byref(self.kv.desc), self.table.data_ptr(), 0,
-                                                compute.cuda_stream))
-            done = (P * self.world)(*[self._flag_ptr(r, 1, self.rank, s)
-                                      for r in range(self.world)])
-            check(lib().hc_stream_signal_flags(compute.cuda_stream, done, self.world, ep))
-        end = torch.cuda.Event()
-        end.record(self.copy)
-        compute.wait_event(end)
+    from . import hcache as H
+    L, d, heads, kvh, _, n, rope = cfg
+    dh = d // heads
+    o = Oracle()
+    meth = list(plan.layer_assignment)
+    hid = [x for x, y in enumerate(meth) if y == H.LayerMethod.HIDDEN]
+    kvl = [x for x, y in enumerate(meth) if y == H.LayerMethod.KV_OFFLOAD]
+    pick = sorted({hid[int(round(k * (len(hid) - 1) / 2))] for k in range(3)}) if hid else []
+    worst = 0.0
+    starts = sorted({0, (n // 2) // 64 * 64, max(0, n - m)})
+    for layer in pick:
+        k, v = kv.gather(layer, table, n)
+        wk, wv = P.layer_wkv(o, layer, d, kvh * dh)
+        a, c = hb * dh, (hb + hc) * dh
+        for s0 in starts:
+            h = P.hidden_rows(o, layer, n, d, s0, min(m, n - s0))
+            kr, vr = o.project(h, np.ascontiguousarray(wk[a:c]), np.ascontiguousarray(wv[a:c]),
+                               hc, s0, True, rope)
+            worst = max(worst, P.max_rel_err(k[s0:s0 + len(h)].float().cpu().numpy(), kr),
+                        P.max_rel_err(v[s0:s0 + len(h)].float().cpu().numpy(), vr))
+    exact = None
+    if kvl:
+        exact = True
+        for layer in kvl:
+            k, v = kv.gather(layer, table, n)
+            exact &= bool(torch.equal(torch.cat([k, v], 1), kv_saved[layer]))
+    return {"heads": [hb, hb + hc], "hidden_layers_checked": pick, "hidden_max_rel": worst,
+            "kv_layers": len(kvl), "kv_bitexact": exact,
+            "ok": bool(worst <= 1e-2 and exact is not False)}

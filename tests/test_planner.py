@@ -259,3 +259,36 @@ def test_token_split_balances_the_lanes():
     # no HIDDEN layer right after the prefix (KV-offload-only plan): no split
     pk = H.RestorationPlan.make(32, 0, C.KV_OFFLOAD)
     assert H.plan_token_split(t, pk, 4096, 32)[0] == 0
+
+
+def _timeline(events, total):
+    from paper_2410_05004_b200 import capi
+    tc = capi.TimelineC()
+    tc.n_events = len(events)
+    tc.total_s = total
+    for i, (lane, a, b) in enumerate(events):
+        tc.events[i].lane, tc.events[i].layer = int(lane), i
+        tc.events[i].start_s, tc.events[i].end_s = a, b
+    return H.Timeline.from_c(tc)
+
+
+def test_device_timeline_counts_overlapping_lanes_once():
+    """The device executor overlaps compute events (K1 launches alternate two
+    streams, statistics on a side stream): busy time is the union of the
+    intervals, so it can never exceed the timeline's total."""
+    ev = [(H.Lane.IO, 0.0, 4.0), (H.Lane.IO, 4.0, 8.0),
+          (H.Lane.COMPUTE, 1.0, 3.0), (H.Lane.COMPUTE, 2.5, 5.0),  # overlap 0.5
+          (H.Lane.COMPUTE, 4.5, 6.0), (H.Lane.COMPUTE, 7.0, 9.0)]
+    tl = _timeline(ev, 9.0)
+    assert tl.lane_busy(H.Lane.IO) == pytest.approx(8.0)
+    assert tl.lane_busy(H.Lane.COMPUTE) == pytest.approx(7.0)  # [1,6] + [7,9]
+    assert tl.bubble_fraction() == pytest.approx(1.0 / 9.0)
+    py = H.Timeline(tl.events, tl.total_s, tl.fill_s)  # the Python-side union
+    assert py.lane_busy(H.Lane.COMPUTE) == pytest.approx(7.0)
+    assert tl.lane_busy(H.Lane.COMPUTE) <= tl.total_s
+
+
+def test_serial_lanes_keep_the_reference_sum():
+    ev = [(H.Lane.COMPUTE, 0.1, 0.3), (H.Lane.COMPUTE, 0.3, 0.7), (H.Lane.COMPUTE, 0.9, 1.0)]
+    tl = _timeline(ev, 1.0)
+    assert tl.lane_busy(H.Lane.COMPUTE) == (0.3 - 0.1) + (0.7 - 0.3) + (1.0 - 0.9)

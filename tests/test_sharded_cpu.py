@@ -1,8 +1,10 @@
 """Head-sharded restore host logic on CPU: 2 processes over gloo run the real
-orchestration (paper_2410_05004_b200.sharded.restore_layers) with host reads
-from the real pinned-store code (hc_store_read_layer_range), a gloo
-all-gather and the oracle projection of each rank's KV heads; the union of
-the ranks' heads must equal the oracle's full projection bit for bit."""
+save path (sharded.save_shard: each rank's store holds only its own token
+range, hc_store_snapshot_range) and orchestration (sharded.restore_layers)
+with host reads from the real pinned-store code (hc_store_read_layer_range),
+a gloo all-gather in place of the peer-memory reads and the oracle
+projection of each rank's KV heads; the union of the ranks' heads must equal
+the oracle's full projection bit for bit. Also the N-GPU planner's inputs."""
 import os
 import socket
 
@@ -52,22 +54,27 @@ def _worker(rank, world, port, n, d, kvh, dh, L, out_q):
     from oracle import Oracle, bf16_round
     from paper_2410_05004_b200 import capi
     from paper_2410_05004_b200 import hcache as H
-    from paper_2410_05004_b200.sharded import ShardPlan, head_range, restore_layers
+    from paper_2410_05004_b200.sharded import ShardPlan, head_range, restore_layers, save_shard
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     o = Oracle()
-    # every rank's store holds the session (shared-storage stand-in), fp32
-    store = H.StorageManager(H.DevicePool(3))
-    store.create_session(H.SessionSeed("s", 1, L, d, 4,
-                                       H.RestorationPlan.make(L, L, H.Complement.NONE),
-                                       list(range(n))))
     hidden = [bf16_round(o.symmetric(n * d, 40 + layer, 0, 1.7320508)).reshape(n, d)
               for layer in range(L)]
+    # this rank's store holds only its share: its token range of every
+    # hidden layer (hc_store_snapshot_range), fp32 as the reference stores
+    ranges = [H.shard_range(n, world, r) for r in range(world)]
+    shard = max(e - b for b, e in ranges)
+    plan = ShardPlan(n, world, rank, ranges, shard)
+    store = H.StorageManager(H.DevicePool(3))
+    rplan = H.RestorationPlan.make(L, L, H.Complement.NONE)
+    save_shard(store, "s", H.SessionSeed("s", 1, L, d, 4, rplan, list(range(n))), rplan, rank,
+               world, lambda layer, b, e: hidden[layer][b:e], None)
+    man = store.open("s")
+    b, e = plan.mine
     for layer in range(L):
-        store.snapshot("s", layer, H.StateKind.HIDDEN, hidden[layer])
-    store.finalize("s")
-    plan = ShardPlan.make(n, world, rank)
+        lc = man.find(layer, H.StateKind.HIDDEN)
+        assert (lc.n_tokens if lc else 0) == (e if e > b else 0)
     hb, hc = head_range(kvh, world, rank)
     got = {}
 
@@ -132,3 +139,17 @@ def test_two_rank_gloo_sharded_restore_matches_full_projection(n, oracle):
 def test_shard_plan_mine():
     p = ShardPlan.make(1000, 4, 2)
     assert p.mine == p.ranges[2]
+
+
+def test_plan_sharded_takes_the_slowest_rank_and_no_recompute():
+    from paper_2410_05004_b200 import hcache as H
+    from paper_2410_05004_b200.sharded import plan_sharded
+    # 70B GQA at N=8: a rank's token range of hidden rows is 4x its heads' KV
+    # bytes -> the planner picks KV offload for every layer (SURVEY finding 6)
+    p, ms, t = plan_sharded([1.22e-3, 1.1e-3], [0.31e-3, 0.3e-3], [0.05e-3, 0.06e-3], 80)
+    assert t.io_h == 1.22e-3 and t.c_h == 0.06e-3
+    assert p.l_re == 0 and p.l_kv == 80
+    # MHA at N=2: hidden rows are half the KV bytes -> mostly hidden
+    p, ms, _ = plan_sharded([0.3e-3], [0.6e-3], [0.1e-3], 32)
+    assert p.l_re == 0 and p.l_h >= 24
+    assert all(m != H.LayerMethod.RECOMPUTE for m in p.layer_assignment)

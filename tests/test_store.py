@@ -263,3 +263,47 @@ def test_read_layer_range_sharded_fetch():
                                               buf.nbytes, 0, None)
     assert st == capi.HC_EINVAL  # begin must be chunk aligned
     del Cc
+
+
+def test_range_snapshot_keeps_chunk_indexing():
+    """hc_store_snapshot_range (the head-sharded save path): a rank stores
+    tokens [128, 300) of a layer; chunk c keeps its reference index, device
+    (layer + c) % ndev and payload; chunks below the range are not held here."""
+    import ctypes as C
+    st = H.StorageManager(H.DevicePool(3))
+    st.create_session(seed("r", 64, 2, tokens=range(300)))
+    rows = pattern(172, 64)
+    assert st.snapshot("r", 1, K.HIDDEN, rows, tok_begin=128)
+    with pytest.raises(ValueError):  # not chunk aligned
+        st.snapshot("r", 0, K.HIDDEN, rows, tok_begin=100)
+    st.finalize("r")
+    lc = st.open("r").find(1, K.HIDDEN)
+    assert (lc.n_chunks, lc.n_tokens) == (5, 300)
+    for c in (2, 3, 4):
+        dev, ptr, nb = st.chunk_info("r", 1, K.HIDDEN, c)
+        assert dev == (1 + c) % 3
+        want = rows[(c - 2) * 64:(c - 1) * 64]
+        got = np.frombuffer((C.c_char * nb).from_address(ptr), dtype=np.float32)
+        assert np.array_equal(got, want.ravel())
+    with pytest.raises(capi.NotFound):  # held by another rank
+        st.chunk_info("r", 1, K.HIDDEN, 1)
+    out = np.empty((172, 64), np.float32)
+    capi.check(capi.lib().hc_store_read_layer_range(st._h, b"r", 1, int(K.HIDDEN), 128, 300,
+                                                    out.ctypes.data, out.nbytes, 0, None))
+    assert np.array_equal(out, rows)
+    bad = np.empty((300, 64), np.float32)
+    with pytest.raises(capi.NotFound):
+        capi.check(capi.lib().hc_store_read_layer_range(st._h, b"r", 1, int(K.HIDDEN), 0, 300,
+                                                        bad.ctypes.data, bad.nbytes, 0, None))
+    assert sum(st.device_chunk_counts()) == 3
+
+
+def test_shard_geometry():
+    for n, world in ((700, 2), (1000, 4), (100, 4), (4096, 8), (32768, 8)):
+        rs = [H.shard_range(n, world, r) for r in range(world)]
+        assert rs[0][0] == 0 and rs[-1][1] == n
+        for (a, b), (c, _) in zip(rs, rs[1:]):
+            assert b == c and (b % 128 == 0 or b == n)
+    assert H.shard_heads(8, 4, 3) == (6, 2)
+    with pytest.raises(ValueError):
+        H.shard_heads(8, 3, 0)
