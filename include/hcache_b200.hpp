@@ -363,6 +363,17 @@ class StorageManager {
     check(st);
     return true;
   }
+  // B200 extension: device rows that are tokens [tok_begin, ..) of the layer
+  // (a head-sharded rank's own range, hc_store_snapshot_range).
+  bool snapshot_device_range(const std::string& sid, int layer, StateKind kind, int64_t tok_begin,
+                             const void* d_rows, int64_t n_rows, int row_width, int dtype,
+                             void* stream) {
+    hc_status st = hc_store_snapshot_range(s_, sid.c_str(), layer, int(kind), tok_begin, d_rows,
+                                           n_rows, row_width, dtype, 1, stream);
+    if (st == HC_EAGAIN) return false;
+    check(st);
+    return true;
+  }
   std::size_t drain(std::size_t max_chunks = std::size_t(-1)) {
     int64_t f = 0;
     check(hc_store_drain(s_, max_chunks == std::size_t(-1) ? -1 : int64_t(max_chunks), &f));
@@ -521,6 +532,62 @@ inline RestoreResult restore(StorageManager& store, const std::string& session_i
   std::vector<hc_timeline> tl(1);
   check(hc_restore(store.get(), session_id.c_str(), w.get(), &plan.raw, &o, &pages.desc,
                    d_page_table, stream, throttle.timeline ? tl.data() : nullptr));
+  RestoreResult r;
+  if (throttle.timeline) r.timeline = Timeline::from(tl[0]);
+  return r;
+}
+
+// ------------------------------------------ multi-GPU head-sharded restore
+// One rank's member of a head-sharded restore (hc_peer_group): its staging
+// slots and flags, exported as an opaque blob that the host hands to every
+// other rank by any transport, then import of every rank's blob.
+class PeerGroup {
+ public:
+  PeerGroup(int world, int rank, int device, int d_hidden, int64_t max_rows, int depth = 2) {
+    check(hc_peer_group_create(world, rank, device, d_hidden, max_rows, depth, &g_));
+  }
+  ~PeerGroup() { hc_peer_group_destroy(g_); }
+  PeerGroup(const PeerGroup&) = delete;
+  PeerGroup& operator=(const PeerGroup&) = delete;
+  std::vector<uint8_t> export_blob() const {
+    std::vector<uint8_t> b(hc_peer_group_blob_size());
+    check(hc_peer_group_export(g_, b.data(), b.size()));
+    return b;
+  }
+  void import_blobs(const std::vector<std::vector<uint8_t>>& blobs) {
+    std::vector<const void*> p;
+    for (const auto& b : blobs) p.push_back(b.data());
+    check(hc_peer_group_import(g_, p.data()));
+  }
+  hc_peer_group* get() const { return g_; }
+
+ private:
+  hc_peer_group* g_ = nullptr;
+};
+
+inline std::pair<int64_t, int64_t> shard_range(int64_t n_tokens, int world, int rank) {
+  int64_t b = 0, e = 0;
+  check(hc_shard_range(n_tokens, world, rank, &b, &e));
+  return {b, e};
+}
+inline std::pair<int, int> shard_heads(int n_kv_heads, int world, int rank) {
+  int32_t b = 0, c = 0;
+  check(hc_shard_heads(n_kv_heads, world, rank, &b, &c));
+  return {b, c};
+}
+
+// restore (restore.hpp:40-42) of this rank's KV heads of a head-sharded
+// context; every rank calls it with the same plan.
+inline RestoreResult restore_sharded(PeerGroup& group, StorageManager& store,
+                                     const std::string& session_id, const DeviceWeights& w,
+                                     const RestorationPlan& plan, const ThrottleConfig& throttle,
+                                     const KvPages& pages, const int32_t* d_page_table,
+                                     void* stream = nullptr) {
+  hc_restore_opts o{throttle.prefetch_depth, throttle.timeline ? 1 : 0, 0, 0};
+  std::vector<hc_timeline> tl(1);
+  check(hc_restore_sharded(group.get(), store.get(), session_id.c_str(), w.get(), &plan.raw, &o,
+                           &pages.desc, d_page_table, stream,
+                           throttle.timeline ? tl.data() : nullptr));
   RestoreResult r;
   if (throttle.timeline) r.timeline = Timeline::from(tl[0]);
   return r;

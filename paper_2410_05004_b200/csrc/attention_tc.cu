@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* p_full = s_empty + 2;  // [2], per P buffer
   uint64_t* o_done = p_full + 2;   // [2], PV_j commits to o_done[j & 1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* v_fix = o_done + 3;    // the last V tile's stale rows are zeroed (see attn_fa_kernel)
   float* xmax = reinterpret_cast<float*>(bars + 32);  // past the barriers + TMEM slot  // [2 parity][2 halves][128 rows]
   // end-of-loop partial sums go into P buffer 0 once every PV has completed
   float* xsum = reinterpret_cast<float*>(sP);  // [2 halves][128 rows]
@@ -135,6 +136,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int h = blockIdx.y, hk = h / a.group;
   const int q0 = qt * kAttnM;
   const int n_tiles = min(qt + 1, (a.n + kAttnN - 1) / kAttnN);
+  const int kv_tiles = (a.n + kAttnN - 1) / kAttnN;
+  const int fix_tile = (a.n % kAttnN) && kv_tiles - 1 < n_tiles ? kv_tiles - 1 : -1;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -157,6 +160,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_init(&p_full[b], 8);
       mbar_init(&o_done[b], 1);
     }
+    mbar_init(v_fix, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -215,6 +219,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (j >= 1) load_tile(j - 1, true);
       }
     }
+    __syncwarp();
+    if (fix_tile >= 0) {  // zero the V rows past the sequence (attn_fa_kernel)
+      const int st = fix_tile % kAttnStages;
+      mbar_wait(&v_full[st], (fix_tile / kAttnStages) & 1);
+      const int r0 = a.n - fix_tile * kAttnN;
+      uint8_t* base = sKV + st * Cfg::kStageBytes + Cfg::kKVBytes;
+      const int nvec = (kAttnN - r0) * 128 / 16;
+      for (int hb = 0; hb < DH / 64; ++hb) {
+        uint4* p = reinterpret_cast<uint4*>(base + hb * Cfg::kHalf + r0 * 128);
+        for (int i = lane; i < nvec; i += 32) p[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(v_fix);
+    }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA
     if (lane == 0) {
@@ -266,7 +285,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         if (next_pv < next_qk) {
           const int j = next_pv;
           if (mbar_test(&p_full[j & 1], (j >> 1) & 1) &&
-              mbar_test(&v_full[j % kAttnStages], (j / kAttnStages) & 1)) {
+              mbar_test(&v_full[j % kAttnStages], (j / kAttnStages) & 1) &&
+              (j != fix_tile || mbar_test(v_fix, 0))) {
             tc_fence_after();
             issue_pv(j);
             ++next_pv;
@@ -488,6 +508,23 @@ __device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
   return r;
 }
 
+// 2^x for a pair with ONE MUFU instruction: ex2.approx.f16x2 on the pair
+// rounded to fp16 (x <= 8 under the lazy max, so P <= 256; fp16 keeps 11
+// significant bits -- more than the bf16 P the PV product reads -- and its
+// subnormals reach 2^-24 of the row max), widened back to fp32 for the row
+// sum and the bf16 pack. MUFU retires 4 lanes / clk per sub-partition, so
+// two exponentials per lane and instruction halve the softmax's MUFU time.
+__device__ __forceinline__ uint64_t ex2_h2(uint64_t x) {
+  uint32_t h;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(f2_hi(x)), "f"(f2_lo(x)));
+  asm("ex2.approx.f16x2 %0, %0;" : "+r"(h));
+  float lo, hi;
+  asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+      : "=f"(lo), "=f"(hi)
+      : "r"(h));
+  return f2_pack(lo, hi);
+}
+
 __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -537,7 +574,7 @@ __device__ unsigned long long* g_fa_cta;
   } while (0)
 #endif
 
-template <int DH>
+template <int DH, bool EX2H>
 __global__ void __launch_bounds__(kFaThreads, 1)
     attn_fa_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK2,
@@ -559,6 +596,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   uint64_t* p_full = bars + 11;     // [tile][key chunk]
   uint64_t* o_done = bars + 15;     // [tile]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* v_fix = bars + 18;      // the last V tile's stale rows are zeroed
   float* xmax = reinterpret_cast<float*>(bars + 32);  // [j parity][tile][half][row]
   float* xsum = xmax + 8 * kFaM;                      // [tile][half][row]
 
@@ -582,6 +620,13 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   const int kv_tiles = (a.n + kAttnN - 1) / kAttnN;
   const int nt_a = min(2 * pt + 1, kv_tiles);
   const int nt_b = min(2 * pt + 2, kv_tiles);  // == nt_a when tile B is past n
+  // The KV tile holding key n-1 also holds rows past the sequence: slots of
+  // its last page that no token wrote (or, clamped, that page again). Their
+  // scores are masked to -inf, so P = 0 there -- but a P x V product over a
+  // stale NaN / Inf row is NaN all the same (caller pages are recycled
+  // memory). Warp 0 zeroes those V rows in shared memory once the tile has
+  // landed, before the PV MMAs of that tile may read it.
+  auto fix_tile_of = [&]() { return (a.n % kAttnN) && kv_tiles - 1 < nt_b ? kv_tiles - 1 : -1; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -600,6 +645,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       mbar_init(&p_full[2 * s + 1], 8);
       mbar_init(&o_done[s], 1);
     }
+    mbar_init(v_fix, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -655,6 +701,23 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         if (j >= 1) load_tile(j - 1, true);
       }
     }
+    __syncwarp();
+    const int fix_tile = fix_tile_of();
+    if (fix_tile >= 0) {
+      // (the tile's stage is never refilled: it is the last V load)
+      const int st = fix_tile & 1;
+      mbar_wait(&v_full[st], (fix_tile >> 1) & 1);
+      const int r0 = a.n - fix_tile * kAttnN;  // first row past the sequence
+      uint8_t* base = sV + st * Cfg::kKVBytes;
+      const int nvec = (kAttnN - r0) * 128 / 16;  // 128-byte rows of each 64-column block
+      for (int hb = 0; hb < DH / 64; ++hb) {
+        uint4* p = reinterpret_cast<uint4*>(base + hb * Cfg::kHalf + r0 * 128);
+        for (int i = lane; i < nvec; i += 32) p[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      fence_proxy_async_smem();  // generic stores -> the tensor core's reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(v_fix);
+    }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA
     // warp-uniform loop; one elected lane issues (see elect_one)
@@ -663,6 +726,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     const uint64_t dq = umma_desc_sw128(smem_u32(sQ));
     const uint64_t dk = umma_desc_sw128(smem_u32(sK));
     const uint64_t dv = umma_desc_sw128_mn(smem_u32(sV), Cfg::kHalf);
+    const int fix_tile = fix_tile_of();
     mbar_wait(q_full, 0);
     tc_fence_after();
     auto issue_qk = [&](int t, int j) {
@@ -688,6 +752,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       const int st = j & 1;
       FA_TRACE(5, t, j);
       mbar_wait(&v_full[st], (j >> 1) & 1);
+      if (j == fix_tile) mbar_wait(v_fix, 0);
       // P arrives in two 32-key chunks per key half; the first chunk's MMAs
       // run while the softmax warps still compute the second
 #pragma unroll
@@ -827,7 +892,9 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         for (int i = 0; i < 16; ++i) {
           const uint64_t x = f2_fma(uint64_t(v[2 * i]) | (uint64_t(v[2 * i + 1]) << 32), sc2, nm2);
           uint64_t pv;
-          if ((i & 7) < kFaEmuPairs) {
+          if (EX2H) {
+            pv = ex2_h2(x);
+          } else if ((i & 7) < kFaEmuPairs) {
             pv = ex2_poly2(x);
           } else {
             pv = f2_pack(ex2_approx(f2_lo(x)), ex2_approx(f2_hi(x)));
@@ -940,8 +1007,11 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(AttnCfg<DH>::kSmem));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_fa_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(FaCfg<DH>::kSmem));
+      e = cudaFuncSetAttribute(attn_fa_kernel<DH, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(FaCfg<DH>::kSmem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_fa_kernel<DH, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(FaCfg<DH>::kSmem));
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
@@ -958,7 +1028,18 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
     const double kv_bytes = double(n) * double(n_kv_heads) * DH * 2 * 2;  // n = total rows
     a.rank_major = kv_bytes <= 80.0 * (1 << 20);
     const dim3 grid = a.rank_major ? dim3(n_heads, n_seqs, pairs) : dim3(pairs, n_heads, n_seqs);
-    attn_fa_kernel<DH><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
+    // softmax exponentials: fp32 MUFU ex2 (default) or ex2.approx.f16x2
+    // (HC_FA_EX2=1, A/B measurements)
+    static const bool ex2h = [] {
+      const char* e = getenv("HC_FA_EX2");
+      return e && atoi(e) == 1;
+    }();
+    if (ex2h)
+      attn_fa_kernel<DH, true><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2,
+                                                                              tv2, a);
+    else
+      attn_fa_kernel<DH, false><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2,
+                                                                               tv2, a);
   } else {
     const dim3 grid((n + kAttnM - 1) / kAttnM, n_heads);
     attn_tc_kernel<DH><<<grid, kAttnThreads, AttnCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);

@@ -32,6 +32,16 @@ __global__ void k(float* out, int iters, long long* clk) {
         a[i] = __uint_as_float(r);
       }
       if (OP == 6) a[i] = fmaxf(a[i], -126.0f) + 0.f;
+      if (OP == 7) {  // ex2.approx.f16x2 (SASS: MUFU.EX2.F16 per half?)
+        uint32_t r = __float_as_uint(a[i]);
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(r));
+        a[i] = __uint_as_float(r);
+      }
+      if (OP == 8) {  // ex2.approx.f16 (scalar)
+        unsigned short r = (unsigned short)__float_as_uint(a[i]);
+        asm volatile("ex2.approx.f16 %0, %0;" : "+h"(r));
+        a[i] = __uint_as_float(r);
+      }
     }
   }
   long long t1 = clock64();
@@ -46,9 +56,10 @@ int main() {
   long long* c;
   cudaMalloc(&o, 148 * 1024 * 4);
   cudaMalloc(&c, 8);
-  const char* names[7] = {"FFMA", "FFMA2", "FADD2", "MUFU.EX2", "F2FP(cvt bf16x2)", "IMAD", "FMNMX+FADD"};
+  const char* names[9] = {"FFMA", "FFMA2", "FADD2", "MUFU.EX2", "F2FP(cvt bf16x2)", "IMAD",
+                          "FMNMX+FADD", "ex2.approx.f16x2", "ex2.approx.f16"};
   for (int w : {1, 2, 4})
-    for (int op = 0; op < 7; ++op) {
+    for (int op = 0; op < 9; ++op) {
       const int iters = 4096;
       auto launch = [&] {
         switch (op) {
@@ -59,6 +70,8 @@ int main() {
           case 4: k<4><<<148, 128 * w>>>(o, iters, c); break;
           case 5: k<5><<<148, 128 * w>>>(o, iters, c); break;
           case 6: k<6><<<148, 128 * w>>>(o, iters, c); break;
+          case 7: k<7><<<148, 128 * w>>>(o, iters, c); break;
+          case 8: k<8><<<148, 128 * w>>>(o, iters, c); break;
         }
       };
       launch();

@@ -4,8 +4,13 @@
 // restore when a B200 is present ("gpu" argument).
 #include <cuda_runtime.h>
 
+#include <sys/wait.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <ctime>
 #include <cstdio>
 #include <cstring>
 #include <random>
@@ -339,7 +344,165 @@ static void serve_tests() {
   for (void* p : bufs) cudaFree(p);
 }
 
+// Head-sharded restore driven from C++ alone (no Python, no torch): `world`
+// processes forked on one GPU, IPC blobs exchanged through files; each rank
+// stores only its token range, restores its heads, and must equal a local K1
+// over the whole rows bit for bit.
+static int sharded_rank(int world, int rank, const std::string& dir) {
+  const int L = 2, d = 512, heads = 8, n = 900, page = 64, dh = d / heads;
+  ModelConfig cfg;
+  cfg.n_layers = L;
+  cfg.d_hidden = d;
+  cfg.n_heads = heads;
+  cfg.d_ffn = 4 * d;
+  cfg.max_seq = 2048;
+  cfg.elem_bytes = 2;
+  const auto hs = shard_heads(heads, world, rank);
+  const int d_kv = hs.second * dh;
+  DeviceWeights w(cfg, hs.first, hs.second);
+  std::vector<void*> full_w(L), wkv(L), hid(L), kp(L), vp(L);
+  const int n_pages = (n + page - 1) / page;
+  for (int l = 0; l < L; ++l) {
+    cudaMalloc(&full_w[l], size_t(2 * d) * d * 2);
+    cudaMalloc(&wkv[l], size_t(2 * d_kv) * d * 2);
+    cudaMalloc(&hid[l], size_t(n) * d * 2);
+    cudaMalloc(&kp[l], size_t(n_pages) * page * d_kv * 2);
+    cudaMalloc(&vp[l], size_t(n_pages) * page * d_kv * 2);
+    check(hc_fill_symmetric(full_w[l], int64_t(2 * d) * d, 1234 + l, 0, 0.0625f, HC_DTYPE_BF16,
+                            nullptr));
+    // this rank's heads: K rows [h0*dh, (h0+hc)*dh) then the same V rows
+    const size_t row = size_t(d) * 2, k0 = size_t(hs.first) * dh;
+    cudaMemcpy(wkv[l], static_cast<char*>(full_w[l]) + k0 * row, size_t(d_kv) * row,
+               cudaMemcpyDeviceToDevice);
+    cudaMemcpy(static_cast<char*>(wkv[l]) + size_t(d_kv) * row,
+               static_cast<char*>(full_w[l]) + (size_t(d) + k0) * row, size_t(d_kv) * row,
+               cudaMemcpyDeviceToDevice);
+    check(hc_fill_symmetric(hid[l], int64_t(n) * d, 7 + l, 0, 1.7320508f, HC_DTYPE_BF16, nullptr));
+    w.set_layer_kv(l, wkv[l]);
+  }
+  const auto rg = shard_range(n, world, rank);
+  StorageManager store(DevicePool{2});
+  SessionSeed s = seed("sh", d, L, 2);
+  s.tokens.assign(size_t(n), 1);
+  s.d_kv = d_kv;
+  store.create_session(s);
+  for (int l = 0; l < L && rg.second > rg.first; ++l)
+    CHECK(store.snapshot_device_range("sh", l, StateKind::Hidden, rg.first,
+                                      static_cast<char*>(hid[l]) + size_t(rg.first) * d * 2,
+                                      rg.second - rg.first, d, HC_DTYPE_BF16, nullptr));
+  store.finalize("sh");
+  int64_t rows_max = 0;
+  for (int r = 0; r < world; ++r) {
+    auto x = shard_range(n, world, r);
+    rows_max = std::max(rows_max, x.second - x.first);
+  }
+  PeerGroup g(world, rank, 0, d, rows_max, 2);
+  {  // blob exchange through files (any transport works)
+    auto mine = g.export_blob();
+    const std::string tmp = dir + "/r" + std::to_string(rank) + ".tmp";
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    std::fwrite(mine.data(), 1, mine.size(), f);
+    std::fclose(f);
+    std::rename(tmp.c_str(), (dir + "/r" + std::to_string(rank) + ".blob").c_str());
+    std::vector<std::vector<uint8_t>> all(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r) {
+      const std::string path = dir + "/r" + std::to_string(r) + ".blob";
+      for (int tries = 0; tries < 6000; ++tries) {
+        FILE* x = std::fopen(path.c_str(), "rb");
+        if (x) {
+          all[size_t(r)].resize(mine.size());
+          const size_t got = std::fread(all[size_t(r)].data(), 1, mine.size(), x);
+          std::fclose(x);
+          if (got == mine.size()) break;
+        }
+        struct timespec ts{0, 10000000};
+        nanosleep(&ts, nullptr);
+      }
+    }
+    g.import_blobs(all);
+  }
+  std::vector<int32_t> table(static_cast<size_t>(n_pages));
+  for (int i = 0; i < n_pages; ++i) table[size_t(i)] = n_pages - 1 - i;
+  int32_t* d_table = nullptr;
+  cudaMalloc(&d_table, table.size() * 4);
+  cudaMemcpy(d_table, table.data(), table.size() * 4, cudaMemcpyHostToDevice);
+  KvPages pages(L, page, n_pages, d_kv, kp, vp);
+  RestorationPlan plan = s.plan;
+  RestoreResult r{};
+  for (int it = 0; it < 3; ++it)  // wraps the 2-slot ring
+    r = restore_sharded(g, store, "sh", w, plan, ThrottleConfig{}, pages, d_table);
+  CHECK(r.timeline.total_s > 0);
+  std::vector<uint16_t> kd(size_t(n) * d_kv), kpg(size_t(n_pages) * page * d_kv);
+  void *dk = nullptr, *dv = nullptr;
+  cudaMalloc(&dk, kd.size() * 2);
+  cudaMalloc(&dv, kd.size() * 2);
+  for (int l = 0; l < L; ++l) {
+    check(hc_project_hidden_to_kv(w.get(), l, hid[l], n, 0, dk, dv, HC_DTYPE_BF16, nullptr));
+    cudaMemcpy(kd.data(), dk, kd.size() * 2, cudaMemcpyDeviceToHost);
+    cudaMemcpy(kpg.data(), kp[l], kpg.size() * 2, cudaMemcpyDeviceToHost);
+    bool same = true;
+    for (int t = 0; t < n && same; ++t) {
+      const int pg = table[size_t(t / page)], slot = t % page;
+      same = std::memcmp(&kd[size_t(t) * d_kv], &kpg[(size_t(pg) * page + slot) * d_kv],
+                         size_t(d_kv) * 2) == 0;
+    }
+    CHECK(same);
+  }
+  // every rank done with the peers' slots before any of them unmaps / exits
+  {
+    const std::string done = dir + "/done" + std::to_string(rank);
+    FILE* f = std::fopen(done.c_str(), "wb");
+    std::fclose(f);
+    for (int q = 0; q < world; ++q)
+      for (int tries = 0; tries < 6000; ++tries) {
+        FILE* x = std::fopen((dir + "/done" + std::to_string(q)).c_str(), "rb");
+        if (x) {
+          std::fclose(x);
+          break;
+        }
+        struct timespec ts{0, 10000000};
+        nanosleep(&ts, nullptr);
+      }
+  }
+  std::printf("rank %d: %d checks, %d failures\n", rank, g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}
+
+static int sharded_tests(int world) {
+  char tmpl[] = "/tmp/hc_facade_XXXXXX";
+  const std::string dir = mkdtemp(tmpl);
+  std::vector<pid_t> kids;
+  for (int r = 0; r < world; ++r) {
+    pid_t pid = fork();
+    if (pid == 0) {
+      int rc = 1;
+      try {
+        rc = sharded_rank(world, r, dir);
+      } catch (const std::exception& e) {
+        std::printf("rank %d: exception %s\n", r, e.what());
+      }
+      std::fflush(stdout);
+      _exit(rc);
+    }
+    kids.push_back(pid);
+  }
+  int bad = 0;
+  for (pid_t k : kids) {
+    int st = 0;
+    waitpid(k, &st, 0);
+    if (!WIFEXITED(st) || WEXITSTATUS(st) != 0) ++bad;
+  }
+  std::printf("sharded (%d ranks): %d failed ranks\n", world, bad);
+  return bad;
+}
+
 int main(int argc, char** argv) {
+  // forked before this process touches CUDA
+  if (argc > 2 && std::string(argv[1]) == "gpu-sharded") {
+    const int bad = sharded_tests(std::atoi(argv[2]));
+    std::printf("%d checks, %d failures\n", bad ? 1 : 0, bad);
+    return bad ? 1 : 0;
+  }
   const bool gpu = argc > 1 && std::string(argv[1]) == "gpu";
   planner_tests();
   pipeline_tests();

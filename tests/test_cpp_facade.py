@@ -27,3 +27,16 @@ def test_cpp_facade_gpu():
     r = subprocess.run([BIN, "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_cpp_facade_sharded_restore(world):
+    """hc_restore_sharded driven by a C++ host alone: `world` forked
+    processes on one GPU, IPC blobs exchanged through files."""
+    if not os.path.exists(BIN):
+        _build()
+    r = subprocess.run([BIN, "gpu-sharded", str(world)], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout and f"sharded ({world} ranks): 0 failed" in r.stdout
