@@ -572,12 +572,13 @@ def run_ours(args, cfg, rank, world):
     h_bytes = L * n * d * 2
     h_bytes_plan = (plan.l_h * n - split) * d * 2 + plan.l_kv * n * 2 * d_kv * 2 + \
         (4 * n if plan.l_re or split else 0)
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath):  # ncu --set full capture of this kernel (scripts/profile_r2.sh)
         t = json.load(open(tpath))
         if t.get("config") == args.config:
             traffic = t.get("dram_bytes_per_launch")
+            traffic_src = f"{t.get('source')}; {t.get('build')}"
 
     cpu_tok_s, cpu_desc = cpu_reference_sample(cfg) if not args.no_cpu_baseline else (None, {})
     if cpu_tok_s is not None:
@@ -629,6 +630,7 @@ def run_ours(args, cfg, rank, world):
                      "frac_of_sustained": k1_tflops / pk.get("bf16_tflops_sustained",
                                                              pk["bf16_tflops"]),
                      "peak_source": pk["_source"], "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "flop_per_launch": flop, "k1_ms": k1_ms.value,
                      "row_stats_ms": stats_ms.value},
         "timeline": {"total_ms": tl.total_s * 1e3, "fill_ms": tl.fill_s * 1e3,

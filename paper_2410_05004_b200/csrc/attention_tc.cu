@@ -508,23 +508,6 @@ __device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
   return r;
 }
 
-// 2^x for a pair with ONE MUFU instruction: ex2.approx.f16x2 on the pair
-// rounded to fp16 (x <= 8 under the lazy max, so P <= 256; fp16 keeps 11
-// significant bits -- more than the bf16 P the PV product reads -- and its
-// subnormals reach 2^-24 of the row max), widened back to fp32 for the row
-// sum and the bf16 pack. MUFU retires 4 lanes / clk per sub-partition, so
-// two exponentials per lane and instruction halve the softmax's MUFU time.
-__device__ __forceinline__ uint64_t ex2_h2(uint64_t x) {
-  uint32_t h;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(f2_hi(x)), "f"(f2_lo(x)));
-  asm("ex2.approx.f16x2 %0, %0;" : "+r"(h));
-  float lo, hi;
-  asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-      : "=f"(lo), "=f"(hi)
-      : "r"(h));
-  return f2_pack(lo, hi);
-}
-
 __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -574,7 +557,7 @@ __device__ unsigned long long* g_fa_cta;
   } while (0)
 #endif
 
-template <int DH, bool EX2H>
+template <int DH>
 __global__ void __launch_bounds__(kFaThreads, 1)
     attn_fa_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK2,
@@ -892,9 +875,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         for (int i = 0; i < 16; ++i) {
           const uint64_t x = f2_fma(uint64_t(v[2 * i]) | (uint64_t(v[2 * i + 1]) << 32), sc2, nm2);
           uint64_t pv;
-          if (EX2H) {
-            pv = ex2_h2(x);
-          } else if ((i & 7) < kFaEmuPairs) {
+          if ((i & 7) < kFaEmuPairs) {
             pv = ex2_poly2(x);
           } else {
             pv = f2_pack(ex2_approx(f2_lo(x)), ex2_approx(f2_hi(x)));
@@ -1007,11 +988,8 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(AttnCfg<DH>::kSmem));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_fa_kernel<DH, false>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(FaCfg<DH>::kSmem));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_fa_kernel<DH, true>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(FaCfg<DH>::kSmem));
+      e = cudaFuncSetAttribute(attn_fa_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(FaCfg<DH>::kSmem));
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
@@ -1028,18 +1006,7 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
     const double kv_bytes = double(n) * double(n_kv_heads) * DH * 2 * 2;  // n = total rows
     a.rank_major = kv_bytes <= 80.0 * (1 << 20);
     const dim3 grid = a.rank_major ? dim3(n_heads, n_seqs, pairs) : dim3(pairs, n_heads, n_seqs);
-    // softmax exponentials: fp32 MUFU ex2 (default) or ex2.approx.f16x2
-    // (HC_FA_EX2=1, A/B measurements)
-    static const bool ex2h = [] {
-      const char* e = getenv("HC_FA_EX2");
-      return e && atoi(e) == 1;
-    }();
-    if (ex2h)
-      attn_fa_kernel<DH, true><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2,
-                                                                              tv2, a);
-    else
-      attn_fa_kernel<DH, false><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2,
-                                                                               tv2, a);
+    attn_fa_kernel<DH><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
   } else {
     const dim3 grid((n + kAttnM - 1) / kAttnM, n_heads);
     attn_tc_kernel<DH><<<grid, kAttnThreads, AttnCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
