@@ -425,7 +425,7 @@ def run_ours(args, cfg, rank, world):
     if not full:
         # no full block weights (GQA configs here): RECOMPUTE is unavailable,
         # the planner splits between hidden states and KV offload only
-        prof.c_token = 1e9
+        prof.c_token = H.RECOMPUTE_UNAVAILABLE
     plan, plan_ms = H.plan_three_way(prof, layer_bytes=n * d * 2)
     # B200 extension: split the first hidden layer between the recompute
     # prefix and the link where that balances the two lanes
@@ -759,7 +759,7 @@ def run_ours_batch(args, cfg, rank, world):
     h2d = H.measure_h2d(256 << 20, 5, dev)
     prof = H.ProfiledTimings(io_h=total * d * 2 / h2d, io_kv=total * 2 * d_kv * 2 / h2d,
                              c_h=ms_resident * 1e-3 / L,
-                             c_token=(ms_re * 1e-3 / L) if ms_re else 1e9, n_layers=L)
+                             c_token=(ms_re * 1e-3 / L) if ms_re else H.RECOMPUTE_UNAVAILABLE, n_layers=L)
     plan, plan_ms = H.plan_three_way(prof, L)
     all_h = H.RestorationPlan.make(L, L, H.Complement.NONE)
     all_kv = H.RestorationPlan.make(L, 0, H.Complement.KV_OFFLOAD)

@@ -195,7 +195,11 @@ hc_status hc_makespan(const hc_plan* p, const hc_timings* t, double* out);
 hc_status hc_brute_force_plan(const hc_timings* t, hc_plan* out);
 /* B200 planner: exhaustive over (l_re, l_h, l_kv), costed by the bounded
  * staging pipeline (simulate_pipeline at prefetch_depth) so the plan is
- * bubble-free under the executor's real buffer bound. */
+ * bubble-free under the executor's real buffer bound. The
+ * RECOMPUTE prefix's last layer is costed c_h: the executor stops it after
+ * its K/V projection (its output is the next layer's stored input).
+ * c_token >= HC_RECOMPUTE_UNAVAILABLE means no RECOMPUTE layers at all. */
+#define HC_RECOMPUTE_UNAVAILABLE 1e9
 hc_status hc_plan_three_way(const hc_timings* t, int32_t prefetch_depth, hc_plan* out,
                             double* makespan_out);
 /* B200 extension: the token split of the plan's first layer after the

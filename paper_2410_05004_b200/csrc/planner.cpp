@@ -162,9 +162,15 @@ void simulate(const hc_pipeline_job* jobs, int n, int depth, hc_timeline* tl) {
 }
 
 // Jobs of a plan in the executor's compute order (restore.cpp:50-63):
-// recompute prefix, hidden layers, KV suffix.
+// recompute prefix, hidden layers, KV suffix. The prefix's last layer costs
+// a projection (c_h), not a block: the executor stops that layer after its
+// K/V (the next layer is restored from its stored input), where the
+// reference's prefill_layers runs the whole block (model.cpp:349-356).
 std::vector<hc_pipeline_job> plan_jobs(const hc_plan* p, const hc_timings* t) {
   std::vector<hc_pipeline_job> jobs;
+  int last_re = -1;
+  for (int L = 0; L < p->n_layers; ++L)
+    if (p->layer_assignment[L] == HC_METHOD_RECOMPUTE) last_re = L;
   auto add = [&](int method) {
     for (int L = 0; L < p->n_layers; ++L) {
       if (p->layer_assignment[L] != method) continue;
@@ -172,7 +178,7 @@ std::vector<hc_pipeline_job> plan_jobs(const hc_plan* p, const hc_timings* t) {
       j.layer = L;
       if (method == HC_METHOD_RECOMPUTE) {
         j.has_compute = 1;
-        j.compute_s = t->c_token;
+        j.compute_s = L == last_re ? t->c_h : t->c_token;
         j.compute_kind = HC_EV_RECOMPUTE;
       } else if (method == HC_METHOD_HIDDEN) {
         j.has_io = j.has_compute = 1;
@@ -335,8 +341,12 @@ hc_status hc_plan_three_way(const hc_timings* t, int32_t prefetch_depth, hc_plan
     double best_cost = 0;
     hc_plan best{}, cand{};
     hc_timeline* tl = new hc_timeline;
+    // c_token >= HC_RECOMPUTE_UNAVAILABLE: no full block weights (or no
+    // whole model on this GPU) -- no RECOMPUTE layers, not even the
+    // projection-only first layer the cost model would otherwise price at c_h
+    const int max_re = t->c_token >= HC_RECOMPUTE_UNAVAILABLE ? 0 : n;
     try {
-      for (int l_re = 0; l_re <= n; ++l_re)
+      for (int l_re = 0; l_re <= max_re; ++l_re)
         for (int l_kv = 0; l_kv + l_re <= n; ++l_kv) {
           const int l_h = n - l_re - l_kv;
           make_mixed(l_re, l_h, l_kv, &cand);
@@ -385,8 +395,9 @@ hc_status hc_plan_token_split(const hc_timings* t, int32_t prefetch_depth, const
       simulate(base.data(), int(base.size()), prefetch_depth, tl);
       best = tl->total_s;
       // split s: the layer's first s tokens join the prefix (recompute cost
-      // linear in s -- the attention part is sub-linear, so this errs high),
-      // the rest is fetched and projected
+      // linear in s -- the attention part is sub-linear, so this errs high:
+      // the previous layer's block for s rows + this layer's projection of
+      // them), the rest is fetched and projected
       for (int sp = HC_CHUNK_TOKENS; ok && sp < n_tokens; sp += HC_CHUNK_TOKENS) {
         const double x = double(sp) / double(n_tokens);
         std::vector<hc_pipeline_job> jobs(base.begin(), base.begin() + long(at));

@@ -113,13 +113,15 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
                   const hc_kv_pages* pages, const int32_t* d_page_table, cudaStream_t stream,
                   const std::function<void(int, bool)>& hook, void* d_layer_inputs,
                   int32_t* next_token, const SeqBatch& sb, int32_t* d_next_tokens,
-                  int64_t n_last = 0) {
+                  int64_t n_last = 0, bool kv_only_last = false) {
   if (!w || !d_tokens || !pages || !d_page_table) fail(HC_EINVAL, "prefill_layers: null argument");
   const auto& c = w->cfg;
   if (lb < 0 || le > c.n_layers || lb > le) fail(HC_EINVAL, "prefill_layers: bad layer range");
   if (n < 1) fail(HC_EINVAL, "forward: empty sequence");
   if (n_last < 0 || n_last > n || (n_last > 0 && (sb.cu || next_token || d_next_tokens)))
     fail(HC_EINVAL, "forward: bad last-layer row count");
+  if (kv_only_last && (next_token || d_next_tokens))
+    fail(HC_EINVAL, "forward: the next token needs the last layer's output");
   if (!sb.cu && n > c.max_seq) fail(HC_EINVAL, "forward: sequence exceeds max_seq");
   if (!w->embedding) fail(HC_EINVAL, "prefill_layers: embedding not set");
   if (w->d_kv != w->d_kv_all) fail(HC_EINVAL, "prefill_layers: needs all KV heads on this GPU");
@@ -145,20 +147,44 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
   int32_t* flag = reinterpret_cast<int32_t*>(mean + 2 * n);
   pm.lap(0);
   HC_CUDA(launch_embed(d_tokens, n, w->embedding, d, x, xb_buf.ptr, stream));
-  const int abox = gemm_a_box(n);
-  CUtensorMap tm_xb = tmap(xb_buf.ptr, d, n, abox);
-  CUtensorMap tm_mix = tmap(mix_buf.ptr, d, n, abox);
-  CUtensorMap tm_h1 = tmap(h1_buf.ptr, dffn, n, abox);
   // LayerNorm statistics of xb + the mean-shifted operand for rows with
   // |mean| >> sigma (launch_center_rows; a no-op unless flagged)
   AltA alt;
   const AltA* altp = nullptr;
   const bool center = c.norm_enabled && ln_center_enabled();
   if (center) {
-    alt.map = tmap(xc_buf.ptr, d, n, abox);
     alt.flag = flag;
     altp = &alt;
   }
+  // tensor maps and tile widths of the GEMMs over the first `rows` rows
+  // (every GEMM of an M-row operand uses the A box and tiles M picks)
+  struct Maps {
+    int64_t rows = -1;
+    CUtensorMap xb, mix, h1, xc;
+    int bn_kv = 0, bn_d = 0, bn_f = 0;
+  };
+  auto make_maps = [&](int64_t rows) {
+    Maps mp;
+    mp.rows = rows;
+    const int ab = gemm_a_box(rows);
+    mp.xb = tmap(xb_buf.ptr, d, n, ab);
+    mp.mix = tmap(mix_buf.ptr, d, n, ab);
+    mp.h1 = tmap(h1_buf.ptr, dffn, n, ab);
+    if (center) mp.xc = tmap(xc_buf.ptr, d, n, ab);
+    // K/V: the exact path (restores must reproduce these K/V bit for bit);
+    // the other projections may split K when the rows are decode-sized
+    mp.bn_kv = pick_bn(rows, 2 * w->d_kv_all, sms);
+    mp.bn_d = gemm_pick_bn_skinny(rows, d, sms);
+    mp.bn_f = gemm_pick_bn_skinny(rows, dffn, sms);
+    return mp;
+  };
+  const Maps full = make_maps(n);
+  Maps part;
+  auto maps = [&](int64_t rows) -> const Maps& {
+    if (rows == n) return full;
+    if (part.rows != rows) part = make_maps(rows);
+    return part;
+  };
   auto ln_stats = [&](int64_t rows) {
     if (!center) {
       HC_CUDA(launch_row_stats(xb_buf.ptr, rows, d, d, true, mean, rstd, stream));
@@ -168,27 +194,22 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     HC_CUDA(launch_row_stats_flagged(xb_buf.ptr, rows, d, d, true, mean, rstd, flag, stream));
     HC_CUDA(launch_center_rows(xb_buf.ptr, rows, d, d, mean, flag, xc_buf.ptr, stream));
   };
-  // K/V: the exact path (restores must reproduce these K/V bit for bit); the
-  // other projections may split K when n is decode-sized
-  int bn_kv = pick_bn(n, 2 * w->d_kv_all, sms), bn_d = gemm_pick_bn_skinny(n, d, sms),
-      bn_f = gemm_pick_bn_skinny(n, dffn, sms);
   pm.lap(1);
   for (int L = lb; L < le; ++L) {
     const auto& lw = w->layers[size_t(L)];
     // rows of this layer: all n, or only the first n_last tokens of the last
     // layer (a restore recomputing part of its first hidden layer)
     const int64_t m = (L == le - 1 && n_last > 0) ? n_last : n;
-    if (m != n) {
-      // the GEMMs of a shorter last layer pick their own tiles and A boxes
-      const int ab = gemm_a_box(m);
-      tm_xb = tmap(xb_buf.ptr, d, n, ab);
-      tm_mix = tmap(mix_buf.ptr, d, n, ab);
-      tm_h1 = tmap(h1_buf.ptr, dffn, n, ab);
-      if (center) alt.map = tmap(xc_buf.ptr, d, n, ab);
-      bn_kv = pick_bn(m, 2 * w->d_kv_all, sms);
-      bn_d = gemm_pick_bn_skinny(m, d, sms);
-      bn_f = gemm_pick_bn_skinny(m, dffn, sms);
-    }
+    // rows of this layer's output the next layer reads. A restore's
+    // RECOMPUTE prefix (kv_only_last) needs only the K/V of its last layer
+    // -- the layer after it is restored from its stored input -- so that
+    // layer stops after its K/V projection, and when that layer is shortened
+    // to n_last rows the layer before it computes only those rows' output
+    // (causal: rows [0, n_last) depend on rows [0, n_last) only). Above the
+    // split-K size, so every GEMM keeps the full layer's summation order.
+    int64_t mo = m;
+    if (kv_only_last && L == le - 1) mo = 0;
+    else if (kv_only_last && L == le - 2 && n_last > 0 && n > 128) mo = n_last;
     hook(L, true);
     if (d_layer_inputs)
       HC_CUDA(cudaMemcpyAsync(static_cast<char*>(d_layer_inputs) + size_t(L) * nd * 2, xb_buf.ptr,
@@ -199,10 +220,21 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     pm.lap(3);
     KvOut kv = kv_out_pages(pages, L, d_page_table, sb.table_stride, sb.cu, sb.n_seqs);
     kv.seq_start = sb.seq_start;
-    HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wkv_all, d, 2 * w->d_kv_all, bn_kv), bn_kv, int(m),
-                              2 * w->d_kv_all, d, true, kv, epi_for(w, lw.colsum_all, mean, rstd),
-                              sms, stream, false, altp));
+    {
+      const Maps& mk = maps(m);
+      if (center) alt.map = mk.xc;
+      HC_CUDA(launch_restore_kv(mk.xb, wmap(lw.wkv_all, d, 2 * w->d_kv_all, mk.bn_kv), mk.bn_kv,
+                                int(m), 2 * w->d_kv_all, d, true, kv,
+                                epi_for(w, lw.colsum_all, mean, rstd), sms, stream, false, altp));
+    }
     pm.lap(4);
+    if (mo == 0) {  // only this layer's K/V was needed
+      hook(L, false);
+      pm.lap(10);
+      continue;
+    }
+    const Maps& mp = maps(mo);
+    if (center) alt.map = mp.xc;
     KvOut qo;
     qo.k_base = q_buf.ptr;
     qo.v_base = q_buf.ptr;
@@ -210,7 +242,8 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     qo.cu_seqlens = sb.cu;
     qo.n_seqs = sb.cu ? sb.n_seqs : 1;
     qo.seq_start = sb.seq_start;
-    HC_CUDA(launch_restore_kv(tm_xb, wmap(lw.wq, d, d, bn_d), bn_d, int(m), d, d, true, qo,
+    if (mo != m) ln_stats(mo);  // statistics of the shorter operand's rows (same values)
+    HC_CUDA(launch_restore_kv(mp.xb, wmap(lw.wq, d, d, mp.bn_d), mp.bn_d, int(mo), d, d, true, qo,
                               epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true, altp));
     pm.lap(5);
     if (sb.cu && sb.from_zero && attention_tc_ok(kv))
@@ -223,18 +256,18 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
                                       c.n_heads, c.n_kv_heads, w->d_head, kv, mix_buf.ptr,
                                       stream));
     else
-      HC_CUDA(attention(q_buf.ptr, int(m), c.n_heads, c.n_kv_heads, w->d_head, kv,
+      HC_CUDA(attention(q_buf.ptr, int(mo), c.n_heads, c.n_kv_heads, w->d_head, kv,
                         int64_t(pages->num_pages) * pages->page_size, mix_buf.ptr, stream));
     pm.lap(6);
     GemmOut resid;
     resid.x = x;
     resid.xb = xb_buf.ptr;
     resid.ldo = d;
-    HC_CUDA(launch_gemm_dense(tm_mix, wmap(lw.wo, d, d, bn_d), bn_d, kEpiResid, int(m), d, d,
-                              resid, EpiArgs{}, sms, stream, true));
+    HC_CUDA(launch_gemm_dense(mp.mix, wmap(lw.wo, d, d, mp.bn_d), mp.bn_d, kEpiResid, int(mo), d,
+                              d, resid, EpiArgs{}, sms, stream, true));
     pm.lap(7);
     // FFN block (ffn_forward, model.cpp:290-303)
-    ln_stats(m);
+    ln_stats(mo);
     pm.lap(8);
     GemmOut g1;
     g1.xb = h1_buf.ptr;
@@ -245,11 +278,11 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
       fold.row_rstd = rstd;
       fold.colsum = lw.colsum_fc1;
     }
-    HC_CUDA(launch_gemm_dense(tm_xb, wmap(lw.fc1, d, dffn, bn_f), bn_f, kEpiGelu, int(m), dffn,
-                              d, g1, fold, sms, stream, true, altp));
+    HC_CUDA(launch_gemm_dense(mp.xb, wmap(lw.fc1, d, dffn, mp.bn_f), mp.bn_f, kEpiGelu, int(mo),
+                              dffn, d, g1, fold, sms, stream, true, altp));
     pm.lap(9);
-    HC_CUDA(launch_gemm_dense(tm_h1, wmap(lw.fc2, dffn, d, bn_d), bn_d, kEpiResid, int(m), d,
-                              dffn, resid, EpiArgs{}, sms, stream, true));
+    HC_CUDA(launch_gemm_dense(mp.h1, wmap(lw.fc2, dffn, d, mp.bn_d), mp.bn_d, kEpiResid, int(mo),
+                              d, dffn, resid, EpiArgs{}, sms, stream, true));
     hook(L, false);
     pm.lap(10);
   }

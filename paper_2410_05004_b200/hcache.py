@@ -110,6 +110,11 @@ class RestorationPlan:
         return f"RestorationPlan({self.serialize()})"
 
 
+# c_token at or above this: no RECOMPUTE layers (no full block weights, or the
+# model is not whole on this GPU) -- include/hcache_b200.h HC_RECOMPUTE_UNAVAILABLE
+RECOMPUTE_UNAVAILABLE = 1e9
+
+
 @dataclass
 class ProfiledTimings:
     """planner.hpp:16-24 (seconds per layer)."""

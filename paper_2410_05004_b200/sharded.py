@@ -138,7 +138,7 @@ def plan_sharded(io_h_rank: List[float], io_kv_rank: List[float], c_h_rank: List
     Deterministic in its inputs, so ranks that share them agree."""
     from . import hcache as H
     t = H.ProfiledTimings(io_h=max(io_h_rank), io_kv=max(io_kv_rank), c_h=max(c_h_rank),
-                          c_token=1e9, n_layers=n_layers)
+                          c_token=H.RECOMPUTE_UNAVAILABLE, n_layers=n_layers)
     return H.plan_three_way(t, prefetch_depth=max(1, depth - 1)) + (t,)
 
 

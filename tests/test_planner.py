@@ -122,9 +122,13 @@ def test_schedule_reproduction_criterion5():
 
 
 # -------------------------------------------------------------- pipeline
-def _jobs(plan, io_h, io_kv, c_h, c_tok):
-    """restore_simulated job list (restore.cpp:89-131) in compute order."""
+def _jobs(plan, io_h, io_kv, c_h, c_tok, kv_only_last=False):
+    """restore_simulated job list (restore.cpp:89-131) in compute order.
+    kv_only_last: the B200 executor's prefix, whose last layer stops after
+    its K/V projection (costed c_h, as hc_plan_three_way does)."""
     jobs = []
+    last_re = max([L for L, m in enumerate(plan.layer_assignment) if m == M.RECOMPUTE],
+                  default=-1)
     for method in (M.RECOMPUTE, M.HIDDEN, M.KV_OFFLOAD):
         for L, m in enumerate(plan.layer_assignment):
             if m != method:
@@ -134,7 +138,8 @@ def _jobs(plan, io_h, io_kv, c_h, c_tok):
             elif m == M.KV_OFFLOAD:
                 jobs.append(H.PipelineJob(L, io_kv, 0, True, False, "fetch_kv", "project"))
             else:
-                jobs.append(H.PipelineJob(L, 0, c_tok, False, True, "fetch", "recompute"))
+                c = c_h if (kv_only_last and L == last_re) else c_tok
+                jobs.append(H.PipelineJob(L, 0, c, False, True, "fetch", "recompute"))
     return jobs
 
 
@@ -191,8 +196,8 @@ def test_staging_depth_finding8():
     for depth in (1, 4, 16, 32):
         p, ms = H.plan_three_way(t, depth)
         assert ms <= all_h + 1e-12
-        assert ms == pytest.approx(H.simulate_pipeline(_jobs(p, t.io_h, t.io_kv, t.c_h, t.c_token),
-                                                       depth).total_s)
+        assert ms == pytest.approx(H.simulate_pipeline(_jobs(p, t.io_h, t.io_kv, t.c_h, t.c_token,
+                                                             True), depth).total_s)
     p32, ms32 = H.plan_three_way(t, 32)
     assert ms32 == pytest.approx(H.makespan(closed, t), rel=0.05) or ms32 < H.makespan(closed, t)
 
@@ -221,8 +226,8 @@ def test_three_way_is_exhaustive_optimum():
         for l_re in range(n + 1):
             for l_kv in range(n + 1 - l_re):
                 q = H.RestorationPlan.make_mixed(l_re, n - l_re - l_kv, l_kv)
-                best = min(best, H.simulate_pipeline(_jobs(q, t.io_h, t.io_kv, t.c_h, t.c_token),
-                                                     depth).total_s)
+                best = min(best, H.simulate_pipeline(_jobs(q, t.io_h, t.io_kv, t.c_h, t.c_token,
+                                                           True), depth).total_s)
         assert ms == pytest.approx(best, rel=1e-12)
 
 
@@ -245,15 +250,16 @@ def test_token_split_balances_the_lanes():
     t = T(0.61e-3, 1.21e-3, 0.20e-3, 1.31e-3, 32)
     for l_re in (0, 6, 7, 8):
         p = H.RestorationPlan.make(32, 32 - l_re, C.RECOMPUTE if l_re else C.NONE)
-        base = H.simulate_pipeline(_jobs(p, t.io_h, t.io_kv, t.c_h, t.c_token), 32).total_s
+        base = H.simulate_pipeline(_jobs(p, t.io_h, t.io_kv, t.c_h, t.c_token, True), 32).total_s
         s, ms = H.plan_token_split(t, p, 4096, 32)
         assert s % 64 == 0 and 0 <= s < 4096
         assert ms <= base + 1e-12
-    p7 = H.RestorationPlan.make(32, 25, C.RECOMPUTE)
-    s, ms = H.plan_token_split(t, p7, 4096, 32)
+    pw, _ = H.plan_three_way(t, 32)  # the best whole-layer plan (8RE+24H)
+    s, ms = H.plan_token_split(t, pw, 4096, 32)
     best_whole = min(H.simulate_pipeline(_jobs(H.RestorationPlan.make(32, 32 - r, C.RECOMPUTE if r
                                                                        else C.NONE),
-                                               t.io_h, t.io_kv, t.c_h, t.c_token), 32).total_s
+                                               t.io_h, t.io_kv, t.c_h, t.c_token, True),
+                                         32).total_s
                      for r in range(0, 12))
     assert s > 0 and ms < best_whole
     # no HIDDEN layer right after the prefix (KV-offload-only plan): no split
@@ -292,3 +298,20 @@ def test_serial_lanes_keep_the_reference_sum():
     ev = [(H.Lane.COMPUTE, 0.1, 0.3), (H.Lane.COMPUTE, 0.3, 0.7), (H.Lane.COMPUTE, 0.9, 1.0)]
     tl = _timeline(ev, 1.0)
     assert tl.lane_busy(H.Lane.COMPUTE) == (0.3 - 0.1) + (0.7 - 0.3) + (1.0 - 0.9)
+
+
+def test_three_way_prices_the_prefix_last_layer_as_a_projection():
+    """The executor stops the RECOMPUTE prefix's last layer after its K/V
+    projection, so a one-layer prefix (layer 0 = embedding + K1, no fetch)
+    costs c_h and the planner takes it whenever the IO lane is the longer
+    one; c_token >= RECOMPUTE_UNAVAILABLE forbids any prefix."""
+    t = T(0.61e-3, 1.21e-3, 0.20e-3, 1.31e-3, 32)
+    p, ms = H.plan_three_way(t, 32)
+    assert p.l_re >= 1
+    one = H.RestorationPlan.make(32, 31, C.RECOMPUTE)
+    assert H.simulate_pipeline(_jobs(one, t.io_h, t.io_kv, t.c_h, t.c_token, True), 32).total_s \
+        < H.simulate_pipeline(_jobs(H.RestorationPlan.make(32, 32, C.NONE), t.io_h, t.io_kv,
+                                    t.c_h, t.c_token), 32).total_s
+    t.c_token = H.RECOMPUTE_UNAVAILABLE
+    p, _ = H.plan_three_way(t, 32)
+    assert p.l_re == 0
