@@ -427,13 +427,7 @@ def run_ours(args, cfg, rank, world):
         # the planner splits between hidden states and KV offload only
         prof.c_token = H.RECOMPUTE_UNAVAILABLE
     plan, plan_ms = H.plan_three_way(prof, layer_bytes=n * d * 2)
-    # B200 extension: split the first hidden layer between the recompute
-    # prefix and the link where that balances the two lanes
-    # (opt-in, HC_SPLIT=1: interleaved A/B runs on B200 did not separate it
-    # from run-to-run noise, scripts/ab_split.sh)
-    split, split_ms = 0, plan_ms
-    if full and os.environ.get("HC_SPLIT") == "1":
-        split, split_ms = H.plan_token_split(prof, plan, n, layer_bytes=n * d * 2)
+    prof0 = prof
     all_h = H.RestorationPlan.make(L, L, H.Complement.NONE)
     all_kv = H.RestorationPlan.make(L, 0, H.Complement.KV_OFFLOAD)
 
@@ -464,7 +458,6 @@ def run_ours(args, cfg, rank, world):
                                         table.data_ptr(), 0, stream))
 
     opts = capi.RestoreOptsC(0, 0, 0)
-    opts_plan = capi.RestoreOptsC(0, 0, split)
     host_ck = torch.empty(16 * d_kv, dtype=torch.bfloat16, pin_memory=True)
 
     def restore_step(sid, p, o=opts):
@@ -484,6 +477,35 @@ def run_ours(args, cfg, rank, world):
 
     resident_step()
     torch.cuda.synchronize()
+    # the planner's costs refined on the restore itself: hc_profile times the
+    # recompute under back-to-back K6 layers (the hardest power-cap case); a
+    # restore's prefix shares the part with the DMA and the K1s. Restore the
+    # plan with a timeline, take each kind's per-event busy time
+    # (hc_timings_from_timeline), re-plan, until the plan is stable.
+    calibration = []
+    if full and not os.environ.get("HC_NO_CALIBRATE"):
+        for it in range(3):
+            save(f"cal{it}", plan)
+            for _ in range(3):
+                res = H.restore(store, f"cal{it}", w, plan, H.ThrottleConfig(0, True), kv, table)
+            prof = H.timings_from_timeline(res.timeline, prof)
+            prof.n_layers = L
+            nxt, nxt_ms = H.plan_three_way(prof, layer_bytes=n * d * 2)
+            calibration.append({"plan": plan.serialize(), "measured_ms": res.timeline.total_s * 1e3,
+                                "c_token_ms": prof.c_token * 1e3, "c_h_ms": prof.c_h * 1e3,
+                                "io_h_ms": prof.io_h * 1e3, "replan": nxt.serialize(),
+                                "replan_predicted_ms": nxt_ms * 1e3})
+            if nxt.serialize() == plan.serialize():
+                break
+            plan, plan_ms = nxt, nxt_ms
+    # B200 extension: split the first hidden layer between the recompute
+    # prefix and the link where that balances the two lanes
+    # (opt-in, HC_SPLIT=1: interleaved A/B runs on B200 did not separate it
+    # from run-to-run noise, scripts/ab_split.sh)
+    split, split_ms = 0, plan_ms
+    if full and os.environ.get("HC_SPLIT") == "1":
+        split, split_ms = H.plan_token_split(prof, plan, n, layer_bytes=n * d * 2)
+    opts_plan = capi.RestoreOptsC(0, 0, split)
     save(b"hcache".decode(), plan, keep=True)
     if plan.serialize() != all_h.serialize():
         save("all_hidden", all_h)
@@ -606,10 +628,15 @@ def run_ours(args, cfg, rank, world):
         "speedup": {"hcache_vs_kv_offload": ms_kv / ms_restore,
                     "hcache_vs_recompute": (ms_re / ms_restore) if ms_re else None,
                     "hcache_vs_all_hidden": ms_allh / ms_restore},
-        "planner": {"profiled": {"io_h_ms": prof.io_h * 1e3, "io_kv_ms": prof.io_kv * 1e3,
-                                 "c_h_ms": prof.c_h * 1e3, "c_token_ms": prof.c_token * 1e3},
+        "planner": {"profiled": {"io_h_ms": prof0.io_h * 1e3, "io_kv_ms": prof0.io_kv * 1e3,
+                                 "c_h_ms": prof0.c_h * 1e3, "c_token_ms": prof0.c_token * 1e3},
+                    "calibrated": {"io_h_ms": prof.io_h * 1e3, "io_kv_ms": prof.io_kv * 1e3,
+                                   "c_h_ms": prof.c_h * 1e3, "c_token_ms": prof.c_token * 1e3},
+                    "calibration": calibration,
                     "plan": plan.serialize(), "split_tokens": split,
-                    "how": "hc_plan_three_way (+ hc_plan_token_split) on hc_profile",
+                    "how": "hc_plan_three_way (+ hc_plan_token_split) on hc_profile, refined on "
+                           "timelines of the restore itself (hc_timings_from_timeline) until "
+                           "the plan is stable",
                     "predicted_ms": plan_ms * 1e3 if plan_ms else None,
                     "predicted_with_split_ms": split_ms * 1e3 if split_ms else None},
         "parity": parity,

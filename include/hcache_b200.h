@@ -249,6 +249,12 @@ typedef struct hc_pipeline_job {
 } hc_pipeline_job;
 
 double hc_timeline_lane_busy(const hc_timeline* tl, int32_t lane);
+/* B200 extension of profile_hardware (harness.cpp:431-490): refine timings
+ * from a measured restore's timeline. io_h / io_kv / c_h / c_token become the
+ * per-event busy time of that kind (union of its intervals / event count;
+ * RECOMPUTE without the prefix's last, projection-only layer, and only when
+ * the prefix has >= 2 layers); kinds without events keep their value. */
+hc_status hc_timings_from_timeline(const hc_timeline* tl, hc_timings* io);
 hc_status hc_timeline_bubble_fraction(const hc_timeline* tl, double* out);
 /* simulate_pipeline (pipeline.cpp:33-104) */
 hc_status hc_simulate_pipeline(const hc_pipeline_job* jobs, int32_t n_jobs,

@@ -145,6 +145,7 @@ _PROTOS = {
     "hc_plan_three_way": (i32, [P(TimingsC), i32, P(PlanC), P(f64)]),
     "hc_plan_token_split": (i32, [P(TimingsC), i32, P(PlanC), i32, P(i32), P(f64)]),
     "hc_timeline_lane_busy": (f64, [P(TimelineC), i32]),
+    "hc_timings_from_timeline": (i32, [P(TimelineC), P(TimingsC)]),
     "hc_timeline_bubble_fraction": (i32, [P(TimelineC), P(f64)]),
     "hc_simulate_pipeline": (i32, [P(PipelineJobC), i32, i32, P(TimelineC)]),
     "hc_store_create": (i32, [P(PoolDescC), C.c_size_t, P(vp)]),

@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -499,11 +500,114 @@ __device__ __forceinline__ void tile_coords_pair(int tile, int num_m, int num_n,
   tile_coords(tile, num_m, num_n, m_blk, n_blk);
 }
 
+// Tail split of the last, partial wave (summation-order-free callers only,
+// split_acc). With T tiles over C clusters the persistent schedule runs
+// floor(T/C) full waves and a last one of R = T mod C tiles that leaves C-R
+// SM pairs idle (N=4096 GEMMs of a 4096-token layer: 256 tiles on 74 pairs,
+// 3.46 waves run as 4). When 2R <= C the R tail tiles are each split into two
+// K halves on two clusters: the first half's raw fp32 accumulators go to a
+// workspace (through L2), the second adds them to its own and runs the
+// epilogue -- the last wave takes half as long. The unit -> (tile, K range)
+// map depends only on the schedule shape (Ms, N, K, C), so a GEMM and its
+// row-truncated copy (Ms fixed, fewer valid rows M) sum every element in the
+// same order.
+struct PairUnit {
+  int tile, kb0, kb1, half, slot;  // half: -1 whole tile, 0/1 K halves of tail tile `slot`
+};
+
+__device__ __forceinline__ PairUnit pair_unit(int u, int full_units, bool split, int num_kb) {
+  PairUnit p;
+  if (!split || u < full_units) {
+    p.tile = u;
+    p.kb0 = 0;
+    p.kb1 = num_kb;
+    p.half = -1;
+    p.slot = -1;
+  } else {
+    const int t = (u - full_units) >> 1, kh = num_kb >> 1;
+    p.tile = full_units + t;
+    p.half = (u - full_units) & 1;
+    p.kb0 = p.half ? kh : 0;
+    p.kb1 = p.half ? num_kb : kh;
+    p.slot = t;
+  }
+  return p;
+}
+
+// Host and device agree on the tail split from the schedule shape alone.
+__host__ __device__ __forceinline__ int pair_full_units(int tiles, int clusters) {
+  return (tiles / clusters) * clusters;
+}
+__host__ __device__ __forceinline__ bool pair_tail_split(int tiles, int clusters, int num_kb) {
+  const int tail = tiles - pair_full_units(tiles, clusters);
+  return tail > 0 && 2 * tail <= clusters && num_kb >= 2;
+}
+
+// Workspace of one tail slot and CTA: 128 rows x 256 fp32 accumulators,
+// chunk-major ((c * 8 + i) * 128 + row) float4s so a warp's accesses are
+// contiguous.
+constexpr size_t kTailSlotFloats = 128 * 256;
+
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void epi_bar_sync() {  // the four epilogue warps of a CTA
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+template <int MODE>
+__device__ __forceinline__ void epilogue_tile_pair(int row, int row_local, int n_blk, int M, int N,
+                                                   const KvOut& out, const GemmOut& gout,
+                                                   const EpiArgs& epi, uint32_t tbase, float* ws,
+                                                   int half) {
+  constexpr int BN = 256;
+  const bool row_ok = row < M;
+  RowMeta meta;
+  if (row_ok && half != 0) meta = row_meta<MODE>(row, out, epi);
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t v[32];
+    tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), v);
+    tmem_wait_ld();
+    float f[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+    float4* w4 = ws ? reinterpret_cast<float4*>(ws) + size_t(c) * 8 * 128 + row_local : nullptr;
+    if (half == 0) {  // first K half: raw accumulators to the workspace
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        __stcg(w4 + i * 128, make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]));
+      continue;
+    }
+    const int col0 = n_blk * BN + c * 32;
+    if (!(row_ok && col0 < N)) continue;
+    if (half == 1) {  // second K half: first half's sums + this half's
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 p = __ldcg(w4 + i * 128);
+        f[4 * i + 0] = p.x + f[4 * i + 0];
+        f[4 * i + 1] = p.y + f[4 * i + 1];
+        f[4 * i + 2] = p.z + f[4 * i + 2];
+        f[4 * i + 3] = p.w + f[4 * i + 3];
+      }
+    }
+    apply_chunk<MODE>(f, row, col0, meta, out, gout, epi);
+  }
+}
+
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ AMaps am,
                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
-                        GemmOut gout, EpiArgs epi, uint32_t idesc) {
+                        GemmOut gout, EpiArgs epi, uint32_t idesc, int Ms, float* tail_ws,
+                        int32_t* tail_flags) {
+  // M: rows stored; Ms >= M: rows the schedule is laid out for (units whose
+  // tile starts at or past M are skipped by every role)
   constexpr int BN = 256, S = kPairStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -520,10 +624,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = int(blockIdx.x >> 1), n_clusters = int(gridDim.x >> 1);
-  const int num_m = (M + 255) / 256;
+  const int num_m = (Ms + 255) / 256;
   const int num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_kb = (K + kBK - 1) / kBK;
+  const bool split = tail_ws != nullptr && pair_tail_split(num_tiles, n_clusters, num_kb);
+  const int full_units = split ? pair_full_units(num_tiles, n_clusters) : num_tiles;
+  const int num_units = split ? num_tiles + (num_tiles - full_units) : num_tiles;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < am.n; ++i) tma_prefetch_desc(&am.m[i]);
@@ -551,10 +658,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         constexpr bool kAlt = decltype(alt_tag)::value;
         int stage = 0;
         uint32_t phase = 0;
-        for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+        for (int u = cluster; u < num_units; u += n_clusters) {
+          const PairUnit pu = pair_unit(u, full_units, split, num_kb);
           int m_blk, n_blk;
-          tile_coords_pair(tile, num_m, num_n, m_blk, n_blk);
-          for (int kb = 0; kb < num_kb; ++kb) {
+          tile_coords_pair(pu.tile, num_m, num_n, m_blk, n_blk);
+          if (m_blk * 256 >= M) continue;
+          for (int kb = pu.kb0; kb < pu.kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
             int a_row;
@@ -582,11 +691,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+      for (int u = cluster; u < num_units; u += n_clusters) {
+        const PairUnit pu = pair_unit(u, full_units, split, num_kb);
+        int m_blk, n_blk;
+        tile_coords_pair(pu.tile, num_m, num_n, m_blk, n_blk);
+        if (m_blk * 256 >= M) continue;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = pu.kb0; kb < pu.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
@@ -595,7 +708,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k)
               umma_f16_pair(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
-                            (kb | k) != 0 ? 1u : 0u);
+                            ((kb - pu.kb0) | k) != 0 ? 1u : 0u);
             umma_commit_pair(&empty[stage], 0x3);  // frees the slot in both CTAs
           }
           __syncwarp();
@@ -615,14 +728,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+    for (int u = cluster; u < num_units; u += n_clusters) {
+      const PairUnit pu = pair_unit(u, full_units, split, num_kb);
       int m_blk, n_blk;
-      tile_coords_pair(tile, num_m, num_n, m_blk, n_blk);
-      const int row = m_blk * 256 + int(rank) * 128 + q * 32 + lane;
+      tile_coords_pair(pu.tile, num_m, num_n, m_blk, n_blk);
+      if (m_blk * 256 >= M) continue;
+      const int row_local = q * 32 + lane;
+      const int row = m_blk * 256 + int(rank) * 128 + row_local;
+      float* ws = pu.half >= 0 ? tail_ws + (size_t(pu.slot) * 2 + rank) * kTailSlotFloats : nullptr;
+      int32_t* flag = pu.half >= 0 ? tail_flags + pu.slot * 2 + int(rank) : nullptr;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      epilogue_tile<BN, MODE>(row, n_blk, M, N, out, gout, epi,
-                              tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN), lane);
+      if (pu.half == 1) {  // the first K half's sums must have landed
+        if (q == 0 && lane == 0)
+          while (ld_acquire_gpu(flag) == 0) __nanosleep(32);
+        epi_bar_sync();
+      }
+      epilogue_tile_pair<MODE>(row, row_local, n_blk, M, N, out, gout, epi,
+                               tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN), ws,
+                               pu.half);
+      if (pu.half == 0) {  // publish: every thread's stores, then one release
+        __threadfence();
+        epi_bar_sync();
+        if (q == 0 && lane == 0) st_release_gpu(flag, 1);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
@@ -849,10 +978,28 @@ __global__ void kv_gather_kernel(KvOut kv, int pos0, int64_t n_rows, uint4* __re
 template <int MODE>
 cudaError_t launch_pair(const AMaps& tmA, const CUtensorMap& tmB128, int M, int N, int K,
                         bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
-                        int num_sms, cudaStream_t stream) {
+                        int num_sms, cudaStream_t stream, int Ms, bool split_acc) {
   const uint32_t idesc = umma_idesc_f16(256, 256, bf16_in);
-  const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  const int tiles = ((Ms + 255) / 256) * ((N + 255) / 256);
   int grid = 2 * (tiles < num_sms / 2 ? tiles : num_sms / 2);
+  // tail split (summation order may change: split_acc callers only)
+  static const bool tail_enabled = [] {
+    const char* e = getenv("HC_PAIR_TAIL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  float* ws = nullptr;
+  int32_t* flags = nullptr;
+  const int num_kb = (K + kBK - 1) / kBK;
+  if (split_acc && tail_enabled && pair_tail_split(tiles, grid / 2, num_kb)) {
+    const int slots = tiles - pair_full_units(tiles, grid / 2);
+    const size_t ws_bytes = size_t(slots) * 2 * kTailSlotFloats * sizeof(float);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws),
+                                    ws_bytes + size_t(slots) * 2 * sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
+    flags = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + ws_bytes);
+    e = cudaMemsetAsync(flags, 0, size_t(slots) * 2 * sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
+  }
   static thread_local int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -864,7 +1011,8 @@ cudaError_t launch_pair(const AMaps& tmA, const CUtensorMap& tmB128, int M, int 
     attr_dev = dev;
   }
   tc_gemm_pair_kernel<MODE><<<grid, kThreads, kPairSmem, stream>>>(tmA, tmB128, M, N, K, out, g,
-                                                                   epi, idesc);
+                                                                   epi, idesc, Ms, ws, flags);
+  if (ws) cudaFreeAsync(ws, stream);
   return cudaGetLastError();
 }
 
@@ -881,7 +1029,8 @@ bool use_pair(int M, int N, int num_sms) {
 template <int BN, int MODE>
 cudaError_t launch_tc(const AMaps& tmA, const CUtensorMap& tmB, int M, int N, int K,
                       bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
-                      int num_sms, cudaStream_t stream, bool split_acc = false) {
+                      int num_sms, cudaStream_t stream, bool split_acc = false, int Ms = 0) {
+  if (Ms < M) Ms = M;
   const uint32_t idesc = umma_idesc_f16(kBM, BN, bf16_in);
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms ? tiles : num_sms;
@@ -895,13 +1044,13 @@ cudaError_t launch_tc(const AMaps& tmA, const CUtensorMap& tmB, int M, int N, in
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  const RingCfg r = ring_cfg<BN>(gemm_a_box(M));
+  const RingCfg r = ring_cfg<BN>(gemm_a_box(Ms));  // the caller's A box follows Ms
   // Decode-sized M: a CTA's time is ~(its K blocks) x (a fixed per-MMA cost),
   // whatever the tile width, so the K loop is split over CTAs (fp32 partials
   // + splitk_epilogue_kernel). Not used where bit-identical K/V matter.
   int k_splits = 1;
   const int num_kb = (K + kBK - 1) / kBK;
-  if (split_acc && M <= kBM && N % 32 == 0) {
+  if (split_acc && Ms <= kBM && N % 32 == 0) {
     k_splits = std::max(1, std::min(num_sms / std::max(1, tiles), num_kb / 2));
     const int kb_per = (num_kb + k_splits - 1) / k_splits;
     k_splits = (num_kb + kb_per - 1) / kb_per;  // no empty K slice
@@ -971,16 +1120,21 @@ namespace {
 template <int MODE>
 cudaError_t launch_tc_bn(int bn, const AMaps& tmA, const CUtensorMap& tmB, int M, int N,
                          int K, bool bf16_in, const KvOut& out, const GemmOut& g,
-                         const EpiArgs& epi, int num_sms, cudaStream_t stream, bool split_acc) {
+                         const EpiArgs& epi, int num_sms, cudaStream_t stream, bool split_acc,
+                         int Ms) {
   switch (bn) {
     case 256:
-      return launch_tc<256, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc);
+      return launch_tc<256, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc,
+                                     Ms);
     case 128:
-      return launch_tc<128, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc);
+      return launch_tc<128, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc,
+                                     Ms);
     case 64:
-      return launch_tc<64, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc);
+      return launch_tc<64, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc,
+                                     Ms);
     case 32:
-      return launch_tc<32, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc);
+      return launch_tc<32, MODE>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, split_acc,
+                                     Ms);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1000,14 +1154,17 @@ AMaps amaps_with_alt(const CUtensorMap& tmA, const AltA* alt) {
 
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream, bool split_acc, const AltA* alt) {
+                              int num_sms, cudaStream_t stream, bool split_acc, const AltA* alt,
+                              int m_sched) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  const int Ms = std::max(M, m_sched);
   GemmOut g;
   const AMaps am = amaps_with_alt(tmA, alt);
-  if (bn == 128 && use_pair(M, N, num_sms))  // tmB has the 128-row box the pair needs
-    return launch_pair<kEpiKv>(am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
+  if (bn == 128 && use_pair(Ms, N, num_sms))  // tmB has the 128-row box the pair needs
+    return launch_pair<kEpiKv>(am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, Ms,
+                               split_acc);
   return launch_tc_bn<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream,
-                              split_acc);
+                              split_acc, Ms);
 }
 
 cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int bn, int M, int N,
@@ -1019,26 +1176,31 @@ cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int
     if (am.row0[i] % kBM) return cudaErrorInvalidValue;  // a tile reads one source
   GemmOut g;
   if (bn == 128 && use_pair(M, N, num_sms))
-    return launch_pair<kEpiKv>(am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream);
+    return launch_pair<kEpiKv>(am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, M, false);
   // (no K split: the multi-source path restores K/V, which stay exact)
-  return launch_tc_bn<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, false);
+  return launch_tc_bn<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, false,
+                              M);
 }
 
 cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,
                               int M, int N, int K, const GemmOut& g, const EpiArgs& epi,
-                              int num_sms, cudaStream_t stream, bool split_acc, const AltA* alt) {
+                              int num_sms, cudaStream_t stream, bool split_acc, const AltA* alt,
+                              int m_sched) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  const int Ms = std::max(M, m_sched);
   KvOut o;
   const AMaps am = amaps_with_alt(tmA, alt);
-  if (bn == 128 && use_pair(M, N, num_sms))
+  if (bn == 128 && use_pair(Ms, N, num_sms))
     return mode == kEpiResid
-               ? launch_pair<kEpiResid>(am, tmB, M, N, K, true, o, g, epi, num_sms, stream)
-               : launch_pair<kEpiGelu>(am, tmB, M, N, K, true, o, g, epi, num_sms, stream);
+               ? launch_pair<kEpiResid>(am, tmB, M, N, K, true, o, g, epi, num_sms, stream, Ms,
+                                        split_acc)
+               : launch_pair<kEpiGelu>(am, tmB, M, N, K, true, o, g, epi, num_sms, stream, Ms,
+                                       split_acc);
   if (mode == kEpiResid)
     return launch_tc_bn<kEpiResid>(bn, am, tmB, M, N, K, true, o, g, epi, num_sms, stream,
-                                   split_acc);
+                                   split_acc, Ms);
   return launch_tc_bn<kEpiGelu>(bn, am, tmB, M, N, K, true, o, g, epi, num_sms, stream,
-                                split_acc);
+                                split_acc, Ms);
 }
 
 cudaError_t launch_row_stats_flagged(const void* x, int64_t rows, int cols, int64_t row_stride,

@@ -102,10 +102,15 @@ struct AltA {
   CUtensorMap map;
   const int32_t* flag;
 };
+// m_sched (> M): lay the tiles and K splits out as for m_sched rows and store
+// only the first M -- a row-truncated GEMM then sums every element in the
+// order of the full one (tensor maps and bn must be those of m_sched rows).
+// With split_acc the CTA-pair kernel may also split the K loop of the tiles
+// of its last, partial wave over two SM pairs (see tc_gemm_pair_kernel).
 cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int M,
                               int N, int K, bool bf16_in, const KvOut& out, const EpiArgs& epi,
                               int num_sms, cudaStream_t stream, bool split_acc = false,
-                              const AltA* alt = nullptr);
+                              const AltA* alt = nullptr, int m_sched = 0);
 // Per-source LayerNorm statistics of a head-sharded layer (the owners'
 // slots, mapped over NVLink): rows [row0[s], row0[s+1]) come from
 // mean[s] / rstd[s].
@@ -133,7 +138,7 @@ cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int
 cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, int bn, int mode,
                               int M, int N, int K, const GemmOut& g, const EpiArgs& epi,
                               int num_sms, cudaStream_t stream, bool split_acc = false,
-                              const AltA* alt = nullptr);
+                              const AltA* alt = nullptr, int m_sched = 0);
 
 // Causal attention over the paged cache for a prefill from position 0
 // (attention_forward, model.cpp:237-288): q [n x n_heads*dh] bf16 (RoPE

@@ -458,6 +458,48 @@ double hc_timeline_lane_busy(const hc_timeline* tl, int32_t lane) {
   return b;
 }
 
+hc_status hc_timings_from_timeline(const hc_timeline* tl, hc_timings* io) {
+  return guard([&] {
+    if (!tl || !io) fail(HC_EINVAL, "timings_from_timeline: null argument");
+    // the prefix's last layer stops after its K/V projection: not a block
+    int last_re = -1, n_re = 0;
+    for (int i = 0; i < tl->n_events; ++i)
+      if (tl->events[i].kind == HC_EV_RECOMPUTE) {
+        last_re = std::max(last_re, tl->events[i].layer);
+        ++n_re;
+      }
+    // per kind: the union of its intervals / its event count -- the lane's
+    // throughput for that kind (K1 launches on two streams overlap)
+    auto per_event = [&](int kind, double* out) {
+      std::vector<std::pair<double, double>> iv;
+      for (int i = 0; i < tl->n_events; ++i) {
+        const hc_event& e = tl->events[i];
+        if (e.kind != kind || e.end_s <= e.start_s) continue;
+        if (kind == HC_EV_RECOMPUTE && n_re > 1 && e.layer == last_re) continue;
+        iv.emplace_back(e.start_s, e.end_s);
+      }
+      if (iv.empty()) return;
+      std::sort(iv.begin(), iv.end());
+      double b = 0, cs = iv[0].first, ce = iv[0].second;
+      for (size_t k = 1; k < iv.size(); ++k) {
+        if (iv[k].first < ce) {
+          ce = std::max(ce, iv[k].second);
+          continue;
+        }
+        b += ce - cs;
+        cs = iv[k].first;
+        ce = iv[k].second;
+      }
+      b += ce - cs;
+      *out = b / double(iv.size());
+    };
+    per_event(HC_EV_FETCH_HIDDEN, &io->io_h);
+    per_event(HC_EV_FETCH_KV, &io->io_kv);
+    per_event(HC_EV_PROJECT, &io->c_h);
+    if (n_re > 1) per_event(HC_EV_RECOMPUTE, &io->c_token);
+  });
+}
+
 hc_status hc_timeline_bubble_fraction(const hc_timeline* tl, double* out) {
   return guard([&] {
     // Timeline::bubble_fraction (pipeline.cpp:16-22)

@@ -178,12 +178,12 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     mp.bn_f = gemm_pick_bn_skinny(rows, dffn, sms);
     return mp;
   };
-  const Maps full = make_maps(n);
-  Maps part;
-  auto maps = [&](int64_t rows) -> const Maps& {
-    if (rows == n) return full;
-    if (part.rows != rows) part = make_maps(rows);
-    return part;
+  const Maps full_maps = make_maps(n);
+  Maps part_maps;
+  auto maps = [&](int64_t rows) -> const Maps* {
+    if (rows == n) return &full_maps;
+    if (part_maps.rows != rows) part_maps = make_maps(rows);
+    return &part_maps;
   };
   auto ln_stats = [&](int64_t rows) {
     if (!center) {
@@ -205,11 +205,12 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     // -- the layer after it is restored from its stored input -- so that
     // layer stops after its K/V projection, and when that layer is shortened
     // to n_last rows the layer before it computes only those rows' output
-    // (causal: rows [0, n_last) depend on rows [0, n_last) only). Above the
-    // split-K size, so every GEMM keeps the full layer's summation order.
+    // (causal: rows [0, n_last) depend on rows [0, n_last) only). Its
+    // GEMMs keep the m-row schedule (m_sched), so every element is summed in
+    // the full layer's order.
     int64_t mo = m;
     if (kv_only_last && L == le - 1) mo = 0;
-    else if (kv_only_last && L == le - 2 && n_last > 0 && n > 128) mo = n_last;
+    else if (kv_only_last && L == le - 2 && n_last > 0) mo = n_last;
     hook(L, true);
     if (d_layer_inputs)
       HC_CUDA(cudaMemcpyAsync(static_cast<char*>(d_layer_inputs) + size_t(L) * nd * 2, xb_buf.ptr,
@@ -221,7 +222,7 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     KvOut kv = kv_out_pages(pages, L, d_page_table, sb.table_stride, sb.cu, sb.n_seqs);
     kv.seq_start = sb.seq_start;
     {
-      const Maps& mk = maps(m);
+      const Maps& mk = *maps(m);
       if (center) alt.map = mk.xc;
       HC_CUDA(launch_restore_kv(mk.xb, wmap(lw.wkv_all, d, 2 * w->d_kv_all, mk.bn_kv), mk.bn_kv,
                                 int(m), 2 * w->d_kv_all, d, true, kv,
@@ -233,7 +234,9 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
       pm.lap(10);
       continue;
     }
-    const Maps& mp = maps(mo);
+    // the GEMMs below store mo rows but keep the m-row schedule (m_sched):
+    // every element is summed in the order of the full layer's GEMMs
+    const Maps& mp = *maps(m);
     if (center) alt.map = mp.xc;
     KvOut qo;
     qo.k_base = q_buf.ptr;
@@ -244,7 +247,8 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     qo.seq_start = sb.seq_start;
     if (mo != m) ln_stats(mo);  // statistics of the shorter operand's rows (same values)
     HC_CUDA(launch_restore_kv(mp.xb, wmap(lw.wq, d, d, mp.bn_d), mp.bn_d, int(mo), d, d, true, qo,
-                              epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true, altp));
+                              epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true, altp,
+                              int(m)));
     pm.lap(5);
     if (sb.cu && sb.from_zero && attention_tc_ok(kv))
       HC_CUDA(launch_attention_tc_varlen(q_buf.ptr, n, sb.n_seqs, sb.max_new, sb.cu, c.n_heads,
@@ -264,7 +268,7 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     resid.xb = xb_buf.ptr;
     resid.ldo = d;
     HC_CUDA(launch_gemm_dense(mp.mix, wmap(lw.wo, d, d, mp.bn_d), mp.bn_d, kEpiResid, int(mo), d,
-                              d, resid, EpiArgs{}, sms, stream, true));
+                              d, resid, EpiArgs{}, sms, stream, true, nullptr, int(m)));
     pm.lap(7);
     // FFN block (ffn_forward, model.cpp:290-303)
     ln_stats(mo);
@@ -279,10 +283,10 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
       fold.colsum = lw.colsum_fc1;
     }
     HC_CUDA(launch_gemm_dense(mp.xb, wmap(lw.fc1, d, dffn, mp.bn_f), mp.bn_f, kEpiGelu, int(mo),
-                              dffn, d, g1, fold, sms, stream, true, altp));
+                              dffn, d, g1, fold, sms, stream, true, altp, int(m)));
     pm.lap(9);
     HC_CUDA(launch_gemm_dense(mp.h1, wmap(lw.fc2, dffn, d, mp.bn_d), mp.bn_d, kEpiResid, int(mo),
-                              d, dffn, resid, EpiArgs{}, sms, stream, true));
+                              d, dffn, resid, EpiArgs{}, sms, stream, true, nullptr, int(m)));
     hook(L, false);
     pm.lap(10);
   }
@@ -323,9 +327,10 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
 void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int lb, int le,
                          const hc_kv_pages* pages, const int32_t* d_page_table,
                          cudaStream_t stream, const std::function<void(int, bool)>& hook,
-                         void* d_layer_inputs, int32_t* next_token, int64_t n_last) {
+                         void* d_layer_inputs, int32_t* next_token, int64_t n_last,
+                         bool kv_only_last) {
   forward_impl(w, d_tokens, n, lb, le, pages, d_page_table, stream, hook, d_layer_inputs,
-               next_token, SeqBatch{}, nullptr, n_last);
+               next_token, SeqBatch{}, nullptr, n_last, kv_only_last);
 }
 
 void forward_batch_dev(const hc_weights* w, const int32_t* d_tokens, int n_seqs, int64_t total,
@@ -348,7 +353,7 @@ void forward_batch_layers(const hc_weights* w, const int32_t* d_tokens, int n_se
                           int max_new, const int32_t* d_cu, const int32_t* d_starts,
                           const hc_kv_pages* pages, const int32_t* d_page_tables,
                           int table_stride, int lb, int le, cudaStream_t stream,
-                          const std::function<void(int, bool)>& hook) {
+                          const std::function<void(int, bool)>& hook, bool kv_only_last) {
   if (!w || n_seqs < 1 || total < 1 || max_new < 1 || !d_cu || !d_starts)
     fail(HC_EINVAL, "forward_batch: bad argument");
   SeqBatch sb;
@@ -359,7 +364,7 @@ void forward_batch_layers(const hc_weights* w, const int32_t* d_tokens, int n_se
   sb.table_stride = table_stride;
   sb.from_zero = true;  // the RECOMPUTE prefix of a restore: every session from position 0
   forward_impl(w, d_tokens, total, lb, le, pages, d_page_tables, stream, hook, nullptr, nullptr,
-               sb, nullptr);
+               sb, nullptr, 0, kv_only_last);
 }
 
 void forward_batch(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
@@ -460,8 +465,10 @@ hc_status hc_prefill_layers(const hc_weights* w, const int32_t* d_tokens, int64_
                             int32_t layer_begin, int32_t layer_end, const hc_kv_pages* pages,
                             const int32_t* d_page_table, void* stream) {
   return guard([&] {
+    // prefill_layers (model.cpp:349-356) discards the last block's output:
+    // only the K/V of its last layer are observable
     prefill_layers_impl(w, d_tokens, n, layer_begin, layer_end, pages, d_page_table,
-                        as_stream(stream), [](int, bool) {});
+                        as_stream(stream), [](int, bool) {}, nullptr, nullptr, 0, true);
   });
 }
 

@@ -11,6 +11,9 @@ namespace hc {
 // prefill_layers (proj/src/model.cpp:349-356): embed d_tokens, run layers
 // [lb, le) from position 0, writing each layer's K/V into the pages. With
 // n_last in (0, n) the last layer runs only for the first n_last tokens.
+// kv_only_last: the caller needs only the K/V of the last layer (a restore's
+// RECOMPUTE prefix, whose next layer is restored from its stored input;
+// prefill_layers), so that layer stops after its K/V projection.
 // hook(layer, start) is called on the host around each layer's enqueue (for
 // CUDA-event timelines). d_layer_inputs (optional, L x n x d bf16) receives
 // each layer's input hidden state (prefill's layer_inputs, model.cpp:316).
@@ -18,7 +21,7 @@ void prefill_layers_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n
                          const hc_kv_pages* pages, const int32_t* d_page_table,
                          cudaStream_t stream, const std::function<void(int, bool)>& hook,
                          void* d_layer_inputs = nullptr, int32_t* next_token = nullptr,
-                         int64_t n_last = 0);
+                         int64_t n_last = 0, bool kv_only_last = false);
 
 // Sequences of a batched forward: nullptr cu = one sequence from position 0.
 struct SeqBatch {
@@ -54,7 +57,7 @@ void forward_batch_layers(const hc_weights* w, const int32_t* d_tokens, int n_se
                           int max_new, const int32_t* d_cu, const int32_t* d_starts,
                           const hc_kv_pages* pages, const int32_t* d_page_tables,
                           int table_stride, int lb, int le, cudaStream_t stream,
-                          const std::function<void(int, bool)>& hook);
+                          const std::function<void(int, bool)>& hook, bool kv_only_last = false);
 
 // Measured seconds of one recompute layer over n tokens at the steady-state
 // clock (after warm_s seconds of back-to-back layers); 0 when the full block

@@ -463,10 +463,10 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
     if (batch)
       forward_batch_layers(w, static_cast<const int32_t*>(d_tok.ptr), n_sessions, n, max_len,
                            d_cu, d_starts, pages, d_page_tables, table_stride, 0, n_re, stream,
-                           hook);
+                           hook, true);
     else
       prefill_layers_impl(w, static_cast<const int32_t*>(d_tok.ptr), n, 0, n_re + (split ? 1 : 0),
-                          pages, d_page_tables, stream, hook, nullptr, nullptr, split);
+                          pages, d_page_tables, stream, hook, nullptr, nullptr, split, true);
   }
 
   issue_fetches(fetches.size());

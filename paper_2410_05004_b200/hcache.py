@@ -770,6 +770,16 @@ def profile_hardware(w: Weights, n_tokens: int) -> ProfiledTimings:
     return ProfiledTimings(t.io_h, t.io_kv, t.c_h, t.c_token, t.n_layers)
 
 
+def timings_from_timeline(tl: "Timeline", base: ProfiledTimings) -> ProfiledTimings:
+    """profile_hardware refined on a measured restore (hc_timings_from_timeline):
+    each kind the timeline holds events of takes its per-event busy time."""
+    if tl._c is None:
+        raise ValueError("timings_from_timeline: needs a device timeline")
+    t = base._c()
+    check(lib().hc_timings_from_timeline(C.byref(tl._c), C.byref(t)))
+    return ProfiledTimings(t.io_h, t.io_kv, t.c_h, t.c_token, t.n_layers)
+
+
 def measure_h2d(bytes_: int, reps: int = 5, device: int = 0) -> float:
     out = C.c_double()
     check(lib().hc_measure_h2d(device, bytes_, reps, C.byref(out)))

@@ -315,3 +315,21 @@ def test_three_way_prices_the_prefix_last_layer_as_a_projection():
     t.c_token = H.RECOMPUTE_UNAVAILABLE
     p, _ = H.plan_three_way(t, 32)
     assert p.l_re == 0
+
+
+def test_timings_from_timeline_per_kind_busy_time():
+    """hc_timings_from_timeline: per-kind union / count; the prefix's last
+    (projection-only) recompute layer is left out of c_token; kinds without
+    events keep the base value."""
+    tl = _timeline([(H.Lane.COMPUTE, 0.0, 1.0), (H.Lane.COMPUTE, 1.0, 2.0),
+                    (H.Lane.COMPUTE, 2.0, 2.2), (H.Lane.IO, 0.0, 0.5), (H.Lane.IO, 0.5, 1.1),
+                    (H.Lane.COMPUTE, 2.2, 2.5), (H.Lane.COMPUTE, 2.4, 2.7)], 2.7)
+    kinds = [3, 3, 3, 0, 0, 2, 2]  # recompute x3 (layers 0-2), fetch_hidden x2, project x2
+    for i, k in enumerate(kinds):
+        tl._c.events[i].kind = k
+    base = T(9.0, 8.0, 7.0, 6.0, 7)
+    t = H.timings_from_timeline(tl, base)
+    assert t.c_token == pytest.approx(1.0)    # layers 0, 1 (layer 2 is the last)
+    assert t.io_h == pytest.approx(0.55)
+    assert t.c_h == pytest.approx(0.25)       # union 0.5 over two overlapping launches
+    assert t.io_kv == 8.0 and t.n_layers == 7
