@@ -76,6 +76,22 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Per-element epilogue arithmetic with explicit rounding (no FMA contraction):
+// every epilogue -- the row-per-thread ones, the CTA pair's transposed one,
+// the split-K reduction -- computes bit-identical values, so K/V written by a
+// decode-sized forward and by a restore's K1 match exactly.
+__device__ __forceinline__ float ln_fold(float acc, float mean, float colsum, float rstd) {
+  return __fmul_rn(rstd, __fsub_rn(acc, __fmul_rn(mean, colsum)));
+}
+__device__ __forceinline__ void rope_rotate(float& a, float& b, float c, float s) {
+  const float a0 = a;
+  a = __fsub_rn(__fmul_rn(a0, c), __fmul_rn(b, s));
+  b = __fadd_rn(__fmul_rn(a0, s), __fmul_rn(b, c));
+}
+__device__ __forceinline__ float gelu_ref(float v) {  // model.cpp:38-40
+  return __fmul_rn(__fmul_rn(0.5f, v), __fadd_rn(1.0f, erff(__fmul_rn(v, 0.70710678118654752f))));
+}
+
 // One thread = one output row; handles 32 consecutive columns [col0, col0+32).
 __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int col0, const KvOut& out,
                                                const EpiArgs& epi, float mean, float rstd,
@@ -85,10 +101,10 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int col0, const K
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       float4 c = __ldg(cs + i);
-      f[4 * i + 0] = rstd * (f[4 * i + 0] - mean * c.x);
-      f[4 * i + 1] = rstd * (f[4 * i + 1] - mean * c.y);
-      f[4 * i + 2] = rstd * (f[4 * i + 2] - mean * c.z);
-      f[4 * i + 3] = rstd * (f[4 * i + 3] - mean * c.w);
+      f[4 * i + 0] = ln_fold(f[4 * i + 0], mean, c.x, rstd);
+      f[4 * i + 1] = ln_fold(f[4 * i + 1], mean, c.y, rstd);
+      f[4 * i + 2] = ln_fold(f[4 * i + 2], mean, c.z, rstd);
+      f[4 * i + 3] = ln_fold(f[4 * i + 3], mean, c.w, rstd);
     }
   }
   const bool is_k = col0 < out.d_kv;
@@ -100,9 +116,7 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int col0, const K
     for (int i = 0; i < 16; ++i) {
       int t = ((ocol + 2 * i) % epi.d_head) >> 1;
       float2 cs = __ldg(row_cs + t);
-      float a = f[2 * i], b = f[2 * i + 1];
-      f[2 * i] = a * cs.x - b * cs.y;
-      f[2 * i + 1] = a * cs.y + b * cs.x;
+      rope_rotate(f[2 * i], f[2 * i + 1], cs.x, cs.y);
     }
   }
   char* dst = is_k ? krow : vrow;
@@ -131,10 +145,10 @@ __device__ __forceinline__ void epilogue_chunk_dense(float (&f)[32], int mode, i
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       float4 x = x4[i];
-      x.x += f[4 * i + 0];
-      x.y += f[4 * i + 1];
-      x.z += f[4 * i + 2];
-      x.w += f[4 * i + 3];
+      x.x = __fadd_rn(x.x, f[4 * i + 0]);
+      x.y = __fadd_rn(x.y, f[4 * i + 1]);
+      x.z = __fadd_rn(x.z, f[4 * i + 2]);
+      x.w = __fadd_rn(x.w, f[4 * i + 3]);
       x4[i] = x;
       f[4 * i + 0] = x.x;
       f[4 * i + 1] = x.y;
@@ -147,14 +161,14 @@ __device__ __forceinline__ void epilogue_chunk_dense(float (&f)[32], int mode, i
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         float4 c = __ldg(cs + i);
-        f[4 * i + 0] = rstd * (f[4 * i + 0] - mean * c.x);
-        f[4 * i + 1] = rstd * (f[4 * i + 1] - mean * c.y);
-        f[4 * i + 2] = rstd * (f[4 * i + 2] - mean * c.z);
-        f[4 * i + 3] = rstd * (f[4 * i + 3] - mean * c.w);
+        f[4 * i + 0] = ln_fold(f[4 * i + 0], mean, c.x, rstd);
+        f[4 * i + 1] = ln_fold(f[4 * i + 1], mean, c.y, rstd);
+        f[4 * i + 2] = ln_fold(f[4 * i + 2], mean, c.z, rstd);
+        f[4 * i + 3] = ln_fold(f[4 * i + 3], mean, c.w, rstd);
       }
     }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) f[i] = 0.5f * f[i] * (1.0f + erff(f[i] * 0.70710678118654752f));
+    for (int i = 0; i < 32; ++i) f[i] = gelu_ref(f[i]);
   }
   uint4* d4 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(g.xb) + off);
 #pragma unroll
@@ -269,14 +283,14 @@ __global__ void splitk_epilogue_kernel(const float* __restrict__ part, int split
   const RowMeta r = row_meta<MODE>(row, out, epi);
   if (MODE == kEpiResid) {
     const size_t off = size_t(row) * size_t(gout.ldo) + size_t(col);
-    const float x = gout.x[off] + v;
+    const float x = __fadd_rn(gout.x[off], v);
     gout.x[off] = x;
     static_cast<__nv_bfloat16*>(gout.xb)[off] = __float2bfloat16(x);
     return;
   }
-  if (epi.row_mean) v = r.rstd * (v - r.mean * __ldg(epi.colsum + col));
+  if (epi.row_mean) v = ln_fold(v, r.mean, __ldg(epi.colsum + col), r.rstd);
   if (MODE == kEpiGelu) {
-    v = 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+    v = gelu_ref(v);
     static_cast<__nv_bfloat16*>(gout.xb)[size_t(row) * size_t(gout.ldo) + size_t(col)] =
         __float2bfloat16(v);
     return;
@@ -287,7 +301,9 @@ __global__ void splitk_epilogue_kernel(const float* __restrict__ part, int split
   const float other = __shfl_xor_sync(0xffffffffu, v, 1);
   if (is_k && epi.rope) {
     const float2 cs = __ldg(epi.rope + size_t(r.pos) * (epi.d_head >> 1) + ((ocol % epi.d_head) >> 1));
-    v = (lane & 1) ? other * cs.y + v * cs.x : v * cs.x - other * cs.y;
+    float a = (lane & 1) ? other : v, b = (lane & 1) ? v : other;
+    rope_rotate(a, b, cs.x, cs.y);
+    v = (lane & 1) ? b : a;
   }
   char* dst = is_k ? r.krow : r.vrow;
   if (out.out_f32) reinterpret_cast<float*>(dst)[ocol] = v;
@@ -490,10 +506,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 // k-block drops from 48 KB (128x256 single-CTA tile) to 32 KB while the MMA
 // work per SM is unchanged. Accumulator rows 0-127 live in the leader's TMEM,
 // 128-255 in the peer's; both run the same epilogue on their own lanes.
+// Epilogue warps of the pair kernel: two per TMEM lane quadrant, each taking
+// half of the tile's columns -- four of them, one per quadrant, left the last
+// tile's epilogue (~11 us, latency-bound per warp) exposed at the end of every
+// launch. (A 5-stage ring that left room for wider scratch starved the MMAs
+// of RESID tiles: 21.5 -> 24.5 us per K=4096 tile.)
+constexpr int kPairEpiWarps = 8;
+constexpr int kPairThreads = 64 + 32 * kPairEpiWarps;
 constexpr int kPairStages = 6;
 constexpr uint32_t kPairHalfBytes = 128 * kBK * 2;             // 16 KB: A half or B half
 constexpr uint32_t kPairStageBytes = 2 * kPairHalfBytes;       // per CTA per stage
-constexpr size_t kPairSmem = size_t(kPairStages) * kPairStageBytes + 1024 + 1024;
+// + the transposing epilogue's scratch (4 warps x kPairEpiWarpBytes, defined
+// below with the epilogue)
+constexpr size_t kPairEpiBytes = kPairEpiWarps * (32 * 16 * 4 + 32 * 32);
+constexpr size_t kPairSmem = size_t(kPairStages) * kPairStageBytes + 1024 + kPairEpiBytes + 1024;
 
 __device__ __forceinline__ void tile_coords_pair(int tile, int num_m, int num_n, int& m_blk,
                                                  int& n_blk) {
@@ -556,52 +582,190 @@ __device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
 __device__ __forceinline__ void st_release_gpu(int32_t* p, int32_t v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void epi_bar_sync() {  // the four epilogue warps of a CTA
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+__device__ __forceinline__ void epi_bar_sync(int n_threads) {  // the epilogue warps of a CTA
+  asm volatile("bar.sync 1, %0;" ::"r"(n_threads) : "memory");
 }
 
+// Epilogue of the CTA pair, one warp = 32 accumulator rows. tcgen05.ld
+// hands each lane one row (32 columns per load); storing from that layout
+// makes every warp-wide 16-byte access touch 32 rows, i.e. 32 L1 wavefronts
+// per instruction -- a RESID tile (x read + written, xb written) then spent
+// as long in its epilogue (~20 us) as in its MMAs, and N=4096 projections
+// ran at ~58 % of the tensor pipe (scripts/pair_trace.cu). So each 32-column
+// chunk is transposed through shared memory in two 16-column halves: lane l
+// then holds 4 consecutive columns of rows 8j + l/4 (j = 0..3), and every
+// global access of a warp covers 8 rows x 64 contiguous bytes. The 16-byte
+// units of a row are XOR-swizzled with (row/2) & 3 so both the row-wise
+// writes and the transposed reads are bank-conflict free. Per-row metadata
+// (LN statistics, RoPE position, K/V row pointers) is computed once per tile
+// by the row's own lane and read back from shared memory. A chunk's global
+// loads (x rows, RoPE coefficients) depend only on rows and columns, so the
+// next chunk's are issued before this chunk is processed.
+struct EpiRow {
+  float mean, rstd;
+  int pos, valid;
+  char* krow;
+  char* vrow;
+};
+constexpr uint32_t kPairEpiWarpBytes = 32 * 16 * 4 + 32 * sizeof(EpiRow);
+
+__device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
+  return make_uint2(pack_bf16(a, b), pack_bf16(c, d));
+}
+// float offset of 16-byte unit u (0..3) of transposed row r
+__device__ __forceinline__ int tunit(int r, int u) { return r * 16 + ((u ^ ((r >> 1) & 3)) << 2); }
+
 template <int MODE>
-__device__ __forceinline__ void epilogue_tile_pair(int row, int row_local, int n_blk, int M, int N,
+__device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n_blk, int M, int N,
                                                    const KvOut& out, const GemmOut& gout,
                                                    const EpiArgs& epi, uint32_t tbase, float* ws,
-                                                   int half) {
+                                                   int half, float* tbuf, EpiRow* meta,
+                                                   int c_begin, int c_end) {
   constexpr int BN = 256;
-  const bool row_ok = row < M;
-  RowMeta meta;
-  if (row_ok && half != 0) meta = row_meta<MODE>(row, out, epi);
+  if (half != 0) {
+    const int row = row_base + lane;
+    EpiRow e{0.f, 1.f, 0, 0, nullptr, nullptr};
+    if (row < M) {
+      const RowMeta r = row_meta<MODE>(row, out, epi);
+      e = EpiRow{r.mean, r.rstd, r.pos, 1, r.krow, r.vrow};
+    }
+    meta[lane] = e;
+  }
+  const int g = lane >> 2, u = lane & 3;  // transposed: rows 8j + g, columns 4u..4u+3
+  __syncwarp();  // meta visible to the warp
+  const bool rope_on = MODE == kEpiKv && epi.rope != nullptr;
+  // loads of chunk c: index 4 * h2 + j (16-column half h2, row 8j + g)
+  auto issue = [&](int c, float4 (&ld)[8]) {
+    const int col0 = n_blk * BN + c * 32;
+    const bool k_half = col0 < out.d_kv;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int h2 = i >> 2, j = i & 3;
+      const EpiRow& e = meta[8 * j + g];
+      const int col = col0 + 16 * h2 + 4 * u;
+      ld[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!e.valid || half == 0 || col0 >= N) continue;
+      if (MODE == kEpiResid)
+        ld[i] = *reinterpret_cast<const float4*>(gout.x + size_t(row_base + 8 * j + g) *
+                                                               size_t(gout.ldo) + col);
+      else if (rope_on && k_half)
+        ld[i] = __ldg(reinterpret_cast<const float4*>(
+            epi.rope + size_t(e.pos) * size_t(epi.d_head >> 1) + ((col % epi.d_head) >> 1)));
+    }
+  };
+  float4 ld[8], ld_next[8];
+  issue(c_begin, ld_next);
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = c_begin; c < c_end; ++c) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ld[i] = ld_next[i];
+    if (c + 1 < c_end) issue(c + 1, ld_next);
     uint32_t v[32];
     tmem_ld_32x32b_x32(tbase + uint32_t(c * 32), v);
     tmem_wait_ld();
     float f[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-    float4* w4 = ws ? reinterpret_cast<float4*>(ws) + size_t(c) * 8 * 128 + row_local : nullptr;
+    float4* w4 = ws ? reinterpret_cast<float4*>(ws) + size_t(c) * 8 * 128 + (row_base & 127) + lane
+                    : nullptr;
     if (half == 0) {  // first K half: raw accumulators to the workspace
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         __stcg(w4 + i * 128, make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]));
       continue;
     }
-    const int col0 = n_blk * BN + c * 32;
-    if (!(row_ok && col0 < N)) continue;
     if (half == 1) {  // second K half: first half's sums + this half's
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float4 p = __ldcg(w4 + i * 128);
-        f[4 * i + 0] = p.x + f[4 * i + 0];
-        f[4 * i + 1] = p.y + f[4 * i + 1];
-        f[4 * i + 2] = p.z + f[4 * i + 2];
-        f[4 * i + 3] = p.w + f[4 * i + 3];
+        f[4 * i + 0] = __fadd_rn(p.x, f[4 * i + 0]);
+        f[4 * i + 1] = __fadd_rn(p.y, f[4 * i + 1]);
+        f[4 * i + 2] = __fadd_rn(p.z, f[4 * i + 2]);
+        f[4 * i + 3] = __fadd_rn(p.w, f[4 * i + 3]);
       }
     }
-    apply_chunk<MODE>(f, row, col0, meta, out, gout, epi);
+    const int col0 = n_blk * BN + c * 32;
+    if (col0 >= N) continue;  // warp-uniform
+    const bool is_k = MODE == kEpiKv && col0 < out.d_kv;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      __syncwarp();  // the previous reads of tbuf are done
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        *reinterpret_cast<float4*>(tbuf + tunit(lane, q4)) =
+            make_float4(f[16 * h2 + 4 * q4], f[16 * h2 + 4 * q4 + 1], f[16 * h2 + 4 * q4 + 2],
+                        f[16 * h2 + 4 * q4 + 3]);
+      __syncwarp();
+      const int col = col0 + 16 * h2 + 4 * u;  // this lane's 4 columns
+      const int ocol = MODE == kEpiKv ? (is_k ? col : col - out.d_kv) : col;
+      float4 cs4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (MODE != kEpiResid && epi.row_mean)
+        cs4 = __ldg(reinterpret_cast<const float4*>(epi.colsum + col));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = 8 * j + g;
+        const EpiRow& e = meta[r];
+        if (!e.valid) continue;
+        const float4 a4 = *reinterpret_cast<const float4*>(tbuf + tunit(r, u));
+        const float4 l4 = ld[4 * h2 + j];
+        float a[4] = {a4.x, a4.y, a4.z, a4.w};
+        if (MODE == kEpiResid) {
+          float4 x = l4;
+          x.x = __fadd_rn(x.x, a[0]);
+          x.y = __fadd_rn(x.y, a[1]);
+          x.z = __fadd_rn(x.z, a[2]);
+          x.w = __fadd_rn(x.w, a[3]);
+          const size_t off = size_t(row_base + r) * size_t(gout.ldo) + col;
+          *reinterpret_cast<float4*>(gout.x + off) = x;
+          *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(gout.xb) + off) =
+              pack4_bf16(x.x, x.y, x.z, x.w);
+          continue;
+        }
+        if (epi.row_mean) {
+          a[0] = ln_fold(a[0], e.mean, cs4.x, e.rstd);
+          a[1] = ln_fold(a[1], e.mean, cs4.y, e.rstd);
+          a[2] = ln_fold(a[2], e.mean, cs4.z, e.rstd);
+          a[3] = ln_fold(a[3], e.mean, cs4.w, e.rstd);
+        }
+        if (MODE == kEpiGelu) {
+          *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(gout.xb) +
+                                    size_t(row_base + r) * size_t(gout.ldo) + col) =
+              pack4_bf16(gelu_ref(a[0]), gelu_ref(a[1]), gelu_ref(a[2]), gelu_ref(a[3]));
+          continue;
+        }
+        if (is_k && rope_on) {
+          rope_rotate(a[0], a[1], l4.x, l4.y);
+          rope_rotate(a[2], a[3], l4.z, l4.w);
+        }
+        char* dst = is_k ? e.krow : e.vrow;
+        if (out.out_f32)
+          *reinterpret_cast<float4*>(dst + size_t(ocol) * 4) = make_float4(a[0], a[1], a[2], a[3]);
+        else
+          *reinterpret_cast<uint2*>(dst + size_t(ocol) * 2) = pack4_bf16(a[0], a[1], a[2], a[3]);
+      }
+    }
   }
 }
 
+// scripts/pair_trace.cu (-DHC_PAIR_TRACE): globaltimer stamps per CTA --
+// [0] start, [1] end, then per unit i of the CTA: 2+4i MMA issue start, +1 MMA
+// issue end, +2 epilogue start (accumulator ready), +3 epilogue end.
+#ifdef HC_PAIR_TRACE
+__device__ unsigned long long* g_pair_trace;
+constexpr int kPairTraceSlots = 40;
+#define PAIR_TRACE(slot)                                                                \
+  do {                                                                                  \
+    if (g_pair_trace && (slot) < kPairTraceSlots)                                       \
+      g_pair_trace[size_t(blockIdx.x) * kPairTraceSlots + (slot)] = global_ns();        \
+  } while (0)
+#else
+#define PAIR_TRACE(slot) \
+  do {                   \
+  } while (0)
+#endif
+
 template <int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ AMaps am,
                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
                         GemmOut gout, EpiArgs epi, uint32_t idesc, int Ms, float* tail_ws,
@@ -618,6 +782,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi_smem = sB + S * kPairHalfBytes + 1024;
+  static_assert(kPairEpiBytes == kPairEpiWarps * kPairEpiWarpBytes, "epilogue scratch size");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -632,6 +798,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int full_units = split ? pair_full_units(num_tiles, n_clusters) : num_tiles;
   const int num_units = split ? num_tiles + (num_tiles - full_units) : num_tiles;
 
+  if (threadIdx.x == 0) PAIR_TRACE(0);
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < am.n; ++i) tma_prefetch_desc(&am.m[i]);
     tma_prefetch_desc(&tmB);
@@ -641,7 +808,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+      mbar_init(&tempty[a], 2 * kPairEpiWarps);  // the epilogue warps of both CTAs
     }
     fence_barrier_init();
   }
@@ -691,13 +858,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = cluster; u < num_units; u += n_clusters) {
+      int ui = 0;
+      for (int u = cluster; u < num_units; u += n_clusters, ++ui) {
         const PairUnit pu = pair_unit(u, full_units, split, num_kb);
         int m_blk, n_blk;
         tile_coords_pair(pu.tile, num_m, num_n, m_blk, n_blk);
         if (m_blk * 256 >= M) continue;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (lane == 0) PAIR_TRACE(2 + 4 * ui);
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
         for (int kb = pu.kb0; kb < pu.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
@@ -719,39 +888,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (elect_one()) umma_commit_pair(&tfull[acc], 0x3);
         __syncwarp();
+        if (lane == 0) PAIR_TRACE(3 + 4 * ui);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else {
     // ---------------- epilogue (both CTAs, their own 128 TMEM lanes) --------
-    const int q = warp & 3;
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int ew = warp - 2, n_epi = 32 * kPairEpiWarps;
+    constexpr int kChunksPerWarp = 8 / (kPairEpiWarps / 4);
+    const int c_begin = (ew / 4) * kChunksPerWarp, c_end = c_begin + kChunksPerWarp;
+    const bool lead = ew == 0 && lane == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int ui = -1;
     for (int u = cluster; u < num_units; u += n_clusters) {
+      ++ui;
       const PairUnit pu = pair_unit(u, full_units, split, num_kb);
       int m_blk, n_blk;
       tile_coords_pair(pu.tile, num_m, num_n, m_blk, n_blk);
       if (m_blk * 256 >= M) continue;
-      const int row_local = q * 32 + lane;
-      const int row = m_blk * 256 + int(rank) * 128 + row_local;
+      const int row_base = m_blk * 256 + int(rank) * 128 + q * 32;
       float* ws = pu.half >= 0 ? tail_ws + (size_t(pu.slot) * 2 + rank) * kTailSlotFloats : nullptr;
       int32_t* flag = pu.half >= 0 ? tail_flags + pu.slot * 2 + int(rank) : nullptr;
+      if (MODE == kEpiResid && pu.half != 0 && row_base + lane < M) {
+        // the residual rows this tile reads, into L2 while its MMAs run
+        const char* xr = reinterpret_cast<const char*>(gout.x + size_t(row_base + lane) *
+                                                                    size_t(gout.ldo) + n_blk * BN);
+        for (int i = c_begin; i < c_end; ++i)
+          if (n_blk * BN + i * 32 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + i * 128));
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (lead) PAIR_TRACE(4 + 4 * ui);
       if (pu.half == 1) {  // the first K half's sums must have landed
-        if (q == 0 && lane == 0)
+        if (lead)
           while (ld_acquire_gpu(flag) == 0) __nanosleep(32);
-        epi_bar_sync();
+        epi_bar_sync(n_epi);
       }
-      epilogue_tile_pair<MODE>(row, row_local, n_blk, M, N, out, gout, epi,
+      uint8_t* my = epi_smem + size_t(ew) * kPairEpiWarpBytes;
+      epilogue_tile_pair<MODE>(row_base, lane, n_blk, M, N, out, gout, epi,
                                tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN), ws,
-                               pu.half);
+                               pu.half, reinterpret_cast<float*>(my),
+                               reinterpret_cast<EpiRow*>(my + 32 * 16 * 4), c_begin, c_end);
       if (pu.half == 0) {  // publish: every thread's stores, then one release
         __threadfence();
-        epi_bar_sync();
-        if (q == 0 && lane == 0) st_release_gpu(flag, 1);
+        epi_bar_sync(n_epi);
+        if (lead) st_release_gpu(flag, 1);
       }
+      if (lead) PAIR_TRACE(5 + 4 * ui);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
@@ -761,6 +947,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   cluster_sync_all();
+  if (threadIdx.x == 0) PAIR_TRACE(1);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair(tmem_base, 512);
@@ -1010,7 +1197,7 @@ cudaError_t launch_pair(const AMaps& tmA, const CUtensorMap& tmB128, int M, int 
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  tc_gemm_pair_kernel<MODE><<<grid, kThreads, kPairSmem, stream>>>(tmA, tmB128, M, N, K, out, g,
+  tc_gemm_pair_kernel<MODE><<<grid, kPairThreads, kPairSmem, stream>>>(tmA, tmB128, M, N, K, out, g,
                                                                    epi, idesc, Ms, ws, flags);
   if (ws) cudaFreeAsync(ws, stream);
   return cudaGetLastError();

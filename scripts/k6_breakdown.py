@@ -66,6 +66,12 @@ def main():
         call()
         torch.cuda.synchronize()
     reps = 6
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    for _ in range(reps):
+        call()
+    host_ms = (time.perf_counter() - h0) * 1e3 / reps  # enqueue only (GPU still running)
+    torch.cuda.synchronize()
     a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps):
@@ -87,11 +93,11 @@ def main():
     for i, nm in enumerate(names):
         rows.append({"i": i, "kernel": nm[:90], "us": float(dur[:, i].mean())})
     span = (evs[per_call * reps - 1].time_range.end - evs[0].time_range.start) / reps
-    out = {"n": n, "layers": L, "call_ms_events": call_ms, "kernels_per_call": per_call,
+    out = {"n": n, "layers": L, "call_ms_events": call_ms, "host_enqueue_ms": host_ms, "kernels_per_call": per_call,
            "kernel_sum_us": float(dur.sum(1).mean()), "span_us": span, "kernels": rows}
     for r in rows:
         print(f"{r['i']:3d} {r['us']:9.1f} us  {r['kernel']}")
-    print(f"call {call_ms:.3f} ms (events), kernel sum {out['kernel_sum_us']:.1f} us, "
+    print(f"host enqueue {host_ms:.3f} ms/call; call {call_ms:.3f} ms (events), kernel sum {out['kernel_sum_us']:.1f} us, "
           f"span {span:.1f} us")
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(out, open(args.out, "w"), indent=1)

@@ -3,7 +3,7 @@ sys.path.insert(0, os.getcwd())
 import numpy as np, torch
 from paper_2410_05004_b200 import hcache as H
 from paper_2410_05004_b200.capi import check, lib
-L, d, heads, dffn, n, vocab = 2, 4096, 32, 11008, 4096, 32000
+L, d, heads, dffn, n, vocab = 2, 4096, 32, 11008, 4096, 32000  # layer 0 full, layer 1 K/V only
 s = torch.cuda.current_stream().cuda_stream
 b = float(np.float32(1) / np.sqrt(np.float32(d)))
 def fill(shape, seed):
@@ -18,10 +18,10 @@ for l in range(L):
 kv = H.KvCache(L, n // 64, 64, d); table = torch.arange(n // 64, dtype=torch.int32, device="cuda")
 tok = torch.randint(0, vocab, (n,), dtype=torch.int32, device="cuda")
 for i in range(4):
-    check(lib().hc_prefill_layers(w._h, tok.data_ptr(), n, 0, 1, C.byref(kv.desc), table.data_ptr(), s))
+    check(lib().hc_prefill_layers(w._h, tok.data_ptr(), n, 0, 2, C.byref(kv.desc), table.data_ptr(), s))
 torch.cuda.synchronize()
 a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 a.record()
 for i in range(5):
-    check(lib().hc_prefill_layers(w._h, tok.data_ptr(), n, 0, 1, C.byref(kv.desc), table.data_ptr(), s))
+    check(lib().hc_prefill_layers(w._h, tok.data_ptr(), n, 0, 2, C.byref(kv.desc), table.data_ptr(), s))
 e.record(); torch.cuda.synchronize(); print("K6 layer ms", a.elapsed_time(e) / 5)
