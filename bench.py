@@ -483,30 +483,78 @@ def run_ours(args, cfg, rank, world):
     # plan with a timeline, take each kind's per-event busy time
     # (hc_timings_from_timeline), re-plan, until the plan is stable.
     calibration = []
+    split_pick = 0
     if full and not os.environ.get("HC_NO_CALIBRATE"):
-        for it in range(3):
+        tried = {}  # plan record -> (plan, median synchronous restore ms)
+
+        def measure(p, sid, o=None, saved=False):
             # back-to-back restores first: the timed loop's sustained power
-            # state (its clock under the cap) is the one the plan must fit
-            save(f"cal{it}", plan)
+            # state (its clock under the cap) is the one the plan must fit;
+            # then the synchronous latency (the e2e leg's measure) and one
+            # restore with a timeline (no overlap with a previous step's tail)
+            o = o or opts
+            if not saved:
+                save(sid, p)
             for _ in range(max(8, args.steps)):
-                restore_step(f"cal{it}".encode(), plan)
-            torch.cuda.synchronize()  # (no overlap with the previous step's tail)
-            res = H.restore(store, f"cal{it}", w, plan, H.ThrottleConfig(0, True), kv, table)
+                restore_step(sid.encode(), p, o)
+            lat = []
+            for _ in range(5):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                restore_step(sid.encode(), p, o)
+                torch.cuda.synchronize()
+                lat.append((time.perf_counter() - t0) * 1e3)
+            res = H.restore(store, sid, w, p, H.ThrottleConfig(0, True), kv, table)
+            return float(np.median(lat)), res
+
+        cand, n_sid = plan, 0
+        for it in range(3):
+            if cand.serialize() in tried:
+                break
+            lat, res = measure(cand, f"cal{n_sid}")
+            n_sid += 1
+            tried[cand.serialize()] = (cand, lat)
             prof = H.timings_from_timeline(res.timeline, prof)
             prof.n_layers = L
             nxt, nxt_ms = H.plan_three_way(prof, layer_bytes=n * d * 2)
-            calibration.append({"plan": plan.serialize(), "measured_ms": res.timeline.total_s * 1e3,
+            calibration.append({"plan": cand.serialize(), "restore_ms": lat,
+                                "timeline_ms": res.timeline.total_s * 1e3,
                                 "c_token_ms": prof.c_token * 1e3, "c_h_ms": prof.c_h * 1e3,
                                 "io_h_ms": prof.io_h * 1e3, "replan": nxt.serialize(),
                                 "replan_predicted_ms": nxt_ms * 1e3})
-            if nxt.serialize() == plan.serialize():
-                break
-            plan, plan_ms = nxt, nxt_ms
+            cand = nxt
+        # the model's choice and its neighbours (one recompute layer more /
+        # fewer), measured: at balanced lanes the pipeline model cannot
+        # separate plans a few percent apart
+        for dre in (-1, 1):
+            l_re = cand.l_re + dre
+            l_h = cand.l_h - dre
+            if l_re < 0 or l_h < 0:
+                continue
+            q = H.RestorationPlan.make_mixed(l_re, l_h, cand.l_kv)
+            if q.serialize() in tried:
+                continue
+            lat, _ = measure(q, f"cal{n_sid}")
+            n_sid += 1
+            tried[q.serialize()] = (q, lat)
+            calibration.append({"plan": q.serialize(), "restore_ms": lat, "neighbour": True})
+        model_plan, model_ms = H.plan_three_way(prof, layer_bytes=n * d * 2)
+        plan, best_ms = min(tried.values(), key=lambda x: x[1])
+        plan_ms = model_ms if plan.serialize() == model_plan.serialize() else None
+        # the token split of the chosen plan's first hidden layer, measured too
+        split_try, _ = H.plan_token_split(prof, plan, n, layer_bytes=n * d * 2)
+        if split_try:
+            sid = [k for k, (q, _) in enumerate(tried.values()) if q.serialize() == plan.serialize()]
+            lat, _ = measure(plan, f"cal{sid[0]}", capi.RestoreOptsC(0, 0, split_try), saved=True)
+            calibration.append({"plan": plan.serialize(), "split_tokens": split_try,
+                                "restore_ms": lat})
+            if lat < best_ms * 0.995:
+                split_pick = split_try
     # B200 extension: split the first hidden layer between the recompute
     # prefix and the link where that balances the two lanes
     # (opt-in, HC_SPLIT=1: interleaved A/B runs on B200 did not separate it
     # from run-to-run noise, scripts/ab_split.sh)
-    split, split_ms = 0, plan_ms
+    split, split_ms = split_pick, plan_ms
     if full and os.environ.get("HC_SPLIT") == "1":
         split, split_ms = H.plan_token_split(prof, plan, n, layer_bytes=n * d * 2)
     opts_plan = capi.RestoreOptsC(0, 0, split)
@@ -640,7 +688,9 @@ def run_ours(args, cfg, rank, world):
                     "plan": plan.serialize(), "split_tokens": split,
                     "how": "hc_plan_three_way (+ hc_plan_token_split) on hc_profile, refined on "
                            "timelines of the restore itself (hc_timings_from_timeline) until "
-                           "the plan is stable",
+                           "the plan is stable; the model's plan, its +-1 recompute-layer "
+                           "neighbours and its token split are then measured (synchronous "
+                           "restore latency after back-to-back restores) and the fastest kept",
                     "predicted_ms": plan_ms * 1e3 if plan_ms else None,
                     "predicted_with_split_ms": split_ms * 1e3 if split_ms else None},
         "parity": parity,

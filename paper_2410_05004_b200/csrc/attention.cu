@@ -16,6 +16,7 @@
 #include <cmath>
 
 #include "kernels.h"
+#include "sm100.cuh"
 
 namespace hc {
 
@@ -360,6 +361,8 @@ __global__ void attn_decode_combine_kernel(const float* __restrict__ part, int n
 
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, int64_t n, const uint4* __restrict__ emb,
                              int d, float* __restrict__ x, uint4* __restrict__ xb) {
+  pdl_wait();
+  pdl_trigger();
   const int vec = d / 8;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * vec;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -555,9 +558,8 @@ cudaError_t launch_embed(const int32_t* tokens, int64_t n, const void* emb, int 
   if (n <= 0) return cudaSuccess;
   int64_t blocks = (n * (d / 8) + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  embed_kernel<<<unsigned(blocks), 256, 0, stream>>>(tokens, n, static_cast<const uint4*>(emb), d,
-                                                     x, static_cast<uint4*>(xb));
-  return cudaGetLastError();
+  return launch_pdl(embed_kernel, dim3(unsigned(blocks)), dim3(256), 0, stream, tokens, n,
+                    static_cast<const uint4*>(emb), d, x, static_cast<uint4*>(xb));
 }
 
 cudaError_t launch_argmax_logits(const void* emb, int vocab, int d, const float* h,

@@ -565,6 +565,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   using Cfg = FaCfg<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023) asm volatile("trap;");
+  pdl_wait();  // (the ragged batch reads cu_seqlens right below)
+  pdl_trigger();
   FA_CTA(0, global_ns());
   uint8_t* sQ = smem_raw;                       // Q_A, Q_B
   uint8_t* sK = sQ + 2 * Cfg::kQBytes;          // K ring, 2 stages
@@ -1006,7 +1008,8 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
     const double kv_bytes = double(n) * double(n_kv_heads) * DH * 2 * 2;  // n = total rows
     a.rank_major = kv_bytes <= 80.0 * (1 << 20);
     const dim3 grid = a.rank_major ? dim3(n_heads, n_seqs, pairs) : dim3(pairs, n_heads, n_seqs);
-    attn_fa_kernel<DH><<<grid, kFaThreads, FaCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);
+    return launch_pdl(attn_fa_kernel<DH>, grid, dim3(kFaThreads), FaCfg<DH>::kSmem, stream, tq,
+                      tk, tv, tk2, tv2, a);
   } else {
     const dim3 grid((n + kAttnM - 1) / kAttnM, n_heads);
     attn_tc_kernel<DH><<<grid, kAttnThreads, AttnCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);

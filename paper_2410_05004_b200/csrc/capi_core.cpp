@@ -116,7 +116,7 @@ void project_rows(const hc_weights* w, int layer, const void* d_hidden, int64_t 
   const int32_t* flag =
       need && ln_center_enabled() ? reinterpret_cast<int32_t*>(mean + 2 * n_rows) : pre_flag;
   if (need && flag) {
-    HC_CUDA(cudaMemsetAsync(const_cast<int32_t*>(flag), 0, sizeof(int32_t), stream));
+    HC_CUDA(launch_zero_i32(const_cast<int32_t*>(flag), 1, stream));
     HC_CUDA(launch_row_stats_flagged(d_hidden, n_rows, d, d, true, mean, mean + n_rows,
                                      const_cast<int32_t*>(flag), stream));
   } else if (need) {

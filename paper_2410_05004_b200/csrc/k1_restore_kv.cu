@@ -20,6 +20,8 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <mutex>
+#include <map>
 #include <cstdlib>
 #include <type_traits>
 
@@ -393,6 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -564,9 +568,14 @@ __device__ __forceinline__ PairUnit pair_unit(int u, int full_units, bool split,
 __host__ __device__ __forceinline__ int pair_full_units(int tiles, int clusters) {
   return (tiles / clusters) * clusters;
 }
+// Only for long K loops: the exchange (first half's epilogue writing 128 KB
+// per CTA, the second's reading it) costs ~8 us, so at K = 4096 (a 9 us half
+// tile) the split measured no better than the idle tail (scripts/pair_trace.cu:
+// 88.6 vs 90.8 us); at K = 11008 it saves 8 us per launch (223 -> 215 us).
+constexpr int kTailMinKb = 96;
 __host__ __device__ __forceinline__ bool pair_tail_split(int tiles, int clusters, int num_kb) {
   const int tail = tiles - pair_full_units(tiles, clusters);
-  return tail > 0 && 2 * tail <= clusters && num_kb >= 2;
+  return tail > 0 && 2 * tail <= clusters && num_kb >= kTailMinKb;
 }
 
 // Workspace of one tail slot and CTA: 128 rows x 256 fp32 accumulators,
@@ -769,7 +778,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ AMaps am,
                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
                         GemmOut gout, EpiArgs epi, uint32_t idesc, int Ms, float* tail_ws,
-                        int32_t* tail_flags) {
+                        int32_t* tail_flags, uint32_t epoch) {
   // M: rows stored; Ms >= M: rows the schedule is laid out for (units whose
   // tile starts at or past M are skipped by every role)
   constexpr int BN = 256, S = kPairStages;
@@ -817,6 +826,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();     // the previous kernel's outputs (A, statistics, flags) are ready
+  pdl_trigger();  // every CTA is resident: the next kernel may launch its prologue
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs; bytes counted on the leader) ----
@@ -924,7 +935,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       if (lead) PAIR_TRACE(4 + 4 * ui);
       if (pu.half == 1) {  // the first K half's sums must have landed
         if (lead)
-          while (ld_acquire_gpu(flag) == 0) __nanosleep(32);
+          while (uint32_t(ld_acquire_gpu(flag)) != epoch) __nanosleep(32);
         epi_bar_sync(n_epi);
       }
       uint8_t* my = epi_smem + size_t(ew) * kPairEpiWarpBytes;
@@ -935,7 +946,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       if (pu.half == 0) {  // publish: every thread's stores, then one release
         __threadfence();
         epi_bar_sync(n_epi);
-        if (lead) st_release_gpu(flag, 1);
+        if (lead) st_release_gpu(flag, int32_t(epoch));
       }
       if (lead) PAIR_TRACE(5 + 4 * ui);
       tc_fence_before();
@@ -1030,6 +1041,8 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const T* __restrict__ x,
                                                         float* __restrict__ mean_out,
                                                         float* __restrict__ rstd_out,
                                                         int32_t* flag) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -1046,6 +1059,8 @@ __global__ void __launch_bounds__(256) center_rows_kernel(const __nv_bfloat16* x
                                                           int64_t row_stride, float* mean,
                                                           const int32_t* flag,
                                                           __nv_bfloat16* out) {
+  pdl_wait();
+  pdl_trigger();
   if (*reinterpret_cast<const volatile int32_t*>(flag) == 0) return;
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1088,6 +1103,18 @@ __global__ void colsum_kernel(const T* __restrict__ w, int64_t rows, int cols,
 }
 
 // ------------------------------------------------------------ synthetic fill
+// Zeroing of small flag arrays as a kernel: a cudaMemsetAsync issued while
+// the copy engines stream hidden states waited ~40-55 us before it ran (CUPTI
+// trace of the restore: every per-layer memset of the recompute prefix
+// stalled its stream that long).
+__global__ void zero_i32_kernel(int32_t* p, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = 0;
+}
+
 __global__ void fill_symmetric_kernel(void* dst, int64_t n, uint64_t seed, uint64_t offset,
                                       float bound, int dtype) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -1107,6 +1134,8 @@ __global__ void fill_symmetric_kernel(void* dst, int64_t n, uint64_t seed, uint6
 // ------------------------------------------------------------ KV scatter (K4)
 // One warp per row: [K_row | V_row] (2*d_kv bf16) -> K page slot, V page slot.
 __global__ void kv_scatter_kernel(const uint4* __restrict__ rows, int64_t n_rows, KvOut out) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -1162,6 +1191,42 @@ __global__ void kv_gather_kernel(KvOut kv, int pos0, int64_t n_rows, uint4* __re
 
 }  // namespace
 
+// Tail-split workspace per (device, stream): stream order makes reuse safe
+// without a per-launch allocation or a flag reset -- a launch's flags carry
+// its epoch, every earlier value differs. (A cudaMallocAsync + flag reset per
+// launch put ~20 us of stream gaps around every split GEMM of a restore.)
+struct TailWs {
+  float* ws = nullptr;
+  int32_t* flags = nullptr;
+  int slots = 0;
+  uint32_t epoch = 0;
+};
+cudaError_t tail_ws_for(int dev, cudaStream_t stream, int slots, TailWs** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, TailWs> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  TailWs& t = cache[{dev, stream}];
+  if (t.slots < slots) {
+    if (t.ws) {  // grow (first large launch on this stream): the old buffer may be in use
+      cudaError_t e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) return e;
+      cudaFree(t.ws);
+      t.ws = nullptr;
+      t.slots = 0;
+    }
+    const size_t ws_bytes = size_t(slots) * 2 * kTailSlotFloats * sizeof(float);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&t.ws), ws_bytes + size_t(slots) * 8);
+    if (e != cudaSuccess) return e;
+    t.flags = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(t.ws) + ws_bytes);
+    e = cudaMemset(t.flags, 0, size_t(slots) * 8);
+    if (e != cudaSuccess) return e;
+    t.slots = slots;
+    t.epoch = 0;
+  }
+  *out = &t;
+  return cudaSuccess;
+}
+
 template <int MODE>
 cudaError_t launch_pair(const AMaps& tmA, const CUtensorMap& tmB128, int M, int N, int K,
                         bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
@@ -1176,20 +1241,23 @@ cudaError_t launch_pair(const AMaps& tmA, const CUtensorMap& tmB128, int M, int 
   }();
   float* ws = nullptr;
   int32_t* flags = nullptr;
+  uint32_t epoch = 0;
   const int num_kb = (K + kBK - 1) / kBK;
-  if (split_acc && tail_enabled && pair_tail_split(tiles, grid / 2, num_kb)) {
-    const int slots = tiles - pair_full_units(tiles, grid / 2);
-    const size_t ws_bytes = size_t(slots) * 2 * kTailSlotFloats * sizeof(float);
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws),
-                                    ws_bytes + size_t(slots) * 2 * sizeof(int32_t), stream);
-    if (e != cudaSuccess) return e;
-    flags = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + ws_bytes);
-    e = cudaMemsetAsync(flags, 0, size_t(slots) * 2 * sizeof(int32_t), stream);
-    if (e != cudaSuccess) return e;
-  }
-  static thread_local int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cap);
+  // (not under graph capture: a replay would reuse the baked-in epoch)
+  if (split_acc && tail_enabled && cap == cudaStreamCaptureStatusNone &&
+      pair_tail_split(tiles, grid / 2, num_kb)) {
+    TailWs* t = nullptr;
+    cudaError_t e = tail_ws_for(dev, stream, tiles - pair_full_units(tiles, grid / 2), &t);
+    if (e != cudaSuccess) return e;
+    ws = t->ws;
+    flags = t->flags;
+    epoch = ++t->epoch;
+  }
+  static thread_local int attr_dev = -1;
   if (attr_dev != dev) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_pair_kernel<MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1197,10 +1265,8 @@ cudaError_t launch_pair(const AMaps& tmA, const CUtensorMap& tmB128, int M, int 
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  tc_gemm_pair_kernel<MODE><<<grid, kPairThreads, kPairSmem, stream>>>(tmA, tmB128, M, N, K, out, g,
-                                                                   epi, idesc, Ms, ws, flags);
-  if (ws) cudaFreeAsync(ws, stream);
-  return cudaGetLastError();
+  return launch_pdl(tc_gemm_pair_kernel<MODE>, dim3(grid), dim3(kPairThreads), kPairSmem, stream,
+                    tmA, tmB128, M, N, K, out, g, epi, idesc, Ms, ws, flags, epoch);
 }
 
 // Pair kernel when the problem has enough 256x256 tiles to fill the SM pairs
@@ -1249,8 +1315,12 @@ cudaError_t launch_tc(const AMaps& tmA, const CUtensorMap& tmB, int M, int N, in
     if (e != cudaSuccess) return e;
   }
   const int grid_k = std::min(num_sms, tiles * k_splits);
-  tc_gemm_kernel<BN, MODE><<<grid_k, kThreads, r.smem, stream>>>(
-      tmA, tmB, M, N, K, out, g, epi, idesc, r.stages, r.kbs, r.stride, r.a_bytes, k_splits, part);
+  {
+    cudaError_t e = launch_pdl(tc_gemm_kernel<BN, MODE>, dim3(grid_k), dim3(kThreads), r.smem,
+                               stream, tmA, tmB, M, N, K, out, g, epi, idesc, r.stages, r.kbs,
+                               r.stride, r.a_bytes, k_splits, part);
+    if (e != cudaSuccess) return e;
+  }
   if (k_splits > 1) {
     const int64_t threads = int64_t(M) * (N / 32) * 32;
     splitk_epilogue_kernel<MODE><<<unsigned((threads + 255) / 256), 256, 0, stream>>>(
@@ -1397,18 +1467,25 @@ cudaError_t launch_row_stats_flagged(const void* x, int64_t rows, int cols, int6
   const int threads = 256, per_block = threads / 32;
   const unsigned grid = unsigned((rows + per_block - 1) / per_block);
   if (bf16_in)
-    row_stats_kernel<__nv_bfloat16><<<grid, threads, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(x), rows, cols, row_stride, mean, rstd, flag);
-  else
-    row_stats_kernel<__half><<<grid, threads, 0, stream>>>(static_cast<const __half*>(x), rows,
-                                                          cols, row_stride, mean, rstd, flag);
-  return cudaGetLastError();
+    return launch_pdl(row_stats_kernel<__nv_bfloat16>, dim3(grid), dim3(threads), 0, stream,
+                      static_cast<const __nv_bfloat16*>(x), rows, cols, row_stride, mean, rstd,
+                      flag);
+  return launch_pdl(row_stats_kernel<__half>, dim3(grid), dim3(threads), 0, stream,
+                    static_cast<const __half*>(x), rows, cols, row_stride, mean, rstd, flag);
 }
 
 cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_stride,
                              bool bf16_in, float* mean, float* rstd, cudaStream_t stream) {
   return launch_row_stats_flagged(x, rows, cols, row_stride, bf16_in, mean, rstd, nullptr,
                                   stream);
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HC_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
 }
 
 bool ln_center_enabled() {
@@ -1425,10 +1502,9 @@ cudaError_t launch_center_rows(const void* x, int64_t rows, int cols, int64_t ro
   if (cols % 8 != 0 || row_stride % 8 != 0) return cudaErrorInvalidValue;
   const int threads = 256, per_block = threads / 32;
   const int64_t blocks = std::min<int64_t>((rows + per_block - 1) / per_block, 148 * 2);
-  center_rows_kernel<<<unsigned(blocks), threads, 0, stream>>>(
-      static_cast<const __nv_bfloat16*>(x), rows, cols, row_stride, mean, flag,
-      static_cast<__nv_bfloat16*>(out));
-  return cudaGetLastError();
+  return launch_pdl(center_rows_kernel, dim3(unsigned(blocks)), dim3(threads), 0, stream,
+                    static_cast<const __nv_bfloat16*>(x), rows, cols, row_stride, mean, flag,
+                    static_cast<__nv_bfloat16*>(out));
 }
 
 cudaError_t launch_colsum(const void* w, int64_t rows, int cols, bool bf16_in, float* out,
@@ -1445,6 +1521,12 @@ cudaError_t launch_colsum(const void* w, int64_t rows, int cols, bool bf16_in, f
   return cudaGetLastError();
 }
 
+cudaError_t launch_zero_i32(int32_t* p, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, 1024));
+  return launch_pdl(zero_i32_kernel, dim3(blocks), dim3(256), 0, stream, p, n);
+}
+
 cudaError_t launch_fill_symmetric(void* dst, int64_t n, uint64_t seed, uint64_t offset,
                                   float bound, int dtype, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
@@ -1459,8 +1541,8 @@ cudaError_t launch_kv_scatter(const void* rows, int64_t n_rows, const KvOut& out
   if (n_rows <= 0) return cudaSuccess;
   const int threads = 256, per_block = threads / 32;
   const unsigned grid = unsigned((n_rows + per_block - 1) / per_block);
-  kv_scatter_kernel<<<grid, threads, 0, stream>>>(static_cast<const uint4*>(rows), n_rows, out);
-  return cudaGetLastError();
+  return launch_pdl(kv_scatter_kernel, dim3(grid), dim3(threads), 0, stream,
+                    static_cast<const uint4*>(rows), n_rows, out);
 }
 
 cudaError_t launch_kv_gather(const KvOut& kv, int pos0, int64_t n_rows, void* rows,

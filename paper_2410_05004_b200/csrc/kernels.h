@@ -7,6 +7,26 @@
 
 namespace hc {
 
+// HC_PDL=0 turns programmatic dependent launch off (A/B measurements).
+bool pdl_enabled();
+// Launch with programmatic stream serialization (see pdl_wait in sm100.cuh):
+// the kernel must call pdl_wait() before its first global memory access.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Where K1 writes K and V. Dense mode (page_table == nullptr): row r of the
 // projection lands at row r of k_base / v_base ([M x d_kv] row-major). Paged
 // mode: row r of sequence s (rows cu_seqlens[s]..cu_seqlens[s+1]) at position
@@ -242,6 +262,8 @@ cudaError_t launch_colsum(const void* w, int64_t rows, int cols, bool bf16_in, f
 
 // Deterministic synthetic data: dst[i] = Rng(seed)::symmetric(bound) draw
 // (offset+i) (reference model.cpp:17-31), stored as bf16/fp16/fp32.
+// p[0, n) = 0 as a kernel (stream-ordered memsets stall behind copy-engine work)
+cudaError_t launch_zero_i32(int32_t* p, int64_t n, cudaStream_t stream);
 cudaError_t launch_fill_symmetric(void* dst, int64_t n, uint64_t seed, uint64_t offset,
                                   float bound, int dtype, cudaStream_t stream);
 

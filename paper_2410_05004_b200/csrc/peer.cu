@@ -238,7 +238,7 @@ hc_status hc_project_multi_source(const hc_weights* w, int32_t layer, int32_t n_
     // reads instead (the sources are other GPUs' buffers: never written here;
     // the copy is only touched when the flag is set)
     StreamScratch centered(center ? size_t(n) * size_t(d) * 2 : 0, s);
-    if (center) HC_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+    if (center) HC_CUDA(launch_zero_i32(flag, 1, s));
     AMaps am;
     am.n = 0;
     const uint32_t abox = uint32_t(gemm_a_box(n));

@@ -140,22 +140,24 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
   const size_t nd = size_t(n) * size_t(d);
   StreamScratch x_buf(nd * 4, stream), xb_buf(nd * 2, stream), q_buf(nd * 2, stream),
       mix_buf(nd * 2, stream), h1_buf(size_t(n) * size_t(dffn) * 2, stream),
-      stats(size_t(n) * 2 * 4 + 16, stream), xc_buf(c.norm_enabled ? nd * 2 : 0, stream);
+      stats(size_t(n) * 2 * 4 + size_t(2 * (le - lb) + 4) * 4, stream),
+      xc_buf(c.norm_enabled ? nd * 2 : 0, stream);
   float* x = static_cast<float*>(x_buf.ptr);
   float* mean = static_cast<float*>(stats.ptr);
   float* rstd = mean + n;
-  int32_t* flag = reinterpret_cast<int32_t*>(mean + 2 * n);
+  // one mean-shift flag per statistics call (two per layer), zeroed once
+  int32_t* flags = reinterpret_cast<int32_t*>(mean + 2 * n);
+  int n_flag = 0;
   pm.lap(0);
   HC_CUDA(launch_embed(d_tokens, n, w->embedding, d, x, xb_buf.ptr, stream));
+  if (c.norm_enabled && ln_center_enabled())
+    HC_CUDA(launch_zero_i32(flags, 2 * (le - lb), stream));
   // LayerNorm statistics of xb + the mean-shifted operand for rows with
   // |mean| >> sigma (launch_center_rows; a no-op unless flagged)
   AltA alt;
   const AltA* altp = nullptr;
   const bool center = c.norm_enabled && ln_center_enabled();
-  if (center) {
-    alt.flag = flag;
-    altp = &alt;
-  }
+  if (center) altp = &alt;
   // tensor maps and tile widths of the GEMMs over the first `rows` rows
   // (every GEMM of an M-row operand uses the A box and tiles M picks)
   struct Maps {
@@ -190,7 +192,8 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
       HC_CUDA(launch_row_stats(xb_buf.ptr, rows, d, d, true, mean, rstd, stream));
       return;
     }
-    HC_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), stream));
+    int32_t* flag = flags + n_flag++;
+    alt.flag = flag;  // the GEMMs that follow read this call's flag
     HC_CUDA(launch_row_stats_flagged(xb_buf.ptr, rows, d, d, true, mean, rstd, flag, stream));
     HC_CUDA(launch_center_rows(xb_buf.ptr, rows, d, d, mean, flag, xc_buf.ptr, stream));
   };
@@ -245,7 +248,6 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     qo.cu_seqlens = sb.cu;
     qo.n_seqs = sb.cu ? sb.n_seqs : 1;
     qo.seq_start = sb.seq_start;
-    if (mo != m) ln_stats(mo);  // statistics of the shorter operand's rows (same values)
     HC_CUDA(launch_restore_kv(mp.xb, wmap(lw.wq, d, d, mp.bn_d), mp.bn_d, int(mo), d, d, true, qo,
                               epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true, altp,
                               int(m)));

@@ -364,7 +364,7 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
   const int lanes = side && restore_lanes == 2 ? k1_lanes(n) : 1;
   StreamScratch hstats(side_stats ? size_t(n_hidden) * 2 * size_t(n) * sizeof(float) : 0, stream);
   StreamScratch hflags(center ? size_t(n_hidden) * sizeof(int32_t) : 0, stream);
-  if (center) HC_CUDA(cudaMemsetAsync(hflags.ptr, 0, size_t(n_hidden) * sizeof(int32_t), stream));
+  if (center) HC_CUDA(launch_zero_i32(static_cast<int32_t*>(hflags.ptr), n_hidden, stream));
 
   // On an exception after work was queued on the side lanes, join them into
   // the caller stream before the scratch buffers above are released
@@ -731,7 +731,7 @@ hc_status hc_restore_resident(const hc_weights* w, const void* const* d_hidden_l
     const int lanes = k1_lanes(n_rows);
     cudaStream_t cs[2] = {s, eng.aux2};
     cudaEvent_t fork = evs.get();
-    if (norm) HC_CUDA(cudaMemsetAsync(fl, 0, size_t(L) * sizeof(int32_t), s));
+    if (norm) HC_CUDA(launch_zero_i32(fl, L, s));
     HC_CUDA(cudaEventRecord(fork, s));
     if (norm) HC_CUDA(cudaStreamWaitEvent(eng.aux, fork, 0));
     if (lanes == 2) HC_CUDA(cudaStreamWaitEvent(eng.aux2, fork, 0));

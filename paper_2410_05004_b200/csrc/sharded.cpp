@@ -229,7 +229,7 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
         float* orr = g->slot_rstd(me, slot);
         if (center) {
           int32_t* fl = g->slot_flag(me, slot);
-          HC_CUDA(cudaMemsetAsync(fl, 0, sizeof(int32_t), eng.aux));
+          HC_CUDA(launch_zero_i32(fl, 1, eng.aux));
           HC_CUDA(launch_row_stats_flagged(data, my_rows, d, d, true, om, orr, fl, eng.aux));
           HC_CUDA(launch_center_rows(data, my_rows, d, d, om, fl, data, eng.aux));
         } else {

@@ -8,6 +8,17 @@
 
 namespace hc {
 
+// Programmatic dependent launch (PDL). A kernel launched with
+// launch_pdl may start while the previous kernel of its stream is still
+// running: everything before pdl_wait() (barrier init, TMEM allocation,
+// descriptor prefetch) overlaps that kernel's tail, and pdl_wait() returns
+// once it has completed and its writes are visible -- so no global memory is
+// touched before it. pdl_trigger() lets this kernel's own dependents launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "r2_pcie_trace.json"))
     ap.add_argument("--trace", default=None)
     ap.add_argument("--plan", default=None, help="e.g. 8,23,1 (l_re,l_h,l_kv); default planner")
+    ap.add_argument("--kernels", action="store_true", help="list every kernel launch")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -146,6 +147,9 @@ def main():
         "first_kernel_start_us": kn[0][0] if kn else None,
         "last_kernel_end_us": max(b for _, b, _ in kn) if kn else None,
     }
+    if args.kernels:  # the compute lane's launches in order (name, start, duration)
+        out["kernel_list"] = [{"name": nm[:60], "start_us": round(a, 1), "us": round(b - a, 1)}
+                              for a, b, nm in kn]
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(out, f, indent=1)
