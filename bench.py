@@ -374,6 +374,19 @@ def verify_restore(kv, table, plan, cfg, tokens, split, kv_rows, m=32):
     return out
 
 
+def qkv_weights(fill, layer, d, d_kv, full):
+    """[W_k;W_v] of a layer (seed 1234+layer) and, for the full block, W_q
+    (seed 5000+layer) laid out right before it in one allocation, so the
+    recompute path projects Q, K and V with one GEMM (hc_weights_set_layer_full
+    fuses them when W_q immediately precedes [W_k;W_v])."""
+    if not full:
+        return fill((2 * d_kv, d), 1234 + layer), None
+    qkv = fill((d + 2 * d_kv, d), 0)
+    fill(qkv[:d], 5000 + layer)
+    fill(qkv[d:], 1234 + layer)
+    return qkv[d:], qkv[:d]
+
+
 def run_ours(args, cfg, rank, world):
     import torch
     from paper_2410_05004_b200 import capi
@@ -397,18 +410,20 @@ def run_ours(args, cfg, rank, world):
     bound = float(np.float32(1) / np.sqrt(np.float32(d)))
 
     def fill(shape, seed):
-        # seeds: oracle/parity.py (the CPU side of the parity check)
-        t = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+        # seeds: oracle/parity.py (the CPU side of the parity check); shape
+        # may be an existing bf16 tensor (filled in place)
+        t = shape if torch.is_tensor(shape) else torch.empty(shape, dtype=torch.bfloat16,
+                                                              device="cuda")
         check(lib().hc_fill_symmetric(t.data_ptr(), t.numel(), seed, 0, bound, 1, stream))
         return t
     emb = fill((vocab, d), 99)
     w.set_embedding(emb)
     full = not args.no_recompute and kvh == heads
     for layer in range(L):
-        wkv = fill((2 * d_kv, d), 1234 + layer)
+        wkv, wq = qkv_weights(fill, layer, d, d_kv, full)
         w.set_layer_kv(layer, wkv)
         if full:
-            w.set_layer_full(layer, fill((d, d), 5000 + layer), wkv, fill((d, d), 6000 + layer),
+            w.set_layer_full(layer, wq, wkv, fill((d, d), 6000 + layer),
                              fill((dffn, d), 7000 + layer), fill((d, dffn), 8000 + layer))
     page = 64
     n_pages = (n + page - 1) // page
@@ -768,16 +783,17 @@ def run_ours_batch(args, cfg, rank, world):
     bound = float(np.float32(1) / np.sqrt(np.float32(d)))
 
     def fill(shape, seed, b=bound):
-        t = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+        t = shape if torch.is_tensor(shape) else torch.empty(shape, dtype=torch.bfloat16,
+                                                              device="cuda")
         check(lib().hc_fill_symmetric(t.data_ptr(), t.numel(), seed, 0, b, 1, stream))
         return t
     w.set_embedding(fill((vocab, d), 99))
     full = not args.no_recompute
     for layer in range(L):
-        wkv = fill((2 * d_kv, d), 1234 + layer)
+        wkv, wq = qkv_weights(fill, layer, d, d_kv, full)
         w.set_layer_kv(layer, wkv)
         if full:
-            w.set_layer_full(layer, fill((d, d), 5000 + layer), wkv, fill((d, d), 6000 + layer),
+            w.set_layer_full(layer, wq, wkv, fill((d, d), 6000 + layer),
                              fill((dffn, d), 7000 + layer), fill((d, dffn), 8000 + layer))
     # pages: each session its own run of pages (no padding to the longest)
     npg = [(n + page - 1) // page for n in lens]

@@ -277,6 +277,7 @@ void hc_weights_destroy(hc_weights* w) {
     if (L.colsum_all) cudaFree(L.colsum_all);
     if (L.colsum_q) cudaFree(L.colsum_q);
     if (L.colsum_fc1) cudaFree(L.colsum_fc1);
+    if (L.colsum_qkv) cudaFree(L.colsum_qkv);
   }
   if (w->rope) cudaFree(w->rope);
   if (prev >= 0) cudaSetDevice(prev);
@@ -322,6 +323,19 @@ hc_status hc_weights_set_layer_full(hc_weights* w, int32_t layer, const void* d_
     HC_CUDA(launch_colsum(d_wkv, rows, d, true, L.colsum_all, nullptr));
     HC_CUDA(launch_colsum(d_wq, d, d, true, L.colsum_q, nullptr));
     HC_CUDA(launch_colsum(d_fc1, w->cfg.d_ffn, d, true, L.colsum_fc1, nullptr));
+    // [W_q ; W_k ; W_v] contiguous: one fused Q/K/V GEMM per recompute layer
+    // (tiles of 256 columns never straddle the Q | K boundary)
+    L.wqkv = nullptr;
+    if (static_cast<const char*>(d_wkv) == static_cast<const char*>(d_wq) + size_t(d) * d * 2 &&
+        d % 256 == 0 && qkv_fusion_enabled()) {
+      if (!L.colsum_qkv)
+        HC_CUDA(cudaMalloc(&L.colsum_qkv, size_t(d + rows) * sizeof(float)));
+      HC_CUDA(cudaMemcpy(L.colsum_qkv, L.colsum_q, size_t(d) * sizeof(float),
+                         cudaMemcpyDeviceToDevice));
+      HC_CUDA(cudaMemcpy(L.colsum_qkv + d, L.colsum_all, size_t(rows) * sizeof(float),
+                         cudaMemcpyDeviceToDevice));
+      L.wqkv = d_wq;
+    }
     HC_CUDA(cudaStreamSynchronize(nullptr));
     L.wq = d_wq;
     L.wkv_all = d_wkv;

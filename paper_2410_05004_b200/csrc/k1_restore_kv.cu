@@ -95,9 +95,10 @@ __device__ __forceinline__ float gelu_ref(float v) {  // model.cpp:38-40
 }
 
 // One thread = one output row; handles 32 consecutive columns [col0, col0+32).
+// Columns [0, q_cols) are Q (fused Q/K/V projection), then K, then V.
 __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int col0, const KvOut& out,
                                                const EpiArgs& epi, float mean, float rstd,
-                                               int pos, char* krow, char* vrow) {
+                                               int pos, char* krow, char* vrow, char* qrow) {
   if (epi.row_mean) {
     const float4* cs = reinterpret_cast<const float4*>(epi.colsum + col0);
 #pragma unroll
@@ -109,9 +110,11 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int col0, const K
       f[4 * i + 3] = ln_fold(f[4 * i + 3], mean, c.w, rstd);
     }
   }
-  const bool is_k = col0 < out.d_kv;
-  const int ocol = is_k ? col0 : col0 - out.d_kv;
-  if (is_k && epi.rope) {
+  const bool is_q = col0 < out.q_cols;
+  const int ckv = col0 - out.q_cols;
+  const bool is_k = !is_q && ckv < out.d_kv;
+  const int ocol = is_q ? col0 : is_k ? ckv : ckv - out.d_kv;
+  if ((is_k || is_q) && epi.rope) {
     const int half = epi.d_head >> 1;
     const float2* row_cs = epi.rope + size_t(pos) * half;
 #pragma unroll
@@ -121,8 +124,8 @@ __device__ __forceinline__ void epilogue_chunk(float (&f)[32], int col0, const K
       rope_rotate(f[2 * i], f[2 * i + 1], cs.x, cs.y);
     }
   }
-  char* dst = is_k ? krow : vrow;
-  if (out.out_f32) {
+  char* dst = is_q ? qrow : is_k ? krow : vrow;
+  if (out.out_f32 && !is_q) {
     float4* d4 = reinterpret_cast<float4*>(dst + size_t(ocol) * 4);
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -186,6 +189,7 @@ struct RowMeta {
   int pos = 0;
   char* krow = nullptr;
   char* vrow = nullptr;
+  char* qrow = nullptr;  // fused Q/K/V: this row's dense Q
 };
 
 template <int MODE>
@@ -215,6 +219,7 @@ __device__ __forceinline__ RowMeta row_meta(int row, const KvOut& out, const Epi
     const size_t esz = out.out_f32 ? 4 : 2;
     r.krow = static_cast<char*>(out.k_base) + size_t(orow) * out.d_kv * esz;
     r.vrow = static_cast<char*>(out.v_base) + size_t(orow) * out.d_kv * esz;
+    if (out.q_base) r.qrow = static_cast<char*>(out.q_base) + size_t(row) * size_t(out.q_cols) * 2;
   }
   if (epi.row_mean) {
     r.mean = __ldg(epi.row_mean + row);
@@ -227,7 +232,8 @@ template <int MODE>
 __device__ __forceinline__ void apply_chunk(float (&f)[32], int row, int col0, const RowMeta& r,
                                             const KvOut& out, const GemmOut& gout,
                                             const EpiArgs& epi) {
-  if (MODE == kEpiKv) epilogue_chunk(f, col0, out, epi, r.mean, r.rstd, r.pos, r.krow, r.vrow);
+  if (MODE == kEpiKv)
+    epilogue_chunk(f, col0, out, epi, r.mean, r.rstd, r.pos, r.krow, r.vrow, r.qrow);
   else epilogue_chunk_dense(f, MODE, row, col0, gout, epi, r.mean, r.rstd);
 }
 
@@ -646,7 +652,7 @@ __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n
   // loads of chunk c: index 4 * h2 + j (16-column half h2, row 8j + g)
   auto issue = [&](int c, float4 (&ld)[8]) {
     const int col0 = n_blk * BN + c * 32;
-    const bool k_half = col0 < out.d_kv;
+    const bool k_half = col0 < out.q_cols + out.d_kv;  // Q or K: rotated
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int h2 = i >> 2, j = i & 3;
@@ -695,7 +701,8 @@ __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n
     }
     const int col0 = n_blk * BN + c * 32;
     if (col0 >= N) continue;  // warp-uniform
-    const bool is_k = MODE == kEpiKv && col0 < out.d_kv;
+    const bool is_q = MODE == kEpiKv && col0 < out.q_cols;
+    const bool is_k = MODE == kEpiKv && !is_q && col0 - out.q_cols < out.d_kv;
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
       __syncwarp();  // the previous reads of tbuf are done
@@ -706,7 +713,9 @@ __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n
                         f[16 * h2 + 4 * q4 + 3]);
       __syncwarp();
       const int col = col0 + 16 * h2 + 4 * u;  // this lane's 4 columns
-      const int ocol = MODE == kEpiKv ? (is_k ? col : col - out.d_kv) : col;
+      const int ocol = MODE == kEpiKv
+                           ? (is_q ? col : is_k ? col - out.q_cols : col - out.q_cols - out.d_kv)
+                           : col;
       float4 cs4 = make_float4(0.f, 0.f, 0.f, 0.f);
       if (MODE != kEpiResid && epi.row_mean)
         cs4 = __ldg(reinterpret_cast<const float4*>(epi.colsum + col));
@@ -742,12 +751,14 @@ __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n
               pack4_bf16(gelu_ref(a[0]), gelu_ref(a[1]), gelu_ref(a[2]), gelu_ref(a[3]));
           continue;
         }
-        if (is_k && rope_on) {
+        if ((is_k || is_q) && rope_on) {
           rope_rotate(a[0], a[1], l4.x, l4.y);
           rope_rotate(a[2], a[3], l4.z, l4.w);
         }
-        char* dst = is_k ? e.krow : e.vrow;
-        if (out.out_f32)
+        char* dst = is_q ? static_cast<char*>(out.q_base) +
+                               size_t(row_base + r) * size_t(out.q_cols) * 2
+                         : is_k ? e.krow : e.vrow;
+        if (out.out_f32 && !is_q)
           *reinterpret_cast<float4*>(dst + size_t(ocol) * 4) = make_float4(a[0], a[1], a[2], a[3]);
         else
           *reinterpret_cast<uint2*>(dst + size_t(ocol) * 2) = pack4_bf16(a[0], a[1], a[2], a[3]);
@@ -1414,6 +1425,7 @@ cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, in
                               int num_sms, cudaStream_t stream, bool split_acc, const AltA* alt,
                               int m_sched) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  if (out.q_cols) split_acc = false;  // K/V columns: the exact summation order
   const int Ms = std::max(M, m_sched);
   GemmOut g;
   const AMaps am = amaps_with_alt(tmA, alt);
@@ -1483,6 +1495,14 @@ cudaError_t launch_row_stats(const void* x, int64_t rows, int cols, int64_t row_
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("HC_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
+bool qkv_fusion_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HC_QKV_FUSED");
     return !e || atoi(e) != 0;
   }();
   return on;

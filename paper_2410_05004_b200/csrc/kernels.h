@@ -44,6 +44,11 @@ struct KvOut {
   int start_pos = 0;
   const int32_t* seq_start = nullptr;  // per-sequence first position (overrides start_pos)
   int out_f32 = 0;  // 0: bf16 KV, 1: fp32 (parity/debug)
+  // Fused Q/K/V projection (recompute layers): the GEMM's first q_cols
+  // columns are Q (RoPE, bf16) stored densely at q_base + row * q_cols, the
+  // next 2*d_kv are K then V as above. q_cols = 0: K/V only.
+  void* q_base = nullptr;
+  int q_cols = 0;
 };
 
 // Epilogue inputs: LayerNorm fold (row stats + column sums of W) and RoPE.
@@ -247,6 +252,9 @@ cudaError_t launch_row_stats_flagged(const void* x, int64_t rows, int cols, int6
                                      cudaStream_t stream);
 // HC_LN_CENTER=0 disables the mean shift (A/B measurements only).
 bool ln_center_enabled();
+// HC_QKV_FUSED=0: the Q and the K/V projections of a recompute layer as two
+// GEMMs even when W_q precedes [W_k;W_v] in memory (A/B measurements only).
+bool qkv_fusion_enabled();
 // When *flag (device) is set: out[r] = bf16(x[r] - c_r), c_r = bf16(mean[r])
 // (exact for |x - c| small against c, Sterbenz), and mean[r] -= c_r in place,
 // so the LayerNorm fold over `out` is well conditioned. A no-op otherwise.

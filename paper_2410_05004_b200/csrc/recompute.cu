@@ -224,12 +224,29 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     pm.lap(3);
     KvOut kv = kv_out_pages(pages, L, d_page_table, sb.table_stride, sb.cu, sb.n_seqs);
     kv.seq_start = sb.seq_start;
+    // Q, K and V as one GEMM over [W_q;W_k;W_v] when the caller laid the
+    // weights out that way (the K/V columns see the same per-element
+    // arithmetic as the separate K/V GEMM, so restores stay bit-identical);
+    // not for the K/V-only last layer of a restore's prefix, nor for
+    // decode-sized steps (there the Q GEMM splits K over the SMs instead)
+    const bool fused = lw.wqkv != nullptr && mo > 0 && m > 128;
     {
       const Maps& mk = *maps(m);
       if (center) alt.map = mk.xc;
-      HC_CUDA(launch_restore_kv(mk.xb, wmap(lw.wkv_all, d, 2 * w->d_kv_all, mk.bn_kv), mk.bn_kv,
-                                int(m), 2 * w->d_kv_all, d, true, kv,
-                                epi_for(w, lw.colsum_all, mean, rstd), sms, stream, false, altp));
+      if (fused) {
+        KvOut kq = kv;
+        kq.q_base = q_buf.ptr;
+        kq.q_cols = d;
+        const int nq = d + 2 * w->d_kv_all;
+        const int bn = pick_bn(m, nq, sms);
+        HC_CUDA(launch_restore_kv(mk.xb, wmap(lw.wqkv, d, nq, bn), bn, int(m), nq, d, true, kq,
+                                  epi_for(w, lw.colsum_qkv, mean, rstd), sms, stream, false,
+                                  altp));
+      } else {
+        HC_CUDA(launch_restore_kv(mk.xb, wmap(lw.wkv_all, d, 2 * w->d_kv_all, mk.bn_kv), mk.bn_kv,
+                                  int(m), 2 * w->d_kv_all, d, true, kv,
+                                  epi_for(w, lw.colsum_all, mean, rstd), sms, stream, false, altp));
+      }
     }
     pm.lap(4);
     if (mo == 0) {  // only this layer's K/V was needed
@@ -241,16 +258,18 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     // every element is summed in the order of the full layer's GEMMs
     const Maps& mp = *maps(m);
     if (center) alt.map = mp.xc;
-    KvOut qo;
-    qo.k_base = q_buf.ptr;
-    qo.v_base = q_buf.ptr;
-    qo.d_kv = d;  // every column is "K": RoPE applies to all of Q
-    qo.cu_seqlens = sb.cu;
-    qo.n_seqs = sb.cu ? sb.n_seqs : 1;
-    qo.seq_start = sb.seq_start;
-    HC_CUDA(launch_restore_kv(mp.xb, wmap(lw.wq, d, d, mp.bn_d), mp.bn_d, int(mo), d, d, true, qo,
-                              epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true, altp,
-                              int(m)));
+    if (!fused) {
+      KvOut qo;
+      qo.k_base = q_buf.ptr;
+      qo.v_base = q_buf.ptr;
+      qo.d_kv = d;  // every column is "K": RoPE applies to all of Q
+      qo.cu_seqlens = sb.cu;
+      qo.n_seqs = sb.cu ? sb.n_seqs : 1;
+      qo.seq_start = sb.seq_start;
+      HC_CUDA(launch_restore_kv(mp.xb, wmap(lw.wq, d, d, mp.bn_d), mp.bn_d, int(mo), d, d, true, qo,
+                                epi_for(w, lw.colsum_q, mean, rstd), sms, stream, true, altp,
+                                int(m)));
+    }
     pm.lap(5);
     if (sb.cu && sb.from_zero && attention_tc_ok(kv))
       HC_CUDA(launch_attention_tc_varlen(q_buf.ptr, n, sb.n_seqs, sb.max_new, sb.cu, c.n_heads,

@@ -31,6 +31,11 @@ struct hc_weights {
     float* colsum_all = nullptr;  // owned, colsum of wkv_all (2*d_kv_all)
     float* colsum_q = nullptr;    // owned, colsum of wq (d)
     float* colsum_fc1 = nullptr;  // owned, colsum of fc1 (d_ffn)
+    // W_q immediately followed by [W_k;W_v] in the caller's memory: the Q, K
+    // and V projections of a recompute layer run as one GEMM over this
+    // [(d + 2*d_kv_all) x d] operand (nullptr: two GEMMs)
+    const void* wqkv = nullptr;
+    float* colsum_qkv = nullptr;  // owned, [colsum_q ; colsum_all] when wqkv is set
     bool full = false;
   };
   std::vector<Layer> layers;

@@ -48,10 +48,17 @@ def main():
     keep = [fill((vocab, d), 1)]
     w.set_embedding(keep[0])
     for layer in range(L):
-        wkv = fill((2 * d, d), 10 + layer)
-        t = [fill((d, d), 20 + layer), fill((d, d), 30 + layer), fill((dffn, d), 40 + layer),
+        # [W_q ; W_k ; W_v] in one allocation (the fused Q/K/V GEMM) unless HC_QKV_SPLIT
+        qkv = fill((3 * d, d), 10 + layer)
+        if os.environ.get("HC_QKV_SPLIT"):
+            qkv = torch.cat([qkv[:d].clone(), torch.zeros((64, d), dtype=qkv.dtype, device="cuda"),
+                             qkv[d:]])
+            wq, wkv = qkv[:d], qkv[d + 64:]
+        else:
+            wq, wkv = qkv[:d], qkv[d:]
+        t = [wq, fill((d, d), 30 + layer), fill((dffn, d), 40 + layer),
              fill((d, dffn), 50 + layer)]
-        keep += [wkv] + t
+        keep += [qkv] + t
         w.set_layer_kv(layer, wkv)
         w.set_layer_full(layer, t[0], wkv, t[1], t[2], t[3])
     kv = H.KvCache(L, n // 64, 64, d)

@@ -43,15 +43,18 @@ def main():
     bound = float(np.float32(1) / np.sqrt(np.float32(d)))
 
     def fill(shape, seed):
-        t = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+        t = shape if torch.is_tensor(shape) else torch.empty(shape, dtype=torch.bfloat16,
+                                                              device="cuda")
         check(lib().hc_fill_symmetric(t.data_ptr(), t.numel(), seed, 0, bound, 1, stream))
         return t
     keep = [fill((vocab, d), 99)]
     w.set_embedding(keep[0])
     for layer in range(L):
-        wkv = fill((2 * d, d), 1234 + layer)
+        qkv = fill((3 * d, d), 0)  # [W_q ; W_k ; W_v]: the fused Q/K/V GEMM
+        keep.append(qkv)
+        wq, wkv = fill(qkv[:d], 5000 + layer), fill(qkv[d:], 1234 + layer)
         w.set_layer_kv(layer, wkv)
-        w.set_layer_full(layer, fill((d, d), 5000 + layer), wkv, fill((d, d), 6000 + layer),
+        w.set_layer_full(layer, wq, wkv, fill((d, d), 6000 + layer),
                          fill((dffn, d), 7000 + layer), fill((d, dffn), 8000 + layer))
     kv = H.KvCache(L, n // 64, 64, d)
     table = torch.arange(n // 64, dtype=torch.int32, device="cuda")

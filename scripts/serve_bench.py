@@ -29,15 +29,17 @@ def build_weights(L, d, heads, dffn, vocab, max_seq, stream):
     keep = []
 
     def fill(shape, seed):
-        t = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+        t = shape if torch.is_tensor(shape) else torch.empty(shape, dtype=torch.bfloat16,
+                                                              device="cuda")
         check(lib().hc_fill_symmetric(t.data_ptr(), t.numel(), seed, 0, bound, 1, stream))
         keep.append(t)
         return t
     w.set_embedding(fill((vocab, d), 99))
     for layer in range(L):
-        wkv = fill((2 * d, d), 1234 + layer)
+        qkv = fill((3 * d, d), 0)  # [W_q ; W_k ; W_v]: the fused Q/K/V GEMM
+        wq, wkv = fill(qkv[:d], 5000 + layer), fill(qkv[d:], 1234 + layer)
         w.set_layer_kv(layer, wkv)
-        w.set_layer_full(layer, fill((d, d), 5000 + layer), wkv, fill((d, d), 6000 + layer),
+        w.set_layer_full(layer, wq, wkv, fill((d, d), 6000 + layer),
                          fill((dffn, d), 7000 + layer), fill((d, dffn), 8000 + layer))
     torch.cuda.synchronize()
     return mc, w, keep

@@ -45,8 +45,11 @@ def dev_bench_model(n_layers, d, heads, d_ffn, vocab, max_seq=4096):
     keep = [dev_symmetric(vocab * d, P.SEED_EMB, 0, b).view(vocab, d)]
     w.set_embedding(keep[0])
     for layer in range(n_layers):
-        wkv = dev_symmetric(2 * d * d, P.SEED_WKV + layer, 0, b).view(2 * d, d)
-        wq = dev_symmetric(d * d, P.SEED_WQ + layer, 0, b).view(d, d)
+        # [W_q ; W_k ; W_v] in one allocation, as bench.py lays it out (fused Q/K/V GEMM)
+        qkv = torch.empty((3 * d, d), dtype=torch.bfloat16, device="cuda")
+        qkv[:d] = dev_symmetric(d * d, P.SEED_WQ + layer, 0, b).view(d, d)
+        qkv[d:] = dev_symmetric(2 * d * d, P.SEED_WKV + layer, 0, b).view(2 * d, d)
+        wq, wkv = qkv[:d], qkv[d:]
         wo = dev_symmetric(d * d, P.SEED_WO + layer, 0, b).view(d, d)
         fc1 = dev_symmetric(d_ffn * d, P.SEED_FC1 + layer, 0, b).view(d_ffn, d)
         fc2 = dev_symmetric(d * d_ffn, P.SEED_FC2 + layer, 0, b).view(d, d_ffn)

@@ -20,8 +20,11 @@ pytestmark = pytest.mark.gpu
 RECOMPUTE_TOL = 5e-2
 
 
-def dev_init_model(n_layers, d, d_ffn, vocab, seed):
-    """init_model's flat stream on the GPU (bf16), split like the reference."""
+def dev_init_model(n_layers, d, d_ffn, vocab, seed, fused=True):
+    """init_model's flat stream on the GPU (bf16), split like the reference.
+    The stream draws wq, wk, wv back to back, so with `fused` W_q and [W_k;W_v]
+    are views of one [3d x d] allocation (the recompute path's fused Q/K/V
+    GEMM); otherwise two separate allocations (two GEMMs)."""
     import torch
     bound = float(np.float32(1.0) / np.sqrt(np.float32(d)))
     dd, df = d * d, d * d_ffn
@@ -29,9 +32,15 @@ def dev_init_model(n_layers, d, d_ffn, vocab, seed):
     layers = []
     for L in range(n_layers):
         base = vocab * d + L * (4 * dd + 2 * df)
+        if fused:
+            qkv = dev_symmetric(3 * dd, seed, base, bound).view(3 * d, d)
+            wq, wkv = qkv[:d], qkv[d:]
+        else:
+            wq = dev_symmetric(dd, seed, base, bound).view(d, d)
+            wkv = dev_symmetric(2 * dd, seed, base + dd, bound).view(2 * d, d)
         layers.append(dict(
-            wq=dev_symmetric(dd, seed, base, bound).view(d, d),
-            wkv=dev_symmetric(2 * dd, seed, base + dd, bound).view(2 * d, d),
+            wq=wq,
+            wkv=wkv,
             wo=dev_symmetric(dd, seed, base + 3 * dd, bound).view(d, d),
             fc1=dev_symmetric(df, seed, base + 4 * dd, bound).view(d_ffn, d),
             fc2=dev_symmetric(df, seed, base + 4 * dd + df, bound).view(d, d_ffn)))
@@ -39,10 +48,11 @@ def dev_init_model(n_layers, d, d_ffn, vocab, seed):
     return emb, layers
 
 
-def build(cfg_kw, seed):
+def build(cfg_kw, seed, fused=True):
     from paper_2410_05004_b200 import hcache as H
     cfg = H.ModelConfig(**cfg_kw)
-    emb, layers = dev_init_model(cfg.n_layers, cfg.d_hidden, cfg.d_ffn, cfg.vocab_size, seed)
+    emb, layers = dev_init_model(cfg.n_layers, cfg.d_hidden, cfg.d_ffn, cfg.vocab_size, seed,
+                                 fused)
     w = H.Weights(cfg)
     w.set_embedding(emb)
     for L, lw in enumerate(layers):
@@ -99,6 +109,32 @@ def test_config1_gpu_prefill_matches_reference_prefill(cuda, oracle):
     # layer 0's input is the embedding itself: exact
     assert worst[0][0] == 0.0
     print("recompute max rel err per layer (inputs, K, V):", worst)
+
+
+@pytest.mark.parametrize("n", [300, 1024])
+def test_fused_qkv_matches_separate_projections(cuda, oracle, n):
+    """[W_q;W_k;W_v] in one allocation runs Q, K and V as one GEMM; separate
+    allocations run the Q GEMM and the K/V GEMM. Layer 0 (same input) must
+    give bit-identical K/V; deeper layers see Q from a different tile
+    schedule (the separate Q GEMM may split its last wave's K loop), so they
+    agree to the recompute tolerance, and both stay within it of the oracle."""
+    import torch
+    cfg_f, w_f = build(CONFIG1, 1234, fused=True)
+    cfg_s, w_s = build(CONFIG1, 1234, fused=False)
+    tokens = [(i * 11 + 1) % 1024 for i in range(n)]
+    kv_f, table, in_f, _ = gpu_prefill(w_f, cfg_f, tokens)
+    kv_s, _, in_s, _ = gpu_prefill(w_s, cfg_s, tokens)
+    ref = oracle_prefill(oracle, cfg_f, 1234, np.array(tokens, np.int32))
+    k_f, v_f = kv_f.gather(0, table, n)
+    k_s, v_s = kv_s.gather(0, table, n)
+    assert torch.equal(k_f, k_s) and torch.equal(v_f, v_s)
+    for L in range(cfg_f.n_layers):
+        k_f, v_f = kv_f.gather(L, table, n)
+        k_s, v_s = kv_s.gather(L, table, n)
+        for g, s_ in ((k_f, k_s), (v_f, v_s)):
+            assert norm_err(g.float().cpu().numpy(), s_.float().cpu().numpy()) < RECOMPUTE_TOL
+        assert norm_err(k_f.float().cpu().numpy(), ref["k"][L]) < RECOMPUTE_TOL
+        assert norm_err(v_f.float().cpu().numpy(), ref["v"][L]) < RECOMPUTE_TOL
 
 
 @pytest.mark.parametrize("n", [1, 7, 64, 130])
