@@ -102,7 +102,11 @@ void hc_weights_destroy(hc_weights* w);
 hc_status hc_weights_set_layer_kv(hc_weights* w, int32_t layer, const void* d_wkv);
 /* Full block weights for the RECOMPUTE path (model.hpp:27-32), bf16,
  * row-major (out x in): wq d x d, wkv as above (all heads), wo d x d,
- * fc1 d_ffn x d, fc2 d x d_ffn. */
+ * fc1 d_ffn x d, fc2 d x d_ffn. When wkv starts right where wq ends
+ * (one [W_q ; W_k ; W_v] allocation, the reference's own draw order,
+ * model.cpp:185-188) and d_hidden % 256 == 0, a recompute layer projects Q,
+ * K and V with one GEMM (HC_QKV_FUSED=0 turns this off); the K/V it writes
+ * are bit-identical either way. */
 hc_status hc_weights_set_layer_full(hc_weights* w, int32_t layer, const void* d_wq,
                                    const void* d_wkv, const void* d_wo, const void* d_fc1,
                                    const void* d_fc2);

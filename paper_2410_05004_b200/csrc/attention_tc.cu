@@ -448,6 +448,9 @@ constexpr int kFaThreads = 576;  // TMA, MMA, 8 softmax warps per Q tile (two th
 #ifndef HC_FA_EMU
 #define HC_FA_EMU 0
 #endif
+#ifndef HC_FA_EXP_NOMAXPASS  // 1: skip the row-max TMEM pass after tile 0 (timing only)
+#define HC_FA_EXP_NOMAXPASS 0
+#endif
 #ifndef HC_FA_PCHUNK  // 1: P published per 32-key chunk, 0: once per tile (experiments)
 #define HC_FA_PCHUNK 1
 #endif
@@ -811,6 +814,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       for (int u = 0; u < 8; ++u) m8[u] = -INFINITY;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
+        if (HC_FA_EXP_NOMAXPASS && j > 0) break;  // timing experiment only (wrong results)
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_s + uint32_t(c * 32), v);
         tmem_wait_ld();

@@ -1118,12 +1118,12 @@ __global__ void colsum_kernel(const T* __restrict__ w, int64_t rows, int cols,
 // the copy engines stream hidden states waited ~40-55 us before it ran (CUPTI
 // trace of the restore: every per-layer memset of the recompute prefix
 // stalled its stream that long).
-__global__ void zero_i32_kernel(int32_t* p, int64_t n) {
+__global__ void zero_i32_kernel(int32_t* p, int64_t n, int32_t step) {
   pdl_wait();
   pdl_trigger();
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
-    p[i] = 0;
+    p[i] = int32_t(i) * step;  // step 0: zeros; 1: 0, 1, 2, .. (identity page table)
 }
 
 __global__ void fill_symmetric_kernel(void* dst, int64_t n, uint64_t seed, uint64_t offset,
@@ -1177,6 +1177,33 @@ __global__ void kv_scatter_kernel(const uint4* __restrict__ rows, int64_t n_rows
     uint4 b = __ldg(src + vec + i);
     kd[i] = a;
     vd[i] = b;
+  }
+}
+
+// One warp per row: columns [col0, col0 + out.d_kv) of a dense all-heads K
+// and V ([n_rows x src_ld] bf16 each) -> this GPU's pages (its heads only;
+// the replicated RECOMPUTE prefix of a head-sharded restore).
+__global__ void kv_slice_kernel(const uint4* __restrict__ k_src, const uint4* __restrict__ v_src,
+                                int src_ld, int col0, int64_t n_rows, KvOut out) {
+  pdl_wait();
+  pdl_trigger();
+  const int warps = blockDim.x >> 5;
+  const int64_t row = int64_t(blockIdx.x) * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  int64_t orow = row;
+  if (out.page_table) {
+    const int64_t pos = out.start_pos + row;
+    orow = int64_t(__ldg(out.page_table + pos / out.page_size)) * out.page_size +
+           pos % out.page_size;
+  }
+  const int vec = out.d_kv / 8;
+  const int64_t so = (row * src_ld + col0) / 8;
+  uint4* kd = static_cast<uint4*>(out.k_base) + orow * vec;
+  uint4* vd = static_cast<uint4*>(out.v_base) + orow * vec;
+  for (int i = lane; i < vec; i += 32) {
+    kd[i] = __ldg(k_src + so + i);
+    vd[i] = __ldg(v_src + so + i);
   }
 }
 
@@ -1544,7 +1571,12 @@ cudaError_t launch_colsum(const void* w, int64_t rows, int cols, bool bf16_in, f
 cudaError_t launch_zero_i32(int32_t* p, int64_t n, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   const int blocks = int(std::min<int64_t>((n + 255) / 256, 1024));
-  return launch_pdl(zero_i32_kernel, dim3(blocks), dim3(256), 0, stream, p, n);
+  return launch_pdl(zero_i32_kernel, dim3(blocks), dim3(256), 0, stream, p, n, int32_t(0));
+}
+cudaError_t launch_iota_i32(int32_t* p, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, 1024));
+  return launch_pdl(zero_i32_kernel, dim3(blocks), dim3(256), 0, stream, p, n, int32_t(1));
 }
 
 cudaError_t launch_fill_symmetric(void* dst, int64_t n, uint64_t seed, uint64_t offset,
@@ -1563,6 +1595,16 @@ cudaError_t launch_kv_scatter(const void* rows, int64_t n_rows, const KvOut& out
   const unsigned grid = unsigned((n_rows + per_block - 1) / per_block);
   return launch_pdl(kv_scatter_kernel, dim3(grid), dim3(threads), 0, stream,
                     static_cast<const uint4*>(rows), n_rows, out);
+}
+
+cudaError_t launch_kv_slice(const void* k_src, const void* v_src, int src_ld, int col0,
+                            int64_t n_rows, const KvOut& out, cudaStream_t stream) {
+  if (n_rows <= 0) return cudaSuccess;
+  if (out.d_kv % 8 || src_ld % 8 || col0 % 8 || out.out_f32) return cudaErrorInvalidValue;
+  const int warps = 8;
+  return launch_pdl(kv_slice_kernel, dim3(unsigned((n_rows + warps - 1) / warps)),
+                    dim3(32 * warps), 0, stream, static_cast<const uint4*>(k_src),
+                    static_cast<const uint4*>(v_src), src_ld, col0, n_rows, out);
 }
 
 cudaError_t launch_kv_gather(const KvOut& kv, int pos0, int64_t n_rows, void* rows,

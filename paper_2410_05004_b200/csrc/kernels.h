@@ -272,6 +272,8 @@ cudaError_t launch_colsum(const void* w, int64_t rows, int cols, bool bf16_in, f
 // (offset+i) (reference model.cpp:17-31), stored as bf16/fp16/fp32.
 // p[0, n) = 0 as a kernel (stream-ordered memsets stall behind copy-engine work)
 cudaError_t launch_zero_i32(int32_t* p, int64_t n, cudaStream_t stream);
+// p[i] = i (an identity page table)
+cudaError_t launch_iota_i32(int32_t* p, int64_t n, cudaStream_t stream);
 cudaError_t launch_fill_symmetric(void* dst, int64_t n, uint64_t seed, uint64_t offset,
                                   float bound, int dtype, cudaStream_t stream);
 
@@ -279,5 +281,9 @@ cudaError_t launch_fill_symmetric(void* dst, int64_t n, uint64_t seed, uint64_t 
 // -> K and V (dense or paged, same KvOut addressing as K1). HBM-bound.
 cudaError_t launch_kv_scatter(const void* rows, int64_t n_rows, const KvOut& out,
                               cudaStream_t stream);
+// Columns [col0, col0 + out.d_kv) of dense all-heads K and V rows ([n_rows x
+// src_ld] bf16, row r at position out.start_pos + r) -> out's pages.
+cudaError_t launch_kv_slice(const void* k_src, const void* v_src, int src_ld, int col0,
+                            int64_t n_rows, const KvOut& out, cudaStream_t stream);
 
 }  // namespace hc

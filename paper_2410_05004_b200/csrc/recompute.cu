@@ -124,7 +124,8 @@ void forward_impl(const hc_weights* w, const int32_t* d_tokens, int64_t n, int l
     fail(HC_EINVAL, "forward: the next token needs the last layer's output");
   if (!sb.cu && n > c.max_seq) fail(HC_EINVAL, "forward: sequence exceeds max_seq");
   if (!w->embedding) fail(HC_EINVAL, "prefill_layers: embedding not set");
-  if (w->d_kv != w->d_kv_all) fail(HC_EINVAL, "prefill_layers: needs all KV heads on this GPU");
+  // (a head-sharded weight set may run the forward too -- its full block
+  // weights hold every head -- into pages of all heads, validated below)
   for (int L = lb; L < le; ++L)
     if (!w->layers[size_t(L)].full) fail(HC_EINVAL, "prefill_layers: full block weights not set");
   validate_pages(w, pages, w->d_kv_all);
@@ -426,7 +427,7 @@ void forward_batch(const hc_weights* w, const int32_t* d_tokens, int n_seqs,
 }
 
 double recompute_layer_seconds(const hc_weights* w, int n, double warm_s) {
-  if (!w || !w->embedding || w->d_kv != w->d_kv_all || n < 1) return 0.0;
+  if (!w || !w->embedding || n < 1) return 0.0;
   int layer = -1;
   for (int l = 0; l < w->cfg.n_layers; ++l)
     if (w->layers[size_t(l)].full) {

@@ -35,6 +35,7 @@
 #include "common.h"
 #include "engine.h"
 #include "kernels.h"
+#include "recompute.h"
 #include "store.h"
 #include "weights.h"
 
@@ -143,10 +144,16 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
   if (n > int64_t(pages->num_pages) * pages->page_size) bad("KV pages too small for the session");
   if (w->cfg.rope_enabled && n > w->rope_rows) bad("session longer than max_seq (RoPE table)");
   const auto order = compute_order(plan);
-  int n_hidden = 0, n_kv = 0;
+  int n_hidden = 0, n_kv = 0, n_re = 0;
   for (const auto& j : order) {
-    if (j.method == HC_METHOD_RECOMPUTE)
-      bad("RECOMPUTE layers need the whole model on one GPU (world > 1)");
+    if (j.method == HC_METHOD_RECOMPUTE) {
+      // replicated prefix: every rank runs layers [0, n_re) for all heads
+      // (the attention of a layer needs every head) and keeps its own heads
+      if (j.layer != n_re) bad("RECOMPUTE layers must form a prefix");
+      ++n_re;
+      if (!w->layers[size_t(j.layer)].full) bad("RECOMPUTE prefix needs full block weights");
+      continue;
+    }
     if (j.method == HC_METHOD_HIDDEN) {
       ++n_hidden;
       if (!w->layers[size_t(j.layer)].ready) bad("layer weights not set for a HIDDEN layer");
@@ -156,6 +163,14 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
   }
   if (n_kv && (m.d_kv != w->d_kv)) bad("KV rows of this rank's heads expected (session d_kv)");
   if (n_kv && pages->dtype != HC_DTYPE_BF16) bad("KV-offload layers need bf16 pages");
+  const int32_t* host_tokens = nullptr;
+  if (n_re) {
+    if (!w->embedding) bad("RECOMPUTE prefix needs the embedding");
+    if (pages->dtype != HC_DTYPE_BF16) bad("RECOMPUTE prefix needs bf16 pages");
+    int64_t n_ids = 0;
+    host_tokens = store.pinned_tokens(sid, &n_ids);
+    if (!host_tokens || n_ids < n) bad("manifest has fewer token ids than tokens");
+  }
   const int W = g->world, me = g->rank, d = g->d;
   std::vector<int64_t> r0(size_t(W) + 1);
   for (int r = 0; r < W; ++r) {
@@ -170,6 +185,7 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
   std::vector<std::vector<CopySeg>> segs(order.size());
   for (size_t i = 0; i < order.size(); ++i) {
     const auto& j = order[i];
+    if (j.method == HC_METHOD_RECOMPUTE) continue;
     if (j.method == HC_METHOD_HIDDEN) {
       if (my_rows > 0)
         segs[i] = store.gather_plan(sid, j.layer, HC_STATE_HIDDEN, int(mb), int(me_e), nullptr);
@@ -203,10 +219,50 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
   HC_CUDA(cudaStreamWaitEvent(eng.aux, t0, 0));
   std::vector<cudaEvent_t> joins, consumed_kv(size_t(nbuf_kv), nullptr);
   const uint32_t abox = uint32_t(gemm_a_box(n));
+
+  // Replicated RECOMPUTE prefix on the compute lane (restore.cpp:177-182):
+  // the IO lane fetches the hidden layers' ranges meanwhile, as far as the
+  // peer group's slot ring reaches. All heads' K/V of a prefix layer go to a
+  // one-layer dense scratch (64-row pages, identity table) that the layer's
+  // attention reads; this rank's head columns are then copied into its pages.
+  const int64_t re_pages = (n + 63) / 64;
+  StreamScratch re_tok(n_re ? sizeof(int32_t) * size_t(n) : 0, stream),
+      re_table(n_re ? sizeof(int32_t) * size_t(re_pages) : 0, stream),
+      re_k(n_re ? size_t(re_pages) * 64 * size_t(w->d_kv_all) * 2 : 0, stream),
+      re_v(n_re ? size_t(re_pages) * 64 * size_t(w->d_kv_all) * 2 : 0, stream);
+  if (n_re) {
+    HC_CUDA(cudaMemcpyAsync(re_tok.ptr, host_tokens, sizeof(int32_t) * size_t(n),
+                            cudaMemcpyHostToDevice, stream));
+    HC_CUDA(launch_iota_i32(static_cast<int32_t*>(re_table.ptr), re_pages, stream));
+    std::vector<void*> kp(size_t(w->cfg.n_layers), re_k.ptr), vp(size_t(w->cfg.n_layers), re_v.ptr);
+    const hc_kv_pages scratch{w->cfg.n_layers, 64, int32_t(re_pages), w->d_kv_all, HC_DTYPE_BF16,
+                              kp.data(), vp.data()};
+    std::vector<cudaEvent_t> marks;
+    auto hook = [&](int layer, bool start) {
+      if (start) {
+        if (timed) {
+          marks.push_back(evp.get());
+          HC_CUDA(cudaEventRecord(marks.back(), stream));
+        }
+        return;
+      }
+      HC_CUDA(launch_kv_slice(re_k.ptr, re_v.ptr, w->d_kv_all, w->head_begin * w->d_head, n,
+                              kv_out_pages(pages, layer, d_page_table, 0, nullptr, 1), stream));
+      if (timed) {
+        cudaEvent_t e = evp.get();
+        HC_CUDA(cudaEventRecord(e, stream));
+        ops.push_back({HC_LANE_COMPUTE, layer, HC_EV_RECOMPUTE, marks.back(), e});
+      }
+    };
+    prefill_layers_impl(w, static_cast<const int32_t*>(re_tok.ptr), n, 0, n_re, &scratch,
+                        static_cast<const int32_t*>(re_table.ptr), stream, hook, nullptr, nullptr,
+                        0, true);
+  }
   int ikv = 0;
   for (size_t i = 0; i < order.size(); ++i) {
     const auto& j = order[i];
     const auto& L = w->layers[size_t(j.layer)];
+    if (j.method == HC_METHOD_RECOMPUTE) continue;  // (the prefix above)
     if (j.method == HC_METHOD_HIDDEN) {
       const uint64_t stp = g->step++;
       const int slot = int(stp % uint64_t(g->depth));

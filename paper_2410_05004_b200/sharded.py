@@ -16,9 +16,11 @@ This module holds what sits around that call:
 * ``save_shard``  -- one rank's save path: its token range of each HIDDEN
   layer (hc_store_snapshot_range) and its heads' KV rows of each KV layer;
 * ``plan_sharded`` -- the bubble-free planner at N GPUs: per-rank costs
-  (PCIe measured with every rank copying at once, K1 on the rank's heads),
-  the three-way planner without RECOMPUTE (the prefix would need the whole
-  model on one GPU), one plan agreed by all ranks;
+  (PCIe measured with every rank copying at once, K1 on the rank's heads,
+  the recompute of a layer -- replicated: every rank runs the RECOMPUTE
+  prefix for all heads, since a layer's attention needs every head, and
+  keeps its own heads' K/V), the three-way planner, one plan agreed by all
+  ranks;
 * ``restore_layers`` -- the orchestration in plain host terms (fetch own
   range, all-gather, project own heads), which the gloo CPU test runs with
   the oracle as the projection;
@@ -124,21 +126,23 @@ def save_shard(store, sid: str, seed, plan, rank: int, world: int,
             rows = kv_rows(layer)
             while not store.snapshot(sid, layer, H.StateKind.KV, rows):
                 store.drain()
-        else:
-            raise ValueError("save_shard: RECOMPUTE layers are not restored per rank")
+        # RECOMPUTE layers store nothing: every rank recomputes them from the
+        # session's token ids
     store.finalize(sid)
 
 
 def plan_sharded(io_h_rank: List[float], io_kv_rank: List[float], c_h_rank: List[float],
-                 n_layers: int, depth: int = 2):
+                 n_layers: int, depth: int = 2, c_token_rank: List[float] = None):
     """The three-way planner at N GPUs: every rank's lanes must finish, so a
     layer costs the slowest rank's fetch (io_h: its token range, io_kv: its
-    heads' KV rows, both measured with all ranks copying at once) and K1
-    (its heads over all n rows). RECOMPUTE is unavailable (c_token = inf).
+    heads' KV rows, both measured with all ranks copying at once), K1 (its
+    heads over all n rows) and recompute (the whole layer, replicated on every
+    rank; None = unavailable, e.g. without the full block weights).
     Deterministic in its inputs, so ranks that share them agree."""
     from . import hcache as H
+    c_tok = max(c_token_rank) if c_token_rank else H.RECOMPUTE_UNAVAILABLE
     t = H.ProfiledTimings(io_h=max(io_h_rank), io_kv=max(io_kv_rank), c_h=max(c_h_rank),
-                          c_token=H.RECOMPUTE_UNAVAILABLE, n_layers=n_layers)
+                          c_token=c_tok, n_layers=n_layers)
     return H.plan_three_way(t, prefetch_depth=max(1, depth - 1)) + (t,)
 
 
@@ -166,20 +170,41 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     hb, hc = H.shard_heads(kvh, world, rank)
     dh = d // heads
     d_kv_all = kvh * dh
+    vocab = 32000
     mc = H.ModelConfig(n_layers=L, d_hidden=d, n_heads=heads, n_kv_heads=kvh, d_ffn=dffn,
-                       max_seq=max(n, 4096), rope_enabled=rope)
+                       vocab_size=vocab, max_seq=max(n, 4096), rope_enabled=rope)
     w = H.Weights(mc, hb, hc, dev)
     bound = float(np.float32(1) / np.sqrt(np.float32(d)))
     a, c = hb * dh, (hb + hc) * dh
+    # the RECOMPUTE complement needs the whole block on every rank (the prefix
+    # is replicated); MHA models as at N=1 (bench.py), not GQA-70B's 140 GB
+    full = not getattr(args, "no_recompute", False) and kvh == heads
     keep = []
+
+    def fill(t, seed):
+        check(lib().hc_fill_symmetric(t.data_ptr(), t.numel(), seed, 0, bound, 1, stream))
+        return t
+
+    def new(shape):
+        return torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+    if full:
+        keep.append(fill(new((vocab, d)), 99))
+        w.set_embedding(keep[-1])
     for layer in range(L):
-        full_w = torch.empty((2 * d_kv_all, d), dtype=torch.bfloat16, device="cuda")
-        check(lib().hc_fill_symmetric(full_w.data_ptr(), full_w.numel(), 1234 + layer, 0, bound,
-                                      1, stream))
+        # [W_q ; W_k ; W_v] (bench.py seeds; the fused Q/K/V GEMM of the prefix)
+        qkv = new((d + 2 * d_kv_all, d)) if full else new((2 * d_kv_all, d))
+        q_rows = d if full else 0
+        full_w = fill(qkv[q_rows:], 1234 + layer)
         mine = torch.cat([full_w[a:c], full_w[d_kv_all + a: d_kv_all + c]]).contiguous()
         w.set_layer_kv(layer, mine)
         keep.append(mine)
-        del full_w
+        if full:
+            fill(qkv[:d], 5000 + layer)
+            blk = [fill(new((d, d)), 6000 + layer), fill(new((dffn, d)), 7000 + layer),
+                   fill(new((d, dffn)), 8000 + layer)]
+            w.set_layer_full(layer, qkv[:d], full_w, *blk)
+            keep += [qkv] + blk
+        del full_w, qkv
     page = 64
     n_pages = (n + page - 1) // page
     kv = H.KvCache(L, n_pages, page, w.d_kv)
@@ -187,7 +212,10 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     ranges = [H.shard_range(n, world, r) for r in range(world)]
     b, e = ranges[rank]
     rows_max = max(1, max(y - x for x, y in ranges))
-    depth = 2
+    # staging slots: enough for the IO lane to run ahead through a RECOMPUTE
+    # prefix (every HIDDEN layer when it fits in ~4 GiB), at least 2
+    slot_bytes = rows_max * d * 2
+    depth = int(max(2, min(L, (4 << 30) // max(1, slot_bytes)))) if full else 2
     group = H.PeerGroup(world, rank, d, rows_max, depth=depth, device=dev,
                         exchange=H.PeerGroup.torch_exchange())
     tokens = [(i * 11 + 1) % 32000 for i in range(n)]
@@ -224,7 +252,12 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                                  C.byref(k1_ms)))
     del hb_probe
     c_h = max_over_ranks(k1_ms.value * 1e-3)
-    plan, plan_s, prof = plan_sharded([io_h], [io_kv], [c_h], L, depth)
+    c_tok = None
+    if full:  # one rank's recompute of a whole layer (all heads), max over ranks
+        dist.barrier()
+        c_tok = max_over_ranks(H.profile_hardware(w, n).c_token)
+    plan, plan_s, prof = plan_sharded([io_h], [io_kv], [c_h], L, depth,
+                                      [c_tok] if c_tok else None)
     # every rank computed the same plan from the same maxima; check it
     plans = [None] * world
     dist.all_gather_object(plans, plan.serialize())
@@ -307,7 +340,7 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     # parity of this rank's heads after one more restore of the plan
     step("hcache")
     torch.cuda.synchronize()
-    par = _verify_shard(kv, table, plan, cfg, hb, hc, kv_saved, w.d_kv)
+    par = _verify_shard(kv, table, plan, cfg, hb, hc, kv_saved, w.d_kv, tokens)
     pars = [None] * world
     dist.all_gather_object(pars, par)
     tl = H.restore_sharded(group, store, "hcache", w, plan, H.ThrottleConfig(0, True), kv, table,
@@ -326,8 +359,10 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                   "hidden_max_rel": max(p_["hidden_max_rel"] for p_ in pars),
                   "kv_bitexact": (all(p_["kv_bitexact"] for p_ in pars)
                                   if pars[0]["kv_bitexact"] is not None else None),
+                  "recompute_norm_err": max((p_["recompute_norm_err"] or 0.0) for p_ in pars),
                   "ok": all(p_["ok"] for p_ in pars),
-                  "tolerances": {"hidden_max_rel": 1e-2, "kv": "bit-exact"}}
+                  "tolerances": {"hidden_max_rel": 1e-2, "kv": "bit-exact",
+                                 "recompute_norm_err": 5e-2}}
         line = {
             "metric": "restored_kv_tokens_per_s", "value": n / (ms * 1e-3), "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -345,10 +380,14 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                         "hcache_vs_recompute": None},
             "planner": {"plan": plan.serialize(),
                         "per_rank_ms": {"io_h": io_h * 1e3, "io_kv": io_kv * 1e3,
-                                        "c_h": c_h * 1e3},
-                        "predicted_ms": plan_s * 1e3,
+                                        "c_h": c_h * 1e3,
+                                        "c_token": c_tok * 1e3 if c_tok else None},
+                        "predicted_ms": plan_s * 1e3, "staging_slots": depth,
                         "how": "hc_plan_three_way on the slowest rank's measured costs (PCIe "
-                               "with all ranks copying at once); RECOMPUTE unavailable at N>1"},
+                               "with all ranks copying at once; c_token = a whole layer's "
+                               "recompute, the RECOMPUTE prefix being replicated on every "
+                               "rank)" + ("" if c_tok else "; RECOMPUTE unavailable (no full "
+                                          "block weights: GQA or --no-recompute)")},
             "pcie": {"per_rank_gbs": bw_rank / 1e9, "slowest_rank_gbs": bw_min / 1e9,
                      "aggregate_gbs": bw_agg / 1e9, "probe_bytes": probe,
                      "how": f"hc_measure_h2d on every rank at once after a barrier; aggregate = "
@@ -369,8 +408,11 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                          "frac": k1_tflops / pk["bf16_tflops"], "peak_source": pk["_source"],
                          "traffic": None, "flop_per_launch": flop, "k1_ms": c_h * 1e3},
             # per step and rank: per HIDDEN layer statistics, mean-shift check,
-            # two flag signals, statistics gather and K1; per KV layer the scatter
-            "gpu_launches": 2 * args.steps * world * (plan.l_h * 6 + plan.l_kv),
+            # two flag signals, statistics gather and K1; per KV layer the
+            # scatter; per RECOMPUTE layer ~12 (stats, centering, GEMMs,
+            # attention, head slice)
+            "gpu_launches": 2 * args.steps * world * (plan.l_h * 6 + plan.l_kv +
+                                                      12 * (L - plan.l_h - plan.l_kv)),
             "clocks": clocks,
         }
         if not args.no_cpu_baseline:
@@ -384,10 +426,12 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     dist.destroy_process_group()
 
 
-def _verify_shard(kv, table, plan, cfg, hb, hc, kv_saved, d_kv_local, m=32):
+def _verify_shard(kv, table, plan, cfg, hb, hc, kv_saved, d_kv_local, tokens, m=32):
     """This rank's heads after the benchmarked restore: HIDDEN layers on
     token slices vs the oracle's project_hidden_to_kv (north-star metric),
-    KV layers bit-exact against the stored rows (oracle/parity.py seeds)."""
+    KV layers bit-exact against the stored rows, RECOMPUTE layers on rows
+    [0, m) vs the oracle's fp32 prefill of those tokens (stated K6 tolerance;
+    oracle/parity.py seeds)."""
     import numpy as np
     import torch
 
@@ -395,19 +439,20 @@ def _verify_shard(kv, table, plan, cfg, hb, hc, kv_saved, d_kv_local, m=32):
     from oracle import parity as P
 
     from . import hcache as H
-    L, d, heads, kvh, _, n, rope = cfg
+    L, d, heads, kvh, dffn, n, rope = cfg
     dh = d // heads
+    a, c = hb * dh, (hb + hc) * dh
     o = Oracle()
     meth = list(plan.layer_assignment)
     hid = [x for x, y in enumerate(meth) if y == H.LayerMethod.HIDDEN]
     kvl = [x for x, y in enumerate(meth) if y == H.LayerMethod.KV_OFFLOAD]
+    rel = [x for x, y in enumerate(meth) if y == H.LayerMethod.RECOMPUTE]
     pick = sorted({hid[int(round(k * (len(hid) - 1) / 2))] for k in range(3)}) if hid else []
     worst = 0.0
     starts = sorted({0, (n // 2) // 64 * 64, max(0, n - m)})
     for layer in pick:
         k, v = kv.gather(layer, table, n)
         wk, wv = P.layer_wkv(o, layer, d, kvh * dh)
-        a, c = hb * dh, (hb + hc) * dh
         for s0 in starts:
             h = P.hidden_rows(o, layer, n, d, s0, min(m, n - s0))
             kr, vr = o.project(h, np.ascontiguousarray(wk[a:c]), np.ascontiguousarray(wv[a:c]),
@@ -420,6 +465,16 @@ def _verify_shard(kv, table, plan, cfg, hb, hc, kv_saved, d_kv_local, m=32):
         for layer in kvl:
             k, v = kv.gather(layer, table, n)
             exact &= bool(torch.equal(torch.cat([k, v], 1), kv_saved[layer]))
+    ne = None
+    if rel:
+        ref = P.recompute_kv(o, d, heads, dffn, tokens[:m], len(rel), rope)
+        ne = 0.0
+        for layer in rel:
+            k, v = kv.gather(layer, table, m)
+            kr, vr = ref[layer]
+            ne = max(ne, P.norm_err(k.float().cpu().numpy(), kr[:, a:c]),
+                     P.norm_err(v.float().cpu().numpy(), vr[:, a:c]))
     return {"heads": [hb, hb + hc], "hidden_layers_checked": pick, "hidden_max_rel": worst,
-            "kv_layers": len(kvl), "kv_bitexact": exact,
-            "ok": bool(worst <= 1e-2 and exact is not False)}
+            "kv_layers": len(kvl), "kv_bitexact": exact, "recompute_layers": rel,
+            "recompute_norm_err": ne,
+            "ok": bool(worst <= 1e-2 and exact is not False and (ne is None or ne <= 5e-2))}

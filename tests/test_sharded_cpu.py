@@ -153,3 +153,19 @@ def test_plan_sharded_takes_the_slowest_rank_and_no_recompute():
     p, ms, _ = plan_sharded([0.3e-3], [0.6e-3], [0.1e-3], 32)
     assert p.l_re == 0 and p.l_h >= 24
     assert all(m != H.LayerMethod.RECOMPUTE for m in p.layer_assignment)
+
+
+def test_plan_sharded_with_replicated_recompute():
+    """With the whole block on every rank the RECOMPUTE prefix is available
+    at N > 1 (replicated: c_token is one rank's cost of a whole layer). A
+    7B-like balance at N=2 (io_h halved, c_h halved, c_token not) still
+    recomputes a prefix, fewer layers than at N=1; the plan is a function of
+    the maxima over ranks only."""
+    from paper_2410_05004_b200.sharded import plan_sharded
+    n1, _, _ = plan_sharded([0.61e-3], [1.21e-3], [0.2e-3], 32, 33, [1.25e-3])
+    n2, ms2, t2 = plan_sharded([0.305e-3, 0.3e-3], [0.6e-3, 0.6e-3], [0.1e-3, 0.11e-3], 32, 33,
+                               [1.25e-3, 1.3e-3])
+    assert t2.c_token == 1.3e-3 and t2.c_h == 0.11e-3
+    assert n1.l_re > n2.l_re > 0
+    p_none, ms_none, _ = plan_sharded([0.305e-3], [0.6e-3], [0.11e-3], 32, 33)
+    assert p_none.l_re == 0 and ms2 < ms_none

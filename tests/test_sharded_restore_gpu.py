@@ -187,3 +187,117 @@ def test_sharded_world_one_is_the_single_gpu_restore(cuda):
     torch.cuda.synchronize()
     for layer in range(L):
         assert torch.equal(kv.k[layer], ref.k[layer]) and torch.equal(kv.v[layer], ref.v[layer])
+
+
+def _worker_recompute(rank, world, port, n, q):
+    """A plan with a RECOMPUTE prefix at world > 1: every rank recomputes
+    layers [0, 2) for all heads from the session's token ids (replicated
+    prefix) and keeps its own heads; then one HIDDEN and one KV layer."""
+    try:
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        from test_recompute_gpu import dev_init_model
+        from paper_2410_05004_b200 import capi
+        from paper_2410_05004_b200 import hcache as H
+        LR, DFF, VOC = 4, 4 * D, 1024
+        hb, hc = H.shard_heads(HEADS, world, rank)
+        dh = D // HEADS
+        a, c = hb * dh, (hb + hc) * dh
+        kw = dict(n_layers=LR, d_hidden=D, n_heads=HEADS, d_ffn=DFF, vocab_size=VOC, max_seq=2048)
+        cfg = H.ModelConfig(**kw)
+        emb, layers = dev_init_model(LR, D, DFF, VOC, 17)
+        w = H.Weights(cfg, hb, hc)
+        w_all = H.Weights(cfg)
+        for ww in (w, w_all):
+            ww.set_embedding(emb)
+        for layer, lw in enumerate(layers):
+            wkv = lw["wkv"]
+            mine = torch.cat([wkv[a:c], wkv[D + a:D + c]]).contiguous()
+            w.set_layer_kv(layer, mine)
+            w.set_layer_full(layer, lw["wq"], wkv, lw["wo"], lw["fc1"], lw["fc2"])
+            w_all.set_layer_kv(layer, wkv)
+            w_all.set_layer_full(layer, lw["wq"], wkv, lw["wo"], lw["fc1"], lw["fc2"])
+            lw["mine"] = mine
+        tokens = [(i * 11 + 1) % VOC for i in range(n)]
+        n_pages = (n + 63) // 64
+        table = torch.randperm(n_pages, generator=torch.Generator().manual_seed(3)).to(
+            torch.int32).cuda()
+        hid = {2: _hidden(2, n, False)}
+        b, e = H.shard_range(n, world, rank)
+        plan = H.RestorationPlan.make_mixed(2, 1, 1)  # RE RE H KV
+        store = H.StorageManager(H.DevicePool(2))
+        store.create_session(H.SessionSeed("s", cfg.hash(), LR, D, 2, plan, tokens, d_kv=w.d_kv))
+        if e > b:
+            assert store.snapshot("s", 2, H.StateKind.HIDDEN, hid[2][b:e].contiguous(),
+                                  tok_begin=b)
+        k3, v3 = H.project_hidden_to_kv(w, 3, _hidden(3, n, False), 0)
+        kv3 = torch.cat([k3, v3], 1).contiguous()
+        assert store.snapshot("s", 3, H.StateKind.KV, kv3)
+        store.finalize("s")
+        rows_max = max(H.shard_range(n, world, r)[1] - H.shard_range(n, world, r)[0]
+                       for r in range(world))
+        g = H.PeerGroup(world, rank, D, rows_max, depth=LR,
+                        exchange=H.PeerGroup.torch_exchange())
+        kv = H.KvCache(LR, n_pages, 64, w.d_kv)
+        for it in range(2):
+            tl = H.restore_sharded(g, store, "s", w, plan, H.ThrottleConfig(), kv, table,
+                                   timeline=(it == 1))
+        torch.cuda.synchronize()
+        assert sum(ev.kind == "recompute" for ev in tl.events) == 2, [ev.kind for ev in tl.events]
+        # reference: single-process prefill of all heads, this rank's columns
+        full = H.KvCache(LR, n_pages, 64, D)
+        s = torch.cuda.current_stream().cuda_stream
+        tok = torch.tensor(tokens, dtype=torch.int32, device="cuda")
+        capi.check(capi.lib().hc_prefill_layers(w_all._h, tok.data_ptr(), n, 0, 2,
+                                                C.byref(full.desc), table.data_ptr(), s))
+        ref = H.KvCache(LR, n_pages, 64, w.d_kv)
+        capi.check(capi.lib().hc_project_to_pages(w._h, 2, hid[2].data_ptr(), n, None, 1,
+                                                  C.byref(ref.desc), table.data_ptr(), 0, s))
+        torch.cuda.synchronize()
+        exact = {}
+        for layer in (0, 1):
+            fk, fv = full.gather(layer, table, n)
+            k, v = kv.gather(layer, table, n)
+            exact[layer] = bool(torch.equal(k, fk[:, a:c]) and torch.equal(v, fv[:, a:c]))
+        k, v = kv.gather(2, table, n)
+        rk, rv = ref.gather(2, table, n)
+        exact[2] = bool(torch.equal(k, rk) and torch.equal(v, rv))
+        k, v = kv.gather(3, table, n)
+        exact[3] = bool(torch.equal(torch.cat([k, v], 1), kv3))
+        dist.barrier()
+        g.close()
+        dist.barrier()
+        q.put((rank, exact, None, None))
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put((rank, None, None, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,n", [(2, 640), (4, 1000)])
+def test_sharded_restore_recompute_prefix(cuda, world, n):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_recompute, args=(r, world, port, n, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = []
+    try:
+        for _ in range(world):
+            res.append(q.get(timeout=300))
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for rank, exact, _, err in res:
+        assert err is None, err
+        assert all(exact.values()), (rank, exact)
