@@ -9,6 +9,10 @@
 #include <algorithm>
 #include <vector>
 
+namespace hc {
+bool pdl_enabled() { return false; }  // (defined in k1_restore_kv.cu in the library)
+}
+
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 4096, heads = 32, dh = 128;
   const size_t sz = size_t(n) * heads * dh * 2;
