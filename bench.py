@@ -449,8 +449,9 @@ def run_ours(args, cfg, rank, world):
     # pinned-host chunk store: the sessions (saved from the device, D2H)
     store = H.StorageManager(H.DevicePool(1), buffer_capacity_bytes=4 << 30)
     kv_rows = {}  # the [K|V] rows stored for the plan's KV-offload layers (parity)
+    kv_rows_all = {}  # ... and for the all-KV session's (the strict plan's parity)
 
-    def save(sid, p, keep=False):
+    def save(sid, p, keep=None):
         store.create_session(H.SessionSeed(sid, mc.hash(), L, d, 2, p, tokens, d_kv=d_kv))
         for layer, m in enumerate(p.layer_assignment):
             if m == H.LayerMethod.HIDDEN:
@@ -460,8 +461,8 @@ def run_ours(args, cfg, rank, world):
                 k_, v_ = kv.gather(layer, table, n)
                 rows = torch.cat([k_, v_], 1).contiguous()
                 kind = H.StateKind.KV
-                if keep:
-                    kv_rows[layer] = rows
+                if keep is not None:
+                    keep[layer] = rows
             else:
                 continue
             while not store.snapshot(sid, layer, kind, rows):
@@ -573,10 +574,10 @@ def run_ours(args, cfg, rank, world):
     if full and os.environ.get("HC_SPLIT") == "1":
         split, split_ms = H.plan_token_split(prof, plan, n, layer_bytes=n * d * 2)
     opts_plan = capi.RestoreOptsC(0, 0, split)
-    save(b"hcache".decode(), plan, keep=True)
+    save(b"hcache".decode(), plan, keep=kv_rows)
     if plan.serialize() != all_h.serialize():
         save("all_hidden", all_h)
-    save("kv_offload", all_kv)
+    save("kv_offload", all_kv, keep=kv_rows_all)
     sid_plan = b"hcache"
     sid_allh = b"hcache" if plan.serialize() == all_h.serialize() else b"all_hidden"
 
@@ -632,6 +633,17 @@ def run_ours(args, cfg, rank, world):
         restore_step(b"kv_offload", all_kv)
     ms_allh = timed(lambda: restore_step(sid_allh, all_h), max(3, args.steps // 2))
     ms_kv = timed(lambda: restore_step(b"kv_offload", all_kv), max(3, args.steps // 2))
+    torch.cuda.synchronize()
+    # the strict plan: every layer restored within the north-star elementwise
+    # bound (no RECOMPUTE layer, whose stated tolerance is normwise); the
+    # faster of all-hidden and all-KV, checked like the headline plan
+    strict_sid, strict_plan, strict_ms = ((sid_allh, all_h, ms_allh) if ms_allh <= ms_kv
+                                          else (b"kv_offload", all_kv, ms_kv))
+    restore_step(strict_sid, strict_plan)
+    torch.cuda.synchronize()
+    strict_par = verify_restore(kv, table, strict_plan, cfg, tokens, 0,
+                                kv_rows if strict_sid == sid_plan else kv_rows_all)
+    e2e_step()  # the cache holds the headline plan's restore again
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     restore_step(sid_plan, plan, opts_plan)
@@ -709,6 +721,14 @@ def run_ours(args, cfg, rank, world):
                     "predicted_ms": plan_ms * 1e3 if plan_ms else None,
                     "predicted_with_split_ms": split_ms * 1e3 if split_ms else None},
         "parity": parity,
+        "strict_plan": {
+            "plan": strict_plan.serialize(), "restore_ms": strict_ms,
+            "value": n / (strict_ms * 1e-3), "unit": "tokens/s",
+            "hidden_max_rel": strict_par["hidden_max_rel"],
+            "kv_bitexact": strict_par["kv_bitexact"], "ok": strict_par["ok"],
+            "note": "every layer within the north-star max relative error 1e-2 (no "
+                    "recomputed layer); the headline plan trades that for its recompute "
+                    "prefix's stated normwise tolerance"},
         "e2e": {"value": n / (ms_e2e * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h_bytes_plan,
                 "d2h_bytes_per_step": int(host_ck.numel() * 2)},
         "path_roofline": {
@@ -890,13 +910,20 @@ def run_ours_batch(args, cfg, rank, world):
         store = save(p)
         for _ in range(2):
             restore_step(store)
-        t0 = time.perf_counter()
         with ClockSampler(dev) as clk:
             ms = timed(lambda: restore_step(store), steps)
-        wall = (time.perf_counter() - t0) * 1e3 / steps
+        # the public call as a user sees it: per step the batch restore, the
+        # D2H read of its result and a stream sync, host clock (mean)
+        walls = []
+        for _ in range(steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            restore_step(store)
+            torch.cuda.synchronize()
+            walls.append((time.perf_counter() - t0) * 1e3)
         tl = H.restore_batch(store, sids, w, H.ThrottleConfig(0, True), kv, tables).timeline
         store.close()
-        return ms, wall, clk.summary(), tl
+        return ms, float(np.mean(walls)), clk.summary(), tl
     ms_e2e, wall_e2e, clocks, tl = leg(plan, args.steps)
     ms_allh = ms_e2e if plan.serialize() == all_h.serialize() else \
         leg(all_h, max(3, args.steps // 2))[0]
@@ -926,7 +953,8 @@ def run_ours_batch(args, cfg, rank, world):
         "config": dict(workload_config(args, cfg), sessions=S, tokens=total,
                        max_session_tokens=max(lens)),
         "measures": "value: hc_restore_batch of the 32 planned sessions from the pinned-host "
-                    "store (H2D inside), device time; e2e: the same with host wall clock; "
+                    "store (H2D inside), steps back to back, device time; e2e: the same public "
+                    "call per step with a D2H read of its result and a stream sync, host clock; "
                     "resident: hidden states already in HBM (K1 only)",
         "restore_latency_ms": {"restore": ms_e2e, "e2e": wall_e2e, "resident": ms_resident,
                                "all_hidden": ms_allh, "kv_offload": ms_kv, "recompute": ms_re},
