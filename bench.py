@@ -609,6 +609,19 @@ def run_ours(args, cfg, rank, world):
             out.append((time.perf_counter() - t) * 1e3)
         return float(np.mean(out)), float(np.median(out))
 
+    # the dominant kernel (K1) timed alone, before the timed legs heat the
+    # part into its power cap: 20 launches back to back on its stream, best of
+    # three (against the burst peak, which MEASURED_PEAKS takes the same way)
+    torch.cuda.synchronize()
+    time.sleep(2.0)
+    k1_alone = []
+    for _ in range(3):
+        a_ms, b_ms = C.c_double(), C.c_double()
+        check(lib().hc_bench_project(w._h, L - 1, hid[L - 1].data_ptr(), n, 20, stream,
+                                     C.byref(a_ms), C.byref(b_ms)))
+        k1_alone.append(b_ms.value)
+    k1_alone_ms = min(k1_alone)
+
     for _ in range(args.warmup):
         resident_step()
         e2e_step()
@@ -660,7 +673,8 @@ def run_ours(args, cfg, rank, world):
                                  C.byref(stats_ms), C.byref(k1_ms)))
     flop = 4.0 * n * d * d_kv
     pk = peaks()
-    k1_tflops = flop / (k1_ms.value * 1e-3) / 1e12
+    k1_tflops = flop / (k1_alone_ms * 1e-3) / 1e12
+    k1_capped_tflops = flop / (k1_ms.value * 1e-3) / 1e12
     h2d = H.measure_h2d(256 << 20, 5, dev)
 
     # restore timeline of one e2e step (fill / bubble / lane busy)
@@ -743,11 +757,18 @@ def run_ours(args, cfg, rank, world):
         "roofline": {"bound": "tensor", "kernel": "k1_restore_kv", "achieved": k1_tflops,
                      "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                      "frac": k1_tflops / pk["bf16_tflops"],
-                     "frac_of_sustained": k1_tflops / pk.get("bf16_tflops_sustained",
-                                                             pk["bf16_tflops"]),
+                     "peak_kind": "burst (K1 timed alone: 20 launches back to back on its "
+                                  "stream, CUDA events, best of 3, after a 2 s rest -- the "
+                                  "way MEASURED_PEAKS takes the burst peak)",
                      "peak_source": pk["_source"], "traffic": traffic,
                      "traffic_source": traffic_src,
-                     "flop_per_launch": flop, "k1_ms": k1_ms.value,
+                     "flop_per_launch": flop, "k1_ms": k1_alone_ms,
+                     "power_capped": {"k1_ms": k1_ms.value, "achieved": k1_capped_tflops,
+                                      "frac_of_sustained": k1_capped_tflops / pk.get(
+                                          "bf16_tflops_sustained", pk["bf16_tflops"]),
+                                      "how": "the same 20 launches after the timed legs, at "
+                                             "the sw_power_cap clock, against the sustained "
+                                             "peak"},
                      "row_stats_ms": stats_ms.value},
         "timeline": {"total_ms": tl.total_s * 1e3, "fill_ms": tl.fill_s * 1e3,
                      "io_busy_ms": tl.lane_busy(H.Lane.IO) * 1e3,
