@@ -391,7 +391,12 @@ typedef struct hc_restore_opts {
    * with the prefix and only tokens [split_tokens, n) are fetched and
    * projected (hc_plan_token_split picks the value that balances the lanes). */
   int32_t split_tokens;
-  int32_t pad_;
+  /* hc_restore_sharded only: 0 = K1 reads every owner's staging slot in
+   * place over NVLink (the all-gather fused into the GEMM); 1 = the owners'
+   * ranges are first gathered by the copy engines into a local buffer (the
+   * all-gather-then-GEMM baseline; also taken automatically for a layer whose
+   * peer slots the driver cannot describe with a TMA tensor map). */
+  int32_t peer_gather;
 } hc_restore_opts;
 
 /* restore (restore.hpp:40-42): executes the plan over a finalized session

@@ -505,6 +505,8 @@ inline std::pair<Matrix, Matrix> split_kv(const Matrix& rows) {
 struct ThrottleConfig {
   int prefetch_depth = 0;  // 0 = auto (stage every hidden layer within 8 GiB)
   bool timeline = true;
+  int split_tokens = 0;    // B200 extension (hc_restore_opts.split_tokens)
+  int peer_gather = 0;     // restore_sharded: 0 fused peer-memory K1, 1 copy-engine gather
 };
 
 struct RestoreResult {
@@ -528,7 +530,8 @@ inline RestoreResult restore(StorageManager& store, const std::string& session_i
                              const DeviceWeights& w, const RestorationPlan& plan,
                              const ThrottleConfig& throttle, const KvPages& pages,
                              const int32_t* d_page_table, void* stream = nullptr) {
-  hc_restore_opts o{throttle.prefetch_depth, throttle.timeline ? 1 : 0, 0, 0};
+  hc_restore_opts o{throttle.prefetch_depth, throttle.timeline ? 1 : 0, throttle.split_tokens,
+                    0};
   std::vector<hc_timeline> tl(1);
   check(hc_restore(store.get(), session_id.c_str(), w.get(), &plan.raw, &o, &pages.desc,
                    d_page_table, stream, throttle.timeline ? tl.data() : nullptr));
@@ -583,7 +586,7 @@ inline RestoreResult restore_sharded(PeerGroup& group, StorageManager& store,
                                      const RestorationPlan& plan, const ThrottleConfig& throttle,
                                      const KvPages& pages, const int32_t* d_page_table,
                                      void* stream = nullptr) {
-  hc_restore_opts o{throttle.prefetch_depth, throttle.timeline ? 1 : 0, 0, 0};
+  hc_restore_opts o{throttle.prefetch_depth, throttle.timeline ? 1 : 0, 0, throttle.peer_gather};
   std::vector<hc_timeline> tl(1);
   check(hc_restore_sharded(group.get(), store.get(), session_id.c_str(), w.get(), &plan.raw, &o,
                            &pages.desc, d_page_table, stream,

@@ -88,7 +88,8 @@ class ManifestC(C.Structure):
 
 
 class RestoreOptsC(C.Structure):
-    _fields_ = [("prefetch_depth", i32), ("timeline", i32), ("split_tokens", i32), ("pad_", i32)]
+    _fields_ = [("prefetch_depth", i32), ("timeline", i32), ("split_tokens", i32),
+                ("peer_gather", i32)]
 
 
 class RequestC(C.Structure):

@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -219,6 +220,16 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
   HC_CUDA(cudaStreamWaitEvent(eng.aux, t0, 0));
   std::vector<cudaEvent_t> joins, consumed_kv(size_t(nbuf_kv), nullptr);
   const uint32_t abox = uint32_t(gemm_a_box(n));
+  // opts->peer_gather == 1 (or HC_SHARDED_GATHER=copy): gather every
+  // owner's range with the copy engines into a local buffer and run K1 over
+  // it (the all-gather-then-GEMM baseline); default: K1 reads the owners'
+  // slots in place (fused)
+  static const bool copy_gather_env = [] {
+    const char* e = getenv("HC_SHARDED_GATHER");
+    return e && std::string(e) == "copy";
+  }();
+  const bool copy_gather = copy_gather_env || (opts && opts->peer_gather == 1);
+  std::unique_ptr<StreamScratch> gathered;  // [n x d], allocated on first use
 
   // Replicated RECOMPUTE prefix on the compute lane (restore.cpp:177-182):
   // the IO lane fetches the hidden layers' ranges meanwhile, as far as the
@@ -302,21 +313,45 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
       StatSources ss;
       ss.n = 0;
       int64_t max_range = 0;
+      bool fused = !copy_gather;
+      for (int r = 0; r < W && fused; ++r) {
+        const int64_t rows = r0[size_t(r) + 1] - r0[size_t(r)];
+        if (rows == 0) continue;
+        // a tensor map over another GPU's slot; should the driver refuse it,
+        // this layer falls back to the copy-engine gather below
+        fused = make_tmap_kmajor_cached(&am.m[am.n], g->slot_data(r, slot), uint64_t(d),
+                                        uint64_t(rows), uint64_t(d) * 2, abox);
+        am.row0[am.n] = int(r0[size_t(r)]);
+        ++am.n;
+      }
+      if (!fused) {
+        // all-gather by the copy engines over NVLink into a local [n x d]
+        // buffer, then K1 over it (one map): the non-fused baseline, and the
+        // fallback where TMA cannot address peer memory
+        if (!gathered) gathered.reset(new StreamScratch(size_t(n) * size_t(d) * 2, stream));
+        char* gbuf = static_cast<char*>(gathered->ptr);
+        for (int r = 0; r < W; ++r) {
+          const int64_t rows = r0[size_t(r) + 1] - r0[size_t(r)];
+          if (rows > 0)
+            HC_CUDA(cudaMemcpyAsync(gbuf + size_t(r0[size_t(r)]) * size_t(d) * 2,
+                                    g->slot_data(r, slot), size_t(rows) * size_t(d) * 2,
+                                    cudaMemcpyDefault, stream));
+        }
+        CUtensorMap gm;
+        if (!make_tmap_kmajor_cached(&gm, gbuf, uint64_t(d), uint64_t(n), uint64_t(d) * 2, abox))
+          fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the gathered hidden rows");
+        am = single_amap(gm);
+      }
       for (int r = 0; r < W; ++r) {
         const int64_t rows = r0[size_t(r) + 1] - r0[size_t(r)];
         if (rows == 0) continue;
-        if (!make_tmap_kmajor_cached(&am.m[am.n], g->slot_data(r, slot), uint64_t(d),
-                                     uint64_t(rows), uint64_t(d) * 2, abox))
-          fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for a peer slot");
-        am.row0[am.n] = int(r0[size_t(r)]);
-        ++am.n;
         ss.mean[ss.n] = g->slot_mean(r, slot);
         ss.rstd[ss.n] = g->slot_rstd(r, slot);
         ss.row0[ss.n] = r0[size_t(r)];
         ++ss.n;
         max_range = std::max(max_range, rows);
       }
-      am.row0[am.n] = 0x7fffffff;
+      if (fused) am.row0[am.n] = 0x7fffffff;
       ss.row0[ss.n] = n;
       if (norm) HC_CUDA(launch_gather_stats(ss, max_range, mean, rstd, stream));
       const int bn = gemm_pick_bn(n, N, sms);

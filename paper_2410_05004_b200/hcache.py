@@ -690,9 +690,11 @@ class ThrottleConfig:
     prefetch_depth: int = 0
     timeline: bool = True
     split_tokens: int = 0  # B200 extension (hc_restore_opts.split_tokens)
+    peer_gather: int = 0   # restore_sharded: 0 fused peer-memory K1, 1 copy-engine gather
 
     def _c(self):
-        return capi.RestoreOptsC(self.prefetch_depth, int(self.timeline), self.split_tokens)
+        return capi.RestoreOptsC(self.prefetch_depth, int(self.timeline), self.split_tokens,
+                                 self.peer_gather)
 
 
 @dataclass

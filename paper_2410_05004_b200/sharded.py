@@ -294,17 +294,19 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     throttle = H.ThrottleConfig(0, False)
     host_ck = torch.empty(16 * w.d_kv, dtype=torch.bfloat16, pin_memory=True)
 
-    def step(sid):
-        H.restore_sharded(group, store, sid, w, sids[sid], throttle, kv, table, stream)
+    throttle_copy = H.ThrottleConfig(0, False, 0, 1)  # copy-engine gather, then K1
+
+    def step(sid, thr=None):
+        H.restore_sharded(group, store, sid, w, sids[sid], thr or throttle, kv, table, stream)
         host_ck.copy_(kv.k[L - 1].view(-1)[: 16 * w.d_kv], non_blocking=True)
 
-    def timed(sid, steps):
+    def timed(sid, steps, thr=None):
         dist.barrier()
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         for _ in range(steps):
-            step(sid)
+            step(sid, thr)
         ev1.record()
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1) / steps
@@ -337,6 +339,12 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     legs = {}
     for sid in ("all_hidden", "kv_offload"):
         legs[sid] = timed(sid, max(3, args.steps // 2)) if sid in sids else ms
+    # the all-gather-then-GEMM baseline of the fused peer-memory K1: the same
+    # plan with every owner's range gathered by the copy engines first
+    legs["copy_gather"] = None
+    if plan.l_h:
+        step("hcache", throttle_copy)
+        legs["copy_gather"] = timed("hcache", max(3, args.steps // 2), throttle_copy)
     # parity of this rank's heads after one more restore of the plan
     step("hcache")
     torch.cuda.synchronize()
@@ -374,10 +382,14 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                         "H2D inside), steps back to back, CUDA events, max over ranks; e2e: per "
                         "step the call + a D2H read + sync, host clock, max over ranks",
             "restore_latency_ms": {"restore": ms, "e2e": ms_e2e, "all_hidden": legs["all_hidden"],
-                                   "kv_offload": legs["kv_offload"], "timeline_total": tl_total},
+                                   "kv_offload": legs["kv_offload"],
+                                   "copy_gather": legs["copy_gather"],
+                                   "timeline_total": tl_total},
             "speedup": {"hcache_vs_kv_offload": legs["kv_offload"] / ms,
                         "hcache_vs_all_hidden": legs["all_hidden"] / ms,
-                        "hcache_vs_recompute": None},
+                        "hcache_vs_recompute": None,
+                        "fused_vs_copy_gather": (legs["copy_gather"] / ms
+                                                 if legs["copy_gather"] else None)},
             "planner": {"plan": plan.serialize(),
                         "per_rank_ms": {"io_h": io_h * 1e3, "io_kv": io_kv * 1e3,
                                         "c_h": c_h * 1e3,

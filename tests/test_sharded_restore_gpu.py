@@ -44,9 +44,12 @@ def _hidden(layer, n, large_mean):
     return h
 
 
-def _worker(rank, world, port, n, large_mean, q):
+def _worker(rank, world, port, n, large_mean, q, gather=None):
     try:
         import ctypes as C
+        import os
+        if gather:  # read once by the library, before the first restore
+            os.environ["HC_SHARDED_GATHER"] = gather
 
         import torch
         import torch.distributed as dist
@@ -125,12 +128,12 @@ def _worker(rank, world, port, n, large_mean, q):
         q.put((rank, None, None, traceback.format_exc()))
 
 
-def _run(world, n, large_mean=False):
+def _run(world, n, large_mean=False, gather=None):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, large_mean, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, large_mean, q, gather))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -151,6 +154,14 @@ def _run(world, n, large_mean=False):
 @pytest.mark.parametrize("world,n", [(2, 700), (2, 1024), (4, 1000)])
 def test_sharded_restore_bit_exact(cuda, world, n):
     for rank, exact, _, _ in _run(world, n):
+        assert all(exact.values()), (rank, exact)
+
+
+def test_sharded_restore_copy_gather_fallback(cuda):
+    """HC_SHARDED_GATHER=copy: the owners' ranges gathered by the copy
+    engines into a local buffer, then K1 over it (the path taken where TMA
+    cannot address a peer's memory) -- the same bits as the fused K1."""
+    for rank, exact, _, _ in _run(2, 1024, gather="copy"):
         assert all(exact.values()), (rank, exact)
 
 
