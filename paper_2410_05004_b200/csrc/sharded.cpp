@@ -130,6 +130,7 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
     return;
   }
   if (!g->imported) bad("peer group not imported (hc_peer_group_import)");
+  if (opts && opts->split_tokens) bad("split_tokens is not supported at world > 1");
   if (w->device != g->device) bad("weights and peer group on different devices");
   Store& store = st->impl;
   const std::string sid(sid_c);
