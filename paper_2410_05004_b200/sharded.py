@@ -290,6 +290,10 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     if plan.serialize() != all_kv.serialize():
         save("kv_offload", all_kv)
         sids["kv_offload"] = all_kv
+    all_re = H.RestorationPlan.make(L, 0, H.Complement.RECOMPUTE)
+    if full:  # the recompute baseline: every layer recomputed on every rank
+        save("recompute", all_re)
+        sids["recompute"] = all_re
     torch.cuda.synchronize()
     throttle = H.ThrottleConfig(0, False)
     host_ck = torch.empty(16 * w.d_kv, dtype=torch.bfloat16, pin_memory=True)
@@ -339,6 +343,10 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     legs = {}
     for sid in ("all_hidden", "kv_offload"):
         legs[sid] = timed(sid, max(3, args.steps // 2)) if sid in sids else ms
+    legs["recompute"] = None
+    if "recompute" in sids:
+        step("recompute")
+        legs["recompute"] = timed("recompute", 3)
     # the all-gather-then-GEMM baseline of the fused peer-memory K1: the same
     # plan with every owner's range gathered by the copy engines first
     legs["copy_gather"] = None
@@ -383,11 +391,15 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                         "step the call + a D2H read + sync, host clock, max over ranks",
             "restore_latency_ms": {"restore": ms, "e2e": ms_e2e, "all_hidden": legs["all_hidden"],
                                    "kv_offload": legs["kv_offload"],
+                                   "recompute": legs["recompute"],
                                    "copy_gather": legs["copy_gather"],
                                    "timeline_total": tl_total},
             "speedup": {"hcache_vs_kv_offload": legs["kv_offload"] / ms,
                         "hcache_vs_all_hidden": legs["all_hidden"] / ms,
-                        "hcache_vs_recompute": None,
+                        "hcache_vs_recompute": (legs["recompute"] / ms
+                                                if legs["recompute"] else None),
+                        "recompute_note": "the recompute path at N ranks is replicated (every "
+                                          "rank runs every layer for all heads)",
                         "fused_vs_copy_gather": (legs["copy_gather"] / ms
                                                  if legs["copy_gather"] else None)},
             "planner": {"plan": plan.serialize(),
