@@ -445,6 +445,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 // ============================================================================
 constexpr int kFaM = 128;       // rows per Q tile (two per CTA)
 constexpr int kFaThreads = 576;  // TMA, MMA, 8 softmax warps per Q tile (two threads per row)
+// ROWS variant: TMA, MMA, 4 softmax warps per Q tile, one thread per query row
+// holding its 128 scores in registers (one TMEM pass over S, no max exchange)
+constexpr int kFaRowsThreads = 320;
+template <bool ROWS>
+constexpr int fa_threads() { return ROWS ? kFaRowsThreads : kFaThreads; }
 #ifndef HC_FA_EMU
 #define HC_FA_EMU 0
 #endif
@@ -560,8 +565,8 @@ __device__ unsigned long long* g_fa_cta;
   } while (0)
 #endif
 
-template <int DH>
-__global__ void __launch_bounds__(kFaThreads, 1)
+template <int DH, bool ROWS>
+__global__ void __launch_bounds__(fa_threads<ROWS>(), 1)
     attn_fa_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK2,
                    const __grid_constant__ CUtensorMap tmV2, AttnArgs a) {
@@ -629,8 +634,9 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[2 * s], 8);  // the tile's 8 softmax warps, per 32-key chunk
-      mbar_init(&p_full[2 * s + 1], 8);
+      // the tile's softmax warps (8, or 4 in the ROWS variant), per P chunk
+      mbar_init(&p_full[2 * s], ROWS ? 4 : 8);
+      mbar_init(&p_full[2 * s + 1], ROWS ? 4 : 8);
       mbar_init(&o_done[s], 1);
     }
     mbar_init(v_fix, 1);
@@ -754,9 +760,11 @@ __global__ void __launch_bounds__(kFaThreads, 1)
           for (int u = 0; u < 4; ++u) {
             // P of keys 16kk..: key half kk/4 wrote its 32 columns at the
             // start of its own 64-column S half, chunk c in columns 16c..
-            const int kk = (u >> 1) * 4 + c * 2 + (u & 1);
-            umma_f16_ts(tmem + 256 + uint32_t(t * 128),
-                        tmem + uint32_t(t * 128 + (kk >> 2) * 64 + (kk & 3) * 8),
+            // (ROWS: one thread per row wrote keys 0..127 to columns 0..63,
+            // chunk c = keys 64c..64c+63)
+            const int kk = ROWS ? c * 4 + u : (u >> 1) * 4 + c * 2 + (u & 1);
+            const int pcol = ROWS ? kk * 8 : (kk >> 2) * 64 + (kk & 3) * 8;
+            umma_f16_ts(tmem + 256 + uint32_t(t * 128), tmem + uint32_t(t * 128 + pcol),
                         v + uint64_t(kk * (2048 >> 4)), id_pv, (j | kk) != 0 ? 1u : 0u);
           }
           if (c == 1) {
@@ -776,6 +784,121 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       }
       issue_pv(1, j);
       if (j + 1 < nt_b) issue_qk(1, j + 1);
+    }
+  } else if (ROWS) {
+    // ------------------------------------------------------------ softmax (ROWS)
+    // warps 2-5 own Q tile A, 6-9 tile B; a thread owns one query row: its
+    // 128 scores come out of TMEM once, the row max needs no exchange, and
+    // the bf16 P of keys 0..127 goes to columns 0..63 of its S row (the
+    // scores are in registers by then). P is published in two 64-key chunks.
+    const int t = (warp - 2) >> 2;
+    const int qd = warp & 3;  // TMEM lane quadrant (warp % 4)
+    const int rloc = qd * 32 + lane;
+    const int row = q0 + t * kFaM + rloc;
+    const int nt = t == 0 ? nt_a : nt_b;
+    const int row_lim = min(row, a.n - 1);
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + uint32_t(t * 128);
+    const uint32_t t_o = tmem + lane_off + 256u + uint32_t(t * 128);
+    float m_run = -INFINITY, l_run = 0.f;
+    const uint64_t sc2 = f2_pack(a.scale_log2, a.scale_log2);
+    for (int j = 0; j < nt; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      if (rloc == 0) FA_TRACE(2, t, j);
+      const int key0 = j * kAttnN;
+      const bool diag = __any_sync(0xffffffffu, key0 + kAttnN - 1 > row_lim);
+      const int lim = row_lim - key0;
+      uint32_t v[128];
+      tmem_ld_32x32b_x32(t_s + 0u, *reinterpret_cast<uint32_t(*)[32]>(v + 0));
+      tmem_ld_32x32b_x32(t_s + 32u, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      tmem_ld_32x32b_x32(t_s + 64u, *reinterpret_cast<uint32_t(*)[32]>(v + 64));
+      tmem_ld_32x32b_x32(t_s + 96u, *reinterpret_cast<uint32_t(*)[32]>(v + 96));
+      tmem_wait_ld();
+      if (diag) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i > lim) v[i] = __float_as_uint(-INFINITY);
+      }
+      if (rloc == 0) FA_TRACE(6, t, j);
+      float m8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = __uint_as_float(v[u]);
+#pragma unroll
+      for (int i = 8; i < 128; i += 16)
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          m8[u] = fmaxf(m8[u], fmaxf(__uint_as_float(v[i + u]),
+                                     __uint_as_float(v[(i + 8 + u) & 127])));
+      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * a.scale_log2;
+      // lazy max: keep m_run unless the tile max exceeds it by > 8 (P <= 2^8)
+      const bool resc = mx > m_run + 8.0f;
+      const float m_use = resc ? mx : m_run;
+      if (rloc == 0) FA_TRACE(7, t, j);
+      if (__any_sync(0xffffffffu, resc)) {
+        const float corr = resc ? ex2_approx(m_run - m_use) : 1.0f;
+        l_run *= corr;
+        if (j > 0) {
+          mbar_wait(&o_done[t], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(t_o + uint32_t(c * 32), o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+            tmem_st_32x32b_x32(t_o + uint32_t(c * 32), o);
+          }
+        }
+        m_run = m_use;
+      }
+      const uint64_t nm2 = f2_pack(-m_use, -m_use);
+      uint64_t sum2 = 0, sum2b = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // 32 keys -> 16 packed columns at a time
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint64_t x = f2_fma(uint64_t(v[32 * c + 2 * i]) |
+                                        (uint64_t(v[32 * c + 2 * i + 1]) << 32),
+                                    sc2, nm2);
+          const uint64_t pv = f2_pack(ex2_approx(f2_lo(x)), ex2_approx(f2_hi(x)));
+          if (i & 1) sum2b = f2_add(sum2b, pv);
+          else sum2 = f2_add(sum2, pv);
+          pk[i] = pack_bf16x2(f2_lo(pv), f2_hi(pv));
+        }
+        tmem_st_32x32b_x16(t_s + uint32_t(c * 16), pk);
+        if (c & 1) {  // keys 64(c/2)..: publish the chunk
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[2 * t + (c >> 1)]);
+        }
+      }
+      sum2 = f2_add(sum2, sum2b);
+      if (rloc == 0) FA_TRACE(3, t, j);
+      l_run += f2_lo(sum2) + f2_hi(sum2);
+    }
+    mbar_wait(&o_done[t], (nt - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.0f / l_run;
+    __nv_bfloat16* dst = a.out + size_t(row0 + row) * size_t(a.n_heads * DH) + size_t(h) * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(t_o + uint32_t(c * 32), o);
+      tmem_wait_ld();
+      if (row < a.n) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          d4[i] = make_uint4(pack_bf16x2(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
+                             pack_bf16x2(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
+                             pack_bf16x2(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
+                             pack_bf16x2(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
+      }
     }
   } else {
     // ------------------------------------------------------------ softmax
@@ -994,8 +1117,11 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(AttnCfg<DH>::kSmem));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_fa_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(FaCfg<DH>::kSmem));
+      e = cudaFuncSetAttribute(attn_fa_kernel<DH, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(FaCfg<DH>::kSmem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_fa_kernel<DH, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(FaCfg<DH>::kSmem));
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
@@ -1012,8 +1138,16 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
     const double kv_bytes = double(n) * double(n_kv_heads) * DH * 2 * 2;  // n = total rows
     a.rank_major = kv_bytes <= 80.0 * (1 << 20);
     const dim3 grid = a.rank_major ? dim3(n_heads, n_seqs, pairs) : dim3(pairs, n_heads, n_seqs);
-    return launch_pdl(attn_fa_kernel<DH>, grid, dim3(kFaThreads), FaCfg<DH>::kSmem, stream, tq,
-                      tk, tv, tk2, tv2, a);
+    // HC_FA_ROWS=1: one softmax thread per query row (ROWS variant)
+    static const bool rows = [] {
+      const char* e = getenv("HC_FA_ROWS");
+      return e && atoi(e) != 0;
+    }();
+    if (rows)
+      return launch_pdl(attn_fa_kernel<DH, true>, grid, dim3(kFaRowsThreads), FaCfg<DH>::kSmem,
+                        stream, tq, tk, tv, tk2, tv2, a);
+    return launch_pdl(attn_fa_kernel<DH, false>, grid, dim3(kFaThreads), FaCfg<DH>::kSmem, stream,
+                      tq, tk, tv, tk2, tv2, a);
   } else {
     const dim3 grid((n + kAttnM - 1) / kAttnM, n_heads);
     attn_tc_kernel<DH><<<grid, kAttnThreads, AttnCfg<DH>::kSmem, stream>>>(tq, tk, tv, tk2, tv2, a);

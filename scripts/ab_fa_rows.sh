@@ -1,0 +1,8 @@
+# attention: two threads per row (default) vs one thread per row (HC_FA_ROWS=1)
+for i in 1 2 3; do
+  echo "pair: $(REPS=50 timeout 120 python scripts/attn_probe.py 4096 2>&1 | tail -1)"
+  echo "rows: $(HC_FA_ROWS=1 REPS=50 timeout 120 python scripts/attn_probe.py 4096 2>&1 | tail -1)"
+done
+echo "rows 16K: $(HC_FA_ROWS=1 REPS=5 timeout 120 python scripts/attn_probe.py 16384 2>&1 | tail -1)"
+echo "pair 16K: $(REPS=5 timeout 120 python scripts/attn_probe.py 16384 2>&1 | tail -1)"
+HC_FA_ROWS=1 timeout 600 python -m pytest tests/test_k6_blocks_gpu.py tests/test_stale_pages_gpu.py tests/test_recompute_gpu.py -q -x -m gpu 2>&1 | tail -3
