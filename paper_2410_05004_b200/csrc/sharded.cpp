@@ -242,14 +242,19 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
       re_table(n_re ? sizeof(int32_t) * size_t(re_pages) : 0, stream),
       re_k(n_re ? size_t(re_pages) * 64 * size_t(w->d_kv_all) * 2 : 0, stream),
       re_v(n_re ? size_t(re_pages) * 64 * size_t(w->d_kv_all) * 2 : 0, stream);
-  if (n_re) {
+  bool prefix_done = n_re == 0;
+  std::vector<cudaEvent_t> marks;
+  std::vector<void*> kp(size_t(w->cfg.n_layers), re_k.ptr), vp(size_t(w->cfg.n_layers), re_v.ptr);
+  // enqueued once the first layer's fetch is on the IO lane, so the link
+  // starts while the host enqueues the prefix
+  auto run_prefix = [&] {
+    if (prefix_done) return;
+    prefix_done = true;
     HC_CUDA(cudaMemcpyAsync(re_tok.ptr, host_tokens, sizeof(int32_t) * size_t(n),
                             cudaMemcpyHostToDevice, stream));
     HC_CUDA(launch_iota_i32(static_cast<int32_t*>(re_table.ptr), re_pages, stream));
-    std::vector<void*> kp(size_t(w->cfg.n_layers), re_k.ptr), vp(size_t(w->cfg.n_layers), re_v.ptr);
     const hc_kv_pages scratch{w->cfg.n_layers, 64, int32_t(re_pages), w->d_kv_all, HC_DTYPE_BF16,
                               kp.data(), vp.data()};
-    std::vector<cudaEvent_t> marks;
     auto hook = [&](int layer, bool start) {
       if (start) {
         if (timed) {
@@ -269,7 +274,7 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
     prefill_layers_impl(w, static_cast<const int32_t*>(re_tok.ptr), n, 0, n_re, &scratch,
                         static_cast<const int32_t*>(re_table.ptr), stream, hook, nullptr, nullptr,
                         0, true);
-  }
+  };
   int ikv = 0;
   for (size_t i = 0; i < order.size(); ++i) {
     const auto& j = order[i];
@@ -305,6 +310,7 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
         }
       }
       HC_CUDA(launch_signal_flags(g->d_ready + size_t(slot) * size_t(W), W, ep, eng.aux));
+      run_prefix();  // (first layer only)
       // compute lane: every owner's range of this layer is in place
       for (int r = 0; r < W; ++r) HC_CUDA(wait_flag_geq(stream, g->my_flag(0, r, slot), ep));
       cudaEvent_t cs = timed ? evp.get() : nullptr;
@@ -377,6 +383,7 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
     cudaEvent_t fetched = evp.get();
     HC_CUDA(cudaEventRecord(fetched, eng.copy));
     if (timed) ops.push_back({HC_LANE_IO, j.layer, HC_EV_FETCH_KV, fs, fetched});
+    run_prefix();  // (first layer only)
     HC_CUDA(cudaStreamWaitEvent(stream, fetched, 0));
     cudaEvent_t cs = timed ? evp.get() : nullptr;
     if (cs) HC_CUDA(cudaEventRecord(cs, stream));
@@ -387,6 +394,7 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
     consumed_kv[size_t(slot)] = done;
     if (timed) ops.push_back({HC_LANE_COMPUTE, j.layer, HC_EV_SCATTER, cs, done});
   }
+  run_prefix();  // an all-RECOMPUTE plan
   // join the owner lane and the IO lane into the caller stream
   for (cudaStream_t lane : {eng.aux, eng.copy}) {
     cudaEvent_t e = evp.get();
