@@ -5,6 +5,7 @@
 #include <initializer_list>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3 (no-op unless a profiler injects)
 
 #include <atomic>
 #include <cstdint>
@@ -31,6 +32,15 @@ inline void check_cuda(cudaError_t e, const char* what) {
 
 void set_last_error(const std::string& m);
 void clear_last_error();
+
+// NVTX range over a public entry point (host enqueue span in nsys / ncu
+// timelines; the device-side lanes are in the CUDA-event Timeline).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Runs fn, mapping exceptions to hc_status + hc_last_error().
 template <typename F>

@@ -487,6 +487,7 @@ hc_status hc_prefill_layers(const hc_weights* w, const int32_t* d_tokens, int64_
                             int32_t layer_begin, int32_t layer_end, const hc_kv_pages* pages,
                             const int32_t* d_page_table, void* stream) {
   return guard([&] {
+    NvtxRange r("hc_prefill_layers");
     // prefill_layers (model.cpp:349-356) discards the last block's output:
     // only the K/V of its last layer are observable
     prefill_layers_impl(w, d_tokens, n, layer_begin, layer_end, pages, d_page_table,
@@ -572,6 +573,7 @@ hc_status hc_prefill(const hc_weights* w, const int32_t* d_tokens, int64_t n,
                      const hc_kv_pages* pages, const int32_t* d_page_table, void* d_layer_inputs,
                      int32_t* next_token, void* stream) {
   return guard([&] {
+    NvtxRange r("hc_prefill");
     if (!w) fail(HC_EINVAL, "prefill: null weights");
     prefill_layers_impl(w, d_tokens, n, 0, w->cfg.n_layers, pages, d_page_table,
                         as_stream(stream), [](int, bool) {}, d_layer_inputs, next_token);

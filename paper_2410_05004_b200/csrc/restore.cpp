@@ -674,6 +674,7 @@ hc_status hc_restore(hc_store* s, const char* sid, const hc_weights* w, const hc
                      const hc_restore_opts* opts, const hc_kv_pages* pages,
                      const int32_t* d_page_table, void* stream, hc_timeline* timeline) {
   return guard([&] {
+    NvtxRange r("hc_restore");
     restore_session(s, sid, w, plan, opts, pages, d_page_table, as_stream(stream), timeline);
   });
 }
@@ -683,6 +684,7 @@ hc_status hc_restore_batch(hc_store* s, const char* const* sids, int32_t n_sessi
                            const hc_kv_pages* pages, const int32_t* d_page_tables,
                            int32_t table_stride, void* stream, hc_timeline* timeline) {
   return guard([&] {
+    NvtxRange r("hc_restore_batch");
     restore_batch(s, sids, n_sessions, w, opts, pages, d_page_tables, table_stride,
                   as_stream(stream), timeline);
   });

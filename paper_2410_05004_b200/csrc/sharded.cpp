@@ -554,6 +554,7 @@ hc_status hc_restore_sharded(hc_peer_group* g, hc_store* s, const char* sid,
                              const hc_restore_opts* opts, const hc_kv_pages* pages,
                              const int32_t* d_page_table, void* stream, hc_timeline* timeline) {
   return guard([&] {
+    NvtxRange r("hc_restore_sharded");
     restore_sharded(g, s, sid, w, plan, opts, pages, d_page_table, as_stream(stream), timeline);
   });
 }

@@ -690,6 +690,7 @@ hc_status hc_store_snapshot(hc_store* s, const char* sid, int32_t layer, int32_t
                             int32_t src_dtype, int32_t src_on_device, void* stream) {
   hc_status st = HC_OK;
   hc_status g = guard([&] {
+    NvtxRange r("hc_store_snapshot");
     if (!S(s).snapshot(SID(sid), layer, kind, rows, n_rows, row_width, src_dtype,
                        src_on_device != 0, as_stream(stream)))
       st = HC_EAGAIN;
