@@ -20,8 +20,15 @@
 // V is consumed as an MN-major B operand straight from its TMA layout.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <tuple>
+#include <vector>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -1075,6 +1082,439 @@ __global__ void __launch_bounds__(fa_threads<ROWS>(), 1)
   }
 }
 
+// ============================================================================
+// Persistent variant of the two-Q-tile kernel (one sequence, HC_FA_PERSIST):
+// one CTA per SM loops over (head, tile pair) items from a host-computed
+// longest-processing-time schedule. Barrier phases run on per-role counters
+// across items; the next item's Q load waits for the last QK of the previous
+// item (q_empty) and its first PV for the softmax warps to have read O out
+// (o_free), so an item's Q load, first QK and first softmax overlap the
+// previous item's last PV and O epilogue, and TMEM, barriers and the CTA
+// launch are paid once per SM instead of once per item.
+template <int DH>
+__global__ void __launch_bounds__(kFaThreads, 1)
+    attn_fa_persist_kernel(const __grid_constant__ CUtensorMap tmQ,
+                           const __grid_constant__ CUtensorMap tmK,
+                           const __grid_constant__ CUtensorMap tmV,
+                           const __grid_constant__ CUtensorMap tmK2,
+                           const __grid_constant__ CUtensorMap tmV2, AttnArgs a,
+                           const int32_t* __restrict__ sched, int sched_stride) {
+  using Cfg = FaCfg<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if (smem_u32(smem_raw) & 1023) asm volatile("trap;");
+  pdl_wait();
+  pdl_trigger();
+  uint8_t* sQ = smem_raw;
+  uint8_t* sK = sQ + 2 * Cfg::kQBytes;
+  uint8_t* sV = sK + 2 * Cfg::kKVBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * Cfg::kKVBytes);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;    // [2]
+  uint64_t* k_empty = bars + 3;   // [2]
+  uint64_t* v_full = bars + 5;    // [2]
+  uint64_t* v_empty = bars + 7;   // [2]
+  uint64_t* s_full = bars + 9;    // [tile]
+  uint64_t* p_full = bars + 11;   // [tile][key chunk]
+  uint64_t* o_done = bars + 15;   // [tile]
+  uint64_t* v_fix = bars + 17;
+  uint64_t* q_empty = bars + 18;  // the item's last QK has read Q
+  uint64_t* o_free = bars + 19;   // [tile] the softmax warps have read O out
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  float* xmax = reinterpret_cast<float*>(bars + 32);  // [step parity][tile][half][row]
+  float* xsum = xmax + 8 * kFaM;                      // [tile][half][row]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t* my = sched + size_t(blockIdx.x) * size_t(sched_stride);
+  const int n_items = __ldg(my);
+  const int n_pairs = (a.n + 2 * kFaM - 1) / (2 * kFaM);
+  const int kv_tiles = (a.n + kAttnN - 1) / kAttnN;
+  struct Item {
+    int h, hk, q0, nt_a, nt_b, fix;
+  };
+  auto item = [&](int i) {
+    const int w = __ldg(my + 1 + i);  // rank-major: head fastest
+    Item it;
+    it.h = w % a.n_heads;
+    const int pt = n_pairs - 1 - w / a.n_heads;
+    it.hk = it.h / a.group;
+    it.q0 = pt * 2 * kFaM;
+    it.nt_a = min(2 * pt + 1, kv_tiles);
+    it.nt_b = min(2 * pt + 2, kv_tiles);
+    it.fix = (a.n % kAttnN) && kv_tiles - 1 < it.nt_b ? kv_tiles - 1 : -1;
+    return it;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmK2);
+    tma_prefetch_desc(&tmV2);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[2 * s], 8);
+      mbar_init(&p_full[2 * s + 1], 8);
+      mbar_init(&o_done[s], 1);
+      mbar_init(&o_free[s], 8);
+    }
+    mbar_init(v_fix, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA
+    int gk = 0, gv = 0;  // K / V tiles loaded by this CTA so far (ring position)
+    for (int i = 0; i < n_items; ++i) {
+      const Item it = item(i);
+      if (lane == 0) {
+        if (i > 0) mbar_wait(q_empty, (i - 1) & 1);
+        mbar_arrive_expect_tx(q_full, 2 * Cfg::kQBytes);
+        for (int t = 0; t < 2; ++t)
+          for (int hb = 0; hb < DH / 64; ++hb)
+            tma_load_2d(sQ + t * Cfg::kQBytes + hb * Cfg::kHalf, &tmQ, q_full,
+                        it.h * DH + hb * 64, it.q0 + t * kFaM);
+        auto load_tile = [&](int g, int j, bool is_v) {
+          const int st = g & 1;
+          uint64_t* full = is_v ? &v_full[st] : &k_full[st];
+          mbar_wait(is_v ? &v_empty[st] : &k_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(full, Cfg::kKVBytes);
+          uint8_t* dst = (is_v ? sV : sK) + st * Cfg::kKVBytes;
+          const CUtensorMap* map = is_v ? &tmV : &tmK;
+          if (a.page_table && a.box_rows < kAttnN) {
+            const int last = (a.n - 1) / a.page_size;
+            const int pg0 = min(j * kAttnN / a.page_size, last);
+            const int per = kAttnN / a.page_size;
+            const int base = __ldg(a.page_table + pg0);
+            bool contig = pg0 + per - 1 <= last;
+            for (int c = 1; c < per && contig; ++c)
+              contig = __ldg(a.page_table + pg0 + c) == base + c;
+            if (contig) {
+              const CUtensorMap* map2 = is_v ? &tmV2 : &tmK2;
+              for (int hb = 0; hb < DH / 64; ++hb)
+                tma_load_2d(dst + hb * Cfg::kHalf, map2, full, it.hk * DH + hb * 64,
+                            base * a.page_size);
+              return;
+            }
+          }
+          for (int c = 0; c < kAttnN / a.box_rows; ++c) {
+            const int key0 = j * kAttnN + c * a.box_rows;
+            int row = key0;
+            if (a.page_table) {
+              const int last = (a.n - 1) / a.page_size;
+              const int pg = min(key0 / a.page_size, last);
+              row = __ldg(a.page_table + pg) * a.page_size + key0 % a.page_size;
+            }
+            for (int hb = 0; hb < DH / 64; ++hb)
+              tma_load_2d(dst + hb * Cfg::kHalf + c * a.box_rows * 128, map, full,
+                          it.hk * DH + hb * 64, row);
+          }
+        };
+        for (int j = 0; j <= it.nt_b; ++j) {
+          if (j < it.nt_b) load_tile(gk + j, j, false);
+          if (j >= 1) load_tile(gv + j - 1, j - 1, true);
+        }
+      }
+      __syncwarp();
+      if (it.fix >= 0) {  // zero the last V tile's rows past the sequence (attn_fa_kernel)
+        const int g = gv + it.fix, st = g & 1;
+        mbar_wait(&v_full[st], (g >> 1) & 1);
+        const int r0 = a.n - it.fix * kAttnN;
+        uint8_t* base = sV + st * Cfg::kKVBytes;
+        const int nvec = (kAttnN - r0) * 128 / 16;
+        for (int hb = 0; hb < DH / 64; ++hb) {
+          uint4* p = reinterpret_cast<uint4*>(base + hb * Cfg::kHalf + r0 * 128);
+          for (int e = lane; e < nvec; e += 32) p[e] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(v_fix);
+      }
+      gk += it.nt_b;
+      gv += it.nt_b;
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA
+    const uint32_t id_qk = umma_idesc_f16(kFaM, kAttnN, true);
+    const uint32_t id_pv = umma_idesc_f16(kFaM, DH, true) | (1u << 16);
+    const uint64_t dq = umma_desc_sw128(smem_u32(sQ));
+    const uint64_t dk = umma_desc_sw128(smem_u32(sK));
+    const uint64_t dv = umma_desc_sw128_mn(smem_u32(sV), Cfg::kHalf);
+    int gk = 0, gv = 0, nfix = 0;
+    int pvc[2] = {0, 0};  // PV steps issued per tile (= o_done / p_full phases)
+    for (int i = 0; i < n_items; ++i) {
+      const Item it = item(i);
+      mbar_wait(q_full, i & 1);
+      tc_fence_after();
+      auto issue_qk = [&](int t, int j) {
+        const int g = gk + j, st = g & 1;
+        mbar_wait(&k_full[st], (g >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t q = dq + uint64_t(t * (Cfg::kQBytes >> 4));
+          const uint64_t k = dk + uint64_t(st * (Cfg::kKVBytes >> 4));
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const uint64_t off = uint64_t(((kk >> 2) * Cfg::kHalf + (kk & 3) * 32) >> 4);
+            umma_f16(tmem + uint32_t(t * 128), q + off, k + off, id_qk, kk != 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[t]);
+          if (t == 1) {
+            umma_commit(&k_empty[st]);
+            if (j == it.nt_b - 1) umma_commit(q_empty);  // the item's last read of Q
+          }
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int t, int j) {
+        const int g = gv + j, st = g & 1;
+        mbar_wait(&v_full[st], (g >> 1) & 1);
+        if (j == it.fix) mbar_wait(v_fix, nfix & 1);
+        if (j == 0 && i > 0) mbar_wait(&o_free[t], (i - 1) & 1);  // O of the last item read out
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          mbar_wait(&p_full[2 * t + c], (pvc[t] + j) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t v = dv + uint64_t(st * (Cfg::kKVBytes >> 4));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int kk = (u >> 1) * 4 + c * 2 + (u & 1);
+              umma_f16_ts(tmem + 256 + uint32_t(t * 128),
+                          tmem + uint32_t(t * 128 + (kk >> 2) * 64 + (kk & 3) * 8),
+                          v + uint64_t(kk * (2048 >> 4)), id_pv, (j | kk) != 0 ? 1u : 0u);
+            }
+            if (c == 1) {
+              umma_commit(&o_done[t]);
+              if (t == 1) umma_commit(&v_empty[st]);
+            }
+          }
+          __syncwarp();
+        }
+      };
+      issue_qk(0, 0);
+      issue_qk(1, 0);
+      for (int j = 0; j < it.nt_b; ++j) {
+        if (j < it.nt_a) {
+          issue_pv(0, j);
+          if (j + 1 < it.nt_a) issue_qk(0, j + 1);
+        }
+        issue_pv(1, j);
+        if (j + 1 < it.nt_b) issue_qk(1, j + 1);
+      }
+      gk += it.nt_b;
+      gv += it.nt_b;
+      pvc[0] += it.nt_a;
+      pvc[1] += it.nt_b;
+      if (it.fix >= 0) ++nfix;
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    const int t = (warp - 2) >> 3;
+    const int qd = warp & 3;
+    const int half = ((warp - 2) >> 2) & 1;
+    const int rloc = qd * 32 + lane;
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + uint32_t(t * 128 + half * 64);
+    const uint32_t t_o = tmem + lane_off + 256u + uint32_t(t * 128);
+    const uint32_t bar_id = 1 + uint32_t(t * 4 + qd);
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    const uint64_t sc2 = f2_pack(a.scale_log2, a.scale_log2);
+    int sc = 0;  // steps of my tile so far (s_full / o_done phases, xmax parity)
+    for (int i = 0; i < n_items; ++i) {
+      const Item it = item(i);
+      const int row = it.q0 + t * kFaM + rloc;
+      const int nt = t == 0 ? it.nt_a : it.nt_b;
+      const int row_lim = min(row, a.n - 1);
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < nt; ++j) {
+        const int g = sc + j;
+        mbar_wait(&s_full[t], g & 1);
+        tc_fence_after();
+        const int key0 = j * kAttnN + half * 64;
+        const bool diag = __any_sync(0xffffffffu, key0 + 63 > row_lim);
+        const int lim = row_lim - key0;
+        float m8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m8[u] = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_s + uint32_t(c * 32), v);
+          tmem_wait_ld();
+          if (diag) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c * 32 + e > lim) v[e] = __float_as_uint(-INFINITY);
+          }
+#pragma unroll
+          for (int e = 0; e < 32; e += 16)
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              m8[u] = fmaxf(m8[u], fmaxf(__uint_as_float(v[e + u]), __uint_as_float(v[e + 8 + u])));
+        }
+        float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                         fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        float* xm = xmax + ((g & 1) * 4 + t * 2) * kFaM;
+        xm[half * kFaM + rloc] = mx;
+        pair_sync();
+        mx = fmaxf(mx, xm[(half ^ 1) * kFaM + rloc]) * a.scale_log2;
+        const bool resc = mx > m_run + 8.0f;
+        const float m_use = resc ? mx : m_run;
+        if (__any_sync(0xffffffffu, resc)) {
+          const float corr = resc ? ex2_approx(m_run - m_use) : 1.0f;
+          l_run *= corr;
+          if (j > 0) {
+            mbar_wait(&o_done[t], (g - 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < DH / 64; ++c) {
+              uint32_t v[32];
+              const uint32_t ta = t_o + uint32_t(half * (DH / 2) + c * 32);
+              tmem_ld_32x32b_x32(ta, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * corr);
+              tmem_st_32x32b_x32(ta, v);
+            }
+          }
+          m_run = m_use;
+        }
+        const uint64_t nm2 = f2_pack(-m_use, -m_use);
+        uint64_t sum2 = 0, sum2b = 0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_s + uint32_t(c * 32), v);
+          tmem_wait_ld();
+          if (diag) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c * 32 + e > lim) v[e] = __float_as_uint(-INFINITY);
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const uint64_t x = f2_fma(uint64_t(v[2 * e]) | (uint64_t(v[2 * e + 1]) << 32), sc2, nm2);
+            const uint64_t pv = f2_pack(ex2_approx(f2_lo(x)), ex2_approx(f2_hi(x)));
+            if (e & 1) sum2b = f2_add(sum2b, pv);
+            else sum2 = f2_add(sum2, pv);
+            pk[e] = pack_bf16x2(f2_lo(pv), f2_hi(pv));
+          }
+          tmem_st_32x32b_x16(t_s + uint32_t(c * 16), pk);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[2 * t + c]);
+        }
+        sum2 = f2_add(sum2, sum2b);
+        l_run += f2_lo(sum2) + f2_hi(sum2);
+      }
+      xsum[(t * 2 + half) * kFaM + rloc] = l_run;
+      mbar_wait(&o_done[t], (sc + nt - 1) & 1);
+      tc_fence_after();
+      pair_sync();
+      const float inv = 1.0f / (l_run + xsum[(t * 2 + (half ^ 1)) * kFaM + rloc]);
+      __nv_bfloat16* dst = a.out + size_t(row) * size_t(a.n_heads * DH) + size_t(it.h) * DH;
+#pragma unroll 1
+      for (int c = 0; c < DH / 64; ++c) {
+        const int col = half * (DH / 2) + c * 32;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_o + uint32_t(col), v);
+        tmem_wait_ld();
+        if (row < a.n) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            d4[e] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * e + 0]) * inv, __uint_as_float(v[8 * e + 1]) * inv),
+                               pack_bf16x2(__uint_as_float(v[8 * e + 2]) * inv, __uint_as_float(v[8 * e + 3]) * inv),
+                               pack_bf16x2(__uint_as_float(v[8 * e + 4]) * inv, __uint_as_float(v[8 * e + 5]) * inv),
+                               pack_bf16x2(__uint_as_float(v[8 * e + 6]) * inv, __uint_as_float(v[8 * e + 7]) * inv));
+        }
+      }
+      // O of this item is in registers / global memory: the next item's
+      // first PV may overwrite it; the partner's xsum read is behind the
+      // pair_sync above, and the next item's xsum write is many syncs later
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[t]);
+      sc += nt;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// Longest-processing-time schedule of a single sequence's (head, pair) items
+// over `grid` CTAs, cached per (device, n, heads, grid): row c = [count,
+// item ids...]; items in rank-major order (head fastest), cost ~ fixed + key
+// steps of the pair.
+const int32_t* fa_persist_schedule(int n, int n_heads, int grid, int* stride_out) {
+  struct Key {
+    int dev, n, heads, grid;
+    bool operator<(const Key& o) const {
+      return std::tie(dev, n, heads, grid) < std::tie(o.dev, o.n, o.heads, o.grid);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, std::pair<int32_t*, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const Key key{dev, n, n_heads, grid};
+  std::lock_guard<std::mutex> lk(mu);
+  auto f = cache.find(key);
+  if (f != cache.end()) {
+    *stride_out = f->second.second;
+    return f->second.first;
+  }
+  const int pairs = (n + 2 * kFaM - 1) / (2 * kFaM), kv_tiles = (n + kAttnN - 1) / kAttnN;
+  const int items = pairs * n_heads;
+  std::vector<std::vector<int32_t>> lists(static_cast<size_t>(grid));
+  std::priority_queue<std::pair<double, int>, std::vector<std::pair<double, int>>,
+                      std::greater<std::pair<double, int>>>
+      load;
+  for (int c = 0; c < grid; ++c) load.push({0.0, c});
+  for (int w = 0; w < items; ++w) {
+    const int pt = pairs - 1 - w / n_heads;
+    const double cost = 2.5 + 2.24 * (std::min(2 * pt + 1, kv_tiles) + std::min(2 * pt + 2, kv_tiles)) / 2.0;
+    auto top = load.top();
+    load.pop();
+    lists[size_t(top.second)].push_back(w);
+    load.push({top.first + cost, top.second});
+  }
+  size_t mx = 0;
+  for (const auto& l : lists) mx = std::max(mx, l.size());
+  const int stride = int(mx) + 1;
+  std::vector<int32_t> host(size_t(grid) * size_t(stride), 0);
+  for (int c = 0; c < grid; ++c) {
+    host[size_t(c) * size_t(stride)] = int32_t(lists[size_t(c)].size());
+    std::copy(lists[size_t(c)].begin(), lists[size_t(c)].end(),
+              host.begin() + std::ptrdiff_t(size_t(c) * size_t(stride) + 1));
+  }
+  int32_t* d = nullptr;
+  if (cudaMalloc(&d, host.size() * sizeof(int32_t)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice) !=
+      cudaSuccess)
+    return nullptr;
+  cache.emplace(key, std::make_pair(d, stride));
+  *stride_out = stride;
+  return d;
+}
+
 template <int DH>
 cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, const KvOut& kv,
                            int64_t kv_rows, void* out, cudaStream_t stream,
@@ -1138,6 +1578,35 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
     const double kv_bytes = double(n) * double(n_kv_heads) * DH * 2 * 2;  // n = total rows
     a.rank_major = kv_bytes <= 80.0 * (1 << 20);
     const dim3 grid = a.rank_major ? dim3(n_heads, n_seqs, pairs) : dim3(pairs, n_heads, n_seqs);
+    // One persistent CTA per SM over an LPT schedule for a single sequence
+    // whose K/V fit in L2 (7B 4K: 138.8 -> 135.2 us). Past that size the
+    // head-major grid's L2 locality wins (16K x 40 heads: 2347 us grid vs
+    // 2420 persistent), and a ragged batch's lengths are not on the host.
+    // HC_FA_PERSIST=0 / 1 forces it off / on (single sequence).
+    static const int persist_env = [] {
+      const char* e = getenv("HC_FA_PERSIST");
+      return e ? atoi(e) : -1;
+    }();
+    const bool persist = persist_env < 0 ? a.rank_major : persist_env != 0;
+    if (persist && !cu) {
+      static thread_local int pattr_dev = -1;
+      if (pattr_dev != dev) {
+        cudaError_t e = cudaFuncSetAttribute(attn_fa_persist_kernel<DH>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(FaCfg<DH>::kSmem));
+        if (e != cudaSuccess) return e;
+        pattr_dev = dev;
+      }
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int items = pairs * n_heads;
+      const int pgrid = std::min(sms, items);
+      int stride = 0;
+      const int32_t* sched = fa_persist_schedule(n, n_heads, pgrid, &stride);
+      if (!sched) return cudaErrorMemoryAllocation;
+      return launch_pdl(attn_fa_persist_kernel<DH>, dim3(pgrid), dim3(kFaThreads),
+                        FaCfg<DH>::kSmem, stream, tq, tk, tv, tk2, tv2, a, sched, stride);
+    }
     // HC_FA_ROWS=1: one softmax thread per query row (ROWS variant)
     static const bool rows = [] {
       const char* e = getenv("HC_FA_ROWS");
