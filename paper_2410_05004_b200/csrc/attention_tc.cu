@@ -1463,18 +1463,20 @@ __global__ void __launch_bounds__(kFaThreads, 1)
 // over `grid` CTAs, cached per (device, n, heads, grid): row c = [count,
 // item ids...]; items in rank-major order (head fastest), cost ~ fixed + key
 // steps of the pair.
-const int32_t* fa_persist_schedule(int n, int n_heads, int grid, int* stride_out) {
+const int32_t* fa_persist_schedule(int n, int n_heads, int grid, bool head_major,
+                                   int* stride_out) {
   struct Key {
     int dev, n, heads, grid;
+    bool hm;
     bool operator<(const Key& o) const {
-      return std::tie(dev, n, heads, grid) < std::tie(o.dev, o.n, o.heads, o.grid);
+      return std::tie(dev, n, heads, grid, hm) < std::tie(o.dev, o.n, o.heads, o.grid, o.hm);
     }
   };
   static std::mutex mu;
   static std::map<Key, std::pair<int32_t*, int>> cache;
   int dev = 0;
   cudaGetDevice(&dev);
-  const Key key{dev, n, n_heads, grid};
+  const Key key{dev, n, n_heads, grid, head_major};
   std::lock_guard<std::mutex> lk(mu);
   auto f = cache.find(key);
   if (f != cache.end()) {
@@ -1488,7 +1490,10 @@ const int32_t* fa_persist_schedule(int n, int n_heads, int grid, int* stride_out
                       std::greater<std::pair<double, int>>>
       load;
   for (int c = 0; c < grid; ++c) load.push({0.0, c});
-  for (int w = 0; w < items; ++w) {
+  // head_major: the items of one head (heaviest pair first) before the next
+  // head's, so the CTAs working at any moment share a few heads' K/V in L2
+  for (int o = 0; o < items; ++o) {
+    const int w = head_major ? (o % pairs) * n_heads + o / pairs : o;
     const int pt = pairs - 1 - w / n_heads;
     const double cost = 2.5 + 2.24 * (std::min(2 * pt + 1, kv_tiles) + std::min(2 * pt + 2, kv_tiles)) / 2.0;
     auto top = load.top();
@@ -1588,6 +1593,7 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
       return e ? atoi(e) : -1;
     }();
     const bool persist = persist_env < 0 ? a.rank_major : persist_env != 0;
+    // (HC_FA_PERSIST=2: persistent with the head-major item order as well)
     if (persist && !cu) {
       static thread_local int pattr_dev = -1;
       if (pattr_dev != dev) {
@@ -1602,7 +1608,8 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
       const int items = pairs * n_heads;
       const int pgrid = std::min(sms, items);
       int stride = 0;
-      const int32_t* sched = fa_persist_schedule(n, n_heads, pgrid, &stride);
+      const int32_t* sched = fa_persist_schedule(n, n_heads, pgrid,
+                                                 !a.rank_major && persist_env == 2, &stride);
       if (!sched) return cudaErrorMemoryAllocation;
       return launch_pdl(attn_fa_persist_kernel<DH>, dim3(pgrid), dim3(kFaThreads),
                         FaCfg<DH>::kSmem, stream, tq, tk, tv, tk2, tv2, a, sched, stride);
