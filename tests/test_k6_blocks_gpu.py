@@ -41,26 +41,33 @@ def test_attention_dense_vs_torch(cuda, n, heads, kvh, dh):
     assert err < 2e-2, err
 
 
-@pytest.mark.parametrize("n,heads", [(4096, 16), (4608, 40)])
-def test_attention_block_orders_vs_torch(cuda, n, heads):
-    """Both block orders of the two-tile kernel: rank-major (every head's
-    heaviest tile pair first; K/V of 4096 x 16 heads = 32 MB) and head-major
-    (K/V of 4608 x 40 heads = 94 MB > the 80 MB L2 budget)."""
+@pytest.mark.parametrize("n,heads,kvh", [(4096, 16, 16), (4608, 40, 40), (4133, 32, 32),
+                                         (4096, 32, 32), (4133, 32, 8)])
+def test_attention_block_orders_vs_torch(cuda, n, heads, kvh):
+    """The launch shapes of the two-tile kernel: the persistent CTAs for a
+    sequence whose K/V fit in L2 -- one item per CTA (4096 x 16 heads: 128
+    items), several per CTA (4096 x 32 heads = the 7B layer, 544 items at
+    4133 tokens, where every CTA's heaviest items also carry the partial
+    last key tile, and a GQA variant) -- and the head-major grid once K/V
+    outgrow the 80 MB L2 budget (4608 x 40 heads = 94 MB)."""
     import torch
     from paper_2410_05004_b200 import capi
     dh = 128
-    g = torch.Generator(device="cuda").manual_seed(n + heads)
+    g = torch.Generator(device="cuda").manual_seed(n + heads + kvh)
     q = torch.randn(n, heads * dh, device="cuda", generator=g).bfloat16()
-    k = torch.randn(n, heads * dh, device="cuda", generator=g).bfloat16()
-    v = torch.randn(n, heads * dh, device="cuda", generator=g).bfloat16()
+    k = torch.randn(n, kvh * dh, device="cuda", generator=g).bfloat16()
+    v = torch.randn(n, kvh * dh, device="cuda", generator=g).bfloat16()
     out = torch.empty(n, heads * dh, device="cuda", dtype=torch.bfloat16)
-    capi.check(capi.lib().hc_attention_dense(q.data_ptr(), n, heads, heads, dh, k.data_ptr(),
-                                             v.data_ptr(), heads * dh, out.data_ptr(),
+    capi.check(capi.lib().hc_attention_dense(q.data_ptr(), n, heads, kvh, dh, k.data_ptr(),
+                                             v.data_ptr(), kvh * dh, out.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
+    grp = heads // kvh
     for h0 in range(0, heads, 8):  # the fp32 reference eight heads at a time
         sl = slice(h0 * dh, (h0 + 8) * dh)
-        ref = _attn_ref(q[:, sl], k[:, sl], v[:, sl], 8, 8, dh)
+        kh0, kh1 = h0 // grp, (h0 + 8 + grp - 1) // grp
+        ksl = slice(kh0 * dh, kh1 * dh)
+        ref = _attn_ref(q[:, sl], k[:, ksl], v[:, ksl], 8, kh1 - kh0, dh)
         err = (out[:, sl].float() - ref).abs().max().item() / ref.abs().max().item()
         assert err < 2e-2, (h0, err)
 
