@@ -14,7 +14,7 @@ from test_recompute_gpu import build
 
 pytestmark = pytest.mark.gpu
 
-CFG = dict(n_layers=2, d_hidden=512, n_heads=8, d_ffn=1024, vocab_size=1024, max_seq=2048)
+CFG = dict(n_layers=2, d_hidden=512, n_heads=8, d_ffn=1024, vocab_size=1024, max_seq=8192)
 
 
 def _kv(H, cfg, w, n_pages, page, poison):
@@ -28,7 +28,9 @@ def _kv(H, cfg, w, n_pages, page, poison):
     return kv
 
 
-@pytest.mark.parametrize("n", [40, 100, 130, 200, 777])
+# (5000 tokens: 160 attention items over the persistent CTAs, several per CTA,
+# the heaviest ending in a partial key tile)
+@pytest.mark.parametrize("n", [40, 100, 130, 200, 777, 5000])
 def test_prefill_ignores_stale_page_rows(cuda, n):
     import torch
     from paper_2410_05004_b200 import hcache as H
