@@ -724,6 +724,8 @@ def run_ours(args, cfg, rank, world):
         recompute_step()
         ms_re = timed(recompute_step, max(3, args.steps // 2))
 
+    launches_restore = count_launches(e2e_step)
+    launches_resident = count_launches(resident_step)
     # dominant kernel (K1): per-launch times with events on its stream
     stats_ms, k1_ms = C.c_double(), C.c_double()
     check(lib().hc_bench_project(w._h, L - 1, hid[L - 1].data_ptr(), n, 20, stream,
@@ -833,14 +835,35 @@ def run_ours(args, cfg, rank, world):
                      "bubble_fraction": tl.bubble_fraction(),
                      "lane_busy": "union of each lane's event intervals"},
         # our kernels launched in the timed region: per headline step the
-        # planned restore's launches (recompute prefix + per hidden layer
-        # statistics / mean-shift check / K1, per KV layer the scatter)
-        "gpu_launches": 2 * args.steps * restore_launches(plan) + args.steps * 3 * L,
+        # planned restore's launches (counted from a CUPTI trace of one step),
+        # 2 x steps restores (back to back + synchronous) and steps resident
+        # steps
+        "gpu_launches": args.steps * (2 * launches_restore + launches_resident),
+        "gpu_launches_per_step": {"restore": launches_restore, "resident": launches_resident,
+                                  "how": "CUPTI kernel records (torch.profiler) of one call, "
+                                         "kernels in namespace hc::"},
         "clocks": clocks,
     }
     if cpu_tok_s is not None:
         line["cpu_baseline"] = dict(cpu_desc, value=cpu_tok_s, unit="tokens/s")
     print(json.dumps(line), flush=True)
+
+
+def count_launches(fn):
+    """Kernel launches of ours (namespace hc::) one call of fn makes, from a
+    CUPTI activity trace (torch.profiler) -- the per-step count behind the
+    bench line's gpu_launches."""
+    import warnings
+
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    warnings.filterwarnings("ignore", message=".*Profiler clears events.*")
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    return sum(1 for e in prof.events()
+               if e.device_type.name == "CUDA" and "hc::" in e.name and "Memcpy" not in e.name)
 
 
 def restore_launches(plan):
@@ -985,6 +1008,7 @@ def run_ours_batch(args, cfg, rank, world):
         read_back()
 
     parity = {}
+    launches = {}
 
     def leg(p, steps, check=False):
         store = save(p)
@@ -993,7 +1017,7 @@ def run_ours_batch(args, cfg, rank, world):
         with ClockSampler(dev) as clk:
             ms = timed(lambda: restore_step(store), steps)
         if check:  # the restored cache of the benchmarked plan vs the oracle
-            restore_step(store)
+            launches["restore"] = count_launches(lambda: restore_step(store))
             torch.cuda.synchronize()
             parity.update(verify_batch(kv, tables, p, cfg, lens, tokens))
         # the public call as a user sees it: per step the batch restore, the
@@ -1112,7 +1136,8 @@ def run_ours_batch(args, cfg, rank, world):
                      "compute_busy_ms": tl.lane_busy(H.Lane.COMPUTE) * 1e3,
                      "bubble_fraction": tl.bubble_fraction(),
                      "lane_busy": "union of each lane's event intervals"},
-        "gpu_launches": args.steps * restore_launches(plan),
+        # the batch restores of the timed region (back to back + synchronous)
+        "gpu_launches": 2 * args.steps * launches.get("restore", restore_launches(plan)),
         "clocks": clocks,
     }
     if cpu_tok_s is not None:
