@@ -353,6 +353,9 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
     if plan.l_h:
         step("hcache", throttle_copy)
         legs["copy_gather"] = timed("hcache", max(3, args.steps // 2), throttle_copy)
+    from bench import count_launches
+    n_launch = count_launches(lambda: step("hcache"))
+    n_launch = int(max_over_ranks(n_launch))
     # parity of this rank's heads after one more restore of the plan
     step("hcache")
     torch.cuda.synchronize()
@@ -431,12 +434,10 @@ def bench(args, cfg, rank, world, dev, clock_sampler=None, peaks=None):
                          "achieved": k1_tflops, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                          "frac": k1_tflops / pk["bf16_tflops"], "peak_source": pk["_source"],
                          "traffic": None, "flop_per_launch": flop, "k1_ms": c_h * 1e3},
-            # per step and rank: per HIDDEN layer statistics, mean-shift check,
-            # two flag signals, statistics gather and K1; per KV layer the
-            # scatter; per RECOMPUTE layer ~12 (stats, centering, GEMMs,
-            # attention, head slice)
-            "gpu_launches": 2 * args.steps * world * (plan.l_h * 6 + plan.l_kv +
-                                                      12 * (L - plan.l_h - plan.l_kv)),
+            # our kernels in the timed region: every rank's restores (back to
+            # back + synchronous), counted from a CUPTI trace of one step
+            "gpu_launches": 2 * args.steps * world * n_launch,
+            "gpu_launches_per_step_and_rank": n_launch,
             "clocks": clocks,
         }
         if not args.no_cpu_baseline:
