@@ -87,7 +87,8 @@ CUtensorMap weight_map(const hc_weights::Layer& L, int bn, int d, int rows) {
   if (bn == 256) return L.tm256;
   if (bn == 128) return L.tm128;
   CUtensorMap m;
-  if (!make_tmap_kmajor(&m, L.wkv, uint64_t(d), uint64_t(rows), uint64_t(d) * 2, uint32_t(bn)))
+  if (!make_tmap_kmajor_cached(&m, L.wkv, uint64_t(d), uint64_t(rows), uint64_t(d) * 2,
+                               uint32_t(bn)))
     fail(HC_ECUDA, "cuTensorMapEncodeTiled failed for the weight operand");
   return m;
 }

@@ -630,13 +630,12 @@ __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) 
 // float offset of 16-byte unit u (0..3) of transposed row r
 __device__ __forceinline__ int tunit(int r, int u) { return r * 16 + ((u ^ ((r >> 1) & 3)) << 2); }
 
-template <int MODE>
+template <int MODE, int BN>
 __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n_blk, int M, int N,
                                                    const KvOut& out, const GemmOut& gout,
                                                    const EpiArgs& epi, uint32_t tbase, float* ws,
                                                    int half, float* tbuf, EpiRow* meta,
                                                    int c_begin, int c_end) {
-  constexpr int BN = 256;
   if (half != 0) {
     const int row = row_base + lane;
     EpiRow e{0.f, 1.f, 0, 0, nullptr, nullptr};
@@ -784,7 +783,7 @@ constexpr int kPairTraceSlots = 40;
   } while (0)
 #endif
 
-template <int MODE>
+template <int MODE, int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ AMaps am,
                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
@@ -792,7 +791,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                         int32_t* tail_flags, uint32_t epoch) {
   // M: rows stored; Ms >= M: rows the schedule is laid out for (units whose
   // tile starts at or past M are skipped by every role)
-  constexpr int BN = 256, S = kPairStages;
+  // BN = 256 or 192 output columns per pair tile; each CTA stages BN/2 B rows
+  constexpr int S = kPairStages;
+  constexpr uint32_t kBHalf = uint32_t(BN / 2) * kBK * 2;
+  static_assert(BN == 256 || BN == 192, "pair tile width");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem;
@@ -854,12 +856,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           if (m_blk * 256 >= M) continue;
           for (int kb = pu.kb0; kb < pu.kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kPairHalfBytes + kBHalf));
             int a_row;
             const CUtensorMap* ma = amap(am, m_blk * 256 + int(rank) * 128, a_row, kAlt);
             tma_load_2d_pair(sA + stage * kPairHalfBytes, ma, &full[stage], kb * kBK, a_row);
             tma_load_2d_pair(sB + stage * kPairHalfBytes, &tmB, &full[stage], kb * kBK,
-                             n_blk * BN + int(rank) * 128);
+                             n_blk * BN + int(rank) * (BN / 2));
             if (++stage == S) {
               stage = 0;
               phase ^= 1;
@@ -919,7 +921,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     // ---------------- epilogue (both CTAs, their own 128 TMEM lanes) --------
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int ew = warp - 2, n_epi = 32 * kPairEpiWarps;
-    constexpr int kChunksPerWarp = 8 / (kPairEpiWarps / 4);
+    constexpr int kChunksPerWarp = (BN / 32) / (kPairEpiWarps / 4);
     const int c_begin = (ew / 4) * kChunksPerWarp, c_end = c_begin + kChunksPerWarp;
     const bool lead = ew == 0 && lane == 0;
     int acc = 0;
@@ -950,7 +952,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         epi_bar_sync(n_epi);
       }
       uint8_t* my = epi_smem + size_t(ew) * kPairEpiWarpBytes;
-      epilogue_tile_pair<MODE>(row_base, lane, n_blk, M, N, out, gout, epi,
+      epilogue_tile_pair<MODE, BN>(row_base, lane, n_blk, M, N, out, gout, epi,
                                tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN), ws,
                                pu.half, reinterpret_cast<float*>(my),
                                reinterpret_cast<EpiRow*>(my + 32 * 16 * 4), c_begin, c_end);
@@ -1265,12 +1267,12 @@ cudaError_t tail_ws_for(int dev, cudaStream_t stream, int slots, TailWs** out) {
   return cudaSuccess;
 }
 
-template <int MODE>
-cudaError_t launch_pair(const AMaps& tmA, const CUtensorMap& tmB128, int M, int N, int K,
-                        bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
-                        int num_sms, cudaStream_t stream, int Ms, bool split_acc) {
-  const uint32_t idesc = umma_idesc_f16(256, 256, bf16_in);
-  const int tiles = ((Ms + 255) / 256) * ((N + 255) / 256);
+template <int MODE, int BN>
+cudaError_t launch_pair_bn(const AMaps& tmA, const CUtensorMap& tmB128, int M, int N, int K,
+                           bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
+                           int num_sms, cudaStream_t stream, int Ms, bool split_acc) {
+  const uint32_t idesc = umma_idesc_f16(256, BN, bf16_in);
+  const int tiles = ((Ms + 255) / 256) * ((N + BN - 1) / BN);
   int grid = 2 * (tiles < num_sms / 2 ? tiles : num_sms / 2);
   // tail split (summation order may change: split_acc callers only)
   static const bool tail_enabled = [] {
@@ -1297,14 +1299,27 @@ cudaError_t launch_pair(const AMaps& tmA, const CUtensorMap& tmB128, int M, int 
   }
   static thread_local int attr_dev = -1;
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_pair_kernel<MODE>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_pair_kernel<MODE, BN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(kPairSmem));
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  return launch_pdl(tc_gemm_pair_kernel<MODE>, dim3(grid), dim3(kPairThreads), kPairSmem, stream,
-                    tmA, tmB128, M, N, K, out, g, epi, idesc, Ms, ws, flags, epoch);
+  return launch_pdl(tc_gemm_pair_kernel<MODE, BN>, dim3(grid), dim3(kPairThreads), kPairSmem,
+                    stream, tmA, tmB128, M, N, K, out, g, epi, idesc, Ms, ws, flags, epoch);
+}
+
+// bn = the B box rows the caller's tensor map has: 128 -> 256-column pair
+// tiles, 96 -> 192-column pair tiles (gemm_pick_bn)
+template <int MODE>
+cudaError_t launch_pair(int bn, const AMaps& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                        bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
+                        int num_sms, cudaStream_t stream, int Ms, bool split_acc) {
+  if (bn == 96)
+    return launch_pair_bn<MODE, 192>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, Ms,
+                                     split_acc);
+  return launch_pair_bn<MODE, 256>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, Ms,
+                                   split_acc);
 }
 
 // Pair kernel when the problem has enough 256x256 tiles to fill the SM pairs
@@ -1379,7 +1394,18 @@ int gemm_a_box(int64_t M) {
 }
 
 int gemm_pick_bn(int64_t M, int N, int num_sms) {
-  if (use_pair(int(M), N, num_sms)) return 128;  // pair kernel: B box of 128 rows
+  if (use_pair(int(M), N, num_sms)) {
+    // pair kernel with 256-column tiles (B box of 128 rows). 192-column
+    // tiles (B box of 96 rows; HC_PAIR_BN=192 for A/B runs) fill the last
+    // wave better -- N=4096 at 4096 rows: 5 waves x 192 vs 4 x 256 columns
+    // -- but measured slower per GEMM on the 7B layer (scripts/ab_pair_bn.sh:
+    // QKV 290 -> 332 us, O 118 -> 126, FC2 280 -> 334), so 256 it is
+    static const int forced = [] {
+      const char* e = getenv("HC_PAIR_BN");
+      return e ? atoi(e) : 0;
+    }();
+    return forced == 192 ? 96 : 128;
+  }
   static const int forced_bn = [] {  // HC_GEMM_BN: force the small-M tile width (experiments)
     const char* e = getenv("HC_GEMM_BN");
     return e ? atoi(e) : 0;
@@ -1456,8 +1482,8 @@ cudaError_t launch_restore_kv(const CUtensorMap& tmA, const CUtensorMap& tmB, in
   const int Ms = std::max(M, m_sched);
   GemmOut g;
   const AMaps am = amaps_with_alt(tmA, alt);
-  if (bn == 128 && use_pair(Ms, N, num_sms))  // tmB has the 128-row box the pair needs
-    return launch_pair<kEpiKv>(am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, Ms,
+  if ((bn == 128 || bn == 96) && use_pair(Ms, N, num_sms))  // a pair B box (128 / 96 rows)
+    return launch_pair<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, Ms,
                                split_acc);
   return launch_tc_bn<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream,
                               split_acc, Ms);
@@ -1471,8 +1497,9 @@ cudaError_t launch_restore_kv_multi(const AMaps& am, const CUtensorMap& tmB, int
   for (int i = 1; i < am.n; ++i)
     if (am.row0[i] % kBM) return cudaErrorInvalidValue;  // a tile reads one source
   GemmOut g;
-  if (bn == 128 && use_pair(M, N, num_sms))
-    return launch_pair<kEpiKv>(am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, M, false);
+  if ((bn == 128 || bn == 96) && use_pair(M, N, num_sms))
+    return launch_pair<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, M,
+                               false);
   // (no K split: the multi-source path restores K/V, which stay exact)
   return launch_tc_bn<kEpiKv>(bn, am, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, false,
                               M);
@@ -1486,11 +1513,11 @@ cudaError_t launch_gemm_dense(const CUtensorMap& tmA, const CUtensorMap& tmB, in
   const int Ms = std::max(M, m_sched);
   KvOut o;
   const AMaps am = amaps_with_alt(tmA, alt);
-  if (bn == 128 && use_pair(Ms, N, num_sms))
+  if ((bn == 128 || bn == 96) && use_pair(Ms, N, num_sms))
     return mode == kEpiResid
-               ? launch_pair<kEpiResid>(am, tmB, M, N, K, true, o, g, epi, num_sms, stream, Ms,
+               ? launch_pair<kEpiResid>(bn, am, tmB, M, N, K, true, o, g, epi, num_sms, stream, Ms,
                                         split_acc)
-               : launch_pair<kEpiGelu>(am, tmB, M, N, K, true, o, g, epi, num_sms, stream, Ms,
+               : launch_pair<kEpiGelu>(bn, am, tmB, M, N, K, true, o, g, epi, num_sms, stream, Ms,
                                        split_acc);
   if (mode == kEpiResid)
     return launch_tc_bn<kEpiResid>(bn, am, tmB, M, N, K, true, o, g, epi, num_sms, stream,
