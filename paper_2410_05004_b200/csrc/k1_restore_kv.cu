@@ -574,11 +574,16 @@ __device__ __forceinline__ PairUnit pair_unit(int u, int full_units, bool split,
 __host__ __device__ __forceinline__ int pair_full_units(int tiles, int clusters) {
   return (tiles / clusters) * clusters;
 }
-// Only for long K loops: the exchange (first half's epilogue writing 128 KB
-// per CTA, the second's reading it) costs ~8 us, so at K = 4096 (a 9 us half
-// tile) the split measured no better than the idle tail (scripts/pair_trace.cu:
-// 88.6 vs 90.8 us); at K = 11008 it saves 8 us per launch (223 -> 215 us).
-constexpr int kTailMinKb = 96;
+// The exchange (first half's epilogue writing 128 KB per CTA, the second's
+// reading it) costs ~8 us: at K = 11008 the split saves 8 us per launch (223
+// -> 215 us); at K = 4096 (a 9 us half tile) it measured no better than the
+// idle tail in round 1 (scripts/pair_trace.cu: 88.6 vs 90.8 us) and 1 %
+// better with the 8-warp epilogue (O projection 114.5 -> 113.4 us, K6 layer
+// span -0.25 %, scripts/ab_tail.sh), so K loops of >= 32 k-blocks split.
+#ifndef HC_TAIL_MIN_KB
+#define HC_TAIL_MIN_KB 32
+#endif
+constexpr int kTailMinKb = HC_TAIL_MIN_KB;
 __host__ __device__ __forceinline__ bool pair_tail_split(int tiles, int clusters, int num_kb) {
   const int tail = tiles - pair_full_units(tiles, clusters);
   return tail > 0 && 2 * tail <= clusters && num_kb >= kTailMinKb;
