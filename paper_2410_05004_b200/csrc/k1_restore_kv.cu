@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // launch. (A 5-stage ring that left room for wider scratch starved the MMAs
 // of RESID tiles: 21.5 -> 24.5 us per K=4096 tile.)
 constexpr int kPairEpiWarps = 8;
+
 constexpr int kPairThreads = 64 + 32 * kPairEpiWarps;
 constexpr int kPairStages = 6;
 constexpr uint32_t kPairHalfBytes = 128 * kBK * 2;             // 16 KB: A half or B half
@@ -635,7 +636,10 @@ __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) 
 // float offset of 16-byte unit u (0..3) of transposed row r
 __device__ __forceinline__ int tunit(int r, int u) { return r * 16 + ((u ^ ((r >> 1) & 3)) << 2); }
 
-template <int MODE, int BN>
+// QKV: the fused Q/K/V projection (first out.q_cols columns are Q). A
+// separate instantiation: the routing, compiled into K1's epilogue, cost it
+// ~3 % (scripts/ab_k1_alone.sh: 182.9 vs 177.9 us per 7B layer).
+template <int MODE, int BN, bool QKV>
 __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n_blk, int M, int N,
                                                    const KvOut& out, const GemmOut& gout,
                                                    const EpiArgs& epi, uint32_t tbase, float* ws,
@@ -656,7 +660,7 @@ __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n
   // loads of chunk c: index 4 * h2 + j (16-column half h2, row 8j + g)
   auto issue = [&](int c, float4 (&ld)[8]) {
     const int col0 = n_blk * BN + c * 32;
-    const bool k_half = col0 < out.q_cols + out.d_kv;  // Q or K: rotated
+    const bool k_half = col0 < (QKV ? out.q_cols : 0) + out.d_kv;  // Q or K: rotated
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int h2 = i >> 2, j = i & 3;
@@ -705,8 +709,9 @@ __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n
     }
     const int col0 = n_blk * BN + c * 32;
     if (col0 >= N) continue;  // warp-uniform
-    const bool is_q = MODE == kEpiKv && col0 < out.q_cols;
-    const bool is_k = MODE == kEpiKv && !is_q && col0 - out.q_cols < out.d_kv;
+    const int qc = QKV ? out.q_cols : 0;
+    const bool is_q = QKV && MODE == kEpiKv && col0 < qc;
+    const bool is_k = MODE == kEpiKv && !is_q && col0 - qc < out.d_kv;
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
       __syncwarp();  // the previous reads of tbuf are done
@@ -717,9 +722,7 @@ __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n
                         f[16 * h2 + 4 * q4 + 3]);
       __syncwarp();
       const int col = col0 + 16 * h2 + 4 * u;  // this lane's 4 columns
-      const int ocol = MODE == kEpiKv
-                           ? (is_q ? col : is_k ? col - out.q_cols : col - out.q_cols - out.d_kv)
-                           : col;
+      const int ocol = MODE == kEpiKv ? (is_q ? col : is_k ? col - qc : col - qc - out.d_kv) : col;
       float4 cs4 = make_float4(0.f, 0.f, 0.f, 0.f);
       if (MODE != kEpiResid && epi.row_mean)
         cs4 = __ldg(reinterpret_cast<const float4*>(epi.colsum + col));
@@ -759,8 +762,7 @@ __device__ __forceinline__ void epilogue_tile_pair(int row_base, int lane, int n
           rope_rotate(a[0], a[1], l4.x, l4.y);
           rope_rotate(a[2], a[3], l4.z, l4.w);
         }
-        char* dst = is_q ? static_cast<char*>(out.q_base) +
-                               size_t(row_base + r) * size_t(out.q_cols) * 2
+        char* dst = is_q ? static_cast<char*>(out.q_base) + size_t(row_base + r) * size_t(qc) * 2
                          : is_k ? e.krow : e.vrow;
         if (out.out_f32 && !is_q)
           *reinterpret_cast<float4*>(dst + size_t(ocol) * 4) = make_float4(a[0], a[1], a[2], a[3]);
@@ -788,7 +790,7 @@ constexpr int kPairTraceSlots = 40;
   } while (0)
 #endif
 
-template <int MODE, int BN>
+template <int MODE, int BN, bool QKV>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ AMaps am,
                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K, KvOut out,
@@ -957,7 +959,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         epi_bar_sync(n_epi);
       }
       uint8_t* my = epi_smem + size_t(ew) * kPairEpiWarpBytes;
-      epilogue_tile_pair<MODE, BN>(row_base, lane, n_blk, M, N, out, gout, epi,
+      epilogue_tile_pair<MODE, BN, QKV>(row_base, lane, n_blk, M, N, out, gout, epi,
                                tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN), ws,
                                pu.half, reinterpret_cast<float*>(my),
                                reinterpret_cast<EpiRow*>(my + 32 * 16 * 4), c_begin, c_end);
@@ -1272,7 +1274,7 @@ cudaError_t tail_ws_for(int dev, cudaStream_t stream, int slots, TailWs** out) {
   return cudaSuccess;
 }
 
-template <int MODE, int BN>
+template <int MODE, int BN, bool QKV>
 cudaError_t launch_pair_bn(const AMaps& tmA, const CUtensorMap& tmB128, int M, int N, int K,
                            bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
                            int num_sms, cudaStream_t stream, int Ms, bool split_acc) {
@@ -1304,13 +1306,13 @@ cudaError_t launch_pair_bn(const AMaps& tmA, const CUtensorMap& tmB128, int M, i
   }
   static thread_local int attr_dev = -1;
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_pair_kernel<MODE, BN>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_pair_kernel<MODE, BN, QKV>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(kPairSmem));
     if (e != cudaSuccess) return e;
     attr_dev = dev;
   }
-  return launch_pdl(tc_gemm_pair_kernel<MODE, BN>, dim3(grid), dim3(kPairThreads), kPairSmem,
+  return launch_pdl(tc_gemm_pair_kernel<MODE, BN, QKV>, dim3(grid), dim3(kPairThreads), kPairSmem,
                     stream, tmA, tmB128, M, N, K, out, g, epi, idesc, Ms, ws, flags, epoch);
 }
 
@@ -1320,11 +1322,18 @@ template <int MODE>
 cudaError_t launch_pair(int bn, const AMaps& tmA, const CUtensorMap& tmB, int M, int N, int K,
                         bool bf16_in, const KvOut& out, const GemmOut& g, const EpiArgs& epi,
                         int num_sms, cudaStream_t stream, int Ms, bool split_acc) {
+  if constexpr (MODE == kEpiKv) {
+    if (out.q_cols)
+      return bn == 96 ? launch_pair_bn<MODE, 192, true>(tmA, tmB, M, N, K, bf16_in, out, g, epi,
+                                                        num_sms, stream, Ms, split_acc)
+                      : launch_pair_bn<MODE, 256, true>(tmA, tmB, M, N, K, bf16_in, out, g, epi,
+                                                        num_sms, stream, Ms, split_acc);
+  }
   if (bn == 96)
-    return launch_pair_bn<MODE, 192>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, Ms,
-                                     split_acc);
-  return launch_pair_bn<MODE, 256>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream, Ms,
-                                   split_acc);
+    return launch_pair_bn<MODE, 192, false>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms,
+                                            stream, Ms, split_acc);
+  return launch_pair_bn<MODE, 256, false>(tmA, tmB, M, N, K, bf16_in, out, g, epi, num_sms, stream,
+                                          Ms, split_acc);
 }
 
 // Pair kernel when the problem has enough 256x256 tiles to fill the SM pairs
