@@ -1483,6 +1483,10 @@ const int32_t* fa_persist_schedule(int n, int n_heads, int grid, bool head_major
     *stride_out = f->second.second;
     return f->second.first;
   }
+  // bounded: schedules are kept for the process (a launch may still read
+  // one), so past 64 shapes (a serving run's many context lengths) new
+  // shapes take the grid kernel instead
+  if (cache.size() >= 64) return nullptr;
   const int pairs = (n + 2 * kFaM - 1) / (2 * kFaM), kv_tiles = (n + kAttnN - 1) / kAttnN;
   const int items = pairs * n_heads;
   std::vector<std::vector<int32_t>> lists(static_cast<size_t>(grid));
@@ -1610,9 +1614,9 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
       int stride = 0;
       const int32_t* sched = fa_persist_schedule(n, n_heads, pgrid,
                                                  !a.rank_major && persist_env == 2, &stride);
-      if (!sched) return cudaErrorMemoryAllocation;
-      return launch_pdl(attn_fa_persist_kernel<DH>, dim3(pgrid), dim3(kFaThreads),
-                        FaCfg<DH>::kSmem, stream, tq, tk, tv, tk2, tv2, a, sched, stride);
+      if (sched)
+        return launch_pdl(attn_fa_persist_kernel<DH>, dim3(pgrid), dim3(kFaThreads),
+                          FaCfg<DH>::kSmem, stream, tq, tk, tv, tk2, tv2, a, sched, stride);
     }
     // HC_FA_ROWS=1: one softmax thread per query row (ROWS variant)
     static const bool rows = [] {
