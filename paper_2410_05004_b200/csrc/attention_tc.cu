@@ -1464,7 +1464,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
 // item ids...]; items in rank-major order (head fastest), cost ~ fixed + key
 // steps of the pair.
 const int32_t* fa_persist_schedule(int n, int n_heads, int grid, bool head_major,
-                                   int* stride_out) {
+                                   cudaStream_t stream, int* stride_out) {
   struct Key {
     int dev, n, heads, grid;
     bool hm;
@@ -1473,15 +1473,23 @@ const int32_t* fa_persist_schedule(int n, int n_heads, int grid, bool head_major
     }
   };
   static std::mutex mu;
-  static std::map<Key, std::pair<int32_t*, int>> cache;
+  struct Entry {
+    int32_t* dev;
+    int stride;
+    std::vector<int32_t> host;  // the copy's source, alive as long as the entry
+    cudaEvent_t ready;          // the upload on the private stream
+  };
+  static std::map<Key, Entry> cache;
+  static std::map<int, cudaStream_t> upload;  // per device, nothing else queued on it
   int dev = 0;
   cudaGetDevice(&dev);
   const Key key{dev, n, n_heads, grid, head_major};
   std::lock_guard<std::mutex> lk(mu);
   auto f = cache.find(key);
   if (f != cache.end()) {
-    *stride_out = f->second.second;
-    return f->second.first;
+    if (cudaStreamWaitEvent(stream, f->second.ready, 0) != cudaSuccess) return nullptr;
+    *stride_out = f->second.stride;
+    return f->second.dev;
   }
   // bounded: schedules are kept for the process (a launch may still read
   // one), so past 64 shapes (a serving run's many context lengths) new
@@ -1514,12 +1522,29 @@ const int32_t* fa_persist_schedule(int n, int n_heads, int grid, bool head_major
     std::copy(lists[size_t(c)].begin(), lists[size_t(c)].end(),
               host.begin() + std::ptrdiff_t(size_t(c) * size_t(stride) + 1));
   }
+  // uploaded on a private stream and ordered before the launch by an event:
+  // no device-wide synchronisation when a new shape shows up in the middle
+  // of a restore or a serving run, and launches on any stream wait for it;
+  // never freed
+  cudaStream_t& up = upload[dev];
+  if (!up && cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
   int32_t* d = nullptr;
-  if (cudaMalloc(&d, host.size() * sizeof(int32_t)) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(d, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice) !=
-      cudaSuccess)
+  cudaEvent_t ev = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&d), host.size() * sizeof(int32_t), up) !=
+          cudaSuccess ||
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
     return nullptr;
-  cache.emplace(key, std::make_pair(d, stride));
+  auto& e = cache[key];
+  e.dev = d;
+  e.stride = stride;
+  e.host = std::move(host);
+  e.ready = ev;
+  if (cudaMemcpyAsync(d, e.host.data(), e.host.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                      up) != cudaSuccess ||
+      cudaEventRecord(ev, up) != cudaSuccess || cudaStreamWaitEvent(stream, ev, 0) != cudaSuccess) {
+    cache.erase(key);
+    return nullptr;
+  }
   *stride_out = stride;
   return d;
 }
@@ -1596,7 +1621,12 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
       const char* e = getenv("HC_FA_PERSIST");
       return e ? atoi(e) : -1;
     }();
-    const bool persist = persist_env < 0 ? a.rank_major : persist_env != 0;
+    bool persist = persist_env < 0 ? a.rank_major : persist_env != 0;
+    if (persist) {  // (the schedule upload is not capturable: graphs keep the grid kernel)
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(stream, &cap);
+      persist = cap == cudaStreamCaptureStatusNone;
+    }
     // (HC_FA_PERSIST=2: persistent with the head-major item order as well)
     if (persist && !cu) {
       static thread_local int pattr_dev = -1;
@@ -1613,7 +1643,8 @@ cudaError_t launch_attn_tc(const void* q, int n, int n_heads, int n_kv_heads, co
       const int pgrid = std::min(sms, items);
       int stride = 0;
       const int32_t* sched = fa_persist_schedule(n, n_heads, pgrid,
-                                                 !a.rank_major && persist_env == 2, &stride);
+                                                 !a.rank_major && persist_env == 2, stream,
+                                                 &stride);
       if (sched)
         return launch_pdl(attn_fa_persist_kernel<DH>, dim3(pgrid), dim3(kFaThreads),
                           FaCfg<DH>::kSmem, stream, tq, tk, tv, tk2, tv2, a, sched, stride);
