@@ -315,6 +315,11 @@ typedef struct hc_store hc_store;
 hc_status hc_store_create(const hc_pool_desc* pool, size_t buffer_capacity_bytes,
                           hc_store** out);
 void hc_store_destroy(hc_store* s);
+/* B200 extension: page-lock `bytes` of pinned arena now (cudaHostAlloc pins
+ * page by page, ~0.1 s per 256 MiB), so later snapshots and chunk extents are
+ * carved from it without pinning on the save path (a serving host reserves
+ * its whole save volume at start-up). */
+hc_status hc_store_reserve(hc_store* s, size_t bytes);
 /* create_session (storage.hpp:90): HC_EINVAL/ HC_ERUNTIME on duplicate id */
 hc_status hc_store_create_session(hc_store* s, const hc_session_seed* seed);
 /* reopen_for_append (storage.hpp:91) */

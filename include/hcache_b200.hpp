@@ -333,6 +333,9 @@ class StorageManager {
   StorageManager(const StorageManager&) = delete;
   StorageManager& operator=(const StorageManager&) = delete;
 
+  // B200 extension: page-lock arena now, off the save path (hc_store_reserve)
+  void reserve(std::size_t bytes) { check(hc_store_reserve(s_, bytes)); }
+
   void create_session(const SessionSeed& seed) {
     std::vector<int32_t> toks(seed.tokens.begin(), seed.tokens.end());
     hc_session_seed c{seed.session_id.c_str(), seed.config_hash, seed.n_layers, seed.d_hidden,

@@ -150,6 +150,7 @@ _PROTOS = {
     "hc_timeline_bubble_fraction": (i32, [P(TimelineC), P(f64)]),
     "hc_simulate_pipeline": (i32, [P(PipelineJobC), i32, i32, P(TimelineC)]),
     "hc_store_create": (i32, [P(PoolDescC), C.c_size_t, P(vp)]),
+    "hc_store_reserve": (i32, [vp, C.c_size_t]),
     "hc_store_destroy": (None, [vp]),
     "hc_store_create_session": (i32, [vp, P(SessionSeedC)]),
     "hc_store_reopen_for_append": (i32, [vp, cp, P(i32), i64]),

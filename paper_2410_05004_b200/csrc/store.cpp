@@ -673,6 +673,13 @@ hc_status hc_store_create(const hc_pool_desc* pool, size_t buffer_capacity_bytes
 
 void hc_store_destroy(hc_store* s) { delete s; }
 
+hc_status hc_store_reserve(hc_store* s, size_t bytes) {
+  return guard([&] {
+    if (!s) fail(HC_EINVAL, "store_reserve: null store");
+    S(s).reserve_pinned(bytes);
+  });
+}
+
 hc_status hc_store_create_session(hc_store* s, const hc_session_seed* seed) {
   return guard([&] {
     if (!seed) fail(HC_EINVAL, "create_session: null seed");

@@ -348,6 +348,10 @@ class StorageManager:
 
     __del__ = close
 
+    def reserve(self, nbytes: int):
+        """Page-lock nbytes of arena now (hc_store_reserve), off the save path."""
+        check(lib().hc_store_reserve(self._h, int(nbytes)))
+
     def create_session(self, seed: SessionSeed):
         toks = (C.c_int32 * max(1, len(seed.tokens)))(*seed.tokens)
         p = seed.plan._c if seed.plan is not None else None
