@@ -296,6 +296,58 @@ bool Store::snapshot(const std::string& sid, int layer, int kind, const void* ro
   rec.kind = kind;
   rec.bytes = bytes;
   rec.tok_begin = tok_begin;
+  // Device rows appended at a chunk boundary of a stream with nothing pending
+  // in stage 1: copy them device->host straight into their chunk slots (the
+  // layer-before-token chunk layout, north star (1)) -- one copy-engine run
+  // per extent run of consecutive slots, no host memcpy -- and keep only the
+  // copy's event in stage 1 (the same byte budget and backpressure).
+  if (src_on_device && bytes && tok_begin < 0 && src_dtype == s.dtype) {
+    LayerStream& ls = s.streams[{layer, kind}];
+    ls.kind = kind;
+    if (ls.partial_bytes == 0 && ls.pending_fifo == 0 &&
+        int(ls.chunks.size()) == ls.next_chunk_idx) {
+      const size_t cb = s.chunk_bytes(kind), tb = s.token_bytes(kind);
+      const int expect = int((s.tokens.size() + HC_CHUNK_TOKENS - 1) / HC_CHUNK_TOKENS);
+      const uint8_t* src = static_cast<const uint8_t*>(rows);
+      uint8_t* run_dst = nullptr;
+      size_t run_src = 0, run_len = 0, off = 0;
+      auto flush_run = [&] {
+        if (run_len)
+          check_cuda(cudaMemcpyAsync(run_dst, src + run_src, run_len, cudaMemcpyDeviceToHost,
+                                     stream),
+                     "snapshot D2H");
+        run_len = 0;
+      };
+      while (off < bytes) {
+        uint8_t* slot = new_slot(s, ls, layer, ls.next_chunk_idx, expect);
+        const size_t take = std::min(cb, bytes - off);
+        if (run_len && run_dst + run_len == slot) {
+          run_len += take;
+        } else {
+          flush_run();
+          run_dst = slot;
+          run_src = off;
+          run_len = take;
+        }
+        ls.n_tokens += int(take / tb);
+        if (take == cb) {
+          ++ls.next_chunk_idx;
+          ++rec.chunks;
+        } else {
+          ls.partial_bytes = take;
+        }
+        off += take;
+      }
+      flush_run();
+      check_cuda(cudaEventCreateWithFlags(&rec.ready, cudaEventDisableTiming), "event create");
+      check_cuda(cudaEventRecord(rec.ready, stream), "event record");
+      rec.direct = true;
+      fifo_bytes_ += bytes;
+      fifo_.push_back(rec);
+      cv_.notify_all();
+      return true;
+    }
+  }
   rec.buf = static_cast<uint8_t*>(pool_mem_.alloc(bytes ? bytes : 1));
   if (src_on_device) {
     if (src_dtype != s.dtype) {
@@ -312,6 +364,7 @@ bool Store::snapshot(const std::string& sid, int layer, int kind, const void* ro
     convert(rows, src_dtype, rec.buf, s.dtype, n_elems);
   }
   fifo_bytes_ += bytes;
+  ++s.streams[{layer, kind}].pending_fifo;
   fifo_.push_back(rec);
   cv_.notify_all();
   return true;
@@ -354,10 +407,12 @@ int64_t Store::flush_record(Record& rec) {
     check_cuda(cudaEventSynchronize(rec.ready), "snapshot D2H wait");
     cudaEventDestroy(rec.ready);
   }
+  if (rec.direct) return rec.chunks;  // already in its slots (see snapshot)
   int64_t flushed = 0;
   Session& s = sessions_.at(rec.sid);
   LayerStream& ls = s.streams[{rec.layer, rec.kind}];
   ls.kind = rec.kind;
+  --ls.pending_fifo;
   const size_t cb = s.chunk_bytes(rec.kind), tb = s.token_bytes(rec.kind);
   // first extent per device: sized for the chunks this stream will hold -- a
   // whole session, or (range snapshots) this record's own chunks

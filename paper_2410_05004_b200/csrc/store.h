@@ -67,6 +67,7 @@ struct LayerStream {
   int first_stored = 0;     // shard streams: chunks [0, first_stored) are held elsewhere
   size_t partial_bytes = 0; // bytes in the chunk being filled
   std::vector<ChunkRef> chunks;  // every started chunk, in chunk order
+  int pending_fifo = 0;     // stage-1 records of this stream awaiting assembly
   // per device: current extent (consecutive slots)
   struct Extent {
     uint8_t* base = nullptr;
@@ -155,6 +156,11 @@ class Store {
     size_t bytes = 0;
     cudaEvent_t ready = nullptr;  // D2H completion (device-sourced rows)
     int64_t tok_begin = -1;       // range snapshot (shard sessions)
+    // direct: the rows were copied device->host straight into their chunk
+    // slots at snapshot time (the stream's bookkeeping is already advanced);
+    // the record only holds the copy's event and its stage-1 byte budget
+    bool direct = false;
+    int64_t chunks = 0;
   };
   // block=false stops at the first record whose device->host copy is still
   // in flight (the daemon never waits on the GPU while holding mu_).

@@ -1,8 +1,9 @@
 """Save-path probe (north star (1)): a 7B prefill's 32 layer inputs (4096
 tokens x 4096, bf16, on the device) snapshotted into the pinned chunk store --
-D2H on a side stream into the stage-1 FIFO, then the stage-2 chunk assembly
-(drain) -- and, for scale, one device->host copy of the same bytes. Prints
-GB/s of each stage; no GPU compute runs meanwhile."""
+device rows at a chunk boundary go D2H on a side stream straight into their
+chunk slots, stage 1 keeps the copy's event -- then drained and finalized; and,
+for scale, one device->host copy of the same bytes. Cold runs pin the arena on
+the way (cudaHostAlloc), reserved runs page-lock it first (hc_store_reserve)."""
 import os
 import sys
 import time
@@ -39,9 +40,9 @@ def main():
         store.drain_all()
         store.finalize("s")
         t2 = time.perf_counter()
-        print(f"run {it} ({'reserved arena' if warm else 'cold: pins on the way'}): snapshot (D2H + FIFO) {nbytes / (t1 - t0) / 1e9:6.1f} GB/s "
+        print(f"run {it} ({'reserved arena' if warm else 'cold: pins on the way'}): snapshot calls {nbytes / (t1 - t0) / 1e9:6.1f} GB/s "
               f"({(t1 - t0) * 1e3:7.1f} ms, {stalls} backpressure drains), "
-              f"total with chunk assembly {nbytes / (t2 - t0) / 1e9:6.1f} GB/s ({(t2 - t0) * 1e3:7.1f} ms)")
+              f"to finalized {nbytes / (t2 - t0) / 1e9:6.1f} GB/s ({(t2 - t0) * 1e3:7.1f} ms)")
         store.close()
     host = torch.empty(n * d, dtype=torch.bfloat16, pin_memory=True)
     torch.cuda.synchronize()
