@@ -301,13 +301,27 @@ bool Store::snapshot(const std::string& sid, int layer, int kind, const void* ro
   // layer-before-token chunk layout, north star (1)) -- one copy-engine run
   // per extent run of consecutive slots, no host memcpy -- and keep only the
   // copy's event in stage 1 (the same byte budget and backpressure).
-  if (src_on_device && bytes && tok_begin < 0 && src_dtype == s.dtype) {
+  if (src_on_device && bytes && src_dtype == s.dtype) {
     LayerStream& ls = s.streams[{layer, kind}];
     ls.kind = kind;
-    if (ls.partial_bytes == 0 && ls.pending_fifo == 0 &&
+    const size_t cb = s.chunk_bytes(kind), tb = s.token_bytes(kind);
+    // range snapshots (a head-sharded rank's token range): a fresh stream
+    // starts at tok_begin, or the range continues the stored one
+    const bool fresh = ls.n_tokens == 0 && ls.chunks.empty();
+    const bool range_ok = tok_begin < 0 || tok_begin == ls.n_tokens || fresh;
+    if (range_ok && ls.partial_bytes == 0 && ls.pending_fifo == 0 &&
         int(ls.chunks.size()) == ls.next_chunk_idx) {
-      const size_t cb = s.chunk_bytes(kind), tb = s.token_bytes(kind);
-      const int expect = int((s.tokens.size() + HC_CHUNK_TOKENS - 1) / HC_CHUNK_TOKENS);
+      int expect = int((s.tokens.size() + HC_CHUNK_TOKENS - 1) / HC_CHUNK_TOKENS);
+      if (tok_begin >= 0) {
+        if (fresh && tok_begin > 0) {  // chunks [0, tok_begin/64) are held by other ranks
+          const int c0 = int(tok_begin / HC_CHUNK_TOKENS);
+          for (int c = 0; c < c0; ++c)
+            ls.chunks.push_back(ChunkRef{(layer + c) % ndev_, nullptr, -1});
+          ls.next_chunk_idx = ls.first_stored = c0;
+          ls.n_tokens = int(tok_begin);
+        }
+        expect = int((bytes + cb - 1) / cb);  // (flush_record's sizing for range records)
+      }
       const uint8_t* src = static_cast<const uint8_t*>(rows);
       uint8_t* run_dst = nullptr;
       size_t run_src = 0, run_len = 0, off = 0;

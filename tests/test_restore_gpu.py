@@ -192,6 +192,44 @@ def test_device_snapshot_roundtrip_bitexact(cuda):
     assert store.read_layer(man, 1, H.StateKind.HIDDEN) is None
 
 
+@pytest.mark.parametrize("b,pieces", [(0, [(0, 384)]), (128, [(128, 300), (300, 333)]),
+                                      (192, [(192, 256), (256, 1000)])])
+def test_device_range_snapshot_roundtrip_bitexact(cuda, b, pieces):
+    """A head-sharded rank's save (snapshot_range from device rows): the
+    direct D2H path starts a fresh stream at tok_begin; a continuation at the
+    stored end keeps it, a ragged one falls back to stage 1. The rank's token
+    range reads back bit-exact; tokens below it are not held."""
+    import torch
+    from paper_2410_05004_b200 import capi
+    from paper_2410_05004_b200 import hcache as H
+    store = H.StorageManager(H.DevicePool(3), buffer_capacity_bytes=64 << 20)
+    plan = H.RestorationPlan.make(2, 2, H.Complement.NONE)
+    n = 1000
+    store.create_session(H.SessionSeed("s", 1, 2, 256, 2, plan, list(range(n))))
+    rows = dev_hidden(n, 256, seed=5)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for x, y in pieces:
+            tb = x if x % 64 == 0 else None
+            assert store.snapshot("s", 0, H.StateKind.HIDDEN, rows[x:y].contiguous(),
+                                  tok_begin=tb, stream=side.cuda_stream)
+    side.synchronize()
+    store.finalize("s")
+    e = pieces[-1][1]
+    back = torch.empty((e - b, 256), dtype=rows.dtype, device="cuda")
+
+    def read(x, y, dst):
+        return capi.lib().hc_store_read_layer_range(
+            store._h, b"s", 0, int(H.StateKind.HIDDEN), x, y, dst.data_ptr(),
+            dst.numel() * dst.element_size(), 1, torch.cuda.current_stream().cuda_stream)
+    capi.check(read(b, e, back))
+    torch.cuda.synchronize()
+    assert torch.equal(back, rows[b:e])
+    if b:
+        assert read(0, 64, back[:64]) == capi.HC_ENOENT  # held by another rank
+
+
 def test_restore_batch_ragged_equals_single(cuda):
     """Config 4 layout: several sessions restored by one grouped K1 per layer."""
     import torch
