@@ -463,6 +463,10 @@ constexpr int fa_threads() { return ROWS ? kFaRowsThreads : kFaThreads; }
 #ifndef HC_FA_EXP_NOMAXPASS  // 1: skip the row-max TMEM pass after tile 0 (timing only)
 #define HC_FA_EXP_NOMAXPASS 0
 #endif
+#ifndef HC_FA_SREG  // 1: pass 1 reads both score chunks with one wait and keeps chunk 0 in
+                    // registers for pass 2, which reads chunk 1 while chunk 0's exponentials run
+#define HC_FA_SREG 1
+#endif
 #ifndef HC_FA_PCHUNK  // 1: P published per 32-key chunk, 0: once per tile (experiments)
 #define HC_FA_PCHUNK 1
 #endif
@@ -942,12 +946,24 @@ __global__ void __launch_bounds__(fa_threads<ROWS>(), 1)
       float m8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) m8[u] = -INFINITY;
+#if HC_FA_SREG
+      // both 32-column loads in flight at once, one wait; the scores stay in
+      // registers for pass 2 (no second TMEM read of S)
+      uint32_t sv0[32], sv1[32];
+      tmem_ld_32x32b_x32(t_s + 0u, sv0);
+      tmem_ld_32x32b_x32(t_s + 32u, sv1);
+      tmem_wait_ld();
+#endif
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         if (HC_FA_EXP_NOMAXPASS && j > 0) break;  // timing experiment only (wrong results)
+#if HC_FA_SREG
+        uint32_t (&v)[32] = c ? sv1 : sv0;
+#else
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_s + uint32_t(c * 32), v);
         tmem_wait_ld();
+#endif
         if (diag) {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
@@ -998,6 +1014,16 @@ __global__ void __launch_bounds__(fa_threads<ROWS>(), 1)
       uint64_t sum2 = 0, sum2b = 0;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
+#if HC_FA_SREG
+        if (c == 0) tmem_ld_32x32b_x32(t_s + 32u, sv1);  // in flight during chunk 0
+        else tmem_wait_ld();
+        uint32_t (&v)[32] = c ? sv1 : sv0;  // chunk 0 masked in pass 1
+        if (c == 1 && diag) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (32 + i > lim) v[i] = __float_as_uint(-INFINITY);
+        }
+#else
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_s + uint32_t(c * 32), v);
         tmem_wait_ld();
@@ -1006,6 +1032,7 @@ __global__ void __launch_bounds__(fa_threads<ROWS>(), 1)
           for (int i = 0; i < 32; ++i)
             if (c * 32 + i > lim) v[i] = __float_as_uint(-INFINITY);
         }
+#endif
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -1347,11 +1374,21 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         float m8[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) m8[u] = -INFINITY;
+#if HC_FA_SREG
+        uint32_t sv0[32], sv1[32];
+        tmem_ld_32x32b_x32(t_s + 0u, sv0);
+        tmem_ld_32x32b_x32(t_s + 32u, sv1);
+        tmem_wait_ld();
+#endif
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
+#if HC_FA_SREG
+          uint32_t (&v)[32] = c ? sv1 : sv0;
+#else
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_s + uint32_t(c * 32), v);
           tmem_wait_ld();
+#endif
           if (diag) {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
@@ -1394,6 +1431,16 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         uint64_t sum2 = 0, sum2b = 0;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
+#if HC_FA_SREG
+          if (c == 0) tmem_ld_32x32b_x32(t_s + 32u, sv1);  // in flight during chunk 0
+          else tmem_wait_ld();
+          uint32_t (&v)[32] = c ? sv1 : sv0;  // chunk 0 masked in pass 1
+          if (c == 1 && diag) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (32 + e > lim) v[e] = __float_as_uint(-INFINITY);
+          }
+#else
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_s + uint32_t(c * 32), v);
           tmem_wait_ld();
@@ -1402,6 +1449,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
             for (int e = 0; e < 32; ++e)
               if (c * 32 + e > lim) v[e] = __float_as_uint(-INFINITY);
           }
+#endif
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
