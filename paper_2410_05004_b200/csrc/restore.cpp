@@ -224,7 +224,9 @@ void restore_group(hc_store* st, const char* const* sids, int n_sessions, const 
     // restore.cpp:228-231
     if (m.n_layers != w->cfg.n_layers) bad("layer count mismatch");
     if (m.d_hidden != w->cfg.d_hidden) bad("d_hidden mismatch");
-    if (m.n_tokens <= 0) bad("empty session");
+    // an empty session has no chunks: the reference's read_layer returns
+    // nullopt and execute_layer throws runtime_error (restore.cpp:70-71)
+    if (m.n_tokens <= 0) fail(HC_ENOENT, std::string(who) + ": missing hidden chunks (empty session)");
     if (plan_serialize(&m.plan) != plan_serialize(plan_arg ? plan_arg : &ms[0].plan))
       bad(plan_arg ? "plan does not match session manifest"
                    : "sessions of one batch must share a plan");

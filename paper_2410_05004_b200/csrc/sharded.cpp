@@ -141,7 +141,7 @@ void restore_sharded(hc_peer_group* g, hc_store* st, const char* sid_c, const hc
   if (m.d_hidden != w->cfg.d_hidden || m.d_hidden != g->d) bad("d_hidden mismatch");
   if (m.elem_bytes != 2 || m.dtype != HC_DTYPE_BF16) bad("bf16 sessions required");
   const int64_t n = m.n_token_ids;  // the context (a shard stores part of it)
-  if (n <= 0) bad("session without token ids");
+  if (n <= 0) fail(HC_ENOENT, "restore_sharded: missing hidden chunks (empty session)");
   validate_pages(w, pages, w->d_kv);
   if (n > int64_t(pages->num_pages) * pages->page_size) bad("KV pages too small for the session");
   if (w->cfg.rope_enabled && n > w->rope_rows) bad("session longer than max_seq (RoPE table)");

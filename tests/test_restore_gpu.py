@@ -166,6 +166,10 @@ def test_restore_error_contract(cuda):
     store.create_session(H.SessionSeed("open", 0, 4, 512, 2, stored, [], d_kv=512))
     with pytest.raises(capi.Incomplete):
         H.restore(store, "open", w, stored, H.ThrottleConfig(), kv, table)
+    # an empty session has no chunks (restore.cpp:70-71: runtime_error)
+    store.finalize("open")
+    with pytest.raises(capi.NotFound):
+        H.restore(store, "open", w, stored, H.ThrottleConfig(), kv, table)
 
 
 def test_device_snapshot_roundtrip_bitexact(cuda):
