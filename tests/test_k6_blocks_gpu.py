@@ -72,6 +72,38 @@ def test_attention_block_orders_vs_torch(cuda, n, heads, kvh):
         assert err < 2e-2, (h0, err)
 
 
+@pytest.mark.parametrize("n,heads,kvh", [(4133, 32, 32), (4096, 32, 8)])
+def test_attention_persistent_equals_grid_bitwise(cuda, n, heads, kvh):
+    """The persistent kernel (default for a sequence whose K/V fit in L2) and
+    the grid kernel (taken under CUDA-graph capture, which cannot hold the
+    persistent schedule's upload) run the same per-tile arithmetic: their
+    outputs are bit-identical."""
+    import torch
+    from paper_2410_05004_b200 import capi
+    dh = 128
+    g = torch.Generator(device="cuda").manual_seed(7 * n + heads)
+    q = torch.randn(n, heads * dh, device="cuda", generator=g).bfloat16()
+    k = torch.randn(n, kvh * dh, device="cuda", generator=g).bfloat16()
+    v = torch.randn(n, kvh * dh, device="cuda", generator=g).bfloat16()
+    outs = [torch.full((n, heads * dh), float("nan"), device="cuda", dtype=torch.bfloat16)
+            for _ in range(2)]
+
+    def run(o, stream):
+        capi.check(capi.lib().hc_attention_dense(q.data_ptr(), n, heads, kvh, dh, k.data_ptr(),
+                                                 v.data_ptr(), kvh * dh, o.data_ptr(), stream))
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run(outs[0], s.cuda_stream)  # persistent
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            run(outs[1], s.cuda_stream)  # grid (captured)
+        graph.replay()
+    s.synchronize()
+    assert not torch.isnan(outs[0].float()).any()
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("m,n,k,split", [
     (200, 256, 512, 0), (1024, 512, 2048, 0), (130, 4096, 256, 0),
