@@ -250,6 +250,8 @@ __global__ void __launch_bounds__(kDecThreads)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ q, int n_heads, int group, KvOut kv,
                        const int32_t* __restrict__ cu_q, const int32_t* __restrict__ seq_start,
                        int n_splits, float scale_log2, float* __restrict__ part) {
+  pdl_wait();  // Q / K / V of this step (programmatic dependent launch)
+  pdl_trigger();
   constexpr int LPK = DH / 8;            // lanes per key
   constexpr int KPW = 32 / LPK;          // keys per warp pass
   constexpr int KPB = KPW * (kDecThreads / 32);  // keys per block pass
@@ -345,6 +347,8 @@ template <int DH>
 __global__ void attn_decode_combine_kernel(const float* __restrict__ part, int n_heads,
                                            int n_splits, const int32_t* __restrict__ cu_q,
                                            __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int h = blockIdx.x, z = blockIdx.y, t = threadIdx.x;
   const float* base = part + (size_t(z) * n_heads + h) * n_splits * (DH + 2);
   float M = -INFINITY;
@@ -534,19 +538,24 @@ cudaError_t launch_attention_extend(const void* q, int n_seqs, int max_new, cons
     const float scale_log2 = (1.0f / sqrtf(float(dh))) * 1.4426950408889634f;
     const dim3 grid{unsigned(n_kv_heads), unsigned(n_seqs), unsigned(splits)};
     if (dh == 128) {
-      attn_decode_kernel<128><<<grid, kDecThreads, 0, stream>>>(
-          static_cast<const __nv_bfloat16*>(q), n_heads, group, kv, cu_q, seq_start, splits,
-          scale_log2, part);
-      attn_decode_combine_kernel<128><<<dim3(unsigned(n_heads), unsigned(n_seqs)), 128, 0, stream>>>(
-          part, n_heads, splits, cu_q, static_cast<__nv_bfloat16*>(out));
+      e = launch_pdl(attn_decode_kernel<128>, grid, dim3(kDecThreads), 0, stream,
+                     static_cast<const __nv_bfloat16*>(q), n_heads, group, kv, cu_q, seq_start,
+                     splits, scale_log2, part);
+      if (e == cudaSuccess)
+        e = launch_pdl(attn_decode_combine_kernel<128>, dim3(unsigned(n_heads), unsigned(n_seqs)),
+                       dim3(128), 0, stream, static_cast<const float*>(part), n_heads, splits, cu_q,
+                       static_cast<__nv_bfloat16*>(out));
     } else {
-      attn_decode_kernel<64><<<grid, kDecThreads, 0, stream>>>(
-          static_cast<const __nv_bfloat16*>(q), n_heads, group, kv, cu_q, seq_start, splits,
-          scale_log2, part);
-      attn_decode_combine_kernel<64><<<dim3(unsigned(n_heads), unsigned(n_seqs)), 64, 0, stream>>>(
-          part, n_heads, splits, cu_q, static_cast<__nv_bfloat16*>(out));
+      e = launch_pdl(attn_decode_kernel<64>, grid, dim3(kDecThreads), 0, stream,
+                     static_cast<const __nv_bfloat16*>(q), n_heads, group, kv, cu_q, seq_start,
+                     splits, scale_log2, part);
+      if (e == cudaSuccess)
+        e = launch_pdl(attn_decode_combine_kernel<64>, dim3(unsigned(n_heads), unsigned(n_seqs)),
+                       dim3(64), 0, stream, static_cast<const float*>(part), n_heads, splits, cu_q,
+                       static_cast<__nv_bfloat16*>(out));
     }
     cudaFreeAsync(part, stream);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
   return attention_launch(q, 0, dim3((max_new + kQ - 1) / kQ, n_heads, n_seqs), cu_q, seq_start,

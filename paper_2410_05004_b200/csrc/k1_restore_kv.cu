@@ -281,6 +281,8 @@ __device__ __forceinline__ void epilogue_tile(int row, int n_blk, int M, int N, 
 template <int MODE>
 __global__ void splitk_epilogue_kernel(const float* __restrict__ part, int splits, int M, int N,
                                        KvOut out, GemmOut gout, EpiArgs epi) {
+  pdl_wait();  // the GEMM's partials (programmatic dependent launch)
+  pdl_trigger();
   const int chunks = N / 32;
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -1390,8 +1392,10 @@ cudaError_t launch_tc(const AMaps& tmA, const CUtensorMap& tmB, int M, int N, in
   }
   if (k_splits > 1) {
     const int64_t threads = int64_t(M) * (N / 32) * 32;
-    splitk_epilogue_kernel<MODE><<<unsigned((threads + 255) / 256), 256, 0, stream>>>(
-        part, k_splits, M, N, out, g, epi);
+    cudaError_t e = launch_pdl(splitk_epilogue_kernel<MODE>, dim3(unsigned((threads + 255) / 256)),
+                               dim3(256), 0, stream, static_cast<const float*>(part), k_splits,
+                               M, N, out, g, epi);
+    if (e != cudaSuccess) return e;
     cudaFreeAsync(part, stream);
   }
   (void)grid;
